@@ -1,0 +1,204 @@
+"""CPU oracle for the GSI hot path — TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package.  The product path
+(``paper_1906_03420_b200``) never imports it and shares no code with it.
+
+Two independent matchers, each citing the definition it follows:
+
+* ``match``        — the C backtracker in ``oracle.c`` (Fig. 2; Def. 2-3).
+* ``brute_force``  — enumerate every injective map V(Q) -> V(G) for tiny inputs and keep
+                     those that satisfy Def. 2's first two bullets;
+                     it pins the backtracker.
+
+plus the signature-filter specification (§III-A) in
+``signatures`` / ``query_signatures`` / ``filter`` and the set fingerprint of SURVEY.md §8(c).
+"""
+from __future__ import annotations
+
+import ctypes
+import itertools
+import os
+import subprocess
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+ERRORS = {-1: "invalid argument", -2: "vertex out of range", -3: "label out of range",
+          -4: "self loop", -5: "duplicate edge", -6: "query disconnected", -7: "query too large",
+          -9: "timeout"}
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c (plain C, OpenMP) into liboracle.so next to it."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-std=c11",
+                               "-o", _LIB, _SRC])
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = ctypes.CDLL(build())
+        P, I32, I64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+        L.og_build.restype = P
+        L.og_build.argtypes = [I64, P, I64, P, P, P, P]
+        L.og_free.argtypes = [P]
+        L.og_match.restype = I64
+        L.og_match.argtypes = [P, I32, P, I32, P, P, P, I32, P, I64, I32, I32, P, I64, P, ctypes.c_double]
+        L.og_neighbors.restype = I64
+        L.og_neighbors.argtypes = [P, I32, I32, P, I64]
+        L.og_degree.restype = I64
+        L.og_degree.argtypes = [P, I32]
+        L.og_signatures.argtypes = [P, P]
+        L.og_query_signatures.argtypes = [I32, P, I32, P, P, P, P]
+        L.og_filter.argtypes = [P, P, I32, P, P, P]
+        L.og_fingerprint_rows.argtypes = [P, I64, I32, P]
+        L.og_sig_group_of.restype = I32
+        L.og_sig_group_of.argtypes = [I32, I32]
+        L.og_max_threads.restype = I32
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _i32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int):
+        super().__init__(f"oracle error {code}: {ERRORS.get(code, '?')}")
+        self.code = code
+
+
+class OracleGraph:
+    """The oracle's own index of G: per-vertex adjacency sorted by (edge label, neighbour)."""
+
+    def __init__(self, g):
+        self.n = int(g.n)
+        self._vl, self._s, self._d, self._e = _i32(g.vlabels), _i32(g.src), _i32(g.dst), _i32(g.elabels)
+        err = ctypes.c_int32(0)
+        self._h = lib().og_build(self.n, _p(self._vl), len(self._s), _p(self._s), _p(self._d), _p(self._e),
+                                 ctypes.byref(err))
+        if not self._h:
+            raise OracleError(err.value)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib().og_free(h)
+            self._h = None
+
+    def neighbors(self, v: int, l: int) -> np.ndarray:
+        """N(v,l) ascending."""
+        cnt = lib().og_neighbors(self._h, v, l, None, 0)
+        out = np.empty(max(cnt, 1), np.int32)
+        lib().og_neighbors(self._h, v, l, _p(out), cnt)
+        return out[:cnt]
+
+    def degree(self, v: int) -> int:
+        return int(lib().og_degree(self._h, v))
+
+
+def match(og: OracleGraph, q, root: int = 0, roots: Optional[Sequence[int]] = None, threads: int = 0,
+          hom: bool = False, table: bool = True, cap: Optional[int] = None,
+          timeout: float = 0.0) -> Tuple[int, Tuple[int, int, int], Optional[np.ndarray]]:
+    """Enumerate R(Q,G).  Returns (count, fingerprint (count, sum, xor), table or None);
+    the table is k int32 per row in query-id order, sorted lexicographically."""
+    qv, qs, qd, qe = _i32(q.vlabels), _i32(q.src), _i32(q.dst), _i32(q.elabels)
+    r = None if roots is None else _i32(roots)
+    fp = np.zeros(3, np.uint64)
+    k = int(q.n)
+    if table:
+        if cap is None:
+            cnt = lib().og_match(og._h, k, _p(qv), len(qs), _p(qs), _p(qd), _p(qe), root,
+                                 None if r is None else _p(r), 0 if r is None else len(r), threads,
+                                 int(hom), None, 0, _p(fp), timeout)
+            if cnt < 0:
+                raise OracleError(int(cnt))
+            cap = cnt
+        out = np.empty((max(cap, 1), k), np.int32)
+    else:
+        out = None
+    cnt = lib().og_match(og._h, k, _p(qv), len(qs), _p(qs), _p(qd), _p(qe), root,
+                         None if r is None else _p(r), 0 if r is None else len(r), threads, int(hom),
+                         None if out is None else _p(out), 0 if out is None else cap, _p(fp), timeout)
+    if cnt < 0:
+        raise OracleError(int(cnt))
+    fpt = (int(fp[0]), int(fp[1]), int(fp[2]))
+    return int(cnt), fpt, (None if out is None else out[: min(cnt, cap)])
+
+
+def fingerprint_rows(rows: np.ndarray, k: int) -> Tuple[int, int, int]:
+    rows = _i32(rows).reshape(-1, k)
+    fp = np.zeros(3, np.uint64)
+    lib().og_fingerprint_rows(_p(rows), rows.shape[0], k, _p(fp))
+    return int(fp[0]), int(fp[1]), int(fp[2])
+
+
+# ------------------------------------------------------------------ signatures ----
+def signatures(og: OracleGraph) -> np.ndarray:
+    """Column-first data signature table, shape (16, n) uint32."""
+    planes = np.zeros((16, og.n), np.uint32)
+    lib().og_signatures(og._h, _p(planes))
+    return planes
+
+
+def query_signatures(q) -> np.ndarray:
+    """Query signatures, shape (k, 16) uint32 (PAPER.md L545 'same encoding strategy')."""
+    out = np.zeros((q.n, 16), np.uint32)
+    lib().og_query_signatures(q.n, _p(_i32(q.vlabels)), len(q.src), _p(_i32(q.src)), _p(_i32(q.dst)),
+                              _p(_i32(q.elabels)), _p(out))
+    return out
+
+
+def filter(og: OracleGraph, planes: np.ndarray, qsig: np.ndarray) -> Tuple[np.ndarray, np.ndarray]:
+    """C(u) bitmaps (k, ceil(n/32)) uint32 and |C(u)| (k,) int64 (reading A4)."""
+    k = qsig.shape[0]
+    words = (og.n + 31) // 32
+    bm = np.zeros((k, max(words, 1)), np.uint32)
+    cnt = np.zeros(k, np.int64)
+    lib().og_filter(og._h, _p(np.ascontiguousarray(planes)), k, _p(np.ascontiguousarray(qsig)), _p(bm), _p(cnt))
+    return bm[:, :words], cnt
+
+
+def sig_group(elabel: int, nlabel: int) -> int:
+    return int(lib().og_sig_group_of(elabel, nlabel))
+
+
+def max_threads() -> int:
+    return int(lib().og_max_threads())
+
+
+# ------------------------------------------------------------------ brute force ----
+def brute_force(g, q, hom: bool = False) -> List[Tuple[int, ...]]:
+    """All maps f: V(Q)->V(G) (injective unless hom) with L_V(f(u)) = L_V(u) and every query
+    edge (a,b,l) present as a data edge {f(a),f(b)} labelled l (Def. 2 bullets 1-2,
+    L278-279; Def. 3).  Pure Python; tiny inputs only (n <= 9, k <= 5)."""
+    n, k = int(g.n), int(q.n)
+    edges = set()
+    for s, d, l in zip(g.src.tolist(), g.dst.tolist(), g.elabels.tolist()):
+        edges.add((s, d, l)); edges.add((d, s, l))
+    qe = list(zip(q.src.tolist(), q.dst.tolist(), q.elabels.tolist()))
+    gl, ql = g.vlabels.tolist(), q.vlabels.tolist()
+    it = itertools.product(range(n), repeat=k) if hom else itertools.permutations(range(n), k)
+    out = []
+    for f in it:
+        if any(gl[f[u]] != ql[u] for u in range(k)):
+            continue
+        if all((f[a], f[b], l) in edges for a, b, l in qe):
+            out.append(tuple(f))
+    out.sort()
+    return out

@@ -1,0 +1,451 @@
+/*
+ * oracle.c — plain, slow, obviously-correct CPU reference for the GSI hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  It shares no code,
+ * header, table or constant generator with paper_1906_03420_b200/csrc (the CUDA path);
+ * the two implement the same written specification independently.
+ *
+ * What it computes (Def. 2-3; N(v,l) at L299):
+ *   R(Q,G) = { f : V(Q) -> V(G) |  f injective,
+ *                                   L_V(f(u)) = L_V(u) for every u,
+ *                                   every query edge (a,b,l) has an undirected data
+ *                                   edge {f(a), f(b)} labelled l }.
+ *   (non-induced / monomorphism reading A1; a match is a mapping, reading A2.)
+ *   Injectivity is the set subtraction of Alg. 3 line 10;
+ *   dropping it gives homomorphism (flag `hom`).
+ *
+ * Algorithm: the classic backtracking search tree (Fig. 2; L430) with a
+ * static BFS query order from a root query vertex (ties to the smallest id), candidates
+ * from the sorted l-adjacency of the earliest-ordered already-mapped neighbour, and
+ * checks for label, injectivity and every other query edge to a mapped vertex (binary
+ * search in the per-vertex (label, neighbour)-sorted adjacency).  OpenMP over root
+ * candidates (dynamic schedule) for timing only.
+ *
+ * Also here: an independent re-implementation of the signature filter specification
+ * (§III-A; stored-label field L1277; N=512, K=32 at L1420; readings
+ * A4/A5/A6 of SURVEY.md §8(c)) used only to compare C(u) bitmaps bit for bit, and the
+ * order-independent set fingerprint of SURVEY.md §8(c).
+ *
+ * Parity pins: see tests/test_oracle.py (Fig. 1 reconstruction, closed forms, brute force
+ * over all injective maps on tiny graphs, signature properties).
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <stdio.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define OG_MAXK 32
+
+/* ---------------------------------------------------------------- graph index ------ */
+typedef struct {
+    int64_t n, m;
+    int32_t *vl;        /* vertex labels                                             */
+    int64_t *off;       /* n+1 offsets into adj                                      */
+    int64_t *adj;       /* packed ((uint64)label << 32) | (uint32)neighbour, sorted  */
+} og_graph;
+
+static int cmp_u64(const void *a, const void *b) {
+    uint64_t x = *(const uint64_t *)a, y = *(const uint64_t *)b;
+    return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+/* err: 0 ok, -1 bad arg, -2 vertex range, -3 label range, -4 self loop, -5 duplicate */
+og_graph *og_build(int64_t n, const int32_t *vl, int64_t m, const int32_t *src,
+                   const int32_t *dst, const int32_t *el, int32_t *err) {
+    *err = 0;
+    if (n < 0 || m < 0) { *err = -1; return NULL; }
+    for (int64_t i = 0; i < n; i++) if (vl[i] < 0) { *err = -3; return NULL; }
+    for (int64_t e = 0; e < m; e++) {
+        if (src[e] < 0 || src[e] >= n || dst[e] < 0 || dst[e] >= n) { *err = -2; return NULL; }
+        if (el[e] < 0) { *err = -3; return NULL; }
+        if (src[e] == dst[e]) { *err = -4; return NULL; }
+    }
+    og_graph *g = (og_graph *)calloc(1, sizeof(og_graph));
+    g->n = n; g->m = m;
+    g->vl = (int32_t *)malloc(sizeof(int32_t) * (n > 0 ? n : 1));
+    memcpy(g->vl, vl, sizeof(int32_t) * n);
+    g->off = (int64_t *)calloc(n + 1, sizeof(int64_t));
+    g->adj = (int64_t *)malloc(sizeof(int64_t) * (2 * m > 0 ? 2 * m : 1));
+    for (int64_t e = 0; e < m; e++) { g->off[src[e] + 1]++; g->off[dst[e] + 1]++; }
+    for (int64_t v = 0; v < n; v++) g->off[v + 1] += g->off[v];
+    int64_t *fill = (int64_t *)malloc(sizeof(int64_t) * (n > 0 ? n : 1));
+    memcpy(fill, g->off, sizeof(int64_t) * n);
+    for (int64_t e = 0; e < m; e++) {
+        uint64_t l = (uint64_t)(uint32_t)el[e] << 32;
+        g->adj[fill[src[e]]++] = (int64_t)(l | (uint32_t)dst[e]);
+        g->adj[fill[dst[e]]++] = (int64_t)(l | (uint32_t)src[e]);
+    }
+    free(fill);
+    #pragma omp parallel for schedule(dynamic, 1024)
+    for (int64_t v = 0; v < n; v++)
+        qsort(g->adj + g->off[v], (size_t)(g->off[v + 1] - g->off[v]), sizeof(int64_t), cmp_u64);
+    for (int64_t v = 0; v < n && !*err; v++)
+        for (int64_t j = g->off[v] + 1; j < g->off[v + 1]; j++)
+            if (g->adj[j] == g->adj[j - 1]) { *err = -5; break; }
+    if (*err) { free(g->vl); free(g->off); free(g->adj); free(g); return NULL; }
+    return g;
+}
+
+void og_free(og_graph *g) {
+    if (!g) return;
+    free(g->vl); free(g->off); free(g->adj); free(g);
+}
+
+/* N(v,l) as a half-open index range [*b, *e) into g->adj. */
+static void og_nbrs(const og_graph *g, int32_t v, int32_t l, int64_t *b, int64_t *e) {
+    uint64_t lo_key = (uint64_t)(uint32_t)l << 32;
+    uint64_t hi_key = lo_key | 0xFFFFFFFFull;
+    int64_t lo = g->off[v], hi = g->off[v + 1];
+    while (lo < hi) { int64_t mid = (lo + hi) >> 1; if ((uint64_t)g->adj[mid] < lo_key) lo = mid + 1; else hi = mid; }
+    *b = lo;
+    hi = g->off[v + 1];
+    while (lo < hi) { int64_t mid = (lo + hi) >> 1; if ((uint64_t)g->adj[mid] <= hi_key) lo = mid + 1; else hi = mid; }
+    *e = lo;
+}
+
+static int og_has_edge(const og_graph *g, int32_t v, int32_t w, int32_t l) {
+    uint64_t key = ((uint64_t)(uint32_t)l << 32) | (uint32_t)w;
+    int64_t lo = g->off[v], hi = g->off[v + 1];
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        uint64_t x = (uint64_t)g->adj[mid];
+        if (x == key) return 1;
+        if (x < key) lo = mid + 1; else hi = mid;
+    }
+    return 0;
+}
+
+int64_t og_degree(const og_graph *g, int32_t v) { return g->off[v + 1] - g->off[v]; }
+
+/* Label-filtered adjacency N(v,l), ascending; returns |N(v,l)|, writes up to cap ids. */
+int64_t og_neighbors(const og_graph *g, int32_t v, int32_t l, int32_t *out, int64_t cap) {
+    int64_t b, e;
+    og_nbrs(g, v, l, &b, &e);
+    for (int64_t j = b; j < e && j - b < cap; j++) out[j - b] = (int32_t)(uint32_t)g->adj[j];
+    return e - b;
+}
+
+/* ------------------------------------------------------------- fingerprint ------- */
+/* SURVEY.md §8(c) 'Set fingerprint': FP(R) = (|R|, sum_rows h1(row) mod 2^64,
+ * xor_rows h2(row)), rows in query-id order.  h(row, seed): h = seed; for each column
+ * c: h = splitmix64_finalizer(h ^ (uint32)row[c]).  Commutative, hence order-free.    */
+#define OG_FP_SEED1 0x243F6A8885A308D3ull
+#define OG_FP_SEED2 0x13198A2E03707344ull
+static uint64_t og_mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+static uint64_t og_rowhash(const int32_t *row, int32_t k, uint64_t seed) {
+    uint64_t h = seed;
+    for (int32_t c = 0; c < k; c++) h = og_mix64(h ^ (uint64_t)(uint32_t)row[c]);
+    return h;
+}
+void og_fingerprint_rows(const int32_t *rows, int64_t nrows, int32_t k, uint64_t fp[3]) {
+    fp[0] = (uint64_t)nrows; fp[1] = 0; fp[2] = 0;
+    for (int64_t i = 0; i < nrows; i++) {
+        fp[1] += og_rowhash(rows + i * k, k, OG_FP_SEED1);
+        fp[2] ^= og_rowhash(rows + i * k, k, OG_FP_SEED2);
+    }
+}
+
+/* --------------------------------------------------------------- backtracker ----- */
+typedef struct {
+    int32_t k;
+    int32_t order[OG_MAXK];          /* order[j] = query vertex at depth j                */
+    int32_t depth_of[OG_MAXK];
+    int32_t qlabel[OG_MAXK];
+    int32_t parent[OG_MAXK];         /* depth of the earliest-ordered mapped neighbour    */
+    int32_t plabel[OG_MAXK];         /* label of the (parent, u) edge used to enumerate   */
+    int32_t nchk[OG_MAXK];           /* other edges to mapped vertices: (depth, label)    */
+    int32_t chk_depth[OG_MAXK][2 * OG_MAXK * 4];
+    int32_t chk_label[OG_MAXK][2 * OG_MAXK * 4];
+    int32_t hom;
+} og_plan;
+
+/* err: -1 bad arg, -6 disconnected, -7 too large */
+static int og_make_plan(int32_t k, const int32_t *qvl, int32_t qm, const int32_t *qs,
+                        const int32_t *qd, const int32_t *qe, int32_t root, int32_t hom, og_plan *p) {
+    if (k < 1) return -1;
+    if (k > OG_MAXK) return -7;
+    if (qm > 4 * OG_MAXK * OG_MAXK) return -7;
+    if (root < 0 || root >= k) return -1;
+    memset(p, 0, sizeof(*p));
+    p->k = k; p->hom = hom;
+    for (int32_t e = 0; e < qm; e++) {
+        if (qs[e] < 0 || qs[e] >= k || qd[e] < 0 || qd[e] >= k || qs[e] == qd[e] || qe[e] < 0) return -1;
+    }
+    /* BFS order from root, neighbours visited in increasing id (ties to the smallest id). */
+    int32_t seen[OG_MAXK] = {0}, head = 0, tail = 0;
+    p->order[tail++] = root; seen[root] = 1;
+    while (head < tail) {
+        int32_t u = p->order[head++];
+        for (int32_t w = 0; w < k; w++) {
+            if (seen[w]) continue;
+            for (int32_t e = 0; e < qm; e++)
+                if ((qs[e] == u && qd[e] == w) || (qd[e] == u && qs[e] == w)) { seen[w] = 1; p->order[tail++] = w; break; }
+        }
+    }
+    if (tail != k) return -6;
+    for (int32_t j = 0; j < k; j++) { p->depth_of[p->order[j]] = j; p->qlabel[j] = qvl[p->order[j]]; }
+    for (int32_t j = 0; j < k; j++) {
+        int32_t u = p->order[j];
+        p->parent[j] = -1; p->plabel[j] = -1; p->nchk[j] = 0;
+        /* parent: earliest-ordered neighbour at a smaller depth; its smallest-label edge */
+        for (int32_t e = 0; e < qm; e++) {
+            int32_t o = qs[e] == u ? qd[e] : (qd[e] == u ? qs[e] : -1);
+            if (o < 0) continue;
+            int32_t d = p->depth_of[o];
+            if (d >= j) continue;
+            if (p->parent[j] < 0 || d < p->parent[j] || (d == p->parent[j] && qe[e] < p->plabel[j])) {
+                p->parent[j] = d; p->plabel[j] = qe[e];
+            }
+        }
+        for (int32_t e = 0; e < qm; e++) {
+            int32_t o = qs[e] == u ? qd[e] : (qd[e] == u ? qs[e] : -1);
+            if (o < 0) continue;
+            int32_t d = p->depth_of[o];
+            if (d >= j) continue;
+            if (d == p->parent[j] && qe[e] == p->plabel[j]) continue;   /* the enumerated edge */
+            if (p->nchk[j] >= 2 * OG_MAXK * 4) return -7;
+            p->chk_depth[j][p->nchk[j]] = d;
+            p->chk_label[j][p->nchk[j]] = qe[e];
+            p->nchk[j]++;
+        }
+    }
+    return 0;
+}
+
+typedef struct {
+    int64_t count;
+    uint64_t fp1, fp2;
+    int32_t *rows; int64_t nrows, cap;   /* collected rows, query-id order */
+    int64_t steps;
+    int timed_out;
+} og_acc;
+
+static void og_emit(og_acc *a, const og_plan *p, const int32_t *f) {
+    int32_t row[OG_MAXK];
+    for (int32_t j = 0; j < p->k; j++) row[p->order[j]] = f[j];
+    a->count++;
+    a->fp1 += og_rowhash(row, p->k, OG_FP_SEED1);
+    a->fp2 ^= og_rowhash(row, p->k, OG_FP_SEED2);
+    if (a->cap > 0) {
+        if (a->nrows == a->cap) {
+            int64_t nc = a->cap * 2;
+            a->rows = (int32_t *)realloc(a->rows, sizeof(int32_t) * nc * p->k);
+            a->cap = nc;
+        }
+        memcpy(a->rows + a->nrows * p->k, row, sizeof(int32_t) * p->k);
+        a->nrows++;
+    }
+}
+
+static double og_now(void) {
+#ifdef _OPENMP
+    return omp_get_wtime();
+#else
+    return 0.0;
+#endif
+}
+
+/* Depth-first extension of a partial map f[0..1) rooted at data vertex v0. */
+static void og_search_root(const og_graph *g, const og_plan *p, int32_t v0, og_acc *a, double deadline) {
+    int32_t f[OG_MAXK];
+    int64_t cur[OG_MAXK], end[OG_MAXK];
+    int32_t k = p->k;
+    if (g->vl[v0] != p->qlabel[0]) return;
+    f[0] = v0;
+    if (k == 1) { og_emit(a, p, f); return; }
+    int32_t j = 1;
+    og_nbrs(g, f[p->parent[1]], p->plabel[1], &cur[1], &end[1]);
+    while (j >= 1) {
+        if (cur[j] >= end[j]) { j--; continue; }
+        int32_t x = (int32_t)(uint32_t)g->adj[cur[j]++];
+        if (((++a->steps) & 0xFFFF) == 0 && deadline > 0 && og_now() > deadline) { a->timed_out = 1; return; }
+        if (g->vl[x] != p->qlabel[j]) continue;
+        int ok = 1;
+        if (!p->hom)
+            for (int32_t i = 0; i < j && ok; i++) if (f[i] == x) ok = 0;
+        for (int32_t c = 0; c < p->nchk[j] && ok; c++)
+            if (!og_has_edge(g, x, f[p->chk_depth[j][c]], p->chk_label[j][c])) ok = 0;
+        if (!ok) continue;
+        f[j] = x;
+        if (j == k - 1) { og_emit(a, p, f); continue; }
+        j++;
+        og_nbrs(g, f[p->parent[j]], p->plabel[j], &cur[j], &end[j]);
+    }
+}
+
+static int cmp_rows_k;
+static int cmp_rows(const void *a, const void *b) {
+    const int32_t *x = (const int32_t *)a, *y = (const int32_t *)b;
+    for (int c = 0; c < cmp_rows_k; c++) { if (x[c] != y[c]) return x[c] < y[c] ? -1 : 1; }
+    return 0;
+}
+
+/*
+ * og_match: enumerate R(Q,G).
+ *   root       query vertex the BFS order starts from (default 0).
+ *   roots      optional subset S of data vertices: only maps with f(root) in S (root-restricted
+ *              parity); NULL = all vertices.
+ *   table/cap  if table != NULL, up to cap rows (k int32 each, query-id order, sorted
+ *              lexicographically) are written.
+ *   fp         out: (count, sum-hash, xor-hash).
+ *   timeout_s  <= 0: none.  On timeout returns -9 and fp holds the partial result.
+ * Returns the count (>= 0) or a negative error code.
+ */
+int64_t og_match(const og_graph *g, int32_t k, const int32_t *qvl, int32_t qm, const int32_t *qs,
+                 const int32_t *qd, const int32_t *qe, int32_t root, const int32_t *roots,
+                 int64_t nroots, int32_t nthreads, int32_t hom, int32_t *table, int64_t cap,
+                 uint64_t fp[3], double timeout_s) {
+    og_plan p;
+    int rc = og_make_plan(k, qvl, qm, qs, qd, qe, root, hom, &p);
+    if (rc) return rc;
+    int64_t ncand = roots ? nroots : g->n;
+    int want_rows = table != NULL;
+    double deadline = timeout_s > 0 ? og_now() + timeout_s : 0;
+    int64_t total = 0; uint64_t s1 = 0, s2 = 0; int timed_out = 0;
+    int32_t *all = NULL; int64_t nall = 0;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#endif
+    #pragma omp parallel
+    {
+        og_acc a; memset(&a, 0, sizeof(a));
+        if (want_rows) { a.cap = 64; a.rows = (int32_t *)malloc(sizeof(int32_t) * 64 * k); }
+        #pragma omp for schedule(dynamic, 16) nowait
+        for (int64_t i = 0; i < ncand; i++) {
+            if (a.timed_out) continue;
+            int32_t v0 = roots ? roots[i] : (int32_t)i;
+            if (v0 < 0 || v0 >= g->n) continue;
+            og_search_root(g, &p, v0, &a, deadline);
+        }
+        #pragma omp critical
+        {
+            total += a.count; s1 += a.fp1; s2 ^= a.fp2; timed_out |= a.timed_out;
+            if (want_rows && a.nrows) {
+                all = (int32_t *)realloc(all, sizeof(int32_t) * (nall + a.nrows) * k);
+                memcpy(all + nall * k, a.rows, sizeof(int32_t) * a.nrows * k);
+                nall += a.nrows;
+            }
+        }
+        free(a.rows);
+    }
+    if (want_rows) {
+        cmp_rows_k = k;
+        qsort(all, (size_t)nall, sizeof(int32_t) * k, cmp_rows);
+        int64_t w = nall < cap ? nall : cap;
+        if (w > 0) memcpy(table, all, sizeof(int32_t) * w * k);
+        free(all);
+    }
+    fp[0] = (uint64_t)total; fp[1] = s1; fp[2] = s2;
+    return timed_out ? -9 : total;
+}
+
+/* ------------------------------------------------------- signature specification -- */
+/* MurmurHash64A (Appleby, MurmurHash2 64-bit) over the 8 little-endian bytes of key.   */
+static uint64_t og_murmur64a_u64(uint64_t key, uint64_t seed) {
+    const uint64_t m = 0xc6a4a7935bd1e995ull;
+    const int r = 47;
+    uint64_t h = seed ^ (8ull * m);
+    uint64_t k = key;
+    k *= m; k ^= k >> r; k *= m;
+    h ^= k; h *= m;
+    h ^= h >> r; h *= m; h ^= h >> r;
+    return h;
+}
+
+#define OG_SIG_SEED 0x9747B28Cull
+#define OG_SIG_GROUPS 240          /* (N-K)/2 with N = 512, K = 32      */
+#define OG_SIG_PLANES 16           /* 512 bits = 16 x 32-bit words                      */
+
+static int og_sig_group(int32_t elabel, int32_t nlabel) {
+    uint64_t key = ((uint64_t)(uint32_t)elabel << 32) | (uint32_t)nlabel;   /* reading A6 */
+    return (int)(og_murmur64a_u64(key, OG_SIG_SEED) % OG_SIG_GROUPS);
+}
+
+/* Encode one signature from a list of (edge label, neighbour label) pairs, counted with
+ * multiplicity (reading A5): group state 00 / 01 / 11 for 0 / 1 / >=2 pairs. */
+static void og_encode(int32_t vlabel, int64_t npairs, const int32_t *pe, const int32_t *pn, uint32_t sig[OG_SIG_PLANES]) {
+    int cnt[OG_SIG_GROUPS];
+    memset(cnt, 0, sizeof(cnt));
+    for (int64_t i = 0; i < npairs; i++) cnt[og_sig_group(pe[i], pn[i])]++;
+    sig[0] = (uint32_t)vlabel;                                   /* stored directly, L1277 */
+    for (int w = 1; w < OG_SIG_PLANES; w++) sig[w] = 0;
+    for (int grp = 0; grp < OG_SIG_GROUPS; grp++) {
+        uint32_t s = cnt[grp] == 0 ? 0u : (cnt[grp] == 1 ? 1u : 3u);
+        sig[1 + grp / 16] |= s << (2 * (grp % 16));
+    }
+}
+
+/* Data signature table, column-first: planes[w * n + v]. */
+void og_signatures(const og_graph *g, uint32_t *planes) {
+    int64_t n = g->n;
+    #pragma omp parallel
+    {
+        int32_t *pe = NULL, *pn = NULL; int64_t cap = 0;
+        #pragma omp for schedule(dynamic, 1024)
+        for (int64_t v = 0; v < n; v++) {
+            int64_t d = g->off[v + 1] - g->off[v];
+            if (d > cap) { cap = d; pe = (int32_t *)realloc(pe, sizeof(int32_t) * cap); pn = (int32_t *)realloc(pn, sizeof(int32_t) * cap); }
+            for (int64_t j = 0; j < d; j++) {
+                uint64_t x = (uint64_t)g->adj[g->off[v] + j];
+                pe[j] = (int32_t)(x >> 32);
+                pn[j] = g->vl[(uint32_t)x];
+            }
+            uint32_t sig[OG_SIG_PLANES];
+            og_encode(g->vl[v], d, pe, pn, sig);
+            for (int w = 0; w < OG_SIG_PLANES; w++) planes[(int64_t)w * n + v] = sig[w];
+        }
+        free(pe); free(pn);
+    }
+}
+
+/* Query signatures: qsig[u * 16 + w] over the query edges incident to u. */
+void og_query_signatures(int32_t k, const int32_t *qvl, int32_t qm, const int32_t *qs, const int32_t *qd,
+                         const int32_t *qe, uint32_t *qsig) {
+    int32_t pe[4 * OG_MAXK * OG_MAXK], pn[4 * OG_MAXK * OG_MAXK];
+    for (int32_t u = 0; u < k; u++) {
+        int64_t c = 0;
+        for (int32_t e = 0; e < qm; e++) {
+            if (qs[e] == u) { pe[c] = qe[e]; pn[c] = qvl[qd[e]]; c++; }
+            else if (qd[e] == u) { pe[c] = qe[e]; pn[c] = qvl[qs[e]]; c++; }
+        }
+        og_encode(qvl[u], c, pe, pn, qsig + (int64_t)u * OG_SIG_PLANES);
+    }
+}
+
+/* C(u) = { v : plane0(v) == plane0(u) and plane_w(v) & plane_w(u) == plane_w(u), w=1..15 }
+ * (PAPER.md L543 with reading A4).  bitmaps[u * ceil(n/32) + v/32] bit v%32.            */
+void og_filter(const og_graph *g, const uint32_t *planes, int32_t k, const uint32_t *qsig,
+               uint32_t *bitmaps, int64_t *counts) {
+    int64_t n = g->n, words = (n + 31) / 32;
+    memset(bitmaps, 0, sizeof(uint32_t) * words * k);
+    for (int32_t u = 0; u < k; u++) {
+        const uint32_t *s = qsig + (int64_t)u * OG_SIG_PLANES;
+        int64_t c = 0;
+        for (int64_t v = 0; v < n; v++) {
+            int ok = planes[v] == s[0];
+            for (int w = 1; w < OG_SIG_PLANES && ok; w++)
+                if ((planes[(int64_t)w * n + v] & s[w]) != s[w]) ok = 0;
+            if (ok) { bitmaps[(int64_t)u * words + v / 32] |= 1u << (v % 32); c++; }
+        }
+        counts[u] = c;
+    }
+}
+
+int32_t og_sig_group_of(int32_t elabel, int32_t nlabel) { return og_sig_group(elabel, nlabel); }
+
+int32_t og_max_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
