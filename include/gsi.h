@@ -1,0 +1,226 @@
+/*
+ * gsi.h — C ABI of the B200-native GSI subgraph-matching library (libgsi_b200.so).
+ *
+ * Problem (Def. 1-3; N(v,l) at L299): given a labelled undirected data
+ * graph G and a connected labelled query graph Q, enumerate every injective map
+ * f : V(Q) -> V(G) with L_V(f(u)) = L_V(u) and, for every query edge (a,b,l), a data
+ * edge {f(a), f(b)} labelled l (non-induced, SURVEY.md §8(c) readings A1/A2).
+ *
+ * Hot path: PCSR build (Def. 4, Alg. 1), signature
+ * table + filter (§III-A), join-order planner (Alg. 2, Alg. 4 line 1
+ * L1119), and the per-level Prealloc-Combine vertex join (Alg. 3, Alg. 4
+ * L1113-1129).  Every device step runs in this library's own sm_100a kernels.
+ *
+ * Conventions
+ *  - Ownership: every `const T*` input is a HOST pointer borrowed for the duration of the
+ *    call and copied; the library never keeps it.  Handles (`gsi_graph*`, `gsi_result*`,
+ *    `gsi_prepared*`) are owned by the caller and released with the matching *_free.
+ *  - Errors: every entry point returns a gsi_status; on error no partial result is
+ *    returned (out handles are set to NULL) and gsi_last_error() gives a thread-local
+ *    message.  The library never aborts the process and never falls back to the CPU:
+ *    with no usable CUDA device every compute call returns GSI_ERR_CUDA.
+ *  - Concurrency: a built graph is immutable and may serve concurrent queries from
+ *    different host threads on different streams.
+ *  - Streams: `stream` fields take a cudaStream_t (NULL = the per-thread default stream).
+ *    Calls return after the work they enqueue has completed (counts are host values).
+ *  - Limits: |V| < 2^31, 2|E| < 2^32, query k <= 32 vertices, labels are int32 >= 0.
+ */
+#ifndef GSI_H
+#define GSI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GSI_MAX_K 32
+#define GSI_SIG_PLANES 16        /* N = 512 bits = 16 uint32 words, K = 32 */
+#define GSI_N_KCLASS 8           /* kernel classes timed when gsi_query_opts.profile = 1   */
+
+typedef enum {
+    GSI_OK = 0,
+    GSI_ERR_INVALID_ARG = -1,
+    GSI_ERR_VERTEX_RANGE = -2,
+    GSI_ERR_LABEL_RANGE = -3,
+    GSI_ERR_SELF_LOOP = -4,
+    GSI_ERR_DUPLICATE_EDGE = -5,
+    GSI_ERR_QUERY_DISCONNECTED = -6,
+    GSI_ERR_QUERY_TOO_LARGE = -7,
+    GSI_ERR_OOM = -8,
+    GSI_ERR_TIMEOUT = -9,
+    GSI_ERR_CUDA = -10,
+    GSI_ERR_INTERNAL = -11
+} gsi_status;
+
+/* Kernel classes reported in gsi_stats (profile mode). */
+enum { GSI_K_FILTER = 0, GSI_K_COMPACT = 1, GSI_K_PROBE = 2, GSI_K_JOIN = 3, GSI_K_LINK = 4,
+       GSI_K_OTHER = 5 };
+
+typedef struct gsi_graph gsi_graph;       /* opaque: PCSR + signature table on one device   */
+typedef struct gsi_result gsi_result;     /* opaque: count, fingerprint, optional table     */
+typedef struct gsi_prepared gsi_prepared; /* opaque: a validated, encoded, device-resident Q */
+
+/* ------------------------------------------------------------------ graph build ----- */
+typedef struct {
+    int32_t gpn;      /* PCSR pairs per group, 2..16; default 16 = one 128 B group */
+    int32_t device;   /* CUDA device ordinal; -1 = current device                               */
+    void *stream;     /* cudaStream_t used for the build                                         */
+} gsi_build_opts;
+
+void gsi_build_opts_default(gsi_build_opts *opts);
+
+/*
+ * gsi_build_graph — PCSR (Def. 4, Alg. 1) for every edge label plus the column-first
+ * signature table, built on the device.
+ *   n        number of vertices; vertex ids are 0..n-1.
+ *   vlabels  n int32 vertex labels (>= 0).
+ *   m        number of undirected edges; each listed ONCE as (src[i], dst[i], elabels[i]).
+ *   Parallel edges with DISTINCT labels are accepted (SURVEY.md reading A3); an exact
+ *   duplicate (v,w,l) in either orientation -> GSI_ERR_DUPLICATE_EDGE; src == dst ->
+ *   GSI_ERR_SELF_LOOP; ids outside [0,n) -> GSI_ERR_VERTEX_RANGE; negative labels ->
+ *   GSI_ERR_LABEL_RANGE.  Edge labels are remapped densely inside the build.
+ *   out      receives the graph handle (NULL on error).
+ */
+gsi_status gsi_build_graph(int64_t n, const int32_t *vlabels, int64_t m, const int32_t *src,
+                           const int32_t *dst, const int32_t *elabels, const gsi_build_opts *opts,
+                           gsi_graph **out);
+
+typedef struct {
+    int64_t n, m;                 /* |V|, |E| (undirected)                                  */
+    int32_t n_elabels;            /* distinct edge labels |L_E|                             */
+    int32_t gpn;
+    int64_t n_groups;             /* sum_l |V(D_l)| (one group allocated per partition vertex) */
+    int32_t max_chain;            /* longest overflow chain in groups  */
+    int64_t overflow_groups;      /* groups whose keys spilled (Alg. 1 lines 5-8)           */
+    uint64_t bytes_groups, bytes_ci, bytes_sig, bytes_total;
+    int32_t device;
+    float ms_build;
+} gsi_graph_info;
+
+gsi_status gsi_graph_info_get(const gsi_graph *g, gsi_graph_info *info);
+
+/* Device buffers of a graph, for replicating it to other GPUs (NCCL broadcast). */
+typedef struct {
+    const char *name;   /* static string                                                  */
+    void *dev_ptr;      /* device pointer owned by the graph                              */
+    uint64_t bytes;
+} gsi_buffer_desc;
+
+#define GSI_MAX_BUFFERS 8
+/* Fill descs[0..*ndesc) (capacity GSI_MAX_BUFFERS) and a host metadata blob (graph
+ * scalars + per-label host tables) of *meta_bytes bytes (meta may be NULL to query size). */
+gsi_status gsi_graph_buffers(const gsi_graph *g, gsi_buffer_desc *descs, int32_t *ndesc,
+                             void *meta, uint64_t *meta_bytes);
+/* Allocate an empty graph on `opts->device` with the buffer sizes / metadata produced by
+ * gsi_graph_buffers on another rank; its descs (same order) can then be filled by a
+ * broadcast.  The graph is usable once every buffer holds the source's bytes. */
+gsi_status gsi_graph_alloc_like(const void *meta, uint64_t meta_bytes, const gsi_build_opts *opts,
+                                gsi_graph **out, gsi_buffer_desc *descs, int32_t *ndesc);
+
+void gsi_graph_free(gsi_graph *g);
+
+/* ------------------------------------------------------------------ query ----------- */
+typedef struct {
+    int32_t want_table;          /* 1: materialise the match table (device, query-id order)  */
+    int32_t homomorphism;        /* 1: drop the injectivity subtraction */
+    int32_t filter_mode;         /* 0: signature filter (L534-552); 1: label-only C(u)        */
+    int32_t e0_mode;             /* 0: per row, the shortest linking list bounds the buffer
+                                    (B200 default; any linking edge bounds it, L967-981);
+                                    1: the paper's min-freq linking label (Alg. 4 line 1)     */
+    const int32_t *force_order;  /* test hook: k query ids (connected prefixes) or NULL        */
+    const int32_t *force_first_edge; /* test hook: [k] per step j the query vertex at the
+                                    other end of e0 (entry 0 ignored, -1 = planner's), or NULL */
+    const int32_t *roots;        /* test hook: restrict f(pi_1) to these data vertices, or NULL */
+    int64_t n_roots;
+    int32_t shard_rank, shard_count; /* M-row sharding; 0/1 = whole query   */
+    uint64_t shard_min_rows;     /* shard at the first level with |M_t| >= this (0 = 65536)    */
+    uint64_t mem_budget_bytes;   /* device bytes the query may use (0 = 90% of free memory)    */
+    double timeout_s;            /* <= 0: none.  Checked between levels.                        */
+    int32_t profile;             /* 1: time every kernel with CUDA events (gsi_stats)          */
+    void *stream;                /* cudaStream_t                                               */
+} gsi_query_opts;
+
+void gsi_query_opts_default(gsi_query_opts *opts);
+
+/*
+ * gsi_query — filter, plan and join Q against g (the whole hot path, §8(a) a3-a9).
+ *   k                 number of query vertices (1..32), ids 0..k-1.
+ *   q_vlabels         k int32.
+ *   qm, q_src, q_dst, q_elabels   query edges, each listed once.
+ * A disconnected Q -> GSI_ERR_QUERY_DISCONNECTED (PAPER.md L299 assumes connectivity);
+ * k > 32 -> GSI_ERR_QUERY_TOO_LARGE; labels absent from G give count 0.
+ */
+gsi_status gsi_query(const gsi_graph *g, int32_t k, const int32_t *q_vlabels, int32_t qm,
+                     const int32_t *q_src, const int32_t *q_dst, const int32_t *q_elabels,
+                     const gsi_query_opts *opts, gsi_result **out);
+
+/* Split of gsi_query: validate + encode Q once (host -> device), then run it.  A prepared
+ * query is bound to its graph and may be run any number of times. */
+gsi_status gsi_query_prepare(const gsi_graph *g, int32_t k, const int32_t *q_vlabels, int32_t qm,
+                             const int32_t *q_src, const int32_t *q_dst, const int32_t *q_elabels,
+                             gsi_prepared **out);
+gsi_status gsi_query_run(const gsi_graph *g, const gsi_prepared *q, const gsi_query_opts *opts,
+                         gsi_result **out);
+void gsi_prepared_free(gsi_prepared *q);
+
+typedef struct {
+    int32_t k, levels;                /* levels = number of join levels executed            */
+    int32_t order[GSI_MAX_K];         /* join order pi (query ids)                          */
+    int64_t cand[GSI_MAX_K];          /* |C(u)| by query id                                 */
+    uint64_t rows[GSI_MAX_K];         /* |M_t| for t = 1..k at index t-1 (this shard)        */
+    uint64_t gba[GSI_MAX_K];          /* |GBA| (prealloc bound F[|M|]) producing M_{t+1}, idx t */
+    uint64_t list_elems[GSI_MAX_K];   /* sum over rows and linking edges of |N(v,l)|, idx t */
+    int32_t n_edges[GSI_MAX_K];       /* |ES| per step (idx t = step producing M_{t+1})     */
+    int32_t first_edge[GSI_MAX_K];    /* planner's e0 other-end query id per step           */
+    uint64_t count;
+    int32_t shard_level;              /* level whose rows were sharded (-1: not sharded)    */
+    uint64_t shard_row_begin, shard_row_end;
+    float ms_total, ms_filter, ms_plan, ms_join;
+    /* profile mode: per kernel class (GSI_K_*) summed device ms, launches, algorithmic bytes */
+    float ms_kernel[GSI_N_KCLASS];
+    uint32_t launches[GSI_N_KCLASS];
+    double alg_bytes[GSI_N_KCLASS];
+    uint32_t total_launches;          /* kernels this library launched for the query         */
+} gsi_stats;
+
+gsi_status gsi_result_count(const gsi_result *r, uint64_t *count);
+/* Order-independent set fingerprint (|R|, sum h1(row), xor h2(row)) over the final rows in
+ * query-id order; computed on the device even in count-only mode. */
+gsi_status gsi_result_fingerprint(const gsi_result *r, uint64_t fp[3]);
+/* Device pointer to the table (nrows x k int32, query-id order), valid until free; rows
+ * are strictly increasing in join-order (pi) column order. Requires want_table. */
+gsi_status gsi_result_table(const gsi_result *r, const int32_t **dev_rows, uint64_t *nrows);
+/* Copy the table to host memory (cap rows of k int32). */
+gsi_status gsi_result_copy_table(const gsi_result *r, int32_t *host_rows, uint64_t cap);
+gsi_status gsi_result_stats(const gsi_result *r, gsi_stats *stats);
+void gsi_result_free(gsi_result *r);
+
+/* ------------------------------------------------------------------ test hooks ------ */
+/* Batch PCSR lookups through the join kernels' device lookup: for each (v[i], l[i]) (raw
+ * edge label) writes len[i] = |N(v,l)| and groups_read[i] (chain length walked); the
+ * neighbour runs are concatenated into nbrs (capacity cap) in query order. */
+gsi_status gsi_debug_lookup(const gsi_graph *g, int64_t nq, const int32_t *v, const int32_t *l,
+                            int64_t *len, int32_t *groups_read, int32_t *nbrs, int64_t cap);
+/* Copy the column-first signature table (16 x n uint32) to host. */
+gsi_status gsi_debug_signatures(const gsi_graph *g, uint32_t *planes);
+/* Run only the filter kernel: bitmaps (k x ceil(n/32) uint32) and |C(u)| to host. */
+gsi_status gsi_debug_filter(const gsi_graph *g, int32_t k, const int32_t *q_vlabels, int32_t qm,
+                            const int32_t *q_src, const int32_t *q_dst, const int32_t *q_elabels,
+                            int32_t filter_mode, uint32_t *bitmaps, int64_t *counts);
+/* Host query signatures (k x 16 uint32) as encoded by the library. */
+gsi_status gsi_debug_query_signatures(int32_t k, const int32_t *q_vlabels, int32_t qm,
+                                      const int32_t *q_src, const int32_t *q_dst,
+                                      const int32_t *q_elabels, uint32_t *qsig);
+
+/* ------------------------------------------------------------------ misc ------------ */
+const char *gsi_last_error(void);
+const char *gsi_version(void);
+/* Number of CUDA devices visible (0 when none); never fails. */
+int32_t gsi_device_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSI_H */

@@ -1,0 +1,1196 @@
+// query.cu — the GSI query hot path on sm_100a: signature filter (§III-A
+// L534-552), join-order planner (Alg. 2), and the per-level Prealloc-Combine vertex
+// join (Alg. 3, Alg. 4) re-designed for B200:
+//
+//   k_filter        one streaming pass over the column-first signature table tests all k
+//                   query signatures; ballot writes C(u) bitmap words, popc gives |C(u)|.
+//   k_compact_*     level 1: M_1 = C(pi_1) in ascending order (Alg. 2 line 7).
+//   k_probe         Prealloc (Alg. 4): one thread per row of M locates N(m_i[c_e], l_e) for
+//                   every linking edge in PCSR (one 128 B group probe each, L740-753), caches
+//                   (off,len), picks the buffer-bounding edge e0 and scans |N(v',l0)| into F
+//                   with a single-pass decoupled look-back (the paper's CUB exclusive scan).
+//   k_join          the hot kernel.  The Prealloc range [0, F[|M|]) is the GBA index space;
+//                   it is cut into equal tiles of 2048 slots (exact work partition — the B200
+//                   form of the 4-layer load balance of L1169-1176: a hub row's buffer is split
+//                   across as many CTAs as its length needs, a tiny row shares a CTA).  Slot s
+//                   of row i tests x = N(v',l0)[s-F_i]: C(u) bitmap bit (L2-resident bitset,
+//                   L1150), set subtraction against the row (Alg. 3 line 10) and membership in
+//                   every other linking list (binary search in the sorted run; all edges in one
+//                   pass instead of one launch per edge, Alg. 3 line 4).  Survivors are compacted
+//                   in slot order through shared memory (the write cache, L1155-1158) and their
+//                   global position comes from the same decoupled look-back — the Combine scan of
+//                   Alg. 3 line 14 fused into the join; nothing is joined twice.
+//   k_link          Combine (Alg. 3 lines 15-21): M'[r] = M[R[r]] || S[r], one thread per output
+//                   int (fully coalesced stores).  The last level is count-only unless the table
+//                   is wanted, and writes the final table in query-id order.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "common.cuh"
+
+namespace gsi {
+
+// ====================================================================== device side ===
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kJoinItems = 8;
+constexpr int kJoinTile = kThreads * kJoinItems;   // 2048 GBA slots per CTA
+constexpr int kSmemF = 2048 + 1;                   // staged F entries per join tile
+
+struct StepParams {
+    int t;                       // columns of M (current level)
+    int E;                       // linking edges
+    int per_row_e0;              // 1: per-row shortest list bounds the buffer
+    int k;                       // query size (final level only)
+    int col[GSI_MAX_K];          // column of linking edge e
+    uint32_t lab[GSI_MAX_K];     // dense label of linking edge e
+    unsigned long long gbase[GSI_MAX_K];
+    uint32_t ngroups[GSI_MAX_K];
+    int n_inj;
+    int inj_col[GSI_MAX_K];      // columns the subtraction must test (same vertex label as u)
+    int pos_of_q[GSI_MAX_K];     // final level: column (0..t) holding query vertex q
+};
+
+// Counters shared by the kernels of one query (device).
+struct Counters {
+    unsigned long long list_elems;   // algorithmic list elements of active rows
+    unsigned long long active_rows;  // rows with a non-empty prealloc buffer
+    unsigned long long count;        // final count (count-only mode) / survivors
+    unsigned long long fp1, fp2;
+    unsigned long long plane_loads;  // filter: vertices whose planes 1..15 were read
+    unsigned long long total;        // scan totals written by the last tile
+    unsigned long long pad;
+};
+
+// ---------------------------------------------------------------------- filter ------
+__global__ void __launch_bounds__(kThreads) k_filter(const uint32_t *__restrict__ sig, long long n, int k,
+                                                     const uint32_t *__restrict__ qsig, int label_only,
+                                                     uint32_t *__restrict__ bitmaps, long long words,
+                                                     unsigned long long *__restrict__ counts,
+                                                     Counters *__restrict__ ctr) {
+    __shared__ uint32_t qs[GSI_MAX_K * kPlanes];
+    __shared__ unsigned long long cnt_s[GSI_MAX_K];
+    __shared__ unsigned long long loads_s;
+    for (int i = threadIdx.x; i < k * kPlanes; i += blockDim.x) qs[i] = qsig[i];
+    if (threadIdx.x < GSI_MAX_K) cnt_s[threadIdx.x] = 0;
+    if (threadIdx.x == 0) loads_s = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long w = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); w < words; w += warps) {
+        const long long v = w * 32 + lane;
+        const bool valid = v < n;
+        const uint32_t lab = valid ? __ldcs(sig + v) : 0u;
+        uint32_t mask = 0;
+        for (int u = 0; u < k; u++)
+            if (valid && lab == qs[u * kPlanes]) mask |= 1u << u;   // label field by equality (A4)
+        if (!label_only && mask) {
+            uint32_t p[kPlanes];
+#pragma unroll
+            for (int pl = 1; pl < kPlanes; pl++) p[pl] = __ldcs(sig + (long long)pl * n + v);
+            uint32_t mm = mask;
+            while (mm) {
+                int u = __ffs(mm) - 1;
+                mm &= mm - 1;
+                const uint32_t *s = qs + u * kPlanes;
+                bool ok = true;
+#pragma unroll
+                for (int pl = 1; pl < kPlanes; pl++) ok &= (p[pl] & s[pl]) == s[pl];   // S(v)&S(u)=S(u), L543
+                if (!ok) mask &= ~(1u << u);
+            }
+        }
+        unsigned loaded = __ballot_sync(0xffffffffu, !label_only && valid && lab != 0xFFFFFFFFu && mask != 0);
+        if (lane == 0 && loaded) atomicAdd(&loads_s, (unsigned long long)__popc(loaded));
+        for (int u = 0; u < k; u++) {
+            unsigned b = __ballot_sync(0xffffffffu, (mask >> u) & 1u);
+            if (lane == 0) {
+                bitmaps[(long long)u * words + w] = b;
+                if (b) atomicAdd(&cnt_s[u], (unsigned long long)__popc(b));
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < k && cnt_s[threadIdx.x]) atomicAdd(&counts[threadIdx.x], cnt_s[threadIdx.x]);
+    if (threadIdx.x == 0 && loads_s) atomicAdd(&ctr->plane_loads, loads_s);
+}
+
+// ------------------------------------------------------------ level-1 compaction ----
+// Tile = 256 bitmap words; M_1 ascending (Alg. 2 line 7: M = C(u_c)).
+__global__ void __launch_bounds__(kThreads) k_compact_bitmap(const uint32_t *__restrict__ bm, long long words,
+                                                             int32_t *__restrict__ out,
+                                                             unsigned long long *status, unsigned *tile_ctr,
+                                                             Counters *ctr) {
+    __shared__ unsigned long long sm[33];
+    __shared__ unsigned tile_s;
+    __shared__ unsigned long long base_s;
+    if (threadIdx.x == 0) tile_s = atomicAdd(tile_ctr, 1u);
+    __syncthreads();
+    const unsigned tile = tile_s;
+    const long long w = (long long)tile * kThreads + threadIdx.x;
+    const uint32_t word = w < words ? bm[w] : 0u;
+    unsigned long long agg;
+    unsigned long long ex = block_exclusive_scan((unsigned long long)__popc(word), sm, &agg);
+    if (threadIdx.x < 32) {
+        unsigned long long pre = lookback_exclusive(status, tile, agg);
+        if (threadIdx.x == 0) base_s = pre;
+    }
+    __syncthreads();
+    unsigned long long pos = base_s + ex;
+    uint32_t x = word;
+    while (x) {
+        int b = __ffs(x) - 1;
+        x &= x - 1;
+        out[pos++] = (int32_t)(w * 32 + b);
+    }
+    if (tile == gridDim.x - 1 && threadIdx.x == 0) ctr->total = base_s + agg;
+}
+
+// Roots restriction (test hook / root-restricted parity): keep sorted roots that are in C(pi_1).
+__global__ void __launch_bounds__(kThreads) k_compact_roots(const int32_t *__restrict__ roots, long long nroots,
+                                                            const uint32_t *__restrict__ bm,
+                                                            int32_t *__restrict__ out,
+                                                            unsigned long long *status, unsigned *tile_ctr,
+                                                            Counters *ctr) {
+    __shared__ unsigned long long sm[33];
+    __shared__ unsigned tile_s;
+    __shared__ unsigned long long base_s;
+    if (threadIdx.x == 0) tile_s = atomicAdd(tile_ctr, 1u);
+    __syncthreads();
+    const unsigned tile = tile_s;
+    const long long i = (long long)tile * kThreads + threadIdx.x;
+    int32_t v = i < nroots ? roots[i] : -1;
+    bool keep = v >= 0 && ((bm[v >> 5] >> (v & 31)) & 1u);
+    unsigned long long agg;
+    unsigned long long ex = block_exclusive_scan(keep ? 1ull : 0ull, sm, &agg);
+    if (threadIdx.x < 32) {
+        unsigned long long pre = lookback_exclusive(status, tile, agg);
+        if (threadIdx.x == 0) base_s = pre;
+    }
+    __syncthreads();
+    if (keep) out[base_s + ex] = v;
+    if (tile == gridDim.x - 1 && threadIdx.x == 0) ctr->total = base_s + agg;
+}
+
+// ---------------------------------------------------------------------- probe -------
+// Alg. 4: F[i] = sum_{i'<i} |N(v'_{i'}, l0)|, F[|M|] = |GBA|.  loc[i*E + e] caches every
+// linking list; in per-row mode entry 0 is the shortest list of the row (any linking
+// edge bounds buf_i, L967-981) and rows with an empty list get a zero-size buffer.
+__global__ void __launch_bounds__(kThreads) k_probe(const int32_t *__restrict__ M, long long nM, StepParams P,
+                                                    const uint2 *__restrict__ groups, int gpn,
+                                                    Loc *__restrict__ loc, unsigned long long *__restrict__ F,
+                                                    unsigned long long *status, unsigned *tile_ctr,
+                                                    Counters *ctr) {
+    __shared__ unsigned long long sm[33];
+    __shared__ unsigned tile_s;
+    __shared__ unsigned long long base_s;
+    if (threadIdx.x == 0) tile_s = atomicAdd(tile_ctr, 1u);
+    __syncthreads();
+    const unsigned tile = tile_s;
+    const long long i = (long long)tile * kThreads + threadIdx.x;
+    unsigned long long len0 = 0, elems = 0;
+    if (i < nM) {
+        const int32_t *row = M + i * P.t;
+        Loc first{0, 0}, best{0, 0};
+        int bi = 0;
+        bool anyzero = false;
+        unsigned long long sum = 0;
+        Loc *L = loc + i * P.E;
+        for (int e = 0; e < P.E; e++) {
+            uint32_t v = (uint32_t)__ldg(row + P.col[e]);
+            Loc r = pcsr_lookup(groups, gpn, P.gbase[e], P.ngroups[e], P.lab[e], v, nullptr);
+            L[e] = r;
+            if (e == 0) { first = r; best = r; }
+            else if (r.len < best.len) { best = r; bi = e; }
+            anyzero |= r.len == 0;
+            sum += r.len;
+        }
+        if (P.per_row_e0) {
+            if (bi != 0) {
+                L[0] = best;
+                L[bi] = first;
+            }
+            len0 = anyzero ? 0ull : best.len;
+            elems = anyzero ? 0ull : sum;
+        } else {
+            len0 = first.len;
+            elems = sum;
+        }
+    }
+    unsigned long long agg;
+    unsigned long long ex = block_exclusive_scan(len0, sm, &agg);
+    if (threadIdx.x < 32) {
+        unsigned long long pre = lookback_exclusive(status, tile, agg);
+        if (threadIdx.x == 0) base_s = pre;
+    }
+    __syncthreads();
+    if (i < nM) F[i] = base_s + ex;
+    if (tile == gridDim.x - 1 && threadIdx.x == kThreads - 1) F[nM] = base_s + agg;
+    // algorithmic accounting
+    unsigned long long e1 = warp_sum_u64(elems), a1 = warp_sum_u64(len0 ? 1ull : 0ull);
+    if ((threadIdx.x & 31) == 0) {
+        if (e1) atomicAdd(&ctr->list_elems, e1);
+        if (a1) atomicAdd(&ctr->active_rows, a1);
+    }
+}
+
+// ---------------------------------------------------------------------- join --------
+__device__ __forceinline__ long long upper_row(const unsigned long long *__restrict__ F, long long lo, long long hi,
+                                               unsigned long long s) {
+    // largest i in [lo, hi) with F[i] <= s  (F non-decreasing, F[lo] <= s)
+    while (hi - lo > 1) {
+        long long mid = (lo + hi) >> 1;
+        if (__ldg(F + mid) <= s) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ bool in_sorted(const int32_t *__restrict__ a, uint32_t n, int32_t x) {
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        uint32_t mid = (lo + hi) >> 1;
+        int32_t y = __ldg(a + mid);
+        if (y < x) lo = mid + 1; else hi = mid;
+    }
+    return lo < n && __ldg(a + lo) == x;
+}
+
+template <bool WRITE, bool FINAL>
+__global__ void __launch_bounds__(kThreads) k_join(const int32_t *__restrict__ M, long long nM,
+                                                   const unsigned long long *__restrict__ F,
+                                                   const Loc *__restrict__ loc, StepParams P,
+                                                   const int32_t *__restrict__ ci,
+                                                   const uint32_t *__restrict__ cu_bitmap,
+                                                   unsigned long long s0, unsigned long long s1,
+                                                   uint32_t *__restrict__ S, uint32_t *__restrict__ R,
+                                                   unsigned long long *status, unsigned *tile_ctr,
+                                                   Counters *ctr) {
+    __shared__ unsigned long long sF[kSmemF];
+    __shared__ unsigned wcnt[kJoinItems][kThreads / 32];
+    __shared__ unsigned wbase[kJoinItems][kThreads / 32];
+    __shared__ unsigned tile_s, agg_s;
+    __shared__ long long rlo_s, rhi_s;
+    __shared__ unsigned long long base_s;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) tile_s = atomicAdd(tile_ctr, 1u);
+    __syncthreads();
+    const unsigned tile = tile_s;
+    const unsigned long long tbase = s0 + (unsigned long long)tile * kJoinTile;
+    const unsigned long long tend = min(tbase + (unsigned long long)kJoinTile, s1);
+    if (tid == 0) rlo_s = upper_row(F, 0, nM + 1, tbase);
+    if (tid == 32) rhi_s = upper_row(F, 0, nM + 1, tend - 1);
+    __syncthreads();
+    const long long rlo = rlo_s, rhi = rhi_s;
+    const long long nr = rhi - rlo + 2;   // F[rlo .. rhi+1]
+    const bool staged = nr <= kSmemF;
+    if (staged)
+        for (long long j = tid; j < nr; j += kThreads) sF[j] = __ldg(F + rlo + j);
+    __syncthreads();
+
+    bool keep[kJoinItems];
+    uint32_t xs[kJoinItems];
+    uint32_t rows[kJoinItems];
+#pragma unroll
+    for (int it = 0; it < kJoinItems; it++) {
+        const unsigned long long s = tbase + (unsigned long long)it * kThreads + tid;
+        keep[it] = false;
+        xs[it] = 0;
+        rows[it] = 0;
+        if (s < tend) {
+            long long i;
+            unsigned long long fi;
+            if (staged) {
+                long long lo = 0, hi = nr - 1;   // search sF[0 .. nr-1)
+                while (hi - lo > 1) {
+                    long long mid = (lo + hi) >> 1;
+                    if (sF[mid] <= s) lo = mid; else hi = mid;
+                }
+                i = rlo + lo;
+                fi = sF[lo];
+            } else {
+                i = upper_row(F, rlo, rhi + 1, s);
+                fi = __ldg(F + i);
+            }
+            const Loc *L = loc + i * P.E;
+            const Loc L0 = L[0];
+            const int32_t x = __ldg(ci + L0.off + (uint32_t)(s - fi));
+            bool k = (__ldg(cu_bitmap + (x >> 5)) >> (x & 31)) & 1u;      // x in C(u)   (L1150)
+            const int32_t *row = M + i * P.t;
+            for (int c = 0; c < P.n_inj && k; c++) k = __ldg(row + P.inj_col[c]) != x;   // Alg. 3 line 10
+            for (int e = 1; e < P.E && k; e++) {
+                const Loc Le = L[e];
+                k = in_sorted(ci + Le.off, Le.len, x);                               // Alg. 3 line 13
+            }
+            keep[it] = k;
+            xs[it] = (uint32_t)x;
+            rows[it] = (uint32_t)i;
+        }
+    }
+
+    if constexpr (!WRITE) {
+        // count-only final level: count + fingerprint of survivors (query-id order rows)
+        unsigned long long c = 0, h1 = 0, h2 = 0;
+#pragma unroll
+        for (int it = 0; it < kJoinItems; it++) {
+            if (!keep[it]) continue;
+            c++;
+            if (FINAL) {
+                const int32_t *row = M + (long long)rows[it] * P.t;
+                unsigned long long a = kFpSeed1, b = kFpSeed2;
+                for (int q = 0; q < P.k; q++) {
+                    int col = P.pos_of_q[q];
+                    uint32_t val = col < P.t ? (uint32_t)__ldg(row + col) : xs[it];
+                    a = fp_mix(a ^ val);
+                    b = fp_mix(b ^ val);
+                }
+                h1 += a;
+                h2 ^= b;
+            }
+        }
+        c = warp_sum_u64(c);
+        h1 = warp_sum_u64(h1);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) h2 ^= __shfl_xor_sync(0xffffffffu, h2, o);
+        if (lane == 0 && c) {
+            atomicAdd(&ctr->count, c);
+            atomicAdd(&ctr->fp1, h1);
+            atomicXor(&ctr->fp2, h2);
+        }
+    } else {
+
+    // ---- ordered compaction through shared memory + decoupled look-back -------------
+    unsigned ballots[kJoinItems];
+#pragma unroll
+    for (int it = 0; it < kJoinItems; it++) {
+        ballots[it] = __ballot_sync(0xffffffffu, keep[it]);
+        if (lane == 0) wcnt[it][warp] = __popc(ballots[it]);
+    }
+    __syncthreads();
+    if (warp == 0) {
+        // 64 (it, warp) counts in slot order: index = it * 8 + warp
+        constexpr int NW = kThreads / 32;
+        unsigned a = wcnt[(2 * lane) / NW][(2 * lane) % NW];
+        unsigned b = wcnt[(2 * lane + 1) / NW][(2 * lane + 1) % NW];
+        unsigned pair = a + b, inc = pair;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        unsigned ex = inc - pair;
+        wbase[(2 * lane) / NW][(2 * lane) % NW] = ex;
+        wbase[(2 * lane + 1) / NW][(2 * lane + 1) % NW] = ex + a;
+        unsigned total = __shfl_sync(0xffffffffu, inc, 31);
+        unsigned long long pre = lookback_exclusive(status, tile, total);
+        if (lane == 0) {
+            base_s = pre;
+            agg_s = total;
+        }
+    }
+    __syncthreads();
+    const unsigned long long base = base_s;
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int it = 0; it < kJoinItems; it++) {
+        if (keep[it]) {
+            unsigned long long pos = base + wbase[it][warp] + __popc(ballots[it] & lt);
+            S[pos] = xs[it];
+            R[pos] = rows[it];
+        }
+    }
+    if (FINAL) {
+        unsigned long long c = 0, h1 = 0, h2 = 0;
+#pragma unroll
+        for (int it = 0; it < kJoinItems; it++) {
+            if (!keep[it]) continue;
+            c++;
+            const int32_t *row = M + (long long)rows[it] * P.t;
+            unsigned long long a = kFpSeed1, b = kFpSeed2;
+            for (int q = 0; q < P.k; q++) {
+                int col = P.pos_of_q[q];
+                uint32_t val = col < P.t ? (uint32_t)__ldg(row + col) : xs[it];
+                a = fp_mix(a ^ val);
+                b = fp_mix(b ^ val);
+            }
+            h1 += a;
+            h2 ^= b;
+        }
+        h1 = warp_sum_u64(h1);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) h2 ^= __shfl_xor_sync(0xffffffffu, h2, o);
+        if (lane == 0 && ballots[0] | ballots[1] | ballots[2] | ballots[3] | ballots[4] | ballots[5] | ballots[6] |
+                             ballots[7]) {
+            atomicAdd(&ctr->fp1, h1);
+            atomicXor(&ctr->fp2, h2);
+        }
+    }
+    if (tile == gridDim.x - 1 && tid == 0) ctr->total = base + agg_s;
+    }
+}
+
+// ---------------------------------------------------------------------- link --------
+// M'[r] = M[R[r]] || S[r]; in FINAL mode the row is written in query-id order.
+template <bool FINAL>
+__global__ void __launch_bounds__(kThreads) k_link(const int32_t *__restrict__ M, int t, const uint32_t *__restrict__ S,
+                                                   const uint32_t *__restrict__ R, unsigned long long nout,
+                                                   StepParams P, int32_t *__restrict__ out) {
+    const int W = t + 1;
+    const unsigned long long total = nout * (unsigned long long)W;
+    for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < total;
+         e += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long r = e / W;
+        const int c = (int)(e - r * W);
+        const int col = FINAL ? P.pos_of_q[c] : c;
+        int32_t v = col < t ? __ldg(M + (unsigned long long)__ldg(R + r) * t + col) : (int32_t)__ldg(S + r);
+        __stcs(out + e, v);
+    }
+}
+
+// Count + fingerprint of a table whose columns are in pi order (k = 1 queries).
+__global__ void k_fp_rows(const int32_t *__restrict__ T, long long nrows, StepParams P, Counters *ctr) {
+    unsigned long long h1 = 0, h2 = 0;
+    for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < nrows; r += (long long)gridDim.x * blockDim.x) {
+        unsigned long long a = kFpSeed1, b = kFpSeed2;
+        for (int q = 0; q < P.k; q++) {
+            uint32_t val = (uint32_t)T[r * P.t + P.pos_of_q[q]];
+            a = fp_mix(a ^ val);
+            b = fp_mix(b ^ val);
+        }
+        h1 += a;
+        h2 ^= b;
+    }
+    h1 = warp_sum_u64(h1);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) h2 ^= __shfl_xor_sync(0xffffffffu, h2, o);
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&ctr->fp1, h1);
+        atomicXor(&ctr->fp2, h2);
+    }
+}
+
+// Shard boundaries: a_r = first row with F[i] >= ceil(r*T/W).
+__global__ void k_shard_bounds(const unsigned long long *F, long long nM, int rank, int W, long long *out) {
+    if (threadIdx.x >= 2) return;
+    const int r = rank + threadIdx.x;
+    const unsigned long long T = F[nM];
+    long long a;
+    if (r >= W) {
+        a = nM;
+    } else {
+        unsigned __int128 num = (unsigned __int128)r * T + (W - 1);
+        unsigned long long target = (unsigned long long)(num / W);
+        long long lo = 0, hi = nM;   // lower_bound over F[0..nM)
+        while (lo < hi) {
+            long long mid = (lo + hi) >> 1;
+            if (F[mid] < target) lo = mid + 1; else hi = mid;
+        }
+        a = r == 0 ? 0 : lo;
+    }
+    out[threadIdx.x] = a;
+    out[2 + threadIdx.x] = (long long)F[a];
+}
+
+}  // namespace
+
+// ====================================================================== host side =====
+void encode_query_signatures(int32_t k, const int32_t *qvl, int32_t qm, const int32_t *qs, const int32_t *qd,
+                             const int32_t *qe, uint32_t *qsig) {
+    // Same written specification as the data side: plane 0 = label (L1277),
+    // 240 two-bit groups with multiplicity counting (reading A5).
+    for (int u = 0; u < k; u++) {
+        int cnt[kSigGroups];
+        std::memset(cnt, 0, sizeof(cnt));
+        for (int e = 0; e < qm; e++) {
+            int other = qs[e] == u ? qd[e] : (qd[e] == u ? qs[e] : -1);
+            if (other < 0) continue;
+            cnt[sig_group((uint32_t)qe[e], (uint32_t)qvl[other])]++;
+        }
+        uint32_t *s = qsig + (size_t)u * kPlanes;
+        s[0] = (uint32_t)qvl[u];
+        for (int w = 1; w < kPlanes; w++) s[w] = 0;
+        for (int gi = 0; gi < kSigGroups; gi++) {
+            uint32_t st = cnt[gi] == 0 ? 0u : (cnt[gi] == 1 ? 1u : 3u);
+            s[1 + gi / 16] |= st << (2 * (gi % 16));
+        }
+    }
+}
+
+}  // namespace gsi
+
+namespace gsi {
+namespace {
+
+inline unsigned grid_for(unsigned long long n, int per) {
+    unsigned long long b = (n + per - 1) / per;
+    if (b < 1) b = 1;
+    return (unsigned)std::min<unsigned long long>(b, 0x7FFFFFFFull);
+}
+
+// Stream-ordered scratch; every allocation is released (stream-ordered) at scope exit.
+struct Arena {
+    cudaStream_t st;
+    std::vector<void *> ptrs;
+    explicit Arena(cudaStream_t s) : st(s) {}
+    template <typename T>
+    gsi_status get(T **p, unsigned long long count) {
+        void *q = nullptr;
+        cudaError_t e = cudaMallocAsync(&q, std::max<unsigned long long>(count, 1) * sizeof(T), st);
+        if (e == cudaErrorMemoryAllocation) {
+            cudaGetLastError();
+            set_error("device memory exhausted");
+            return GSI_ERR_OOM;
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+        ptrs.push_back(q);
+        *p = (T *)q;
+        return GSI_OK;
+    }
+    void release(void *p) {
+        for (auto &q : ptrs)
+            if (q == p) {
+                cudaFreeAsync(q, st);
+                q = nullptr;
+            }
+    }
+    ~Arena() {
+        for (void *q : ptrs)
+            if (q) cudaFreeAsync(q, st);
+    }
+};
+
+struct Prof {
+    bool on = false;
+    cudaStream_t st = nullptr;
+    struct Rec {
+        int cls;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> recs;
+    uint32_t launches[GSI_N_KCLASS] = {0};
+    uint32_t total = 0;
+    void begin(int cls) {
+        total++;
+        launches[cls]++;
+        if (!on) return;
+        Rec r{cls, nullptr, nullptr};
+        cudaEventCreate(&r.a);
+        cudaEventCreate(&r.b);
+        cudaEventRecord(r.a, st);
+        recs.push_back(r);
+    }
+    void end() {
+        if (on && !recs.empty()) cudaEventRecord(recs.back().b, st);
+    }
+    void finish(gsi_stats *s) {
+        for (int c = 0; c < GSI_N_KCLASS; c++) {
+            s->launches[c] = launches[c];
+            s->ms_kernel[c] = 0.f;
+        }
+        s->total_launches = total;
+        for (auto &r : recs) {
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) s->ms_kernel[r.cls] += ms;
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+        recs.clear();
+    }
+    ~Prof() {
+        for (auto &r : recs) {
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+    }
+};
+
+double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ prepare --------
+gsi_status prepare_impl(const gsi_graph *g, int32_t k, const int32_t *qvl, int32_t qm, const int32_t *qs,
+                        const int32_t *qd, const int32_t *qe, gsi_prepared **out) {
+    *out = nullptr;
+    if (!g || k < 1 || qm < 0 || !qvl || (qm > 0 && (!qs || !qd || !qe))) {
+        set_error("invalid query arguments");
+        return GSI_ERR_INVALID_ARG;
+    }
+    if (k > GSI_MAX_K) {
+        set_error("query has more than 32 vertices");
+        return GSI_ERR_QUERY_TOO_LARGE;
+    }
+    if (qm > 4 * GSI_MAX_K * GSI_MAX_K) {
+        set_error("query has too many edges");
+        return GSI_ERR_QUERY_TOO_LARGE;
+    }
+    for (int u = 0; u < k; u++)
+        if (qvl[u] < 0) {
+            set_error("negative query vertex label");
+            return GSI_ERR_LABEL_RANGE;
+        }
+    for (int e = 0; e < qm; e++) {
+        if (qs[e] < 0 || qs[e] >= k || qd[e] < 0 || qd[e] >= k) {
+            set_error("query edge endpoint out of range");
+            return GSI_ERR_VERTEX_RANGE;
+        }
+        if (qs[e] == qd[e]) {
+            set_error("query self-loop");
+            return GSI_ERR_SELF_LOOP;
+        }
+        if (qe[e] < 0) {
+            set_error("negative query edge label");
+            return GSI_ERR_LABEL_RANGE;
+        }
+        for (int f = 0; f < e; f++) {
+            bool same = (qs[f] == qs[e] && qd[f] == qd[e]) || (qs[f] == qd[e] && qd[f] == qs[e]);
+            if (same && qe[f] == qe[e]) {
+                set_error("duplicate query edge");
+                return GSI_ERR_DUPLICATE_EDGE;
+            }
+        }
+    }
+    // connectivity
+    {
+        std::vector<int> seen(k, 0), stack{0};
+        seen[0] = 1;
+        int cnt = 1;
+        while (!stack.empty()) {
+            int u = stack.back();
+            stack.pop_back();
+            for (int e = 0; e < qm; e++) {
+                int o = qs[e] == u ? qd[e] : (qd[e] == u ? qs[e] : -1);
+                if (o >= 0 && !seen[o]) {
+                    seen[o] = 1;
+                    cnt++;
+                    stack.push_back(o);
+                }
+            }
+        }
+        if (cnt != k) {
+            set_error("query graph is disconnected (PAPER.md L299 assumes connectivity)");
+            return GSI_ERR_QUERY_DISCONNECTED;
+        }
+    }
+    auto p = std::make_unique<gsi_prepared>();
+    p->g = g;
+    p->k = k;
+    p->qvl.assign(qvl, qvl + k);
+    p->qs.assign(qs, qs + qm);
+    p->qd.assign(qd, qd + qm);
+    p->qe.assign(qe, qe + qm);
+    p->qe_dense.resize(qm);
+    for (int e = 0; e < qm; e++) {
+        p->qe_dense[e] = g->dense_label(qe[e]);
+        if (p->qe_dense[e] < 0) p->absent_label = true;
+    }
+    p->qsig.resize((size_t)k * kPlanes);
+    encode_query_signatures(k, qvl, qm, qs, qd, qe, p->qsig.data());
+    GSI_CUDA(cudaSetDevice(g->device));
+    GSI_CUDA(cudaMalloc(&p->d_qsig, p->qsig.size() * 4));
+    GSI_CUDA(cudaMemcpy(p->d_qsig, p->qsig.data(), p->qsig.size() * 4, cudaMemcpyHostToDevice));
+    *out = p.release();
+    return GSI_OK;
+}
+
+// ------------------------------------------------------------------ planner --------
+// Alg. 2: score(u) = |C(u)| / deg(u); first vertex = argmin; next =
+// argmin among unmatched vertices adjacent to Q'; after adding u_c every neighbour's score is
+// multiplied by freq(L_E(u_c u')).  Ties go to the smallest query id (reading A8).
+static gsi_status plan_order(const gsi_prepared *q, const std::vector<long long> &cand,
+                             const int32_t *force_order, std::vector<int> &order) {
+    const gsi_graph *g = q->g;
+    const int k = q->k, qm = (int)q->qs.size();
+    order.clear();
+    auto adjacent = [&](int a, int b) {
+        for (int e = 0; e < qm; e++)
+            if ((q->qs[e] == a && q->qd[e] == b) || (q->qs[e] == b && q->qd[e] == a)) return true;
+        return false;
+    };
+    if (force_order) {
+        std::vector<int> seen(k, 0);
+        for (int j = 0; j < k; j++) {
+            int u = force_order[j];
+            if (u < 0 || u >= k || seen[u]) {
+                set_error("force_order is not a permutation");
+                return GSI_ERR_INVALID_ARG;
+            }
+            if (j > 0) {
+                bool conn = false;
+                for (int c = 0; c < j && !conn; c++) conn = adjacent(u, order[c]);
+                if (!conn) {
+                    set_error("force_order prefix is not connected");
+                    return GSI_ERR_INVALID_ARG;
+                }
+            }
+            seen[u] = 1;
+            order.push_back(u);
+        }
+        return GSI_OK;
+    }
+    std::vector<double> score(k);
+    std::vector<int> deg(k, 0), in(k, 0);
+    for (int e = 0; e < qm; e++) {
+        deg[q->qs[e]]++;
+        deg[q->qd[e]]++;
+    }
+    for (int u = 0; u < k; u++) score[u] = deg[u] ? (double)cand[u] / deg[u] : (double)cand[u];
+    auto freq_of = [&](int e) -> double {
+        int d = q->qe_dense[e];
+        return d < 0 ? 0.0 : (double)g->freq[d];
+    };
+    for (int i = 0; i < k; i++) {
+        int best = -1;
+        for (int u = 0; u < k; u++) {
+            if (in[u]) continue;
+            if (i > 0) {
+                bool conn = false;
+                for (int c = 0; c < i && !conn; c++) conn = adjacent(u, order[c]);
+                if (!conn) continue;
+            }
+            if (best < 0 || score[u] < score[best]) best = u;
+        }
+        order.push_back(best);
+        in[best] = 1;
+        for (int e = 0; e < qm; e++) {
+            int o = q->qs[e] == best ? q->qd[e] : (q->qd[e] == best ? q->qs[e] : -1);
+            if (o >= 0) score[o] *= freq_of(e);
+        }
+    }
+    return GSI_OK;
+}
+
+struct Step {
+    int u;                 // query vertex joined at this step
+    int t;                 // columns of M before the step
+    std::vector<int> col;  // linking edges: column
+    std::vector<int> lab;  // dense label
+    std::vector<int> rawlab;
+    std::vector<int> other;   // query id at the other end
+    int paper_e0 = 0;      // index into the edge list (Alg. 4 line 1)
+};
+
+static gsi_status build_steps(const gsi_prepared *q, const std::vector<int> &order, const int32_t *force_e0,
+                              std::vector<Step> &steps) {
+    const gsi_graph *g = q->g;
+    const int k = q->k, qm = (int)q->qs.size();
+    std::vector<int> pos(k, -1);
+    for (int j = 0; j < k; j++) pos[order[j]] = j;
+    steps.clear();
+    for (int j = 1; j < k; j++) {
+        Step s;
+        s.u = order[j];
+        s.t = j;
+        for (int e = 0; e < qm; e++) {
+            int o = q->qs[e] == s.u ? q->qd[e] : (q->qd[e] == s.u ? q->qs[e] : -1);
+            if (o < 0 || pos[o] >= j) continue;
+            s.col.push_back(pos[o]);
+            s.lab.push_back(q->qe_dense[e]);
+            s.rawlab.push_back(q->qe[e]);
+            s.other.push_back(o);
+        }
+        // e0: min freq(l); ties (min raw label id, min column) (reading A9)
+        int best = 0;
+        for (size_t e = 1; e < s.col.size(); e++) {
+            long long fb = g->freq[s.lab[best]], fe = g->freq[s.lab[e]];
+            if (fe < fb || (fe == fb && (s.rawlab[e] < s.rawlab[best] ||
+                                         (s.rawlab[e] == s.rawlab[best] && s.col[e] < s.col[best]))))
+                best = (int)e;
+        }
+        if (force_e0 && force_e0[j] >= 0) {
+            int f = -1;
+            for (size_t e = 0; e < s.col.size(); e++)
+                if (s.other[e] == force_e0[j] && (f < 0 || g->freq[s.lab[e]] < g->freq[s.lab[f]])) f = (int)e;
+            if (f < 0) {
+                set_error("force_first_edge names a vertex not linked to the joined vertex");
+                return GSI_ERR_INVALID_ARG;
+            }
+            best = f;
+        }
+        s.paper_e0 = best;
+        steps.push_back(std::move(s));
+    }
+    return GSI_OK;
+}
+
+// ------------------------------------------------------------------ run -----------
+gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_opts *opts_in, gsi_result **out) {
+    *out = nullptr;
+    if (!g || !q || q->g != g) {
+        set_error("prepared query does not belong to this graph");
+        return GSI_ERR_INVALID_ARG;
+    }
+    gsi_query_opts opts;
+    gsi_query_opts_default(&opts);
+    if (opts_in) opts = *opts_in;
+    const double t_start = now_ms();
+    GSI_CUDA(cudaSetDevice(g->device));
+    cudaStream_t st = opts.stream ? (cudaStream_t)opts.stream : cudaStreamPerThread;
+    const int k = q->k;
+    const long long n = g->n;
+    const long long words = (n + 31) / 32;
+    const int W = opts.shard_count > 1 ? opts.shard_count : 1;
+    const int rank = W > 1 ? opts.shard_rank : 0;
+    if (rank < 0 || rank >= W) {
+        set_error("shard_rank out of range");
+        return GSI_ERR_INVALID_ARG;
+    }
+    auto res = std::make_unique<gsi_result>();
+    res->device = g->device;
+    res->k = k;
+    gsi_stats &S = res->stats;
+    std::memset(&S, 0, sizeof(S));
+    S.k = k;
+    S.shard_level = -1;
+    Arena A(st);
+    Prof prof;
+    prof.on = opts.profile != 0;
+    prof.st = st;
+
+    Counters *ctr = nullptr;
+    GSI_TRY(A.get(&ctr, 1));
+    GSI_CUDA(cudaMemsetAsync(ctr, 0, sizeof(Counters), st));
+
+    // ---------------- filter (a3) ----------------
+    uint32_t *bm = nullptr;
+    unsigned long long *d_counts = nullptr;
+    GSI_TRY(A.get(&bm, (unsigned long long)words * k));
+    GSI_TRY(A.get(&d_counts, k));
+    GSI_CUDA(cudaMemsetAsync(d_counts, 0, 8ull * k, st));
+    {
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
+        unsigned grid = (unsigned)std::min<long long>((words + 7) / 8, (long long)sms * 8);
+        if (grid < 1) grid = 1;
+        prof.begin(GSI_K_FILTER);
+        k_filter<<<grid, kThreads, 0, st>>>(g->sig, n, k, q->d_qsig, opts.filter_mode == 1, bm, words, d_counts, ctr);
+        prof.end();
+    }
+    std::vector<long long> cand(k);
+    Counters hc;
+    GSI_CUDA(cudaMemcpyAsync(cand.data(), d_counts, 8ull * k, cudaMemcpyDeviceToHost, st));
+    GSI_CUDA(cudaMemcpyAsync(&hc, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+    GSI_CUDA(cudaStreamSynchronize(st));
+    GSI_CUDA(cudaGetLastError());
+    const double t_filter = now_ms();
+    S.ms_filter = (float)(t_filter - t_start);
+    for (int u = 0; u < k; u++) S.cand[u] = cand[u];
+    S.alg_bytes[GSI_K_FILTER] = 4.0 * n + 60.0 * hc.plane_loads + 4.0 * words * k;
+
+    // ---------------- plan (a4) ----------------
+    std::vector<int> order;
+    GSI_TRY(plan_order(q, cand, opts.force_order, order));
+    std::vector<Step> steps;
+    GSI_TRY(build_steps(q, order, opts.force_first_edge, steps));
+    for (int j = 0; j < k; j++) S.order[j] = order[j];
+    for (auto &s : steps) {
+        S.n_edges[s.t] = (int)s.col.size();
+        S.first_edge[s.t] = s.other[s.paper_e0];
+    }
+    std::vector<int> pos_of_q(k);
+    for (int j = 0; j < k; j++) pos_of_q[order[j]] = j;
+    const double t_plan = now_ms();
+    S.ms_plan = (float)(t_plan - t_filter);
+
+    bool empty = q->absent_label;
+    for (int u = 0; u < k; u++) empty |= cand[u] == 0;
+
+    auto finish = [&](gsi_status st_code) -> gsi_status {
+        if (st_code != GSI_OK) return st_code;
+        cudaError_t e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return cuda_fail(e, "query sync");
+        prof.finish(&S);
+        S.count = res->count;
+        S.ms_join = (float)(now_ms() - t_plan);
+        S.ms_total = (float)(now_ms() - t_start);
+        *out = res.release();
+        return GSI_OK;
+    };
+    if (empty) {
+        res->count = 0;
+        res->has_table = opts.want_table != 0;
+        return finish(GSI_OK);
+    }
+
+    // ---------------- level 1 (a5) ----------------
+    auto bitmap_of = [&](int u) { return bm + (long long)u * words; };
+    int32_t *M = nullptr;
+    unsigned long long nM = 0;
+    {
+        unsigned long long *status = nullptr;
+        const int u1 = order[0];
+        if (opts.roots && opts.n_roots > 0) {
+            std::vector<int32_t> roots(opts.roots, opts.roots + opts.n_roots);
+            std::sort(roots.begin(), roots.end());
+            roots.erase(std::unique(roots.begin(), roots.end()), roots.end());
+            while (!roots.empty() && roots.back() >= n) roots.pop_back();
+            while (!roots.empty() && roots.front() < 0) roots.erase(roots.begin());
+            long long nr = (long long)roots.size();
+            int32_t *d_roots = nullptr;
+            GSI_TRY(A.get(&d_roots, nr));
+            if (nr) GSI_CUDA(cudaMemcpyAsync(d_roots, roots.data(), 4ull * nr, cudaMemcpyHostToDevice, st));
+            GSI_TRY(A.get(&M, nr));
+            unsigned tiles = grid_for(nr, kThreads);
+            GSI_TRY(A.get(&status, tiles + 1));
+            GSI_CUDA(cudaMemsetAsync(status, 0, 8ull * (tiles + 1), st));
+            prof.begin(GSI_K_COMPACT);
+            k_compact_roots<<<tiles, kThreads, 0, st>>>(d_roots, nr, bitmap_of(u1), M, status + 1,
+                                                        (unsigned *)status, ctr);
+            prof.end();
+            GSI_CUDA(cudaMemcpyAsync(&hc, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+            GSI_CUDA(cudaStreamSynchronize(st));
+            nM = hc.total;
+            S.alg_bytes[GSI_K_COMPACT] += 8.0 * nr + 4.0 * nM;
+        } else {
+            nM = (unsigned long long)cand[u1];
+            GSI_TRY(A.get(&M, nM));
+            unsigned tiles = grid_for(words, kThreads);
+            GSI_TRY(A.get(&status, tiles + 1));
+            GSI_CUDA(cudaMemsetAsync(status, 0, 8ull * (tiles + 1), st));
+            prof.begin(GSI_K_COMPACT);
+            k_compact_bitmap<<<tiles, kThreads, 0, st>>>(bitmap_of(u1), words, M, status + 1, (unsigned *)status,
+                                                         ctr);
+            prof.end();
+            S.alg_bytes[GSI_K_COMPACT] += 4.0 * words + 4.0 * nM;
+        }
+        A.release(status);
+    }
+    S.rows[0] = nM;
+    S.levels = 1;
+
+    StepParams P;
+    std::memset(&P, 0, sizeof(P));
+    P.k = k;
+    for (int qv = 0; qv < k; qv++) P.pos_of_q[qv] = pos_of_q[qv];
+
+    if (k == 1) {
+        P.t = 1;
+        GSI_CUDA(cudaMemsetAsync(ctr, 0, sizeof(Counters), st));
+        if (nM) {
+            prof.begin(GSI_K_OTHER);
+            k_fp_rows<<<grid_for(nM, kThreads), kThreads, 0, st>>>(M, (long long)nM, P, ctr);
+            prof.end();
+        }
+        GSI_CUDA(cudaMemcpyAsync(&hc, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+        GSI_CUDA(cudaStreamSynchronize(st));
+        res->count = nM;
+        res->fp[0] = nM;
+        res->fp[1] = hc.fp1;
+        res->fp[2] = hc.fp2;
+        if (opts.want_table) {
+            res->has_table = true;
+            res->nrows = nM;
+            GSI_CUDA(cudaMalloc(&res->table, 4ull * (nM ? nM : 1)));
+            if (nM) GSI_CUDA(cudaMemcpyAsync(res->table, M, 4ull * nM, cudaMemcpyDeviceToDevice, st));
+        }
+        return finish(GSI_OK);
+    }
+
+    const uint64_t shard_min = opts.shard_min_rows ? opts.shard_min_rows : 65536;
+    bool sharded = W == 1;
+    const double deadline = opts.timeout_s > 0 ? t_start + 1000.0 * opts.timeout_s : 0;
+
+    for (size_t si = 0; si < steps.size(); si++) {
+        const Step &s = steps[si];
+        const int t = s.t;
+        const bool last = si + 1 == steps.size();
+        if (deadline > 0 && now_ms() > deadline) {
+            set_error("query timeout");
+            return GSI_ERR_TIMEOUT;
+        }
+        // ---- step parameters ----
+        const int E = (int)s.col.size();
+        P.t = t;
+        P.E = E;
+        P.per_row_e0 = opts.e0_mode == 0 ? 1 : 0;
+        // paper mode: e0 first
+        std::vector<int> eorder(E);
+        for (int e = 0; e < E; e++) eorder[e] = e;
+        std::swap(eorder[0], eorder[s.paper_e0]);
+        for (int e = 0; e < E; e++) {
+            int src = eorder[e];
+            P.col[e] = s.col[src];
+            P.lab[e] = (uint32_t)s.lab[src];
+            P.gbase[e] = (unsigned long long)g->gbase[s.lab[src]];
+            P.ngroups[e] = g->ngroups[s.lab[src]];
+        }
+        P.n_inj = 0;
+        if (!opts.homomorphism) {
+            for (int c = 0; c < t; c++) {
+                if (q->qvl[order[c]] != q->qvl[s.u]) continue;   // different label: C(u) excludes it
+                bool linked = false;
+                for (int e = 0; e < E; e++) linked |= P.col[e] == c;   // x in N(m[c],l) => x != m[c]
+                if (!linked) P.inj_col[P.n_inj++] = c;
+            }
+        }
+        // ---- probe + Prealloc scan (a6) ----
+        Loc *loc = nullptr;
+        unsigned long long *F = nullptr, *status = nullptr;
+        GSI_TRY(A.get(&loc, nM * (unsigned long long)E));
+        GSI_TRY(A.get(&F, nM + 1));
+        unsigned ptiles = grid_for(nM, kThreads);
+        GSI_TRY(A.get(&status, ptiles + 1));
+        GSI_CUDA(cudaMemsetAsync(status, 0, 8ull * (ptiles + 1), st));
+        GSI_CUDA(cudaMemsetAsync(ctr, 0, sizeof(Counters), st));
+        if (nM == 0) GSI_CUDA(cudaMemsetAsync(F, 0, 8, st));
+        else {
+            prof.begin(GSI_K_PROBE);
+            k_probe<<<ptiles, kThreads, 0, st>>>(M, (long long)nM, P, g->groups, g->gpn, loc, F, status + 1,
+                                                 (unsigned *)status, ctr);
+            prof.end();
+        }
+        unsigned long long gba = 0;
+        GSI_CUDA(cudaMemcpyAsync(&gba, F + nM, 8, cudaMemcpyDeviceToHost, st));
+        GSI_CUDA(cudaMemcpyAsync(&hc, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+        GSI_CUDA(cudaStreamSynchronize(st));
+        A.release(status);
+        S.gba[t] = gba;
+        S.list_elems[t] = hc.list_elems;
+        S.alg_bytes[GSI_K_PROBE] += (double)nM * (20.0 * E + 8.0);
+        const unsigned long long active = hc.active_rows, elems = hc.list_elems;
+
+        // ---- shard the rows of this level ----
+        unsigned long long s0 = 0, s1 = gba;
+        if (!sharded && (nM >= shard_min || last)) {
+            long long *bounds = nullptr;
+            GSI_TRY(A.get(&bounds, 4));
+            prof.begin(GSI_K_OTHER);
+            k_shard_bounds<<<1, 32, 0, st>>>(F, (long long)nM, rank, W, bounds);
+            prof.end();
+            long long hb[4];
+            GSI_CUDA(cudaMemcpyAsync(hb, bounds, sizeof(hb), cudaMemcpyDeviceToHost, st));
+            GSI_CUDA(cudaStreamSynchronize(st));
+            s0 = (unsigned long long)hb[2];
+            s1 = (unsigned long long)hb[3];
+            S.shard_level = t;
+            S.shard_row_begin = (uint64_t)hb[0];
+            S.shard_row_end = (uint64_t)hb[1];
+            sharded = true;
+        }
+
+        // ---- join (a7) + combine (a8) ----
+        const unsigned long long slots = s1 - s0;
+        const bool write = !last || opts.want_table;
+        uint32_t *Sv = nullptr, *Rv = nullptr;
+        unsigned long long nout = 0;
+        GSI_CUDA(cudaMemsetAsync(ctr, 0, sizeof(Counters), st));
+        if (slots > 0) {
+            unsigned jt = grid_for(slots, kJoinTile);
+            GSI_TRY(A.get(&status, jt + 1));
+            GSI_CUDA(cudaMemsetAsync(status, 0, 8ull * (jt + 1), st));
+            if (write) {
+                GSI_TRY(A.get(&Sv, slots));
+                GSI_TRY(A.get(&Rv, slots));
+            }
+            prof.begin(GSI_K_JOIN);
+            if (write && last)
+                k_join<true, true><<<jt, kThreads, 0, st>>>(M, (long long)nM, F, loc, P, g->ci, bitmap_of(s.u), s0,
+                                                            s1, Sv, Rv, status + 1, (unsigned *)status, ctr);
+            else if (write)
+                k_join<true, false><<<jt, kThreads, 0, st>>>(M, (long long)nM, F, loc, P, g->ci, bitmap_of(s.u),
+                                                             s0, s1, Sv, Rv, status + 1, (unsigned *)status, ctr);
+            else
+                k_join<false, true><<<jt, kThreads, 0, st>>>(M, (long long)nM, F, loc, P, g->ci, bitmap_of(s.u),
+                                                             s0, s1, Sv, Rv, status + 1, (unsigned *)status, ctr);
+            prof.end();
+            GSI_CUDA(cudaMemcpyAsync(&hc, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+            GSI_CUDA(cudaStreamSynchronize(st));
+            GSI_CUDA(cudaGetLastError());
+            A.release(status);
+            nout = write ? hc.total : hc.count;
+        } else {
+            std::memset(&hc, 0, sizeof(hc));
+        }
+        // algorithmic bytes of the join over the rows it touched
+        {
+            double frac = gba ? (double)slots / (double)gba : 0.0;
+            S.alg_bytes[GSI_K_JOIN] += frac * (4.0 * t * active + 4.0 * elems + (8.0 * E + 8.0) * active) +
+                                       (write ? 8.0 * nout : 0.0);
+        }
+        if (last) {
+            res->count = nout;
+            res->fp[0] = nout;
+            res->fp[1] = hc.fp1;
+            res->fp[2] = hc.fp2;
+        }
+        A.release(loc);
+        A.release(F);
+        S.rows[t] = nout;
+        S.levels = t + 1;
+        if (!write) {
+            A.release(M);
+            break;
+        }
+        // link
+        int32_t *M2 = nullptr;
+        const unsigned long long nint = nout * (unsigned long long)(t + 1);
+        if (last) {
+            GSI_CUDA(cudaMalloc(&res->table, 4ull * (nint ? nint : 1)));
+            M2 = res->table;
+            res->has_table = true;
+            res->nrows = nout;
+        } else {
+            GSI_TRY(A.get(&M2, nint));
+        }
+        if (nout) {
+            unsigned lg = grid_for(nint, kThreads * 4);
+            prof.begin(GSI_K_LINK);
+            if (last) k_link<true><<<lg, kThreads, 0, st>>>(M, t, Sv, Rv, nout, P, M2);
+            else k_link<false><<<lg, kThreads, 0, st>>>(M, t, Sv, Rv, nout, P, M2);
+            prof.end();
+            S.alg_bytes[GSI_K_LINK] += (double)nout * (4.0 * (t + 1) + 4.0 * t + 8.0);
+        }
+        A.release(Sv);
+        A.release(Rv);
+        A.release(M);
+        M = M2;
+        nM = nout;
+        if (nM == 0 && !last) {
+            // nothing survives: the remaining levels are empty
+            res->count = 0;
+            res->fp[0] = res->fp[1] = res->fp[2] = 0;
+            res->has_table = opts.want_table != 0;
+            break;
+        }
+    }
+    return finish(GSI_OK);
+}
+
+}  // namespace gsi
+
+// ====================================================================== debug filter ===
+namespace gsi {
+gsi_status debug_filter_impl(const gsi_graph *g, int32_t k, const int32_t *qvl, int32_t qm, const int32_t *qs,
+                             const int32_t *qd, const int32_t *qe, int32_t mode, uint32_t *bitmaps, int64_t *counts) {
+    gsi_prepared *pp = nullptr;
+    GSI_TRY(prepare_impl(g, k, qvl, qm, qs, qd, qe, &pp));
+    std::unique_ptr<gsi_prepared> p(pp);
+    cudaStream_t st = cudaStreamPerThread;
+    const long long n = g->n, words = (n + 31) / 32;
+    Arena A(st);
+    uint32_t *bm = nullptr;
+    unsigned long long *cnt = nullptr;
+    Counters *ctr = nullptr;
+    GSI_TRY(A.get(&bm, (unsigned long long)words * k));
+    GSI_TRY(A.get(&cnt, k));
+    GSI_TRY(A.get(&ctr, 1));
+    GSI_CUDA(cudaMemsetAsync(cnt, 0, 8ull * k, st));
+    GSI_CUDA(cudaMemsetAsync(ctr, 0, sizeof(Counters), st));
+    unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>((words + 7) / 8, 148 * 8));
+    k_filter<<<grid, kThreads, 0, st>>>(g->sig, n, k, p->d_qsig, mode == 1, bm, words, cnt, ctr);
+    if (bitmaps && words)
+        GSI_CUDA(cudaMemcpyAsync(bitmaps, bm, 4ull * words * k, cudaMemcpyDeviceToHost, st));
+    std::vector<unsigned long long> hc(k);
+    GSI_CUDA(cudaMemcpyAsync(hc.data(), cnt, 8ull * k, cudaMemcpyDeviceToHost, st));
+    GSI_CUDA(cudaStreamSynchronize(st));
+    GSI_CUDA(cudaGetLastError());
+    for (int u = 0; u < k; u++)
+        if (counts) counts[u] = (int64_t)hc[u];
+    return GSI_OK;
+}
+}  // namespace gsi

@@ -1,0 +1,339 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+All inputs are seeded synthetic graphs from workloads/ (shapes of SURVEY.md §8(d)); every
+expected value comes from oracle/ or from the paper's printed numbers.  Integer work: the bar
+is bit-exact equality (sorted match tables, C(u) bitmaps, signature planes, PCSR runs).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from paper_1906_03420_b200 import gsi
+
+pytestmark = pytest.mark.gpu
+
+if gsi.gsi_device_count() == 0:
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+
+def canon(tab: np.ndarray) -> np.ndarray:
+    if len(tab) == 0:
+        return tab.reshape(0, tab.shape[1] if tab.ndim == 2 else 0)
+    return tab[np.lexsort(tab.T[::-1])]
+
+
+def strictly_increasing_in_order(tab: np.ndarray, order) -> bool:
+    """Rows emitted in pi-column order must be strictly increasing (order-preserving join)."""
+    if len(tab) < 2:
+        return True
+    t = tab[:, list(order)].astype(np.int64)
+    a, b = t[:-1], t[1:]
+    # lexicographic a < b
+    diff = a != b
+    first = np.argmax(diff, axis=1)
+    anyd = diff.any(axis=1)
+    idx = np.arange(len(a))
+    return bool(anyd.all() and (a[idx, first] < b[idx, first]).all())
+
+
+def run_both(g, q, graph=None, og=None, **kw):
+    graph = graph or gsi.build(g)
+    og = og or oracle.OracleGraph(g)
+    r = gsi.query(graph, q, want_table=True, **kw)
+    tab = r.table()
+    hom = kw.get("homomorphism", False)
+    cnt, fp, otab = oracle.match(og, q, hom=hom)
+    return r, tab, cnt, fp, otab
+
+
+# ------------------------------------------------------------------ paper example ----
+def test_fig1_default_path():
+    """SURVEY.md §8(c) 'C1 default-path trace' and the single match."""
+    g, q = W.fig1()
+    r, tab, cnt, fp, otab = run_both(g, q)
+    assert r.count == 1 == cnt
+    assert tab.tolist() == [[0, 100, 201, 200]]
+    assert r.fingerprint() == fp
+    s = r.stats()
+    assert s["cand"][:4] == [1, 1, 1, 100]
+    assert s["order"][:4] == [1, 0, 2, 3]
+    assert s["rows"][:4] == [1, 1, 1, 1]
+    r2 = gsi.query(gsi.build(g), q, e0_mode=1)
+    assert r2.stats()["gba"][1:4] == [3, 1, 3]
+
+
+def test_fig7_prealloc_numbers():
+    """Fig. 7: forced order (u0,u1,u2), label-only filter, paper e0:
+    first edge u1u2 gives |GBA| = 200; the planner's own first edge (label b) gives 100."""
+    g, q = W.fig1()
+    graph = gsi.build(g)
+    fo = [0, 1, 2, 3]
+    r = gsi.query(graph, q, want_table=True, force_order=fo, filter_mode=1, e0_mode=1,
+                  force_first_edge=[-1, -1, 1, -1])
+    s = r.stats()
+    assert s["rows"][1] == 100                       # M = {(v0, vj)}, 100 rows (L572-576)
+    assert s["gba"][2] == 200                        # L1066
+    assert s["first_edge"][2] == 1
+    assert r.table().tolist() == [[0, 100, 201, 200]]
+    r = gsi.query(graph, q, force_order=fo, filter_mode=1, e0_mode=1)
+    assert r.stats()["gba"][2] == 100                # L1067 (b is the rarer label, L1068)
+    assert r.stats()["first_edge"][2] == 0
+    assert r.count == 1
+
+
+# ------------------------------------------------------------------ PCSR -------------
+@pytest.mark.parametrize("gpn", [16, 8, 4, 2])
+def test_pcsr_lookup_equals_adjacency(gpn):
+    """Every (v,l): GPU N(v,l) equals the oracle's label-filtered adjacency;
+    Claim 1 is exercised by small gpn (overflow chains)."""
+    g = W.chung_lu(3000, 20000, 400, nlv=3, nle=5, seed=21)
+    graph = gsi.build(g, gpn=gpn)
+    og = oracle.OracleGraph(g)
+    info = graph.info()
+    vs = np.repeat(np.arange(g.n), 6)
+    ls = np.tile(np.arange(6), g.n)                  # label 5 is absent: empty runs
+    lens, reads, nb = gsi.gsi_debug_lookup(graph, vs, ls)
+    pos = 0
+    for v, l, n_ in zip(vs.tolist(), ls.tolist(), lens.tolist()):
+        exp = og.neighbors(v, l)
+        assert n_ == len(exp)
+        assert nb[pos:pos + n_].tolist() == exp.tolist(), (v, l)
+        pos += n_
+    assert reads.max() <= info["max_chain"]
+    if gpn == 2:
+        assert info["max_chain"] > 1 and info["overflow_groups"] > 0
+    assert info["n_groups"] == sum(len(np.unique(np.concatenate([g.src[g.elabels == l], g.dst[g.elabels == l]])))
+                                   for l in range(5))
+
+
+def test_pcsr_fig1_partition_b():
+    g, _ = W.fig1()
+    graph = gsi.build(g)
+    lens, _, nb = gsi.gsi_debug_lookup(graph, [0, 1, 101, 201, 5], [1, 1, 1, 1, 1])
+    assert lens.tolist() == [1, 1, 1, 1, 0]
+    lens, _, nb = gsi.gsi_debug_lookup(graph, [0], [0])
+    assert nb.tolist() == list(range(1, 101))       # L746-747
+
+
+# ------------------------------------------------------------------ signatures/filter -
+def test_signature_table_bit_exact():
+    g = W.chung_lu(5000, 30000, 600, nlv=5, nle=7, seed=22)
+    graph = gsi.build(g)
+    og = oracle.OracleGraph(g)
+    assert np.array_equal(gsi.gsi_debug_signatures(graph), oracle.signatures(og))
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_filter_bitmaps_bit_exact(mode):
+    g = W.chung_lu(5000, 30000, 600, nlv=5, nle=7, seed=23)
+    graph = gsi.build(g)
+    og = oracle.OracleGraph(g)
+    planes = oracle.signatures(og)
+    for s in range(6):
+        q = W.random_walk_query(g, 8, 300 + s)
+        bm, cnt = gsi.gsi_debug_filter(graph, q.vlabels, q.src, q.dst, q.elabels, filter_mode=mode)
+        if mode == 0:
+            obm, ocnt = oracle.filter(og, planes, oracle.query_signatures(q))
+        else:
+            iso = W.Query(q.n, q.vlabels, np.zeros(0), np.zeros(0), np.zeros(0))   # label-only = no pairs
+            obm, ocnt = oracle.filter(og, planes, oracle.query_signatures(iso))
+        assert np.array_equal(bm, obm) and np.array_equal(cnt, ocnt)
+
+
+# ------------------------------------------------------------------ closed forms -----
+@pytest.mark.parametrize("n,k", [(6, 2), (7, 4), (8, 5), (9, 3)])
+def test_clique_counts_and_levels(n, k):
+    graph = gsi.build(W.complete_graph(n))
+    r = gsi.query(graph, W.clique_query(k), want_table=True)
+    assert r.count == math.perm(n, k)
+    s = r.stats()
+    assert s["rows"][:k] == [math.perm(n, t) for t in range(1, k + 1)]
+    assert len({tuple(x) for x in r.table().tolist()}) == r.count
+
+
+@pytest.mark.parametrize("n,k", [(5, 3), (12, 12), (40, 9)])
+def test_path_in_cycle_levels(n, k):
+    graph = gsi.build(W.cycle_graph(n))
+    r = gsi.query(graph, W.path_query(k))
+    assert r.count == 2 * n
+    s = r.stats()
+    assert s["rows"][0] == n and all(x == 2 * n for x in s["rows"][1:k])
+
+
+def test_square_in_grid_and_star():
+    graph = gsi.build(W.grid_graph(6, 9))
+    assert gsi.query(graph, W.cycle_query(4)).count == 8 * 5 * 8
+    g = W.chung_lu(300, 1200, 40, nlv=1, nle=1, seed=3)
+    deg = np.bincount(np.concatenate([g.src, g.dst]), minlength=g.n)
+    graph = gsi.build(g)
+    for leaves in (1, 2, 3):
+        assert gsi.query(graph, W.star_query(leaves)).count == sum(math.perm(int(d), leaves) for d in deg)
+
+
+# ------------------------------------------------------------------ random parity ----
+def test_tiny_random_vs_oracle():
+    """Seeded tiny instances (n <= 9, k <= 5, parallel edges with distinct labels included)."""
+    for s in range(300):
+        g = W.random_tiny_graph(s, nlv=1 + s % 3, nle=1 + s % 2)
+        if g.m == 0:
+            continue
+        q = W.random_connected_query(20_000 + s, 1 + s % 5, nlv=1 + s % 3, nle=1 + s % 2)
+        r, tab, cnt, fp, otab = run_both(g, q)
+        assert r.count == cnt, s
+        assert np.array_equal(canon(tab), otab), s
+        assert r.fingerprint() == fp, s
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_medium_random_walk_queries(seed):
+    """Power-law graphs with several tiles of rows and ragged tails; exact sorted tables."""
+    g = W.chung_lu(20_000, 120_000, 2_000, nlv=4, nle=6, seed=seed)
+    graph = gsi.build(g)
+    og = oracle.OracleGraph(g)
+    for j in range(8):
+        q = W.random_walk_query(g, 4 + (j % 6), 5000 + 10 * seed + j)
+        r, tab, cnt, fp, otab = run_both(g, q, graph, og)
+        assert r.count == cnt and r.fingerprint() == fp
+        assert np.array_equal(canon(tab), otab)
+        assert strictly_increasing_in_order(tab, r.stats()["order"][:q.n])
+        assert tuple(q.embedding.tolist()) in {tuple(x) for x in tab.tolist()}
+
+
+def test_enron_shaped_config():
+    """Config C2 (enron-shaped, 36 692 V / 183 831 E, |L_V|=10, |L_E|=100), 12-vertex walks."""
+    g = W.make_config("C2")
+    graph = gsi.build(g)
+    og = oracle.OracleGraph(g)
+    for j in range(10):
+        q = W.random_walk_query(g, 12, 1000 + j)
+        r, tab, cnt, fp, otab = run_both(g, q, graph, og)
+        assert r.count == cnt and np.array_equal(canon(tab), otab)
+
+
+# ------------------------------------------------------------------ invariances -------
+def test_order_e0_and_filter_invariance():
+    g = W.chung_lu(4000, 30000, 500, nlv=3, nle=4, seed=31)
+    graph = gsi.build(g)
+    og = oracle.OracleGraph(g)
+    rng = np.random.default_rng(0)
+    for j in range(6):
+        q = W.random_walk_query(g, 6, 700 + j)
+        _, _, otab = oracle.match(og, q)
+        base = canon(gsi.query(graph, q, want_table=True).table())
+        assert np.array_equal(base, otab)
+        for trial in range(4):
+            # random connected order
+            order = [int(rng.integers(q.n))]
+            while len(order) < q.n:
+                cand = [u for u in range(q.n) if u not in order and any(
+                    (a == u and b in order) or (b == u and a in order) for a, b in zip(q.src.tolist(), q.dst.tolist()))]
+                order.append(int(rng.choice(cand)))
+            for e0 in (0, 1):
+                for fm in (0, 1):
+                    t = gsi.query(graph, q, want_table=True, force_order=order, e0_mode=e0, filter_mode=fm).table()
+                    assert np.array_equal(canon(t), otab)
+
+
+def test_sharding_concatenates_to_full():
+    """M-row sharding run sequentially: shards in rank order == 1-GPU table."""
+    g = W.chung_lu(20_000, 150_000, 3_000, nlv=2, nle=3, seed=41)
+    graph = gsi.build(g)
+    for j in range(4):
+        q = W.random_walk_query(g, 5, 900 + j)
+        full = gsi.query(graph, q, want_table=True)
+        ft = full.table()
+        for W_ in (2, 3, 8):
+            for smin in (1, 1 << 30):
+                parts = [gsi.query(graph, q, want_table=True, shard_rank=r, shard_count=W_, shard_min_rows=smin)
+                         for r in range(W_)]
+                cat = np.concatenate([p.table() for p in parts])
+                assert np.array_equal(cat, ft)
+                assert sum(p.count for p in parts) == full.count
+                fps = [p.fingerprint() for p in parts]
+                assert sum(f[1] for f in fps) % (1 << 64) == full.fingerprint()[1]
+
+
+def test_roots_restriction_matches_oracle():
+    g = W.chung_lu(10_000, 60_000, 900, nlv=3, nle=3, seed=51)
+    graph = gsi.build(g)
+    og = oracle.OracleGraph(g)
+    rng = np.random.default_rng(1)
+    for j in range(4):
+        q = W.random_walk_query(g, 6, 1100 + j)
+        r0 = gsi.query(graph, q)
+        root = r0.stats()["order"][0]
+        roots = rng.choice(g.n, 500, replace=False)
+        r = gsi.query(graph, q, want_table=True, roots=roots)
+        cnt, fp, otab = oracle.match(og, q, root=root, roots=roots)
+        assert r.count == cnt and np.array_equal(canon(r.table()), otab)
+
+
+def test_homomorphism_matches_oracle():
+    for s in range(60):
+        g = W.random_tiny_graph(100 + s, nlv=1 + s % 2, nle=1 + s % 2)
+        if g.m == 0:
+            continue
+        q = W.random_connected_query(30_000 + s, 2 + s % 4, nlv=1 + s % 2, nle=1 + s % 2)
+        graph = gsi.build(g)
+        og = oracle.OracleGraph(g)
+        r = gsi.query(graph, q, want_table=True, homomorphism=True, filter_mode=1)
+        cnt, fp, otab = oracle.match(og, q, hom=True)
+        assert r.count == cnt and np.array_equal(canon(r.table()), otab), s
+
+
+def test_k1_and_empty_cases():
+    g = W.chung_lu(2000, 8000, 100, nlv=3, nle=2, seed=61)
+    graph = gsi.build(g)
+    q = W.Query(1, np.array([1]), np.zeros(0), np.zeros(0), np.zeros(0))
+    r = gsi.query(graph, q, want_table=True)
+    assert r.count == int((g.vlabels == 1).sum())
+    assert r.table()[:, 0].tolist() == np.nonzero(g.vlabels == 1)[0].tolist()
+    assert r.fingerprint() == oracle.match(oracle.OracleGraph(g), q)[1]
+    q = W.edge_query(0, 1, 99)                                  # edge label absent from G
+    assert gsi.query(graph, q, want_table=True).count == 0
+    q = W.edge_query(0, 77, 0)                                  # vertex label absent
+    assert gsi.query(graph, q).count == 0
+
+
+def test_errors():
+    g = W.cycle_graph(6)
+    graph = gsi.build(g)
+    with pytest.raises(gsi.GsiError) as e:
+        gsi.gsi_query(graph, [0, 0, 0, 0], [0, 2], [1, 3], [0, 0])
+    assert e.value.status == "GSI_ERR_QUERY_DISCONNECTED"
+    with pytest.raises(gsi.GsiError) as e:
+        gsi.gsi_query(graph, np.zeros(33), np.arange(32), np.arange(1, 33), np.zeros(32))
+    assert e.value.status == "GSI_ERR_QUERY_TOO_LARGE"
+    for bad, code in [((3, [0, 0, 0], [0], [0], [0]), "GSI_ERR_SELF_LOOP"),
+                      ((3, [0, 0, 0], [0, 1], [1, 0], [0, 0]), "GSI_ERR_DUPLICATE_EDGE"),
+                      ((3, [0, 0, 0], [0], [5], [0]), "GSI_ERR_VERTEX_RANGE"),
+                      ((3, [0, -1, 0], [0], [1], [0]), "GSI_ERR_LABEL_RANGE")]:
+        with pytest.raises(gsi.GsiError) as e:
+            gsi.gsi_build_graph(*bad)
+        assert e.value.status == code
+    gsi.gsi_build_graph(3, [0, 0, 0], [0, 1], [1, 0], [0, 1])   # distinct-label parallel edges: OK
+    empty = gsi.gsi_build_graph(4, [0, 0, 0, 0], [], [], [])
+    assert gsi.query(empty, W.edge_query()).count == 0
+
+
+def test_prepared_and_buffers_roundtrip():
+    g = W.chung_lu(3000, 15000, 300, nlv=3, nle=3, seed=71)
+    graph = gsi.build(g)
+    q = W.random_walk_query(g, 6, 1300)
+    p = gsi.prepare(graph, q)
+    a = gsi.gsi_query_run(graph, p, want_table=True)
+    b = gsi.query(graph, q, want_table=True)
+    assert np.array_equal(a.table(), b.table())
+    # replicate the graph through its buffer descriptors (what the NCCL broadcast does)
+    import torch
+    descs, meta = gsi.gsi_graph_buffers(graph)
+    g2, descs2 = gsi.gsi_graph_alloc_like(meta)
+    for (n1, p1, b1), (n2, p2, b2) in zip(descs, descs2):
+        assert n1 == n2 and b1 == b2
+        gsi.torch_view(p2, b2).copy_(gsi.torch_view(p1, b1))
+    torch.cuda.synchronize()
+    c = gsi.query(g2, q, want_table=True)
+    assert np.array_equal(c.table(), b.table())
