@@ -1,0 +1,419 @@
+#!/usr/bin/env python
+"""bench.py — GSI subgraph matching on B200: matches/s and ms/query (BASELINE.json metric).
+
+One "step" = one pass of the whole hot path (filter -> plan -> every join level, SURVEY.md
+§8(a)) over one batch of Q seeded random-walk queries against a
+seeded synthetic data graph shaped like the paper's workloads.  The graph
+(PCSR + signatures, tens of GB) is built once, outside the timed region, like the paper's
+offline preprocessing; it is far larger than the 126 MB L2, so no L2
+flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5b] [--queries Q]
+  python bench.py --impl reference ...     # the CPU oracle arm (rank 0 only)
+
+Multi-GPU (torchrun, one rank per GPU): rank 0 builds the graph and broadcasts its device
+buffers over NCCL; every query's rows are sharded across ranks and the
+per-query counts are all-reduced (NCCL) — total work is fixed, so scaling is "strong".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+# Workloads.  C5b is the join-stress scale-free config the HBM target is
+# evaluated on; the others are selectable for context.
+BENCH_CONFIGS = {
+    "C2": dict(kind="C2", desc="enron-shaped Chung-Lu n=36692 m=183831 |L_V|=10 |L_E|=100"),
+    "C3": dict(kind="C3", desc="gowalla-shaped Chung-Lu n=196591 m=950327 |L_V|=|L_E|=100"),
+    "C4": dict(kind="C4", desc="road-shaped lattice 3742^2 m=17M |L_V|=|L_E|=1000"),
+    "C5a": dict(kind="C5a", desc="R-MAT scale 25 ef 8 (~250M E) |L_V|=1000 |L_E|=86"),
+    "C5b": dict(kind="C5b", desc="R-MAT scale 25 ef 8 (~250M E) |L_V|=10 |L_E|=86"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            parts = [x.strip() for x in l.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nme, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nme)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def make_workload(cfg: str, nq: int, k: int, device: str, seed: int = 1, scale: int | None = None):
+    t0 = time.time()
+    kind = BENCH_CONFIGS[cfg]["kind"]
+    over = {}
+    if scale is not None and kind.startswith("C5"):
+        over["scale"] = scale
+    g = W.make_config(kind, seed=seed, device=device, **over)
+    t1 = time.time()
+    adj = W._Adj(g, device=device)
+    qs = [W.random_walk_query(g, k, 1000 + i, adj) for i in range(nq)]
+    del adj
+    log(f"[bench] workload {cfg}: n={g.n} m={g.m} gen {t1 - t0:.1f}s queries {time.time() - t1:.1f}s")
+    return g, qs
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------------------ CPU oracle -----
+def oracle_sample(og, qs, budget_s: float, per_query_timeout: float, threads: int, start: int = 0):
+    """Run the oracle (as it stands) over queries start, start+1, ... until budget_s elapses.
+    Returns (matches, seconds, queries_done, timeouts)."""
+    import oracle
+    matches, secs, done, touts = 0, 0.0, 0, 0
+    i = start
+    while secs < budget_s and done < len(qs):
+        q = qs[i % len(qs)]
+        t = time.perf_counter()
+        try:
+            c, fp, _ = oracle.match(og, q, table=False, threads=threads, timeout=per_query_timeout)
+        except oracle.OracleError as e:
+            if e.code != -9:
+                raise
+            c = 0
+            touts += 1
+        secs += time.perf_counter() - t
+        matches += c
+        done += 1
+        i += 1
+    return matches, secs, done, touts
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        if rank != 0:
+            dist.barrier()
+            return
+    import oracle
+    dev = "cuda" if _cuda_ok() else "cpu"
+    g, qs = make_workload(args.config, args.queries, args.k, dev, scale=args.scale)
+    t = time.time()
+    og = oracle.OracleGraph(g)
+    log(f"[bench] oracle index {time.time() - t:.1f}s")
+    threads = len(os.sched_getaffinity(0))
+    per_step = args.ref_step_budget
+    for _ in range(args.warmup):
+        oracle_sample(og, qs, min(per_step, 2.0), args.ref_query_timeout, threads)
+    tot_m, tot_s, tot_q, tot_to = 0, 0.0, 0, 0
+    pos = 0
+    for _ in range(args.steps):
+        m, s, d, to = oracle_sample(og, qs, per_step, args.ref_query_timeout, threads, start=pos)
+        pos += d
+        tot_m += m; tot_s += s; tot_q += d; tot_to += to
+    value = tot_m / tot_s if tot_s > 0 else 0.0
+    line = {
+        "impl": "reference", "metric": "matches/s", "value": value, "unit": "matches/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * tot_s / max(args.steps, 1),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic", "config": workload_config(args, g),
+        "ms_per_query": 1000.0 * tot_s / max(tot_q, 1),
+        "cpu_baseline": {"value": value, "unit": "matches/s", "cores": threads, "kind": "oracle",
+                         "sample": f"{tot_q} queries of the batch (cycled), per-query timeout "
+                                   f"{args.ref_query_timeout}s ({tot_to} timed out, partial counts kept), "
+                                   f"~{per_step}s per step"},
+        "e2e": {"value": value, "unit": "matches/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def _cuda_ok():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+def workload_config(args, g):
+    return {"workload": f"{args.config}: {BENCH_CONFIGS[args.config]['desc']}", "n": int(g.n), "m": int(g.m),
+            "queries_per_step": args.queries, "query_k": args.k, "query_seeds": f"1000..{999 + args.queries}",
+            "graph_seed": 1, "mode": "count-only (final level fused count + fingerprint)",
+            "l2": "inputs larger than L2 (PCSR+signatures >> 126 MB); no flush"}
+
+
+# ------------------------------------------------------------------------ GPU arm --------
+def run_gsi(args):
+    import torch
+    import torch.distributed as dist
+    from paper_1906_03420_b200 import gsi
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+
+    # ---- workload + graph (rank 0 builds; replicas via NCCL broadcast) ----------------
+    if rank == 0:
+        g, qs = make_workload(args.config, args.queries, args.k, "cuda", scale=args.scale)
+        t = time.time()
+        graph = gsi.build(g, device=local)
+        torch.cuda.synchronize()
+        info = graph.info()
+        log(f"[bench] gsi_build_graph {time.time() - t:.2f}s: groups={info['n_groups']} "
+            f"max_chain={info['max_chain']} bytes={info['bytes_total'] / 1e9:.2f} GB")
+    if ws > 1:
+        from paper_1906_03420_b200 import dist as gd
+        t = time.time()
+        if rank == 0:
+            descs, meta = gsi.gsi_graph_buffers(graph)
+            views = [gsi.torch_view(p, b, device=f"cuda:{local}") for (_, p, b) in descs]
+        else:
+            meta, views = None, None
+
+        def alloc_like(m):
+            gr, ds = gsi.gsi_graph_alloc_like(m, device=local)
+            return gr, [gsi.torch_view(p, b, device=f"cuda:{local}") for (_, p, b) in ds]
+
+        other, views, meta = gd.broadcast_graph(meta, views, alloc_like)
+        if rank != 0:
+            graph = other
+        qarr = gd.broadcast_queries([(q.vlabels, q.src, q.dst, q.elabels) for q in qs] + [(g.n, g.m)]
+                                    if rank == 0 else None)
+        if rank != 0:
+            nm = qarr[-1]
+            qs = [W.Query(len(a[0]), *a) for a in qarr[:-1]]
+            g = W.Graph(nm[0], np.zeros(0), np.zeros(nm[1]), np.zeros(nm[1]), np.zeros(nm[1]))
+        torch.cuda.synchronize()
+        if rank == 0:
+            log(f"[bench] NCCL broadcast of the graph {time.time() - t:.2f}s")
+    info = graph.info()
+
+    shard = dict(shard_rank=rank, shard_count=ws) if ws > 1 else {}
+    prepared = [gsi.prepare(graph, q) for q in qs]
+    counts = torch.zeros(len(qs), dtype=torch.int64, device="cuda")
+
+    def step(profile=False, stats=None):
+        for i, p in enumerate(prepared):
+            r = gsi.gsi_query_run(graph, p, stream=sptr, timeout_s=args.query_timeout, profile=profile, **shard)
+            counts[i] = r.count
+            if stats is not None:
+                stats.append(r.stats())
+        if ws > 1:
+            dist.all_reduce(counts)
+        return counts
+
+    def e2e_step():
+        for i, q in enumerate(qs):
+            r = gsi.gsi_query(graph, q.vlabels, q.src, q.dst, q.elabels, stream=sptr,
+                              timeout_s=args.query_timeout, **shard)
+            counts[i] = r.count
+        if ws > 1:
+            dist.all_reduce(counts)
+        return int(counts.sum().item())
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    total_matches = int(step().sum().item())
+
+    # ---- timed region: device-timed, prepared (resident) queries ------------------------
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launch_stats = []
+    with ClockSampler(local) as clk:
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step(stats=launch_stats)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if ws > 1:
+            dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if ws > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    ms_per_step = ms / args.steps
+    value = total_matches * args.steps / (ms / 1000.0)
+    launches = sum(s["total_launches"] for s in launch_stats)
+
+    # ---- e2e: public API from host arrays, H2D of the query + D2H of the count -----------
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        m_e2e = e2e_step()
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    e2e_t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    if ws > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_s = float(e2e_t.item())
+    h2d = sum(4 * q.n + 12 * len(q.src) + 64 * q.n for q in qs)        # query arrays + signatures
+    d2h = sum(8 * q.n + 64 * (2 * q.n + 2) for q in qs)                # |C(u)|, per-level sizes, count
+
+    # ---- profiled pass: per-kernel CUDA-event times + algorithmic bytes -----------------
+    pstats = []
+    step(profile=True, stats=pstats)
+    torch.cuda.synchronize()
+    ms_k = np.zeros(8)
+    bytes_k = np.zeros(8)
+    launches_k = np.zeros(8)
+    for s in pstats:
+        ms_k += np.array(s["ms_kernel"])
+        bytes_k += np.array(s["alg_bytes"])
+        launches_k += np.array(s["launches"])
+    dom = int(np.argmax(ms_k))
+    peak, peak_src = load_peaks()
+    achieved = (bytes_k[dom] / (ms_k[dom] / 1e3)) / 1e9 if ms_k[dom] > 0 else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        tt = json.load(open(tp)).get(args.config, {}).get(gsi.KCLASS[dom])
+        if tt is not None:
+            traffic = tt
+    roofline = {"bound": "hbm", "kernel": f"k_{gsi.KCLASS[dom]}", "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "share_of_step": float(ms_k[dom] / max(ms_k.sum(), 1e-9)),
+                "per_kernel_ms": {gsi.KCLASS[i]: float(ms_k[i]) for i in range(6)},
+                "per_kernel_alg_GBps": {gsi.KCLASS[i]: float(bytes_k[i] / (ms_k[i] / 1e3) / 1e9) if ms_k[i] else 0.0
+                                        for i in range(6)},
+                "launches_per_step": {gsi.KCLASS[i]: int(launches_k[i]) for i in range(6)}}
+
+    if rank != 0:
+        if ws > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    cpu = None
+    if ws == 1 and not args.no_cpu_baseline:
+        import oracle
+        t = time.time()
+        og = oracle.OracleGraph(g)
+        threads = len(os.sched_getaffinity(0))
+        m, s, d, to = oracle_sample(og, qs, args.cpu_budget, args.ref_query_timeout, threads)
+        cpu = {"value": m / s if s > 0 else 0.0, "unit": "matches/s", "cores": threads, "kind": "oracle",
+               "sample": f"first {d} queries of the batch, per-query timeout {args.ref_query_timeout}s "
+                         f"({to} timed out, partial counts kept); {s:.1f}s of CPU work",
+               "ms_per_query": 1000.0 * s / max(d, 1)}
+        log(f"[bench] oracle baseline {time.time() - t:.1f}s incl. index build")
+
+    line = {
+        "metric": "matches/s", "value": value, "unit": "matches/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic", "config": workload_config(args, g),
+        "ms_per_query": ms_per_step / len(qs), "matches_per_step": total_matches,
+        "e2e": {"value": m_e2e * args.steps / e2e_s, "unit": "matches/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_query": 1000.0 * e2e_s / args.steps / len(qs)},
+        "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": launches,
+        "graph": {"n_groups": info["n_groups"], "max_chain": info["max_chain"],
+                  "bytes_total": info["bytes_total"], "build_ms": info["ms_build"]},
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["gsi", "reference"], default="gsi")
+    ap.add_argument("--config", choices=sorted(BENCH_CONFIGS), default="C5b")
+    ap.add_argument("--scale", type=int, default=None, help="override the R-MAT scale (C5 only)")
+    ap.add_argument("--queries", type=int, default=100)
+    ap.add_argument("--k", type=int, default=12)
+    ap.add_argument("--query-timeout", type=float, default=0.0)
+    ap.add_argument("--ref-query-timeout", type=float, default=5.0)
+    ap.add_argument("--ref-step-budget", type=float, default=8.0)
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gsi(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -140,6 +140,10 @@ typedef struct {
     double timeout_s;            /* <= 0: none.  Checked between levels.                        */
     int32_t profile;             /* 1: time every kernel with CUDA events (gsi_stats)          */
     void *stream;                /* cudaStream_t                                               */
+    uint64_t chunk_slots;        /* GBA slots per chunk (0 = derived from the memory budget);
+                                    a level whose |GBA| exceeds it runs depth-first in chunks  */
+    int32_t partial_on_timeout;  /* 1: on timeout return GSI_OK with stats.capped = 1 and the
+                                    exact count of the completed chunk prefix                  */
 } gsi_query_opts;
 
 void gsi_query_opts_default(gsi_query_opts *opts);
@@ -183,6 +187,9 @@ typedef struct {
     uint32_t launches[GSI_N_KCLASS];
     double alg_bytes[GSI_N_KCLASS];
     uint32_t total_launches;          /* kernels this library launched for the query         */
+    uint32_t n_chunks;                /* slot-range chunks executed below the memory budget   */
+    int32_t capped;                   /* 1: timed out with partial_on_timeout                 */
+    uint64_t h2d_bytes, d2h_bytes;    /* host<->device bytes this query copied                */
 } gsi_stats;
 
 gsi_status gsi_result_count(const gsi_result *r, uint64_t *count);

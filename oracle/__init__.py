@@ -97,8 +97,11 @@ class OracleGraph:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
-            lib().og_free(h)
+        if h and _lib is not None:
+            try:
+                _lib.og_free(h)
+            except Exception:
+                pass
             self._h = None
 
     def neighbors(self, v: int, l: int) -> np.ndarray:

@@ -238,7 +238,9 @@ gsi_status gsi_query(const gsi_graph *g, int32_t k, const int32_t *qvl, int32_t 
     gsi_prepared *p = nullptr;
     GSI_TRY(prepare_impl(g, k, qvl, qm, qs, qd, qe, &p));
     std::unique_ptr<gsi_prepared> guard(p);
-    return run_impl(g, p, opts, out);
+    gsi_status rc = run_impl(g, p, opts, out);
+    if (rc == GSI_OK) (*out)->stats.h2d_bytes += 4ull * p->qsig.size();   // encoded Q signatures
+    return rc;
 }
 
 gsi_status gsi_result_count(const gsi_result *r, uint64_t *count) {

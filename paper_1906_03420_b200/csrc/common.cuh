@@ -128,6 +128,42 @@ __device__ __forceinline__ bool probe_group_generic(const uint2 *__restrict__ G,
     return false;
 }
 
+// Sector-wise probe of one GPN=16 group (B200: DRAM/L2 move 32 B sectors, not the 128 B
+// transactions the paper sized the group for).  Pairs 4j..4j+3 form sector j.  A group is
+// prefix-packed and only a FULL group can carry a GID (overflow comes from full home groups
+// and every non-final chain group is full), so an empty slot ends the search.  With |V(D)|
+// keys in |V(D)| groups (one-to-one hash) almost every lookup touches one sector.
+__device__ __forceinline__ int probe_group16_sectored(const uint2 *__restrict__ G, uint32_t v, Loc &out,
+                                                      uint32_t &gid) {
+    const uint4 *G4 = reinterpret_cast<const uint4 *>(G);
+#pragma unroll
+    for (int sec = 0; sec < 4; sec++) {
+        const uint4 a = __ldg(G4 + 2 * sec), b = __ldg(G4 + 2 * sec + 1);
+        const uint32_t vs[4] = {a.x, a.z, b.x, b.z};
+        const uint32_t os[4] = {a.y, a.w, b.y, b.w};
+#pragma unroll
+        for (int s = 0; s < 4; s++) {
+            const int slot = 4 * sec + s;
+            if (slot == 15) {          // trailer (GID, END)
+                gid = vs[s];
+                return 0;
+            }
+            if (vs[s] == v) {
+                out.off = os[s];
+                if (s < 3) out.len = os[s + 1] - os[s];
+                else out.len = __ldg(G + slot + 1).y - os[s];
+                return 1;
+            }
+            if (vs[s] == kEmpty) {
+                gid = kEmpty;
+                return 0;
+            }
+        }
+    }
+    gid = kEmpty;
+    return 0;
+}
+
 // N(v, l) for dense label l: (offset into ci, length); len = 0 if v is not in P(G,l).
 // *groups_read counts the groups visited (follow GID until found or -1).
 __device__ __forceinline__ Loc pcsr_lookup(const uint2 *__restrict__ groups, int gpn, uint64_t gbase,
@@ -141,7 +177,7 @@ __device__ __forceinline__ Loc pcsr_lookup(const uint2 *__restrict__ groups, int
         uint32_t gid = kEmpty;
         bool hit;
         reads++;
-        if (gpn == 16) hit = probe_group<16>(G, v, r, gid);
+        if (gpn == 16) hit = probe_group16_sectored(G, v, r, gid);
         else if (gpn == 8) hit = probe_group<8>(G, v, r, gid);
         else hit = probe_group_generic(G, gpn, v, r, gid);
         if (hit || gid == kEmpty) break;

@@ -607,6 +607,15 @@ struct Prof {
     }
 };
 
+cudaError_t d2h(gsi_stats &S, void *dst, const void *src, size_t bytes, cudaStream_t st) {
+    S.d2h_bytes += bytes;
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st);
+}
+cudaError_t h2d(gsi_stats &S, void *dst, const void *src, size_t bytes, cudaStream_t st) {
+    S.h2d_bytes += bytes;
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
+}
+
 double now_ms() {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -819,24 +828,225 @@ static gsi_status build_steps(const gsi_prepared *q, const std::vector<int> &ord
 }
 
 // ------------------------------------------------------------------ run -----------
+// One query = filter -> plan -> level 1 -> recursive levels.  A level whose Prealloc bound
+// |GBA| exceeds the chunk capacity is processed as consecutive slot ranges, each carried
+// depth-first to the last level (the bound F is exact before the join runs, so the chunk
+// sizes are known in advance; memory <= depth x chunk).  Chunks are taken in slot order,
+// so the concatenated output keeps the 1-GPU row order.  Sharding cuts
+// the slot range of one level by F into W contiguous pieces; rank r keeps piece r.
+namespace {
+
+struct QueryCtx {
+    const gsi_graph *g = nullptr;
+    const gsi_prepared *q = nullptr;
+    gsi_query_opts opts;
+    cudaStream_t st = nullptr;
+    Arena *A = nullptr;
+    Prof *prof = nullptr;
+    Counters *ctr = nullptr;
+    gsi_stats *S = nullptr;
+    const uint32_t *bm = nullptr;
+    long long words = 0;
+    std::vector<Step> steps;
+    std::vector<int> order, pos_of_q;
+    int W = 1, rank = 0;
+    bool sharded = true;
+    unsigned long long shard_min = 65536;
+    unsigned long long cap_slots = 0;
+    double deadline = 0;
+    bool capped = false;
+    unsigned long long count = 0, fp1 = 0, fp2 = 0;
+    std::vector<std::pair<int32_t *, unsigned long long>> pieces;   // final table pieces (device)
+};
+
+void fill_params(QueryCtx &C, const Step &s, StepParams &P) {
+    const gsi_graph *g = C.g;
+    std::memset(&P, 0, sizeof(P));
+    const int E = (int)s.col.size();
+    P.t = s.t;
+    P.E = E;
+    P.k = C.q->k;
+    P.per_row_e0 = C.opts.e0_mode == 0 ? 1 : 0;
+    for (int qv = 0; qv < C.q->k; qv++) P.pos_of_q[qv] = C.pos_of_q[qv];
+    std::vector<int> eorder(E);
+    for (int e = 0; e < E; e++) eorder[e] = e;
+    std::swap(eorder[0], eorder[s.paper_e0]);   // paper mode: e0 first (Alg. 3 line 9)
+    for (int e = 0; e < E; e++) {
+        int src = eorder[e];
+        P.col[e] = s.col[src];
+        P.lab[e] = (uint32_t)s.lab[src];
+        P.gbase[e] = (unsigned long long)g->gbase[s.lab[src]];
+        P.ngroups[e] = g->ngroups[s.lab[src]];
+    }
+    P.n_inj = 0;
+    if (!C.opts.homomorphism) {
+        for (int c = 0; c < s.t; c++) {
+            if (C.q->qvl[C.order[c]] != C.q->qvl[s.u]) continue;   // different label: C(u) excludes it
+            bool linked = false;
+            for (int e = 0; e < E; e++) linked |= P.col[e] == c;    // x in N(m[c],l) => x != m[c]
+            if (!linked) P.inj_col[P.n_inj++] = c;
+        }
+    }
+}
+
+gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM) {
+    const Step &s = C.steps[si];
+    const int t = s.t;
+    const bool last = si + 1 == C.steps.size();
+    gsi_stats &S = *C.S;
+    Arena &A = *C.A;
+    Prof &prof = *C.prof;
+    cudaStream_t st = C.st;
+    const gsi_graph *g = C.g;
+    StepParams P;
+    fill_params(C, s, P);
+    const int E = P.E;
+    S.rows[t - 1] += nM;
+    if (S.levels < t) S.levels = t;
+    if (nM == 0) return GSI_OK;
+
+    // ---- probe + Prealloc scan (a6) ----
+    Loc *loc = nullptr;
+    unsigned long long *F = nullptr, *status = nullptr;
+    GSI_TRY(A.get(&loc, nM * (unsigned long long)E));
+    GSI_TRY(A.get(&F, nM + 1));
+    const unsigned ptiles = grid_for(nM, kThreads);
+    GSI_TRY(A.get(&status, ptiles + 1));
+    GSI_CUDA(cudaMemsetAsync(status, 0, 8ull * (ptiles + 1), st));
+    GSI_CUDA(cudaMemsetAsync(C.ctr, 0, sizeof(Counters), st));
+    prof.begin(GSI_K_PROBE);
+    k_probe<<<ptiles, kThreads, 0, st>>>(M, (long long)nM, P, g->groups, g->gpn, loc, F, status + 1,
+                                         (unsigned *)status, C.ctr);
+    prof.end();
+    Counters hc;
+    unsigned long long gba = 0;
+    GSI_CUDA(d2h(S, &gba, F + nM, 8, st));
+    GSI_CUDA(d2h(S, &hc, C.ctr, sizeof(Counters), st));
+    GSI_CUDA(cudaStreamSynchronize(st));
+    A.release(status);
+    S.gba[t] += gba;
+    S.list_elems[t] += hc.list_elems;
+    S.alg_bytes[GSI_K_PROBE] += (double)nM * (20.0 * E + 8.0);
+    const unsigned long long active = hc.active_rows, elems = hc.list_elems;
+
+    // ---- shard this level's slot range ----
+    unsigned long long s0 = 0, s1 = gba;
+    if (!C.sharded && (nM >= C.shard_min || gba > C.cap_slots || last)) {
+        long long *bounds = nullptr;
+        GSI_TRY(A.get(&bounds, 4));
+        prof.begin(GSI_K_OTHER);
+        k_shard_bounds<<<1, 32, 0, st>>>(F, (long long)nM, C.rank, C.W, bounds);
+        prof.end();
+        long long hb[4];
+        GSI_CUDA(d2h(S, hb, bounds, sizeof(hb), st));
+        GSI_CUDA(cudaStreamSynchronize(st));
+        A.release(bounds);
+        s0 = (unsigned long long)hb[2];
+        s1 = (unsigned long long)hb[3];
+        S.shard_level = t;
+        S.shard_row_begin = (uint64_t)hb[0];
+        S.shard_row_end = (uint64_t)hb[1];
+        C.sharded = true;
+    }
+
+    const bool write = !last || C.opts.want_table;
+    const unsigned long long chunk = write ? std::max<unsigned long long>(C.cap_slots, kJoinTile) : (s1 - s0);
+    gsi_status rc = GSI_OK;
+    for (unsigned long long c0 = s0; c0 < s1 && rc == GSI_OK; c0 += chunk) {
+        if (C.deadline > 0 && now_ms() > C.deadline) {
+            C.capped = true;
+            break;
+        }
+        const unsigned long long c1 = std::min(s1, c0 + chunk), slots = c1 - c0;
+        if (c0 != s0 || c1 != s1) S.n_chunks++;
+        const unsigned jt = grid_for(slots, kJoinTile);
+        uint32_t *Sv = nullptr, *Rv = nullptr;
+        GSI_TRY(A.get(&status, jt + 1));
+        GSI_CUDA(cudaMemsetAsync(status, 0, 8ull * (jt + 1), st));
+        GSI_CUDA(cudaMemsetAsync(C.ctr, 0, sizeof(Counters), st));
+        if (write) {
+            GSI_TRY(A.get(&Sv, slots));
+            GSI_TRY(A.get(&Rv, slots));
+        }
+        const uint32_t *cu = C.bm + (long long)s.u * C.words;
+        prof.begin(GSI_K_JOIN);
+        if (write && last)
+            k_join<true, true><<<jt, kThreads, 0, st>>>(M, (long long)nM, F, loc, P, g->ci, cu, c0, c1, Sv, Rv,
+                                                        status + 1, (unsigned *)status, C.ctr);
+        else if (write)
+            k_join<true, false><<<jt, kThreads, 0, st>>>(M, (long long)nM, F, loc, P, g->ci, cu, c0, c1, Sv, Rv,
+                                                         status + 1, (unsigned *)status, C.ctr);
+        else
+            k_join<false, true><<<jt, kThreads, 0, st>>>(M, (long long)nM, F, loc, P, g->ci, cu, c0, c1, Sv, Rv,
+                                                         status + 1, (unsigned *)status, C.ctr);
+        prof.end();
+        GSI_CUDA(d2h(S, &hc, C.ctr, sizeof(Counters), st));
+        GSI_CUDA(cudaStreamSynchronize(st));
+        GSI_CUDA(cudaGetLastError());
+        A.release(status);
+        const unsigned long long nout = write ? hc.total : hc.count;
+        const double frac = gba ? (double)slots / (double)gba : 0.0;
+        S.alg_bytes[GSI_K_JOIN] +=
+            frac * (4.0 * t * active + 4.0 * elems + (8.0 * E + 8.0) * active) + (write ? 8.0 * nout : 0.0);
+        if (last) {
+            C.count += nout;
+            C.fp1 += hc.fp1;
+            C.fp2 ^= hc.fp2;
+            S.rows[t] += nout;
+            if (S.levels < t + 1) S.levels = t + 1;
+        }
+        if (write && nout) {
+            const unsigned long long nint = nout * (unsigned long long)(t + 1);
+            int32_t *M2 = nullptr;
+            if (last) {
+                GSI_CUDA(cudaMallocAsync(&M2, 4ull * nint, st));
+                C.pieces.push_back({M2, nout});
+            } else {
+                GSI_TRY(A.get(&M2, nint));
+            }
+            const unsigned lg = grid_for(nint, kThreads * 4);
+            prof.begin(GSI_K_LINK);
+            if (last) k_link<true><<<lg, kThreads, 0, st>>>(M, t, Sv, Rv, nout, P, M2);
+            else k_link<false><<<lg, kThreads, 0, st>>>(M, t, Sv, Rv, nout, P, M2);
+            prof.end();
+            S.alg_bytes[GSI_K_LINK] += (double)nout * (4.0 * (t + 1) + 4.0 * t + 8.0);
+            A.release(Sv);
+            A.release(Rv);
+            if (!last) {
+                rc = level(C, si + 1, M2, nout);
+                A.release(M2);
+            }
+        } else {
+            A.release(Sv);
+            A.release(Rv);
+        }
+    }
+    A.release(loc);
+    A.release(F);
+    return rc;
+}
+
+}  // namespace
+
 gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_opts *opts_in, gsi_result **out) {
     *out = nullptr;
     if (!g || !q || q->g != g) {
         set_error("prepared query does not belong to this graph");
         return GSI_ERR_INVALID_ARG;
     }
-    gsi_query_opts opts;
-    gsi_query_opts_default(&opts);
-    if (opts_in) opts = *opts_in;
+    QueryCtx C;
+    gsi_query_opts_default(&C.opts);
+    if (opts_in) C.opts = *opts_in;
+    const gsi_query_opts &opts = C.opts;
     const double t_start = now_ms();
     GSI_CUDA(cudaSetDevice(g->device));
     cudaStream_t st = opts.stream ? (cudaStream_t)opts.stream : cudaStreamPerThread;
     const int k = q->k;
     const long long n = g->n;
     const long long words = (n + 31) / 32;
-    const int W = opts.shard_count > 1 ? opts.shard_count : 1;
-    const int rank = W > 1 ? opts.shard_rank : 0;
-    if (rank < 0 || rank >= W) {
+    C.W = opts.shard_count > 1 ? opts.shard_count : 1;
+    C.rank = C.W > 1 ? opts.shard_rank : 0;
+    if (C.rank < 0 || C.rank >= C.W) {
         set_error("shard_rank out of range");
         return GSI_ERR_INVALID_ARG;
     }
@@ -851,10 +1061,16 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     Prof prof;
     prof.on = opts.profile != 0;
     prof.st = st;
+    C.g = g;
+    C.q = q;
+    C.st = st;
+    C.A = &A;
+    C.prof = &prof;
+    C.S = &S;
+    C.words = words;
 
-    Counters *ctr = nullptr;
-    GSI_TRY(A.get(&ctr, 1));
-    GSI_CUDA(cudaMemsetAsync(ctr, 0, sizeof(Counters), st));
+    GSI_TRY(A.get(&C.ctr, 1));
+    GSI_CUDA(cudaMemsetAsync(C.ctr, 0, sizeof(Counters), st));
 
     // ---------------- filter (a3) ----------------
     uint32_t *bm = nullptr;
@@ -862,19 +1078,21 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     GSI_TRY(A.get(&bm, (unsigned long long)words * k));
     GSI_TRY(A.get(&d_counts, k));
     GSI_CUDA(cudaMemsetAsync(d_counts, 0, 8ull * k, st));
+    C.bm = bm;
     {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
         unsigned grid = (unsigned)std::min<long long>((words + 7) / 8, (long long)sms * 8);
         if (grid < 1) grid = 1;
         prof.begin(GSI_K_FILTER);
-        k_filter<<<grid, kThreads, 0, st>>>(g->sig, n, k, q->d_qsig, opts.filter_mode == 1, bm, words, d_counts, ctr);
+        k_filter<<<grid, kThreads, 0, st>>>(g->sig, n, k, q->d_qsig, opts.filter_mode == 1, bm, words, d_counts,
+                                            C.ctr);
         prof.end();
     }
     std::vector<long long> cand(k);
     Counters hc;
-    GSI_CUDA(cudaMemcpyAsync(cand.data(), d_counts, 8ull * k, cudaMemcpyDeviceToHost, st));
-    GSI_CUDA(cudaMemcpyAsync(&hc, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+    GSI_CUDA(d2h(S, cand.data(), d_counts, 8ull * k, st));
+    GSI_CUDA(d2h(S, &hc, C.ctr, sizeof(Counters), st));
     GSI_CUDA(cudaStreamSynchronize(st));
     GSI_CUDA(cudaGetLastError());
     const double t_filter = now_ms();
@@ -883,66 +1101,63 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     S.alg_bytes[GSI_K_FILTER] = 4.0 * n + 60.0 * hc.plane_loads + 4.0 * words * k;
 
     // ---------------- plan (a4) ----------------
-    std::vector<int> order;
-    GSI_TRY(plan_order(q, cand, opts.force_order, order));
-    std::vector<Step> steps;
-    GSI_TRY(build_steps(q, order, opts.force_first_edge, steps));
-    for (int j = 0; j < k; j++) S.order[j] = order[j];
-    for (auto &s : steps) {
+    GSI_TRY(plan_order(q, cand, opts.force_order, C.order));
+    GSI_TRY(build_steps(q, C.order, opts.force_first_edge, C.steps));
+    for (int j = 0; j < k; j++) S.order[j] = C.order[j];
+    for (auto &s : C.steps) {
         S.n_edges[s.t] = (int)s.col.size();
         S.first_edge[s.t] = s.other[s.paper_e0];
     }
-    std::vector<int> pos_of_q(k);
-    for (int j = 0; j < k; j++) pos_of_q[order[j]] = j;
+    C.pos_of_q.assign(k, 0);
+    for (int j = 0; j < k; j++) C.pos_of_q[C.order[j]] = j;
     const double t_plan = now_ms();
     S.ms_plan = (float)(t_plan - t_filter);
+
+    // memory budget -> chunk capacity in GBA slots (bytes per slot per level: S,R 8 B,
+    // M' 4(t+1) B, the child level's loc/F 8E+8 B), over the k-1 levels that may nest.
+    {
+        size_t fr = 0, tot = 0;
+        GSI_CUDA(cudaMemGetInfo(&fr, &tot));
+        unsigned long long budget = opts.mem_budget_bytes ? opts.mem_budget_bytes : (unsigned long long)(0.85 * fr);
+        int maxE = 1;
+        for (auto &s : C.steps) maxE = std::max(maxE, (int)s.col.size());
+        const double per_slot = 8.0 + 4.0 * (k + 1) + 8.0 * maxE + 8.0;
+        const double levels = std::max(1, k - 1);
+        C.cap_slots = (unsigned long long)std::max(1.0, budget / (per_slot * levels));
+        if (opts.chunk_slots) C.cap_slots = opts.chunk_slots;
+    }
+    C.shard_min = opts.shard_min_rows ? opts.shard_min_rows : 65536;
+    C.sharded = C.W == 1;
+    C.deadline = opts.timeout_s > 0 ? t_start + 1000.0 * opts.timeout_s : 0;
 
     bool empty = q->absent_label;
     for (int u = 0; u < k; u++) empty |= cand[u] == 0;
 
-    auto finish = [&](gsi_status st_code) -> gsi_status {
-        if (st_code != GSI_OK) return st_code;
-        cudaError_t e = cudaStreamSynchronize(st);
-        if (e != cudaSuccess) return cuda_fail(e, "query sync");
-        prof.finish(&S);
-        S.count = res->count;
-        S.ms_join = (float)(now_ms() - t_plan);
-        S.ms_total = (float)(now_ms() - t_start);
-        *out = res.release();
-        return GSI_OK;
-    };
-    if (empty) {
-        res->count = 0;
-        res->has_table = opts.want_table != 0;
-        return finish(GSI_OK);
-    }
-
     // ---------------- level 1 (a5) ----------------
-    auto bitmap_of = [&](int u) { return bm + (long long)u * words; };
     int32_t *M = nullptr;
     unsigned long long nM = 0;
-    {
+    if (!empty) {
         unsigned long long *status = nullptr;
-        const int u1 = order[0];
+        const int u1 = C.order[0];
+        const uint32_t *bm1 = bm + (long long)u1 * words;
         if (opts.roots && opts.n_roots > 0) {
             std::vector<int32_t> roots(opts.roots, opts.roots + opts.n_roots);
             std::sort(roots.begin(), roots.end());
             roots.erase(std::unique(roots.begin(), roots.end()), roots.end());
-            while (!roots.empty() && roots.back() >= n) roots.pop_back();
-            while (!roots.empty() && roots.front() < 0) roots.erase(roots.begin());
+            roots.erase(std::remove_if(roots.begin(), roots.end(), [&](int32_t v) { return v < 0 || v >= n; }),
+                        roots.end());
             long long nr = (long long)roots.size();
             int32_t *d_roots = nullptr;
             GSI_TRY(A.get(&d_roots, nr));
-            if (nr) GSI_CUDA(cudaMemcpyAsync(d_roots, roots.data(), 4ull * nr, cudaMemcpyHostToDevice, st));
+            if (nr) GSI_CUDA(h2d(S, d_roots, roots.data(), 4ull * nr, st));
             GSI_TRY(A.get(&M, nr));
             unsigned tiles = grid_for(nr, kThreads);
             GSI_TRY(A.get(&status, tiles + 1));
             GSI_CUDA(cudaMemsetAsync(status, 0, 8ull * (tiles + 1), st));
             prof.begin(GSI_K_COMPACT);
-            k_compact_roots<<<tiles, kThreads, 0, st>>>(d_roots, nr, bitmap_of(u1), M, status + 1,
-                                                        (unsigned *)status, ctr);
+            k_compact_roots<<<tiles, kThreads, 0, st>>>(d_roots, nr, bm1, M, status + 1, (unsigned *)status, C.ctr);
             prof.end();
-            GSI_CUDA(cudaMemcpyAsync(&hc, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+            GSI_CUDA(d2h(S, &hc, C.ctr, sizeof(Counters), st));
             GSI_CUDA(cudaStreamSynchronize(st));
             nM = hc.total;
             S.alg_bytes[GSI_K_COMPACT] += 8.0 * nr + 4.0 * nM;
@@ -953,212 +1168,83 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
             GSI_TRY(A.get(&status, tiles + 1));
             GSI_CUDA(cudaMemsetAsync(status, 0, 8ull * (tiles + 1), st));
             prof.begin(GSI_K_COMPACT);
-            k_compact_bitmap<<<tiles, kThreads, 0, st>>>(bitmap_of(u1), words, M, status + 1, (unsigned *)status,
-                                                         ctr);
+            k_compact_bitmap<<<tiles, kThreads, 0, st>>>(bm1, words, M, status + 1, (unsigned *)status, C.ctr);
             prof.end();
             S.alg_bytes[GSI_K_COMPACT] += 4.0 * words + 4.0 * nM;
         }
         A.release(status);
     }
-    S.rows[0] = nM;
-    S.levels = 1;
 
-    StepParams P;
-    std::memset(&P, 0, sizeof(P));
-    P.k = k;
-    for (int qv = 0; qv < k; qv++) P.pos_of_q[qv] = pos_of_q[qv];
-
-    if (k == 1) {
+    gsi_status rc = GSI_OK;
+    if (!empty && k == 1) {
+        S.rows[0] = nM;
+        S.levels = 1;
+        StepParams P;
+        std::memset(&P, 0, sizeof(P));
+        P.k = 1;
         P.t = 1;
-        GSI_CUDA(cudaMemsetAsync(ctr, 0, sizeof(Counters), st));
+        GSI_CUDA(cudaMemsetAsync(C.ctr, 0, sizeof(Counters), st));
         if (nM) {
             prof.begin(GSI_K_OTHER);
-            k_fp_rows<<<grid_for(nM, kThreads), kThreads, 0, st>>>(M, (long long)nM, P, ctr);
+            k_fp_rows<<<grid_for(nM, kThreads), kThreads, 0, st>>>(M, (long long)nM, P, C.ctr);
             prof.end();
         }
-        GSI_CUDA(cudaMemcpyAsync(&hc, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+        GSI_CUDA(d2h(S, &hc, C.ctr, sizeof(Counters), st));
         GSI_CUDA(cudaStreamSynchronize(st));
-        res->count = nM;
-        res->fp[0] = nM;
-        res->fp[1] = hc.fp1;
-        res->fp[2] = hc.fp2;
-        if (opts.want_table) {
-            res->has_table = true;
-            res->nrows = nM;
-            GSI_CUDA(cudaMalloc(&res->table, 4ull * (nM ? nM : 1)));
-            if (nM) GSI_CUDA(cudaMemcpyAsync(res->table, M, 4ull * nM, cudaMemcpyDeviceToDevice, st));
+        C.count = nM;
+        C.fp1 = hc.fp1;
+        C.fp2 = hc.fp2;
+        if (opts.want_table && nM) {
+            int32_t *T = nullptr;
+            GSI_CUDA(cudaMallocAsync(&T, 4ull * nM, st));
+            GSI_CUDA(cudaMemcpyAsync(T, M, 4ull * nM, cudaMemcpyDeviceToDevice, st));
+            C.pieces.push_back({T, nM});
         }
-        return finish(GSI_OK);
+    } else if (!empty) {
+        rc = level(C, 0, M, nM);
     }
-
-    const uint64_t shard_min = opts.shard_min_rows ? opts.shard_min_rows : 65536;
-    bool sharded = W == 1;
-    const double deadline = opts.timeout_s > 0 ? t_start + 1000.0 * opts.timeout_s : 0;
-
-    for (size_t si = 0; si < steps.size(); si++) {
-        const Step &s = steps[si];
-        const int t = s.t;
-        const bool last = si + 1 == steps.size();
-        if (deadline > 0 && now_ms() > deadline) {
-            set_error("query timeout");
-            return GSI_ERR_TIMEOUT;
-        }
-        // ---- step parameters ----
-        const int E = (int)s.col.size();
-        P.t = t;
-        P.E = E;
-        P.per_row_e0 = opts.e0_mode == 0 ? 1 : 0;
-        // paper mode: e0 first
-        std::vector<int> eorder(E);
-        for (int e = 0; e < E; e++) eorder[e] = e;
-        std::swap(eorder[0], eorder[s.paper_e0]);
-        for (int e = 0; e < E; e++) {
-            int src = eorder[e];
-            P.col[e] = s.col[src];
-            P.lab[e] = (uint32_t)s.lab[src];
-            P.gbase[e] = (unsigned long long)g->gbase[s.lab[src]];
-            P.ngroups[e] = g->ngroups[s.lab[src]];
-        }
-        P.n_inj = 0;
-        if (!opts.homomorphism) {
-            for (int c = 0; c < t; c++) {
-                if (q->qvl[order[c]] != q->qvl[s.u]) continue;   // different label: C(u) excludes it
-                bool linked = false;
-                for (int e = 0; e < E; e++) linked |= P.col[e] == c;   // x in N(m[c],l) => x != m[c]
-                if (!linked) P.inj_col[P.n_inj++] = c;
+    if (M) A.release(M);
+    if (rc != GSI_OK) {
+        for (auto &p : C.pieces) cudaFreeAsync(p.first, st);
+        cudaStreamSynchronize(st);
+        return rc;
+    }
+    if (C.capped && !opts.partial_on_timeout) {
+        for (auto &p : C.pieces) cudaFreeAsync(p.first, st);
+        cudaStreamSynchronize(st);
+        set_error("query timeout");
+        return GSI_ERR_TIMEOUT;
+    }
+    // ---------------- finalize (a9) ----------------
+    res->count = C.count;
+    res->fp[0] = C.count;
+    res->fp[1] = C.fp1;
+    res->fp[2] = C.fp2;
+    S.capped = C.capped ? 1 : 0;
+    if (opts.want_table) {
+        res->has_table = true;
+        res->nrows = C.count;
+        if (C.pieces.size() == 1) {
+            res->table = C.pieces[0].first;
+        } else if (!C.pieces.empty()) {
+            GSI_CUDA(cudaMallocAsync(&res->table, 4ull * C.count * k, st));
+            unsigned long long off = 0;
+            for (auto &p : C.pieces) {
+                GSI_CUDA(cudaMemcpyAsync(res->table + off * k, p.first, 4ull * p.second * k,
+                                         cudaMemcpyDeviceToDevice, st));
+                off += p.second;
+                cudaFreeAsync(p.first, st);
             }
         }
-        // ---- probe + Prealloc scan (a6) ----
-        Loc *loc = nullptr;
-        unsigned long long *F = nullptr, *status = nullptr;
-        GSI_TRY(A.get(&loc, nM * (unsigned long long)E));
-        GSI_TRY(A.get(&F, nM + 1));
-        unsigned ptiles = grid_for(nM, kThreads);
-        GSI_TRY(A.get(&status, ptiles + 1));
-        GSI_CUDA(cudaMemsetAsync(status, 0, 8ull * (ptiles + 1), st));
-        GSI_CUDA(cudaMemsetAsync(ctr, 0, sizeof(Counters), st));
-        if (nM == 0) GSI_CUDA(cudaMemsetAsync(F, 0, 8, st));
-        else {
-            prof.begin(GSI_K_PROBE);
-            k_probe<<<ptiles, kThreads, 0, st>>>(M, (long long)nM, P, g->groups, g->gpn, loc, F, status + 1,
-                                                 (unsigned *)status, ctr);
-            prof.end();
-        }
-        unsigned long long gba = 0;
-        GSI_CUDA(cudaMemcpyAsync(&gba, F + nM, 8, cudaMemcpyDeviceToHost, st));
-        GSI_CUDA(cudaMemcpyAsync(&hc, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
-        GSI_CUDA(cudaStreamSynchronize(st));
-        A.release(status);
-        S.gba[t] = gba;
-        S.list_elems[t] = hc.list_elems;
-        S.alg_bytes[GSI_K_PROBE] += (double)nM * (20.0 * E + 8.0);
-        const unsigned long long active = hc.active_rows, elems = hc.list_elems;
-
-        // ---- shard the rows of this level ----
-        unsigned long long s0 = 0, s1 = gba;
-        if (!sharded && (nM >= shard_min || last)) {
-            long long *bounds = nullptr;
-            GSI_TRY(A.get(&bounds, 4));
-            prof.begin(GSI_K_OTHER);
-            k_shard_bounds<<<1, 32, 0, st>>>(F, (long long)nM, rank, W, bounds);
-            prof.end();
-            long long hb[4];
-            GSI_CUDA(cudaMemcpyAsync(hb, bounds, sizeof(hb), cudaMemcpyDeviceToHost, st));
-            GSI_CUDA(cudaStreamSynchronize(st));
-            s0 = (unsigned long long)hb[2];
-            s1 = (unsigned long long)hb[3];
-            S.shard_level = t;
-            S.shard_row_begin = (uint64_t)hb[0];
-            S.shard_row_end = (uint64_t)hb[1];
-            sharded = true;
-        }
-
-        // ---- join (a7) + combine (a8) ----
-        const unsigned long long slots = s1 - s0;
-        const bool write = !last || opts.want_table;
-        uint32_t *Sv = nullptr, *Rv = nullptr;
-        unsigned long long nout = 0;
-        GSI_CUDA(cudaMemsetAsync(ctr, 0, sizeof(Counters), st));
-        if (slots > 0) {
-            unsigned jt = grid_for(slots, kJoinTile);
-            GSI_TRY(A.get(&status, jt + 1));
-            GSI_CUDA(cudaMemsetAsync(status, 0, 8ull * (jt + 1), st));
-            if (write) {
-                GSI_TRY(A.get(&Sv, slots));
-                GSI_TRY(A.get(&Rv, slots));
-            }
-            prof.begin(GSI_K_JOIN);
-            if (write && last)
-                k_join<true, true><<<jt, kThreads, 0, st>>>(M, (long long)nM, F, loc, P, g->ci, bitmap_of(s.u), s0,
-                                                            s1, Sv, Rv, status + 1, (unsigned *)status, ctr);
-            else if (write)
-                k_join<true, false><<<jt, kThreads, 0, st>>>(M, (long long)nM, F, loc, P, g->ci, bitmap_of(s.u),
-                                                             s0, s1, Sv, Rv, status + 1, (unsigned *)status, ctr);
-            else
-                k_join<false, true><<<jt, kThreads, 0, st>>>(M, (long long)nM, F, loc, P, g->ci, bitmap_of(s.u),
-                                                             s0, s1, Sv, Rv, status + 1, (unsigned *)status, ctr);
-            prof.end();
-            GSI_CUDA(cudaMemcpyAsync(&hc, ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
-            GSI_CUDA(cudaStreamSynchronize(st));
-            GSI_CUDA(cudaGetLastError());
-            A.release(status);
-            nout = write ? hc.total : hc.count;
-        } else {
-            std::memset(&hc, 0, sizeof(hc));
-        }
-        // algorithmic bytes of the join over the rows it touched
-        {
-            double frac = gba ? (double)slots / (double)gba : 0.0;
-            S.alg_bytes[GSI_K_JOIN] += frac * (4.0 * t * active + 4.0 * elems + (8.0 * E + 8.0) * active) +
-                                       (write ? 8.0 * nout : 0.0);
-        }
-        if (last) {
-            res->count = nout;
-            res->fp[0] = nout;
-            res->fp[1] = hc.fp1;
-            res->fp[2] = hc.fp2;
-        }
-        A.release(loc);
-        A.release(F);
-        S.rows[t] = nout;
-        S.levels = t + 1;
-        if (!write) {
-            A.release(M);
-            break;
-        }
-        // link
-        int32_t *M2 = nullptr;
-        const unsigned long long nint = nout * (unsigned long long)(t + 1);
-        if (last) {
-            GSI_CUDA(cudaMalloc(&res->table, 4ull * (nint ? nint : 1)));
-            M2 = res->table;
-            res->has_table = true;
-            res->nrows = nout;
-        } else {
-            GSI_TRY(A.get(&M2, nint));
-        }
-        if (nout) {
-            unsigned lg = grid_for(nint, kThreads * 4);
-            prof.begin(GSI_K_LINK);
-            if (last) k_link<true><<<lg, kThreads, 0, st>>>(M, t, Sv, Rv, nout, P, M2);
-            else k_link<false><<<lg, kThreads, 0, st>>>(M, t, Sv, Rv, nout, P, M2);
-            prof.end();
-            S.alg_bytes[GSI_K_LINK] += (double)nout * (4.0 * (t + 1) + 4.0 * t + 8.0);
-        }
-        A.release(Sv);
-        A.release(Rv);
-        A.release(M);
-        M = M2;
-        nM = nout;
-        if (nM == 0 && !last) {
-            // nothing survives: the remaining levels are empty
-            res->count = 0;
-            res->fp[0] = res->fp[1] = res->fp[2] = 0;
-            res->has_table = opts.want_table != 0;
-            break;
-        }
+        C.pieces.clear();
     }
-    return finish(GSI_OK);
+    GSI_CUDA(cudaStreamSynchronize(st));
+    prof.finish(&S);
+    S.count = res->count;
+    S.ms_join = (float)(now_ms() - t_plan);
+    S.ms_total = (float)(now_ms() - t_start);
+    *out = res.release();
+    return GSI_OK;
 }
 
 }  // namespace gsi

@@ -41,7 +41,8 @@ class gsi_query_opts(ctypes.Structure):
     _fields_ = [("want_table", I32), ("homomorphism", I32), ("filter_mode", I32), ("e0_mode", I32),
                 ("force_order", P), ("force_first_edge", P), ("roots", P), ("n_roots", I64),
                 ("shard_rank", I32), ("shard_count", I32), ("shard_min_rows", U64),
-                ("mem_budget_bytes", U64), ("timeout_s", ctypes.c_double), ("profile", I32), ("stream", P)]
+                ("mem_budget_bytes", U64), ("timeout_s", ctypes.c_double), ("profile", I32), ("stream", P),
+                ("chunk_slots", U64), ("partial_on_timeout", I32)]
 
 
 class gsi_graph_info(ctypes.Structure):
@@ -62,7 +63,8 @@ class gsi_stats(ctypes.Structure):
                 ("ms_total", ctypes.c_float), ("ms_filter", ctypes.c_float), ("ms_plan", ctypes.c_float),
                 ("ms_join", ctypes.c_float), ("ms_kernel", ctypes.c_float * GSI_N_KCLASS),
                 ("launches", U32 * GSI_N_KCLASS), ("alg_bytes", ctypes.c_double * GSI_N_KCLASS),
-                ("total_launches", U32)]
+                ("total_launches", U32), ("n_chunks", U32), ("capped", I32), ("h2d_bytes", U64),
+                ("d2h_bytes", U64)]
 
 
 _SIGS = {
@@ -253,7 +255,8 @@ class Prepared:
 
 def _opts(want_table=False, homomorphism=False, filter_mode=0, e0_mode=0, force_order=None,
           force_first_edge=None, roots=None, shard_rank=0, shard_count=1, shard_min_rows=0,
-          mem_budget_bytes=0, timeout_s=0.0, profile=False, stream=None):
+          mem_budget_bytes=0, timeout_s=0.0, profile=False, stream=None, chunk_slots=0,
+          partial_on_timeout=False):
     o = gsi_query_opts()
     lib.gsi_query_opts_default(ctypes.byref(o))
     keep = []
@@ -267,6 +270,7 @@ def _opts(want_table=False, homomorphism=False, filter_mode=0, e0_mode=0, force_
     o.shard_rank, o.shard_count, o.shard_min_rows = shard_rank, shard_count, shard_min_rows
     o.mem_budget_bytes, o.timeout_s, o.profile = mem_budget_bytes, timeout_s, int(profile)
     o.stream = stream
+    o.chunk_slots, o.partial_on_timeout = chunk_slots, int(partial_on_timeout)
     return o, keep
 
 

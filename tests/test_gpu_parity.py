@@ -39,6 +39,24 @@ def strictly_increasing_in_order(tab: np.ndarray, order) -> bool:
     return bool(anyd.all() and (a[idx, first] < b[idx, first]).all())
 
 
+def bounded_queries(g, og, k, seeds, lo=1, hi=2_000_000, want=None):
+    """Random-walk queries whose oracle count is in [lo, hi] (so both sides can materialise
+    the table); selection uses only the oracle."""
+    out = []
+    adj = W._Adj(g)
+    for s in seeds:
+        q = W.random_walk_query(g, k(s) if callable(k) else k, s, adj)
+        try:
+            c = oracle.match(og, q, table=False, timeout=5.0)[0]
+        except oracle.OracleError:
+            continue
+        if lo <= c <= hi:
+            out.append(q)
+        if want and len(out) >= want:
+            break
+    return out
+
+
 def run_both(g, q, graph=None, og=None, **kw):
     graph = graph or gsi.build(g)
     og = og or oracle.OracleGraph(g)
@@ -190,16 +208,31 @@ def test_tiny_random_vs_oracle():
 @pytest.mark.parametrize("seed", [1, 2, 3])
 def test_medium_random_walk_queries(seed):
     """Power-law graphs with several tiles of rows and ragged tails; exact sorted tables."""
-    g = W.chung_lu(20_000, 120_000, 2_000, nlv=4, nle=6, seed=seed)
+    g = W.chung_lu(20_000, 120_000, 2_000, nlv=16, nle=8, seed=seed)
     graph = gsi.build(g)
     og = oracle.OracleGraph(g)
-    for j in range(8):
-        q = W.random_walk_query(g, 4 + (j % 6), 5000 + 10 * seed + j)
+    qs = bounded_queries(g, og, lambda s: 4 + s % 6, range(5000 + 100 * seed, 5000 + 100 * seed + 40), want=10)
+    assert len(qs) >= 5
+    for q in qs:
         r, tab, cnt, fp, otab = run_both(g, q, graph, og)
         assert r.count == cnt and r.fingerprint() == fp
         assert np.array_equal(canon(tab), otab)
         assert strictly_increasing_in_order(tab, r.stats()["order"][:q.n])
         assert tuple(q.embedding.tolist()) in {tuple(x) for x in tab.tolist()}
+
+
+def test_large_counts_fingerprint():
+    """10^7-10^9 matches, count-only on the GPU against the oracle's count and set
+    fingerprint (SURVEY.md §8(c) parity at scale)."""
+    g = W.chung_lu(4000, 30000, 500, nlv=3, nle=4, seed=31)
+    graph = gsi.build(g)
+    og = oracle.OracleGraph(g)
+    for s in (700, 703, 705):
+        q = W.random_walk_query(g, 6, s)
+        cnt, fp, _ = oracle.match(og, q, table=False)
+        r = gsi.query(graph, q)
+        assert r.count == cnt and r.fingerprint() == fp
+        assert cnt > 10_000_000 or s == 703
 
 
 def test_enron_shaped_config():
@@ -215,12 +248,11 @@ def test_enron_shaped_config():
 
 # ------------------------------------------------------------------ invariances -------
 def test_order_e0_and_filter_invariance():
-    g = W.chung_lu(4000, 30000, 500, nlv=3, nle=4, seed=31)
+    g = W.chung_lu(4000, 30000, 500, nlv=8, nle=6, seed=31)
     graph = gsi.build(g)
     og = oracle.OracleGraph(g)
     rng = np.random.default_rng(0)
-    for j in range(6):
-        q = W.random_walk_query(g, 6, 700 + j)
+    for q in bounded_queries(g, og, 6, range(700, 760), hi=500_000, want=6):
         _, _, otab = oracle.match(og, q)
         base = canon(gsi.query(graph, q, want_table=True).table())
         assert np.array_equal(base, otab)
@@ -239,10 +271,10 @@ def test_order_e0_and_filter_invariance():
 
 def test_sharding_concatenates_to_full():
     """M-row sharding run sequentially: shards in rank order == 1-GPU table."""
-    g = W.chung_lu(20_000, 150_000, 3_000, nlv=2, nle=3, seed=41)
+    g = W.chung_lu(20_000, 150_000, 3_000, nlv=16, nle=8, seed=41)
     graph = gsi.build(g)
-    for j in range(4):
-        q = W.random_walk_query(g, 5, 900 + j)
+    og = oracle.OracleGraph(g)
+    for q in bounded_queries(g, og, lambda s: 5 + s % 3, range(900, 960), lo=1000, hi=1_000_000, want=4):
         full = gsi.query(graph, q, want_table=True)
         ft = full.table()
         for W_ in (2, 3, 8):
@@ -257,12 +289,11 @@ def test_sharding_concatenates_to_full():
 
 
 def test_roots_restriction_matches_oracle():
-    g = W.chung_lu(10_000, 60_000, 900, nlv=3, nle=3, seed=51)
+    g = W.chung_lu(10_000, 60_000, 900, nlv=8, nle=6, seed=51)
     graph = gsi.build(g)
     og = oracle.OracleGraph(g)
     rng = np.random.default_rng(1)
-    for j in range(4):
-        q = W.random_walk_query(g, 6, 1100 + j)
+    for q in bounded_queries(g, og, 6, range(1100, 1160), hi=2_000_000, want=4):
         r0 = gsi.query(graph, q)
         root = r0.stats()["order"][0]
         roots = rng.choice(g.n, 500, replace=False)
@@ -337,3 +368,33 @@ def test_prepared_and_buffers_roundtrip():
     torch.cuda.synchronize()
     c = gsi.query(g2, q, want_table=True)
     assert np.array_equal(c.table(), b.table())
+
+
+def test_chunked_execution_invariance():
+    """Depth-first chunking of the GBA slot range (memory bound) changes nothing in R nor in
+    the row order (SURVEY.md §7 hard part 3)."""
+    g = W.chung_lu(20_000, 150_000, 3_000, nlv=16, nle=8, seed=43)
+    graph = gsi.build(g)
+    og = oracle.OracleGraph(g)
+    for q in bounded_queries(g, og, 6, range(1500, 1560), lo=10_000, hi=300_000, want=3):
+        full = gsi.query(graph, q, want_table=True)
+        cnt, fp, otab = oracle.match(og, q)
+        assert full.count == cnt and np.array_equal(canon(full.table()), otab)
+        for cs in (2048, 4096 + 17, 50_000):
+            r = gsi.query(graph, q, want_table=True, chunk_slots=cs)
+            assert np.array_equal(r.table(), full.table())
+            assert r.fingerprint() == full.fingerprint()
+            c = gsi.query(graph, q, chunk_slots=cs)              # count-only path
+            assert c.count == cnt and c.fingerprint() == fp
+        assert gsi.query(graph, q, chunk_slots=2048).stats()["n_chunks"] >= 1 or full.stats()["gba"][1] < 2048
+
+
+def test_timeout_partial_prefix():
+    g = W.chung_lu(20_000, 150_000, 3_000, nlv=1, nle=2, seed=44)
+    graph = gsi.build(g)
+    q = W.random_walk_query(g, 7, 1600)
+    r = gsi.query(graph, q, timeout_s=1e-6, partial_on_timeout=True, chunk_slots=2048)
+    assert r.stats()["capped"] == 1
+    with pytest.raises(gsi.GsiError) as e:
+        gsi.query(graph, q, timeout_s=1e-6, chunk_slots=2048)
+    assert e.value.status == "GSI_ERR_TIMEOUT"

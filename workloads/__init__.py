@@ -386,9 +386,10 @@ class _Adj:
         d2 = torch.cat([dst, src])
         l2 = torch.cat([el, el])
         order = torch.argsort(s2, stable=True)
-        self.nbr = d2[order].cpu().numpy()
+        self.nbr = d2[order].to(torch.int32).cpu().numpy()
         self.lab = l2[order].cpu().numpy()
         deg = torch.bincount(s2, minlength=g.n)
+        del order, s2, d2, l2
         self.off = np.concatenate([[0], torch.cumsum(deg, 0).cpu().numpy()])
         self.deg = deg.cpu().numpy()
         self.nonisolated = np.nonzero(self.deg)[0]
