@@ -268,7 +268,8 @@ def run_gsi(args):
 
     def step(profile=False, stats=None):
         for i, p in enumerate(prepared):
-            r = gsi.gsi_query_run(graph, p, stream=sptr, timeout_s=args.query_timeout, profile=profile, **shard)
+            r = gsi.gsi_query_run(graph, p, stream=sptr, timeout_s=args.query_timeout, profile=profile,
+                                  partial_on_timeout=True, **shard)
             counts[i] = r.count
             if stats is not None:
                 stats.append(r.stats())
@@ -279,7 +280,7 @@ def run_gsi(args):
     def e2e_step():
         for i, q in enumerate(qs):
             r = gsi.gsi_query(graph, q.vlabels, q.src, q.dst, q.elabels, stream=sptr,
-                              timeout_s=args.query_timeout, **shard)
+                              timeout_s=args.query_timeout, partial_on_timeout=True, **shard)
             counts[i] = r.count
         if ws > 1:
             dist.all_reduce(counts)
