@@ -144,6 +144,8 @@ typedef struct {
                                     a level whose |GBA| exceeds it runs depth-first in chunks  */
     int32_t partial_on_timeout;  /* 1: on timeout return GSI_OK with stats.capped = 1 and the
                                     exact count of the completed chunk prefix                  */
+    int32_t fingerprint;         /* 1: compute the set fingerprint of the final rows (costs ~2k
+                                    hash rounds per match); 0: fingerprint = (count, 0, 0)      */
 } gsi_query_opts;
 
 void gsi_query_opts_default(gsi_query_opts *opts);

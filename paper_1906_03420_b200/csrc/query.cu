@@ -54,6 +54,7 @@ struct StepParams {
     int n_inj;
     int inj_col[GSI_MAX_K];      // columns the subtraction must test (same vertex label as u)
     int pos_of_q[GSI_MAX_K];     // final level: column (0..t) holding query vertex q
+    int fp;                      // final level: accumulate the set fingerprint
 };
 
 // Counters shared by the kernels of one query (device).
@@ -64,7 +65,7 @@ struct Counters {
     unsigned long long fp1, fp2;
     unsigned long long plane_loads;  // filter: vertices whose planes 1..15 were read
     unsigned long long total;        // scan totals written by the last tile
-    unsigned long long pad;
+    unsigned long long total2;       // F'[|M'|] of the probe-ahead (J_NEXT)
 };
 
 // ---------------------------------------------------------------------- filter ------
@@ -177,9 +178,47 @@ __global__ void __launch_bounds__(kThreads) k_compact_roots(const int32_t *__res
 }
 
 // ---------------------------------------------------------------------- probe -------
-// Alg. 4: F[i] = sum_{i'<i} |N(v'_{i'}, l0)|, F[|M|] = |GBA|.  loc[i*E + e] caches every
-// linking list; in per-row mode entry 0 is the shortest list of the row (any linking
-// edge bounds buf_i, L967-981) and rows with an empty list get a zero-size buffer.
+// Alg. 4 for one row: locate N(v', l_e) for every linking edge of the next step (one PCSR
+// group probe each), write the row's loc entries and return its buffer bound.
+// In per-row mode entry 0 becomes the row's shortest list (any linking edge bounds buf_i,
+// L967-981) and a row with an empty list gets a zero-size buffer.  Column c of the row is
+// row[c] for c < t_parent and `newv` for c == t_parent (the vertex the join just added).
+__device__ __forceinline__ void probe_row(const int32_t *__restrict__ row, int t_parent, uint32_t newv,
+                                          const StepParams &P, const uint2 *__restrict__ groups, int gpn,
+                                          Loc *__restrict__ L, unsigned long long &len0, unsigned long long &elems) {
+    Loc first{0, 0}, best{0, 0};
+    int bi = 0;
+    bool anyzero = false;
+    unsigned long long sum = 0;
+    for (int e = 0; e < P.E; e++) {
+        const int c = P.col[e];
+        const uint32_t v = c < t_parent ? (uint32_t)__ldg(row + c) : newv;
+        const Loc r = pcsr_lookup(groups, gpn, P.gbase[e], P.ngroups[e], P.lab[e], v, nullptr);
+        L[e] = r;
+        if (e == 0) {
+            first = r;
+            best = r;
+        } else if (r.len < best.len) {
+            best = r;
+            bi = e;
+        }
+        anyzero |= r.len == 0;
+        sum += r.len;
+    }
+    if (P.per_row_e0) {
+        if (bi != 0) {
+            L[0] = best;
+            L[bi] = first;
+        }
+        len0 = anyzero ? 0ull : best.len;
+        elems = anyzero ? 0ull : sum;
+    } else {
+        len0 = first.len;
+        elems = sum;
+    }
+}
+
+// Level 1: F[i] = sum_{i'<i} |N(v'_{i'}, l0)|, F[|M|] = |GBA|, by decoupled look-back.
 __global__ void __launch_bounds__(kThreads) k_probe(const int32_t *__restrict__ M, long long nM, StepParams P,
                                                     const uint2 *__restrict__ groups, int gpn,
                                                     Loc *__restrict__ loc, unsigned long long *__restrict__ F,
@@ -193,45 +232,17 @@ __global__ void __launch_bounds__(kThreads) k_probe(const int32_t *__restrict__ 
     const unsigned tile = tile_s;
     const long long i = (long long)tile * kThreads + threadIdx.x;
     unsigned long long len0 = 0, elems = 0;
-    if (i < nM) {
-        const int32_t *row = M + i * P.t;
-        Loc first{0, 0}, best{0, 0};
-        int bi = 0;
-        bool anyzero = false;
-        unsigned long long sum = 0;
-        Loc *L = loc + i * P.E;
-        for (int e = 0; e < P.E; e++) {
-            uint32_t v = (uint32_t)__ldg(row + P.col[e]);
-            Loc r = pcsr_lookup(groups, gpn, P.gbase[e], P.ngroups[e], P.lab[e], v, nullptr);
-            L[e] = r;
-            if (e == 0) { first = r; best = r; }
-            else if (r.len < best.len) { best = r; bi = e; }
-            anyzero |= r.len == 0;
-            sum += r.len;
-        }
-        if (P.per_row_e0) {
-            if (bi != 0) {
-                L[0] = best;
-                L[bi] = first;
-            }
-            len0 = anyzero ? 0ull : best.len;
-            elems = anyzero ? 0ull : sum;
-        } else {
-            len0 = first.len;
-            elems = sum;
-        }
-    }
+    if (i < nM) probe_row(M + i * P.t, P.t, 0u, P, groups, gpn, loc + i * P.E, len0, elems);
     unsigned long long agg;
-    unsigned long long ex = block_exclusive_scan(len0, sm, &agg);
+    const unsigned long long ex = block_exclusive_scan(len0, sm, &agg);
     if (threadIdx.x < 32) {
-        unsigned long long pre = lookback_exclusive(status, tile, agg);
+        const unsigned long long pre = lookback_exclusive(status, tile, agg);
         if (threadIdx.x == 0) base_s = pre;
     }
     __syncthreads();
     if (i < nM) F[i] = base_s + ex;
     if (tile == gridDim.x - 1 && threadIdx.x == kThreads - 1) F[nM] = base_s + agg;
-    // algorithmic accounting
-    unsigned long long e1 = warp_sum_u64(elems), a1 = warp_sum_u64(len0 ? 1ull : 0ull);
+    const unsigned long long e1 = warp_sum_u64(elems), a1 = warp_sum_u64(len0 ? 1ull : 0ull);
     if ((threadIdx.x & 31) == 0) {
         if (e1) atomicAdd(&ctr->list_elems, e1);
         if (a1) atomicAdd(&ctr->active_rows, a1);
@@ -259,22 +270,54 @@ __device__ __forceinline__ bool in_sorted(const int32_t *__restrict__ a, uint32_
     return lo < n && __ldg(a + lo) == x;
 }
 
-template <bool WRITE, bool FINAL>
+__device__ __forceinline__ void row_hash(const int32_t *__restrict__ row, uint32_t x, const StepParams &P,
+                                         unsigned long long &h1, unsigned long long &h2) {
+    unsigned long long a = kFpSeed1, b = kFpSeed2;
+    for (int q = 0; q < P.k; q++) {
+        const int col = P.pos_of_q[q];
+        const uint32_t val = col < P.t ? (uint32_t)__ldg(row + col) : x;
+        a = fp_mix(a ^ val);
+        b = fp_mix(b ^ val);
+    }
+    h1 += a;
+    h2 ^= b;
+}
+
+enum JoinMode { J_COUNT = 0, J_TABLE = 1, J_NEXT = 2 };
+
+// The fused level kernel.  Slots [s0, s1) of the Prealloc space (GBA) of this level are cut
+// into 2048-slot tiles.  Per slot: the candidate x = N(v', l0)[s - F_i] of row i is kept iff
+// x in C(u) (bitset, L1150), x not in m_i (Alg. 3 line 10) and x in every other linking list
+// (Alg. 3 line 13).  Survivors are compacted in slot order into shared memory (the write
+// cache, L1155-1158), their output offset comes from a decoupled look-back (the Combine scan
+// of Alg. 3 line 14), and the CTA writes its contiguous block of new rows m_i || x with
+// coalesced stores (Alg. 3 lines 15-21).
+//   J_COUNT : final level, count + fingerprint only (no table).
+//   J_TABLE : final level, rows written in query-id order + fingerprint.
+//   J_NEXT  : rows of M_{t+1} written, and the NEXT step's Prealloc probe runs on each new
+//             row while it is in registers (loc2, and F2 by a second look-back chain), so the
+//             next level never re-reads M_{t+1} just to size its buffers.
+template <int MODE>
 __global__ void __launch_bounds__(kThreads) k_join(const int32_t *__restrict__ M, long long nM,
                                                    const unsigned long long *__restrict__ F,
-                                                   const Loc *__restrict__ loc, StepParams P,
+                                                   const Loc *__restrict__ loc, StepParams P, StepParams P2,
                                                    const int32_t *__restrict__ ci,
                                                    const uint32_t *__restrict__ cu_bitmap,
+                                                   const uint2 *__restrict__ groups, int gpn,
                                                    unsigned long long s0, unsigned long long s1,
-                                                   uint32_t *__restrict__ S, uint32_t *__restrict__ R,
-                                                   unsigned long long *status, unsigned *tile_ctr,
-                                                   Counters *ctr) {
-    __shared__ unsigned long long sF[kSmemF];
+                                                   int32_t *__restrict__ out, Loc *__restrict__ loc2,
+                                                   unsigned long long *__restrict__ F2,
+                                                   unsigned long long *status, unsigned long long *status2,
+                                                   unsigned *tile_ctr, Counters *ctr) {
+    __shared__ unsigned long long sF[kSmemF];          // staged F; reused for len0' of new rows
+    __shared__ uint32_t sx[MODE == J_COUNT ? 1 : kJoinTile];
+    __shared__ uint32_t si[MODE == J_COUNT ? 1 : kJoinTile];
     __shared__ unsigned wcnt[kJoinItems][kThreads / 32];
     __shared__ unsigned wbase[kJoinItems][kThreads / 32];
+    __shared__ unsigned long long sm[33];
     __shared__ unsigned tile_s, agg_s;
     __shared__ long long rlo_s, rhi_s;
-    __shared__ unsigned long long base_s;
+    __shared__ unsigned long long base_s, base2_s;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) tile_s = atomicAdd(tile_ctr, 1u);
     __syncthreads();
@@ -304,7 +347,7 @@ __global__ void __launch_bounds__(kThreads) k_join(const int32_t *__restrict__ M
             long long i;
             unsigned long long fi;
             if (staged) {
-                long long lo = 0, hi = nr - 1;   // search sF[0 .. nr-1)
+                long long lo = 0, hi = nr - 1;
                 while (hi - lo > 1) {
                     long long mid = (lo + hi) >> 1;
                     if (sF[mid] <= s) lo = mid; else hi = mid;
@@ -318,12 +361,12 @@ __global__ void __launch_bounds__(kThreads) k_join(const int32_t *__restrict__ M
             const Loc *L = loc + i * P.E;
             const Loc L0 = L[0];
             const int32_t x = __ldg(ci + L0.off + (uint32_t)(s - fi));
-            bool k = (__ldg(cu_bitmap + (x >> 5)) >> (x & 31)) & 1u;      // x in C(u)   (L1150)
+            bool k = (__ldg(cu_bitmap + (x >> 5)) >> (x & 31)) & 1u;                 // x in C(u)
             const int32_t *row = M + i * P.t;
-            for (int c = 0; c < P.n_inj && k; c++) k = __ldg(row + P.inj_col[c]) != x;   // Alg. 3 line 10
+            for (int c = 0; c < P.n_inj && k; c++) k = __ldg(row + P.inj_col[c]) != x;   // subtraction
             for (int e = 1; e < P.E && k; e++) {
                 const Loc Le = L[e];
-                k = in_sorted(ci + Le.off, Le.len, x);                               // Alg. 3 line 13
+                k = in_sorted(ci + Le.off, Le.len, x);                                   // intersection
             }
             keep[it] = k;
             xs[it] = (uint32_t)x;
@@ -331,25 +374,13 @@ __global__ void __launch_bounds__(kThreads) k_join(const int32_t *__restrict__ M
         }
     }
 
-    if constexpr (!WRITE) {
-        // count-only final level: count + fingerprint of survivors (query-id order rows)
+    if constexpr (MODE == J_COUNT) {
         unsigned long long c = 0, h1 = 0, h2 = 0;
 #pragma unroll
         for (int it = 0; it < kJoinItems; it++) {
             if (!keep[it]) continue;
             c++;
-            if (FINAL) {
-                const int32_t *row = M + (long long)rows[it] * P.t;
-                unsigned long long a = kFpSeed1, b = kFpSeed2;
-                for (int q = 0; q < P.k; q++) {
-                    int col = P.pos_of_q[q];
-                    uint32_t val = col < P.t ? (uint32_t)__ldg(row + col) : xs[it];
-                    a = fp_mix(a ^ val);
-                    b = fp_mix(b ^ val);
-                }
-                h1 += a;
-                h2 ^= b;
-            }
+            if (P.fp) row_hash(M + (long long)rows[it] * P.t, xs[it], P, h1, h2);
         }
         c = warp_sum_u64(c);
         h1 = warp_sum_u64(h1);
@@ -361,92 +392,121 @@ __global__ void __launch_bounds__(kThreads) k_join(const int32_t *__restrict__ M
             atomicXor(&ctr->fp2, h2);
         }
     } else {
-
-    // ---- ordered compaction through shared memory + decoupled look-back -------------
-    unsigned ballots[kJoinItems];
-#pragma unroll
-    for (int it = 0; it < kJoinItems; it++) {
-        ballots[it] = __ballot_sync(0xffffffffu, keep[it]);
-        if (lane == 0) wcnt[it][warp] = __popc(ballots[it]);
-    }
-    __syncthreads();
-    if (warp == 0) {
-        // 64 (it, warp) counts in slot order: index = it * 8 + warp
-        constexpr int NW = kThreads / 32;
-        unsigned a = wcnt[(2 * lane) / NW][(2 * lane) % NW];
-        unsigned b = wcnt[(2 * lane + 1) / NW][(2 * lane + 1) % NW];
-        unsigned pair = a + b, inc = pair;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += y;
-        }
-        unsigned ex = inc - pair;
-        wbase[(2 * lane) / NW][(2 * lane) % NW] = ex;
-        wbase[(2 * lane + 1) / NW][(2 * lane + 1) % NW] = ex + a;
-        unsigned total = __shfl_sync(0xffffffffu, inc, 31);
-        unsigned long long pre = lookback_exclusive(status, tile, total);
-        if (lane == 0) {
-            base_s = pre;
-            agg_s = total;
-        }
-    }
-    __syncthreads();
-    const unsigned long long base = base_s;
-    const unsigned lt = (1u << lane) - 1u;
-#pragma unroll
-    for (int it = 0; it < kJoinItems; it++) {
-        if (keep[it]) {
-            unsigned long long pos = base + wbase[it][warp] + __popc(ballots[it] & lt);
-            S[pos] = xs[it];
-            R[pos] = rows[it];
-        }
-    }
-    if (FINAL) {
-        unsigned long long c = 0, h1 = 0, h2 = 0;
+        // ---- ordered compaction into the shared-memory write cache + look-back ------------
+        unsigned ballots[kJoinItems];
 #pragma unroll
         for (int it = 0; it < kJoinItems; it++) {
-            if (!keep[it]) continue;
-            c++;
-            const int32_t *row = M + (long long)rows[it] * P.t;
-            unsigned long long a = kFpSeed1, b = kFpSeed2;
-            for (int q = 0; q < P.k; q++) {
-                int col = P.pos_of_q[q];
-                uint32_t val = col < P.t ? (uint32_t)__ldg(row + col) : xs[it];
-                a = fp_mix(a ^ val);
-                b = fp_mix(b ^ val);
-            }
-            h1 += a;
-            h2 ^= b;
+            ballots[it] = __ballot_sync(0xffffffffu, keep[it]);
+            if (lane == 0) wcnt[it][warp] = __popc(ballots[it]);
         }
-        h1 = warp_sum_u64(h1);
+        __syncthreads();
+        if (warp == 0) {
+            constexpr int NW = kThreads / 32;   // 64 (it, warp) counts in slot order: it * 8 + warp
+            const unsigned a = wcnt[(2 * lane) / NW][(2 * lane) % NW];
+            const unsigned b = wcnt[(2 * lane + 1) / NW][(2 * lane + 1) % NW];
+            const unsigned pair = a + b;
+            unsigned inc = pair;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) h2 ^= __shfl_xor_sync(0xffffffffu, h2, o);
-        if (lane == 0 && ballots[0] | ballots[1] | ballots[2] | ballots[3] | ballots[4] | ballots[5] | ballots[6] |
-                             ballots[7]) {
-            atomicAdd(&ctr->fp1, h1);
-            atomicXor(&ctr->fp2, h2);
+            for (int o = 1; o < 32; o <<= 1) {
+                unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            const unsigned ex = inc - pair;
+            wbase[(2 * lane) / NW][(2 * lane) % NW] = ex;
+            wbase[(2 * lane + 1) / NW][(2 * lane + 1) % NW] = ex + a;
+            const unsigned total = __shfl_sync(0xffffffffu, inc, 31);
+            const unsigned long long pre = lookback_exclusive(status, tile, total);
+            if (lane == 0) {
+                base_s = pre;
+                agg_s = total;
+            }
         }
-    }
-    if (tile == gridDim.x - 1 && tid == 0) ctr->total = base + agg_s;
-    }
-}
+        __syncthreads();
+        const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+        for (int it = 0; it < kJoinItems; it++) {
+            if (keep[it]) {
+                const unsigned lp = wbase[it][warp] + __popc(ballots[it] & lt);
+                sx[lp] = xs[it];
+                si[lp] = rows[it];
+            }
+        }
+        __syncthreads();
+        const unsigned long long base = base_s;
+        const unsigned cnt = agg_s;
 
-// ---------------------------------------------------------------------- link --------
-// M'[r] = M[R[r]] || S[r]; in FINAL mode the row is written in query-id order.
-template <bool FINAL>
-__global__ void __launch_bounds__(kThreads) k_link(const int32_t *__restrict__ M, int t, const uint32_t *__restrict__ S,
-                                                   const uint32_t *__restrict__ R, unsigned long long nout,
-                                                   StepParams P, int32_t *__restrict__ out) {
-    const int W = t + 1;
-    const unsigned long long total = nout * (unsigned long long)W;
-    for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < total;
-         e += (unsigned long long)gridDim.x * blockDim.x) {
-        const unsigned long long r = e / W;
-        const int c = (int)(e - r * W);
-        const int col = FINAL ? P.pos_of_q[c] : c;
-        int32_t v = col < t ? __ldg(M + (unsigned long long)__ldg(R + r) * t + col) : (int32_t)__ldg(S + r);
-        __stcs(out + e, v);
+        if constexpr (MODE == J_TABLE) {
+            unsigned long long h1 = 0, h2 = 0;
+            if (P.fp)
+                for (unsigned j = tid; j < cnt; j += kThreads) row_hash(M + (long long)si[j] * P.t, sx[j], P, h1, h2);
+            h1 = warp_sum_u64(h1);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) h2 ^= __shfl_xor_sync(0xffffffffu, h2, o);
+            if (lane == 0 && (h1 | h2)) {
+                atomicAdd(&ctr->fp1, h1);
+                atomicXor(&ctr->fp2, h2);
+            }
+            const int k = P.k;
+            int32_t *o = out + base * (unsigned long long)k;
+            for (unsigned e = tid; e < cnt * (unsigned)k; e += kThreads) {
+                const unsigned r = e / k, q = e - r * k;
+                const int col = P.pos_of_q[q];
+                o[e] = col < P.t ? __ldg(M + (long long)si[r] * P.t + col) : (int32_t)sx[r];
+            }
+            if (tile == gridDim.x - 1 && tid == 0) ctr->total = base + cnt;
+        } else {
+            // ---- probe-ahead: the next step's Prealloc on the new rows ------------------------
+            uint32_t *sl = reinterpret_cast<uint32_t *>(sF);   // len0' per new row (2048 x 4 B)
+            unsigned long long elems = 0, act = 0;
+            for (unsigned j = tid; j < cnt; j += kThreads) {
+                unsigned long long l0, el;
+                probe_row(M + (long long)si[j] * P.t, P.t, sx[j], P2, groups, gpn,
+                          loc2 + (base + j) * (unsigned long long)P2.E, l0, el);
+                sl[j] = (uint32_t)l0;
+                elems += el;
+                act += l0 ? 1 : 0;
+            }
+            elems = warp_sum_u64(elems);
+            act = warp_sum_u64(act);
+            if (lane == 0 && elems) atomicAdd(&ctr->list_elems, elems);
+            if (lane == 0 && act) atomicAdd(&ctr->active_rows, act);
+            __syncthreads();
+            // scan of len0' over the tile's new rows (thread tid owns rows [8 tid, 8 tid + 8))
+            unsigned long long mine = 0;
+#pragma unroll
+            for (int q = 0; q < kJoinItems; q++) {
+                const unsigned j = tid * kJoinItems + q;
+                if (j < cnt) mine += sl[j];
+            }
+            unsigned long long agg2;
+            const unsigned long long ex2 = block_exclusive_scan(mine, sm, &agg2);
+            if (warp == 0) {
+                const unsigned long long pre2 = lookback_exclusive(status2, tile, agg2);
+                if (lane == 0) base2_s = pre2;
+            }
+            __syncthreads();
+            unsigned long long run = base2_s + ex2;
+#pragma unroll
+            for (int q = 0; q < kJoinItems; q++) {
+                const unsigned j = tid * kJoinItems + q;
+                if (j < cnt) {
+                    F2[base + j] = run;
+                    run += sl[j];
+                }
+            }
+            // ---- coalesced write of the contiguous block of new rows ------------------------
+            const int W = P.t + 1;
+            int32_t *o = out + base * (unsigned long long)W;
+            for (unsigned e = tid; e < cnt * (unsigned)W; e += kThreads) {
+                const unsigned r = e / W, c = e - r * W;
+                o[e] = (int)c < P.t ? __ldg(M + (long long)si[r] * P.t + c) : (int32_t)sx[r];
+            }
+            if (tile == gridDim.x - 1 && tid == 0) {
+                ctr->total = base + cnt;
+                ctr->total2 = base2_s + agg2;
+                F2[base + cnt] = base2_s + agg2;
+            }
+        }
     }
 }
 
@@ -868,6 +928,7 @@ void fill_params(QueryCtx &C, const Step &s, StepParams &P) {
     P.k = C.q->k;
     P.per_row_e0 = C.opts.e0_mode == 0 ? 1 : 0;
     for (int qv = 0; qv < C.q->k; qv++) P.pos_of_q[qv] = C.pos_of_q[qv];
+    P.fp = C.opts.fingerprint != 0;
     std::vector<int> eorder(E);
     for (int e = 0; e < E; e++) eorder[e] = e;
     std::swap(eorder[0], eorder[s.paper_e0]);   // paper mode: e0 first (Alg. 3 line 9)
@@ -889,7 +950,10 @@ void fill_params(QueryCtx &C, const Step &s, StepParams &P) {
     }
 }
 
-gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM) {
+// Level t = steps[si].t: M (nM x t) with its Prealloc (loc, F, |GBA| = gba) already computed
+// (by k_probe for level 1, by the previous level's fused kernel otherwise).
+gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc *loc, unsigned long long *F,
+                 unsigned long long gba, unsigned long long active, unsigned long long elems) {
     const Step &s = C.steps[si];
     const int t = s.t;
     const bool last = si + 1 == C.steps.size();
@@ -898,36 +962,16 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM) {
     Prof &prof = *C.prof;
     cudaStream_t st = C.st;
     const gsi_graph *g = C.g;
-    StepParams P;
+    StepParams P, P2;
     fill_params(C, s, P);
+    if (!last) fill_params(C, C.steps[si + 1], P2);
+    else std::memset(&P2, 0, sizeof(P2));
     const int E = P.E;
     S.rows[t - 1] += nM;
     if (S.levels < t) S.levels = t;
-    if (nM == 0) return GSI_OK;
-
-    // ---- probe + Prealloc scan (a6) ----
-    Loc *loc = nullptr;
-    unsigned long long *F = nullptr, *status = nullptr;
-    GSI_TRY(A.get(&loc, nM * (unsigned long long)E));
-    GSI_TRY(A.get(&F, nM + 1));
-    const unsigned ptiles = grid_for(nM, kThreads);
-    GSI_TRY(A.get(&status, ptiles + 1));
-    GSI_CUDA(cudaMemsetAsync(status, 0, 8ull * (ptiles + 1), st));
-    GSI_CUDA(cudaMemsetAsync(C.ctr, 0, sizeof(Counters), st));
-    prof.begin(GSI_K_PROBE);
-    k_probe<<<ptiles, kThreads, 0, st>>>(M, (long long)nM, P, g->groups, g->gpn, loc, F, status + 1,
-                                         (unsigned *)status, C.ctr);
-    prof.end();
-    Counters hc;
-    unsigned long long gba = 0;
-    GSI_CUDA(d2h(S, &gba, F + nM, 8, st));
-    GSI_CUDA(d2h(S, &hc, C.ctr, sizeof(Counters), st));
-    GSI_CUDA(cudaStreamSynchronize(st));
-    A.release(status);
     S.gba[t] += gba;
-    S.list_elems[t] += hc.list_elems;
-    S.alg_bytes[GSI_K_PROBE] += (double)nM * (20.0 * E + 8.0);
-    const unsigned long long active = hc.active_rows, elems = hc.list_elems;
+    S.list_elems[t] += elems;
+    if (nM == 0 || gba == 0) return GSI_OK;
 
     // ---- shard this level's slot range ----
     unsigned long long s0 = 0, s1 = gba;
@@ -949,8 +993,10 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM) {
         C.sharded = true;
     }
 
-    const bool write = !last || C.opts.want_table;
-    const unsigned long long chunk = write ? std::max<unsigned long long>(C.cap_slots, kJoinTile) : (s1 - s0);
+    const int mode = !last ? J_NEXT : (C.opts.want_table ? J_TABLE : J_COUNT);
+    const unsigned long long chunk =
+        mode == J_COUNT ? std::max<unsigned long long>(s1 - s0, 1) : std::max<unsigned long long>(C.cap_slots, kJoinTile);
+    const uint32_t *cu = C.bm + (long long)s.u * C.words;
     gsi_status rc = GSI_OK;
     for (unsigned long long c0 = s0; c0 < s1 && rc == GSI_OK; c0 += chunk) {
         if (C.deadline > 0 && now_ms() > C.deadline) {
@@ -960,34 +1006,44 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM) {
         const unsigned long long c1 = std::min(s1, c0 + chunk), slots = c1 - c0;
         if (c0 != s0 || c1 != s1) S.n_chunks++;
         const unsigned jt = grid_for(slots, kJoinTile);
-        uint32_t *Sv = nullptr, *Rv = nullptr;
-        GSI_TRY(A.get(&status, jt + 1));
-        GSI_CUDA(cudaMemsetAsync(status, 0, 8ull * (jt + 1), st));
+        unsigned long long *status = nullptr;
+        GSI_TRY(A.get(&status, 2ull * jt + 2));
+        GSI_CUDA(cudaMemsetAsync(status, 0, 8ull * (2ull * jt + 2), st));
+        unsigned *tctr = (unsigned *)status;
+        unsigned long long *st1 = status + 1, *st2 = status + 2 + jt;
         GSI_CUDA(cudaMemsetAsync(C.ctr, 0, sizeof(Counters), st));
-        if (write) {
-            GSI_TRY(A.get(&Sv, slots));
-            GSI_TRY(A.get(&Rv, slots));
+        int32_t *out = nullptr;
+        Loc *loc2 = nullptr;
+        unsigned long long *F2 = nullptr;
+        if (mode == J_TABLE) GSI_TRY(A.get(&out, slots * (unsigned long long)C.q->k));
+        if (mode == J_NEXT) {
+            GSI_TRY(A.get(&out, slots * (unsigned long long)(t + 1)));
+            GSI_TRY(A.get(&loc2, slots * (unsigned long long)P2.E));
+            GSI_TRY(A.get(&F2, slots + 1));
+            GSI_CUDA(cudaMemsetAsync(F2, 0, 8, st));
         }
-        const uint32_t *cu = C.bm + (long long)s.u * C.words;
         prof.begin(GSI_K_JOIN);
-        if (write && last)
-            k_join<true, true><<<jt, kThreads, 0, st>>>(M, (long long)nM, F, loc, P, g->ci, cu, c0, c1, Sv, Rv,
-                                                        status + 1, (unsigned *)status, C.ctr);
-        else if (write)
-            k_join<true, false><<<jt, kThreads, 0, st>>>(M, (long long)nM, F, loc, P, g->ci, cu, c0, c1, Sv, Rv,
-                                                         status + 1, (unsigned *)status, C.ctr);
+        if (mode == J_COUNT)
+            k_join<J_COUNT><<<jt, kThreads, 0, st>>>(M, (long long)nM, F, loc, P, P2, g->ci, cu, g->groups, g->gpn,
+                                                     c0, c1, out, loc2, F2, st1, st2, tctr, C.ctr);
+        else if (mode == J_TABLE)
+            k_join<J_TABLE><<<jt, kThreads, 0, st>>>(M, (long long)nM, F, loc, P, P2, g->ci, cu, g->groups, g->gpn,
+                                                     c0, c1, out, loc2, F2, st1, st2, tctr, C.ctr);
         else
-            k_join<false, true><<<jt, kThreads, 0, st>>>(M, (long long)nM, F, loc, P, g->ci, cu, c0, c1, Sv, Rv,
-                                                         status + 1, (unsigned *)status, C.ctr);
+            k_join<J_NEXT><<<jt, kThreads, 0, st>>>(M, (long long)nM, F, loc, P, P2, g->ci, cu, g->groups, g->gpn,
+                                                    c0, c1, out, loc2, F2, st1, st2, tctr, C.ctr);
         prof.end();
+        Counters hc;
         GSI_CUDA(d2h(S, &hc, C.ctr, sizeof(Counters), st));
         GSI_CUDA(cudaStreamSynchronize(st));
         GSI_CUDA(cudaGetLastError());
         A.release(status);
-        const unsigned long long nout = write ? hc.total : hc.count;
+        const unsigned long long nout = mode == J_COUNT ? hc.count : hc.total;
         const double frac = gba ? (double)slots / (double)gba : 0.0;
-        S.alg_bytes[GSI_K_JOIN] +=
-            frac * (4.0 * t * active + 4.0 * elems + (8.0 * E + 8.0) * active) + (write ? 8.0 * nout : 0.0);
+        double jb = frac * (4.0 * t * active + 4.0 * elems + (8.0 * E + 8.0) * active);
+        if (mode == J_TABLE) jb += 4.0 * C.q->k * nout;
+        if (mode == J_NEXT) jb += nout * (4.0 * (t + 1) + 16.0 * P2.E + 8.0);
+        S.alg_bytes[GSI_K_JOIN] += jb;
         if (last) {
             C.count += nout;
             C.fp1 += hc.fp1;
@@ -995,34 +1051,21 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM) {
             S.rows[t] += nout;
             if (S.levels < t + 1) S.levels = t + 1;
         }
-        if (write && nout) {
-            const unsigned long long nint = nout * (unsigned long long)(t + 1);
-            int32_t *M2 = nullptr;
-            if (last) {
-                GSI_CUDA(cudaMallocAsync(&M2, 4ull * nint, st));
-                C.pieces.push_back({M2, nout});
-            } else {
-                GSI_TRY(A.get(&M2, nint));
+        if (mode == J_TABLE) {
+            if (nout) {
+                int32_t *piece = nullptr;
+                GSI_CUDA(cudaMallocAsync(&piece, 4ull * nout * C.q->k, st));
+                GSI_CUDA(cudaMemcpyAsync(piece, out, 4ull * nout * C.q->k, cudaMemcpyDeviceToDevice, st));
+                C.pieces.push_back({piece, nout});
             }
-            const unsigned lg = grid_for(nint, kThreads * 4);
-            prof.begin(GSI_K_LINK);
-            if (last) k_link<true><<<lg, kThreads, 0, st>>>(M, t, Sv, Rv, nout, P, M2);
-            else k_link<false><<<lg, kThreads, 0, st>>>(M, t, Sv, Rv, nout, P, M2);
-            prof.end();
-            S.alg_bytes[GSI_K_LINK] += (double)nout * (4.0 * (t + 1) + 4.0 * t + 8.0);
-            A.release(Sv);
-            A.release(Rv);
-            if (!last) {
-                rc = level(C, si + 1, M2, nout);
-                A.release(M2);
-            }
-        } else {
-            A.release(Sv);
-            A.release(Rv);
+            A.release(out);
+        } else if (mode == J_NEXT) {
+            if (nout) rc = level(C, si + 1, out, nout, loc2, F2, hc.total2, hc.active_rows, hc.list_elems);
+            A.release(out);
+            A.release(loc2);
+            A.release(F2);
         }
     }
-    A.release(loc);
-    A.release(F);
     return rc;
 }
 
@@ -1184,7 +1227,7 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
         P.k = 1;
         P.t = 1;
         GSI_CUDA(cudaMemsetAsync(C.ctr, 0, sizeof(Counters), st));
-        if (nM) {
+        if (nM && opts.fingerprint) {
             prof.begin(GSI_K_OTHER);
             k_fp_rows<<<grid_for(nM, kThreads), kThreads, 0, st>>>(M, (long long)nM, P, C.ctr);
             prof.end();
@@ -1201,7 +1244,33 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
             C.pieces.push_back({T, nM});
         }
     } else if (!empty) {
-        rc = level(C, 0, M, nM);
+        // level-1 Prealloc (Alg. 4) on M_1 = C(pi_1)
+        StepParams P;
+        fill_params(C, C.steps[0], P);
+        Loc *loc = nullptr;
+        unsigned long long *F = nullptr, *status = nullptr;
+        GSI_TRY(A.get(&loc, std::max<unsigned long long>(nM, 1) * (unsigned long long)P.E));
+        GSI_TRY(A.get(&F, nM + 1));
+        const unsigned ptiles = grid_for(nM, kThreads);
+        GSI_TRY(A.get(&status, ptiles + 1));
+        GSI_CUDA(cudaMemsetAsync(status, 0, 8ull * (ptiles + 1), st));
+        GSI_CUDA(cudaMemsetAsync(C.ctr, 0, sizeof(Counters), st));
+        GSI_CUDA(cudaMemsetAsync(F, 0, 8, st));
+        if (nM) {
+            prof.begin(GSI_K_PROBE);
+            k_probe<<<ptiles, kThreads, 0, st>>>(M, (long long)nM, P, g->groups, g->gpn, loc, F, status + 1,
+                                                 (unsigned *)status, C.ctr);
+            prof.end();
+        }
+        unsigned long long gba = 0;
+        GSI_CUDA(d2h(S, &gba, F + nM, 8, st));
+        GSI_CUDA(d2h(S, &hc, C.ctr, sizeof(Counters), st));
+        GSI_CUDA(cudaStreamSynchronize(st));
+        A.release(status);
+        S.alg_bytes[GSI_K_PROBE] += (double)nM * (20.0 * P.E + 8.0);
+        rc = level(C, 0, M, nM, loc, F, gba, hc.active_rows, hc.list_elems);
+        A.release(loc);
+        A.release(F);
     }
     if (M) A.release(M);
     if (rc != GSI_OK) {

@@ -42,7 +42,7 @@ class gsi_query_opts(ctypes.Structure):
                 ("force_order", P), ("force_first_edge", P), ("roots", P), ("n_roots", I64),
                 ("shard_rank", I32), ("shard_count", I32), ("shard_min_rows", U64),
                 ("mem_budget_bytes", U64), ("timeout_s", ctypes.c_double), ("profile", I32), ("stream", P),
-                ("chunk_slots", U64), ("partial_on_timeout", I32)]
+                ("chunk_slots", U64), ("partial_on_timeout", I32), ("fingerprint", I32)]
 
 
 class gsi_graph_info(ctypes.Structure):
@@ -256,7 +256,7 @@ class Prepared:
 def _opts(want_table=False, homomorphism=False, filter_mode=0, e0_mode=0, force_order=None,
           force_first_edge=None, roots=None, shard_rank=0, shard_count=1, shard_min_rows=0,
           mem_budget_bytes=0, timeout_s=0.0, profile=False, stream=None, chunk_slots=0,
-          partial_on_timeout=False):
+          partial_on_timeout=False, fingerprint=True):
     o = gsi_query_opts()
     lib.gsi_query_opts_default(ctypes.byref(o))
     keep = []
@@ -271,6 +271,7 @@ def _opts(want_table=False, homomorphism=False, filter_mode=0, e0_mode=0, force_
     o.mem_budget_bytes, o.timeout_s, o.profile = mem_budget_bytes, timeout_s, int(profile)
     o.stream = stream
     o.chunk_slots, o.partial_on_timeout = chunk_slots, int(partial_on_timeout)
+    o.fingerprint = int(fingerprint)   # binding default: on (the C default is off)
     return o, keep
 
 
