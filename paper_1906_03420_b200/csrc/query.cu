@@ -28,6 +28,7 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -260,6 +261,26 @@ __device__ __forceinline__ long long upper_row(const unsigned long long *__restr
     return lo;
 }
 
+// Warp-cooperative 32-ary search (all lanes): largest i in [lo, hi) with F[i] <= s, given
+// F[lo] <= s.  log32 steps of one coalesced-ish probe each instead of log2 dependent loads.
+__device__ __forceinline__ long long warp_upper_row(const unsigned long long *__restrict__ F, long long lo,
+                                                    long long hi, unsigned long long s) {
+    const int lane = threadIdx.x & 31;
+    while (hi - lo > 32) {
+        const long long step = (hi - lo + 31) / 32;
+        const long long idx = lo + lane * step;
+        const bool le = idx < hi && __ldg(F + idx) <= s;
+        const unsigned m = __ballot_sync(0xffffffffu, le);
+        const int last = 31 - __clz(m);
+        lo = lo + last * step;
+        hi = min(hi, lo + step);
+    }
+    const long long idx = lo + lane;
+    const bool le = idx < hi && __ldg(F + idx) <= s;
+    const unsigned m = __ballot_sync(0xffffffffu, le);
+    return lo + (31 - __clz(m));
+}
+
 __device__ __forceinline__ bool in_sorted(const int32_t *__restrict__ a, uint32_t n, int32_t x) {
     uint32_t lo = 0, hi = n;
     while (lo < hi) {
@@ -324,8 +345,13 @@ __global__ void __launch_bounds__(kThreads) k_join(const int32_t *__restrict__ M
     const unsigned tile = tile_s;
     const unsigned long long tbase = s0 + (unsigned long long)tile * kJoinTile;
     const unsigned long long tend = min(tbase + (unsigned long long)kJoinTile, s1);
-    if (tid == 0) rlo_s = upper_row(F, 0, nM + 1, tbase);
-    if (tid == 32) rhi_s = upper_row(F, 0, nM + 1, tend - 1);
+    if (warp == 0) {
+        const long long r = warp_upper_row(F, 0, nM + 1, tbase);
+        if (lane == 0) rlo_s = r;
+    } else if (warp == 1) {
+        const long long r = warp_upper_row(F, 0, nM + 1, tend - 1);
+        if (lane == 0) rhi_s = r;
+    }
     __syncthreads();
     const long long rlo = rlo_s, rhi = rhi_s;
     const long long nr = rhi - rlo + 2;   // F[rlo .. rhi+1]
@@ -334,43 +360,61 @@ __global__ void __launch_bounds__(kThreads) k_join(const int32_t *__restrict__ M
         for (long long j = tid; j < nr; j += kThreads) sF[j] = __ldg(F + rlo + j);
     __syncthreads();
 
+    // Phased over the 8 slots of this thread so that each phase's independent loads are in
+    // flight together (row search -> loc -> ci -> C(u) bit -> subtraction -> other lists).
     bool keep[kJoinItems];
     uint32_t xs[kJoinItems];
     uint32_t rows[kJoinItems];
+    unsigned long long fi[kJoinItems];
+    Loc L0[kJoinItems];
 #pragma unroll
     for (int it = 0; it < kJoinItems; it++) {
         const unsigned long long s = tbase + (unsigned long long)it * kThreads + tid;
-        keep[it] = false;
-        xs[it] = 0;
-        rows[it] = 0;
-        if (s < tend) {
-            long long i;
-            unsigned long long fi;
+        keep[it] = s < tend;
+        long long i = rlo;
+        unsigned long long f = 0;
+        if (keep[it]) {
             if (staged) {
                 long long lo = 0, hi = nr - 1;
                 while (hi - lo > 1) {
-                    long long mid = (lo + hi) >> 1;
+                    const long long mid = (lo + hi) >> 1;
                     if (sF[mid] <= s) lo = mid; else hi = mid;
                 }
                 i = rlo + lo;
-                fi = sF[lo];
+                f = sF[lo];
             } else {
                 i = upper_row(F, rlo, rhi + 1, s);
-                fi = __ldg(F + i);
+                f = __ldg(F + i);
             }
-            const Loc *L = loc + i * P.E;
-            const Loc L0 = L[0];
-            const int32_t x = __ldg(ci + L0.off + (uint32_t)(s - fi));
-            bool k = (__ldg(cu_bitmap + (x >> 5)) >> (x & 31)) & 1u;                 // x in C(u)
-            const int32_t *row = M + i * P.t;
-            for (int c = 0; c < P.n_inj && k; c++) k = __ldg(row + P.inj_col[c]) != x;   // subtraction
-            for (int e = 1; e < P.E && k; e++) {
+        }
+        rows[it] = (uint32_t)i;
+        fi[it] = s - f;   // position inside the row's buffer
+    }
+#pragma unroll
+    for (int it = 0; it < kJoinItems; it++)
+        L0[it] = keep[it] ? loc[(long long)rows[it] * P.E] : Loc{0u, 0u};
+#pragma unroll
+    for (int it = 0; it < kJoinItems; it++)
+        xs[it] = keep[it] ? (uint32_t)__ldg(ci + L0[it].off + (uint32_t)fi[it]) : 0u;
+#pragma unroll
+    for (int it = 0; it < kJoinItems; it++) {                                    // x in C(u)
+        const uint32_t x = xs[it];
+        if (keep[it]) keep[it] = (__ldg(cu_bitmap + (x >> 5)) >> (x & 31)) & 1u;
+    }
+    for (int c = 0; c < P.n_inj; c++) {                                         // Alg. 3 line 10
+        const int col = P.inj_col[c];
+#pragma unroll
+        for (int it = 0; it < kJoinItems; it++)
+            if (keep[it]) keep[it] = __ldg(M + (long long)rows[it] * P.t + col) != (int32_t)xs[it];
+    }
+    if (P.E > 1) {                                                               // Alg. 3 line 13
+#pragma unroll
+        for (int it = 0; it < kJoinItems; it++) {
+            const Loc *L = loc + (long long)rows[it] * P.E;
+            for (int e = 1; e < P.E && keep[it]; e++) {
                 const Loc Le = L[e];
-                k = in_sorted(ci + Le.off, Le.len, x);                                   // intersection
+                keep[it] = in_sorted(ci + Le.off, Le.len, (int32_t)xs[it]);
             }
-            keep[it] = k;
-            xs[it] = (uint32_t)x;
-            rows[it] = (uint32_t)i;
         }
     }
 
@@ -674,6 +718,35 @@ cudaError_t d2h(gsi_stats &S, void *dst, const void *src, size_t bytes, cudaStre
 cudaError_t h2d(gsi_stats &S, void *dst, const void *src, size_t bytes, cudaStream_t st) {
     S.h2d_bytes += bytes;
     return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
+}
+
+// Keep freed stream-ordered allocations in the device pool (the default release threshold of
+// 0 returns them to the driver at every synchronisation, and re-mapping tens of GB per level
+// costs far more than the kernels).  Budget = free + reserved-but-unused pool memory.
+std::mutex g_pool_mu;
+bool g_pool_ready[64] = {false};
+void ensure_pool(int dev) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (dev < 0 || dev >= 64 || g_pool_ready[dev]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    g_pool_ready[dev] = true;
+}
+unsigned long long available_bytes(int dev) {
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    cudaMemPool_t pool;
+    uint64_t reserved = 0, used = 0;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    }
+    cudaGetLastError();
+    return (unsigned long long)fr + (reserved > used ? reserved - used : 0);
 }
 
 double now_ms() {
@@ -1083,6 +1156,7 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     const gsi_query_opts &opts = C.opts;
     const double t_start = now_ms();
     GSI_CUDA(cudaSetDevice(g->device));
+    ensure_pool(g->device);
     cudaStream_t st = opts.stream ? (cudaStream_t)opts.stream : cudaStreamPerThread;
     const int k = q->k;
     const long long n = g->n;
@@ -1159,9 +1233,8 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     // memory budget -> chunk capacity in GBA slots (bytes per slot per level: S,R 8 B,
     // M' 4(t+1) B, the child level's loc/F 8E+8 B), over the k-1 levels that may nest.
     {
-        size_t fr = 0, tot = 0;
-        GSI_CUDA(cudaMemGetInfo(&fr, &tot));
-        unsigned long long budget = opts.mem_budget_bytes ? opts.mem_budget_bytes : (unsigned long long)(0.85 * fr);
+        unsigned long long budget =
+            opts.mem_budget_bytes ? opts.mem_budget_bytes : (unsigned long long)(0.85 * available_bytes(g->device));
         int maxE = 1;
         for (auto &s : C.steps) maxE = std::max(maxE, (int)s.col.size());
         const double per_slot = 8.0 + 4.0 * (k + 1) + 8.0 * maxE + 8.0;

@@ -146,7 +146,7 @@ class GraphHandle:
 
     def __del__(self):
         h = getattr(self, "h", None)
-        if h:
+        if h and lib is not None:
             lib.gsi_graph_free(h)
             self.h = None
 
@@ -205,7 +205,7 @@ class Result:
 
     def __del__(self):
         h = getattr(self, "h", None)
-        if h:
+        if h and lib is not None:
             lib.gsi_result_free(h)
             self.h = None
 
@@ -248,7 +248,7 @@ class Prepared:
 
     def __del__(self):
         h = getattr(self, "h", None)
-        if h:
+        if h and lib is not None:
             lib.gsi_prepared_free(h)
             self.h = None
 
