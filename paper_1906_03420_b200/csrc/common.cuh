@@ -187,6 +187,44 @@ __device__ __forceinline__ Loc pcsr_lookup(const uint2 *__restrict__ groups, int
     return r;
 }
 
+// N independent lookups in one partition, phased so that their first-sector loads are all in
+// flight together (the common case resolves from sector 0: a hit in slots 0-2, or an empty
+// slot proving absence).  Anything else falls back to the full lookup.
+template <int N>
+__device__ __forceinline__ void pcsr_lookup_batch(const uint2 *__restrict__ groups, int gpn, uint64_t gbase,
+                                                  uint32_t ngroups, uint32_t l_dense, const uint32_t (&v)[N],
+                                                  const bool (&valid)[N], Loc (&out)[N]) {
+    if (gpn != 16 || ngroups == 0) {
+#pragma unroll
+        for (int q = 0; q < N; q++)
+            out[q] = valid[q] ? pcsr_lookup(groups, gpn, gbase, ngroups, l_dense, v[q], nullptr) : Loc{0u, 0u};
+        return;
+    }
+    uint4 a[N], b[N];
+#pragma unroll
+    for (int q = 0; q < N; q++) {
+        if (valid[q]) {
+            const uint4 *G4 = reinterpret_cast<const uint4 *>(groups + (gbase + pcsr_home(v[q], l_dense, ngroups)) * 16ull);
+            a[q] = __ldg(G4);
+            b[q] = __ldg(G4 + 1);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < N; q++) {
+        out[q] = Loc{0u, 0u};
+        if (!valid[q]) continue;
+        const uint32_t x = v[q];
+        bool done = true;
+        if (a[q].x == x) out[q] = Loc{a[q].y, a[q].w - a[q].y};
+        else if (a[q].z == x) out[q] = Loc{a[q].w, b[q].y - a[q].w};
+        else if (b[q].x == x) out[q] = Loc{b[q].y, b[q].w - b[q].y};
+        else if (b[q].z == x) done = false;                                   // slot 3: run ends in sector 1
+        else if (a[q].x == kEmpty || a[q].z == kEmpty || b[q].x == kEmpty || b[q].z == kEmpty) done = true;  // absent
+        else done = false;                                                    // full sector: keep probing
+        if (!done) out[q] = pcsr_lookup(groups, gpn, gbase, ngroups, l_dense, x, nullptr);
+    }
+}
+
 // ------------------------------------------------------- decoupled look-back scan ---
 constexpr uint64_t kFlagA = 1ull << 62;
 constexpr uint64_t kFlagP = 2ull << 62;
@@ -333,7 +371,7 @@ struct gsi_prepared {
     uint32_t *d_qsig = nullptr;
     bool absent_label = false;
     ~gsi_prepared() {
-        if (d_qsig) cudaFree(d_qsig);
+        if (d_qsig) cudaFreeAsync(d_qsig, cudaStreamPerThread);
     }
 };
 
@@ -347,6 +385,6 @@ struct gsi_result {
     bool has_table = false;
     gsi_stats stats;
     ~gsi_result() {
-        if (table) cudaFree(table);
+        if (table) cudaFreeAsync(table, cudaStreamPerThread);
     }
 };

@@ -41,7 +41,6 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kJoinItems = 8;
 constexpr int kJoinTile = kThreads * kJoinItems;   // 2048 GBA slots per CTA
-constexpr int kSmemF = 2048 + 1;                   // staged F entries per join tile
 
 struct StepParams {
     int t;                       // columns of M (current level)
@@ -251,16 +250,6 @@ __global__ void __launch_bounds__(kThreads) k_probe(const int32_t *__restrict__ 
 }
 
 // ---------------------------------------------------------------------- join --------
-__device__ __forceinline__ long long upper_row(const unsigned long long *__restrict__ F, long long lo, long long hi,
-                                               unsigned long long s) {
-    // largest i in [lo, hi) with F[i] <= s  (F non-decreasing, F[lo] <= s)
-    while (hi - lo > 1) {
-        long long mid = (lo + hi) >> 1;
-        if (__ldg(F + mid) <= s) lo = mid; else hi = mid;
-    }
-    return lo;
-}
-
 // Warp-cooperative 32-ary search (all lanes): largest i in [lo, hi) with F[i] <= s, given
 // F[lo] <= s.  log32 steps of one coalesced-ish probe each instead of log2 dependent loads.
 __device__ __forceinline__ long long warp_upper_row(const unsigned long long *__restrict__ F, long long lo,
@@ -330,7 +319,8 @@ __global__ void __launch_bounds__(kThreads) k_join(const int32_t *__restrict__ M
                                                    unsigned long long *__restrict__ F2,
                                                    unsigned long long *status, unsigned long long *status2,
                                                    unsigned *tile_ctr, Counters *ctr) {
-    __shared__ unsigned long long sF[kSmemF];          // staged F; reused for len0' of new rows
+    __shared__ int sR[kJoinTile];                       // row offset (from rlo) of every tile slot
+    __shared__ uint32_t sl[MODE == J_NEXT ? kJoinTile : 1];   // len0' of the new rows
     __shared__ uint32_t sx[MODE == J_COUNT ? 1 : kJoinTile];
     __shared__ uint32_t si[MODE == J_COUNT ? 1 : kJoinTile];
     __shared__ unsigned wcnt[kJoinItems][kThreads / 32];
@@ -352,16 +342,42 @@ __global__ void __launch_bounds__(kThreads) k_join(const int32_t *__restrict__ M
         const long long r = warp_upper_row(F, 0, nM + 1, tend - 1);
         if (lane == 0) rhi_s = r;
     }
+    for (int j = tid; j < kJoinTile; j += kThreads) sR[j] = 0;
     __syncthreads();
     const long long rlo = rlo_s, rhi = rhi_s;
-    const long long nr = rhi - rlo + 2;   // F[rlo .. rhi+1]
-    const bool staged = nr <= kSmemF;
-    if (staged)
-        for (long long j = tid; j < nr; j += kThreads) sF[j] = __ldg(F + rlo + j);
+    // Row of every slot of the tile without a per-slot search (load-balanced search): each row
+    // overlapping the tile marks its first tile-local slot, then an inclusive max-scan over the
+    // 2048 slots spreads the row offset to all its slots.
+    for (long long r = tid; r <= rhi - rlo; r += kThreads) {
+        const unsigned long long a = __ldg(F + rlo + r), b = __ldg(F + rlo + r + 1);
+        if (a < b && b > tbase && a < tend) sR[a > tbase ? (unsigned)(a - tbase) : 0u] = (int)r;
+    }
+    __syncthreads();
+    {
+        int v[kJoinItems], m = 0;
+#pragma unroll
+        for (int q = 0; q < kJoinItems; q++) {
+            v[q] = sR[tid * kJoinItems + q];
+            m = max(m, v[q]);
+            v[q] = m;
+        }
+        int inc = m;   // inclusive max-scan of thread maxima across the block
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) inc = max(inc, __shfl_up_sync(0xffffffffu, inc, o) * (lane >= o));
+        if (lane == 31) wcnt[0][warp] = (unsigned)inc;
+        __syncthreads();
+        int carry = 0;
+        for (int w = 0; w < warp; w++) carry = max(carry, (int)wcnt[0][w]);
+        int prev = __shfl_up_sync(0xffffffffu, inc, 1);
+        if (lane == 0) prev = 0;
+        carry = max(carry, prev);
+#pragma unroll
+        for (int q = 0; q < kJoinItems; q++) sR[tid * kJoinItems + q] = max(v[q], carry);
+    }
     __syncthreads();
 
     // Phased over the 8 slots of this thread so that each phase's independent loads are in
-    // flight together (row search -> loc -> ci -> C(u) bit -> subtraction -> other lists).
+    // flight together (loc -> ci -> C(u) bit -> subtraction -> other lists).
     bool keep[kJoinItems];
     uint32_t xs[kJoinItems];
     uint32_t rows[kJoinItems];
@@ -371,24 +387,9 @@ __global__ void __launch_bounds__(kThreads) k_join(const int32_t *__restrict__ M
     for (int it = 0; it < kJoinItems; it++) {
         const unsigned long long s = tbase + (unsigned long long)it * kThreads + tid;
         keep[it] = s < tend;
-        long long i = rlo;
-        unsigned long long f = 0;
-        if (keep[it]) {
-            if (staged) {
-                long long lo = 0, hi = nr - 1;
-                while (hi - lo > 1) {
-                    const long long mid = (lo + hi) >> 1;
-                    if (sF[mid] <= s) lo = mid; else hi = mid;
-                }
-                i = rlo + lo;
-                f = sF[lo];
-            } else {
-                i = upper_row(F, rlo, rhi + 1, s);
-                f = __ldg(F + i);
-            }
-        }
+        const long long i = rlo + sR[it * kThreads + tid];
         rows[it] = (uint32_t)i;
-        fi[it] = s - f;   // position inside the row's buffer
+        fi[it] = keep[it] ? s - __ldg(F + i) : 0ull;   // position inside the row's buffer
     }
 #pragma unroll
     for (int it = 0; it < kJoinItems; it++)
@@ -500,15 +501,39 @@ __global__ void __launch_bounds__(kThreads) k_join(const int32_t *__restrict__ M
             if (tile == gridDim.x - 1 && tid == 0) ctr->total = base + cnt;
         } else {
             // ---- probe-ahead: the next step's Prealloc on the new rows ------------------------
-            uint32_t *sl = reinterpret_cast<uint32_t *>(sF);   // len0' per new row (2048 x 4 B)
             unsigned long long elems = 0, act = 0;
-            for (unsigned j = tid; j < cnt; j += kThreads) {
-                unsigned long long l0, el;
-                probe_row(M + (long long)si[j] * P.t, P.t, sx[j], P2, groups, gpn,
-                          loc2 + (base + j) * (unsigned long long)P2.E, l0, el);
-                sl[j] = (uint32_t)l0;
-                elems += el;
-                act += l0 ? 1 : 0;
+            if (P2.E == 1) {
+                // tree-shaped step (one linking edge): batched, phased first-sector probes
+                const int c2 = P2.col[0];
+                uint32_t v[kJoinItems];
+                bool ok[kJoinItems];
+                Loc r[kJoinItems];
+#pragma unroll
+                for (int q = 0; q < kJoinItems; q++) {
+                    const unsigned j = tid + q * kThreads;
+                    ok[q] = j < cnt;
+                    v[q] = 0;
+                    if (ok[q]) v[q] = c2 < P.t ? (uint32_t)__ldg(M + (long long)si[j] * P.t + c2) : sx[j];
+                }
+                pcsr_lookup_batch<kJoinItems>(groups, gpn, P2.gbase[0], P2.ngroups[0], P2.lab[0], v, ok, r);
+#pragma unroll
+                for (int q = 0; q < kJoinItems; q++) {
+                    const unsigned j = tid + q * kThreads;
+                    if (!ok[q]) continue;
+                    loc2[base + j] = r[q];
+                    sl[j] = r[q].len;
+                    elems += r[q].len;
+                    act += r[q].len ? 1 : 0;
+                }
+            } else {
+                for (unsigned j = tid; j < cnt; j += kThreads) {
+                    unsigned long long l0, el;
+                    probe_row(M + (long long)si[j] * P.t, P.t, sx[j], P2, groups, gpn,
+                              loc2 + (base + j) * (unsigned long long)P2.E, l0, el);
+                    sl[j] = (uint32_t)l0;
+                    elems += el;
+                    act += l0 ? 1 : 0;
+                }
             }
             elems = warp_sum_u64(elems);
             act = warp_sum_u64(act);
@@ -834,8 +859,12 @@ gsi_status prepare_impl(const gsi_graph *g, int32_t k, const int32_t *qvl, int32
     p->qsig.resize((size_t)k * kPlanes);
     encode_query_signatures(k, qvl, qm, qs, qd, qe, p->qsig.data());
     GSI_CUDA(cudaSetDevice(g->device));
-    GSI_CUDA(cudaMalloc(&p->d_qsig, p->qsig.size() * 4));
-    GSI_CUDA(cudaMemcpy(p->d_qsig, p->qsig.data(), p->qsig.size() * 4, cudaMemcpyHostToDevice));
+    // stream-ordered allocation: a plain cudaMalloc here would make the driver trim the
+    // stream-ordered pool the join levels keep reserved
+    GSI_CUDA(cudaMallocAsync(&p->d_qsig, p->qsig.size() * 4, cudaStreamPerThread));
+    GSI_CUDA(cudaMemcpyAsync(p->d_qsig, p->qsig.data(), p->qsig.size() * 4, cudaMemcpyHostToDevice,
+                             cudaStreamPerThread));
+    GSI_CUDA(cudaStreamSynchronize(cudaStreamPerThread));
     *out = p.release();
     return GSI_OK;
 }
