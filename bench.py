@@ -40,6 +40,7 @@ BENCH_CONFIGS = {
     "C4": dict(kind="C4", desc="road-shaped lattice 3742^2 m=17M |L_V|=|L_E|=1000"),
     "C5a": dict(kind="C5a", desc="R-MAT scale 25 ef 8 (~250M E) |L_V|=1000 |L_E|=86"),
     "C5b": dict(kind="C5b", desc="R-MAT scale 25 ef 8 (~250M E) |L_V|=10 |L_E|=86"),
+    "C5m": dict(kind="C5m", desc="R-MAT scale 25 ef 8 (~264M E) |L_V|=100 |L_E|=86 (join-stress, bounded)"),
 }
 
 
@@ -313,6 +314,8 @@ def run_gsi(args):
     ms_per_step = ms / args.steps
     value = total_matches * args.steps / (ms / 1000.0)
     launches = sum(s["total_launches"] for s in launch_stats)
+    capped = sum(s["capped"] for s in launch_stats) / args.steps
+    q_ms = np.array([s["ms_total"] for s in launch_stats])
 
     # ---- e2e: public API from host arrays, H2D of the query + D2H of the count -----------
     if ws > 1:
@@ -382,6 +385,8 @@ def run_gsi(args):
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "int32", "data": "synthetic", "config": workload_config(args, g),
         "ms_per_query": ms_per_step / len(qs), "matches_per_step": total_matches,
+        "query_ms_p50": float(np.percentile(q_ms, 50)), "query_ms_p95": float(np.percentile(q_ms, 95)),
+        "capped_queries_per_step": capped, "query_timeout_s": args.query_timeout,
         "e2e": {"value": m_e2e * args.steps / e2e_s, "unit": "matches/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_query": 1000.0 * e2e_s / args.steps / len(qs)},
         "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": launches,
@@ -400,11 +405,12 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["gsi", "reference"], default="gsi")
-    ap.add_argument("--config", choices=sorted(BENCH_CONFIGS), default="C5b")
+    ap.add_argument("--config", choices=sorted(BENCH_CONFIGS), default="C5m")
     ap.add_argument("--scale", type=int, default=None, help="override the R-MAT scale (C5 only)")
-    ap.add_argument("--queries", type=int, default=100)
+    ap.add_argument("--queries", type=int, default=16)
     ap.add_argument("--k", type=int, default=12)
-    ap.add_argument("--query-timeout", type=float, default=0.0)
+    ap.add_argument("--query-timeout", type=float, default=1.0,
+                    help="per-query cap; a capped query reports the exact count of its completed prefix")
     ap.add_argument("--ref-query-timeout", type=float, default=5.0)
     ap.add_argument("--ref-step-budget", type=float, default=8.0)
     ap.add_argument("--cpu-budget", type=float, default=20.0)

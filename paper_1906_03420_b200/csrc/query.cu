@@ -83,35 +83,52 @@ __global__ void __launch_bounds__(kThreads) k_filter(const uint32_t *__restrict_
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-    for (long long w = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); w < words; w += warps) {
-        const long long v = w * 32 + lane;
-        const bool valid = v < n;
-        const uint32_t lab = valid ? __ldcs(sig + v) : 0u;
-        uint32_t mask = 0;
-        for (int u = 0; u < k; u++)
-            if (valid && lab == qs[u * kPlanes]) mask |= 1u << u;   // label field by equality (A4)
-        if (!label_only && mask) {
-            uint32_t p[kPlanes];
+    constexpr int kFW = 4;   // bitmap words per warp per iteration: 4 coalesced plane-0 loads in flight
+    for (long long w0 = (blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5)) * kFW; w0 < words;
+         w0 += warps * kFW) {
+        uint32_t lab[kFW], mask[kFW];
 #pragma unroll
-            for (int pl = 1; pl < kPlanes; pl++) p[pl] = __ldcs(sig + (long long)pl * n + v);
-            uint32_t mm = mask;
-            while (mm) {
-                int u = __ffs(mm) - 1;
-                mm &= mm - 1;
-                const uint32_t *s = qs + u * kPlanes;
-                bool ok = true;
+        for (int j = 0; j < kFW; j++) {
+            const long long v = (w0 + j) * 32 + lane;
+            lab[j] = (w0 + j < words && v < n) ? __ldcs(sig + v) : 0xFFFFFFFFu;   // labels are < 2^31
+        }
 #pragma unroll
-                for (int pl = 1; pl < kPlanes; pl++) ok &= (p[pl] & s[pl]) == s[pl];   // S(v)&S(u)=S(u), L543
-                if (!ok) mask &= ~(1u << u);
+        for (int j = 0; j < kFW; j++) {
+            mask[j] = 0;
+            for (int u = 0; u < k; u++)
+                if (lab[j] == qs[u * kPlanes]) mask[j] |= 1u << u;   // label field by equality (A4)
+        }
+        if (!label_only) {
+#pragma unroll
+            for (int j = 0; j < kFW; j++) {
+                if (!mask[j]) continue;
+                const long long v = (w0 + j) * 32 + lane;
+                uint32_t p[kPlanes];
+#pragma unroll
+                for (int pl = 1; pl < kPlanes; pl++) p[pl] = __ldcs(sig + (long long)pl * n + v);
+                uint32_t mm = mask[j];
+                while (mm) {
+                    const int u = __ffs(mm) - 1;
+                    mm &= mm - 1;
+                    const uint32_t *sq = qs + u * kPlanes;
+                    bool ok = true;
+#pragma unroll
+                    for (int pl = 1; pl < kPlanes; pl++) ok &= (p[pl] & sq[pl]) == sq[pl];   // S(v)&S(u)=S(u)
+                    if (!ok) mask[j] &= ~(1u << u);
+                }
             }
         }
-        unsigned loaded = __ballot_sync(0xffffffffu, !label_only && valid && lab != 0xFFFFFFFFu && mask != 0);
-        if (lane == 0 && loaded) atomicAdd(&loads_s, (unsigned long long)__popc(loaded));
-        for (int u = 0; u < k; u++) {
-            unsigned b = __ballot_sync(0xffffffffu, (mask >> u) & 1u);
-            if (lane == 0) {
-                bitmaps[(long long)u * words + w] = b;
-                if (b) atomicAdd(&cnt_s[u], (unsigned long long)__popc(b));
+#pragma unroll
+        for (int j = 0; j < kFW; j++) {
+            if (w0 + j >= words) break;
+            const unsigned loaded = __ballot_sync(0xffffffffu, !label_only && lab[j] != 0xFFFFFFFFu && mask[j] != 0);
+            if (lane == 0 && loaded) atomicAdd(&loads_s, (unsigned long long)__popc(loaded));
+            for (int u = 0; u < k; u++) {
+                const unsigned b = __ballot_sync(0xffffffffu, (mask[j] >> u) & 1u);
+                if (lane == 0) {
+                    bitmaps[(long long)u * words + w0 + j] = b;
+                    if (b) atomicAdd(&cnt_s[u], (unsigned long long)__popc(b));
+                }
             }
         }
     }
@@ -1228,7 +1245,7 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
-        unsigned grid = (unsigned)std::min<long long>((words + 7) / 8, (long long)sms * 8);
+        unsigned grid = (unsigned)std::min<long long>((words + 31) / 32, (long long)sms * 8);
         if (grid < 1) grid = 1;
         prof.begin(GSI_K_FILTER);
         k_filter<<<grid, kThreads, 0, st>>>(g->sig, n, k, q->d_qsig, opts.filter_mode == 1, bm, words, d_counts,

@@ -49,6 +49,7 @@ for i, q in enumerate(qs):
     tot_c += r.count
     tot_ms += ms
     print(json.dumps({"q": i, "E": q.m, "count": r.count, "ms": round(ms, 2), "capped": s["capped"],
-                      "rows": s["rows"][:q.n], "gba": s["gba"][1:q.n], "chunks": s["n_chunks"],
+                      "rows": s["rows"][:q.n], "gba": s["gba"][1:q.n], "chunks": s["n_chunks"], "ms_filter": round(s["ms_filter"], 3), "ms_plan": round(s["ms_plan"], 3),
+                      "ms_join": round(s["ms_join"], 3), "launches": s["total_launches"],
                       "cand": s["cand"][:q.n]}), flush=True)
 print(f"TOTAL matches={tot_c} ms={tot_ms:.1f} matches/s={tot_c / (tot_ms / 1e3):.3e}")

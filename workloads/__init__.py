@@ -451,6 +451,9 @@ CONFIGS = {
     "C4": ("road_grid", dict(side=3_742, m=17_000_000, nlv=1_000, nle=1_000)),
     "C5a": ("rmat", dict(scale=25, edge_factor=8, nlv=1_000, nle=86)),
     "C5b": ("rmat", dict(scale=25, edge_factor=8, nlv=10, nle=86)),
+    # join-stress variant sized for a bounded bench: |L_V| = 10 gives 10^10-10^11 matches per
+    # 12-vertex walk query at scale 25, |L_V| = 1000 gives 1-100
+    "C5m": ("rmat", dict(scale=25, edge_factor=8, nlv=100, nle=86)),
 }
 
 
