@@ -214,14 +214,17 @@ gsi_status gsi_debug_lookup(const gsi_graph *g, int64_t nq, const int32_t *v, co
                             int64_t *len, int32_t *groups_read, int32_t *nbrs, int64_t cap);
 /* Copy the column-first signature table (16 x n uint32) to host. */
 gsi_status gsi_debug_signatures(const gsi_graph *g, uint32_t *planes);
-/* Run only the filter kernel: bitmaps (k x ceil(n/32) uint32) and |C(u)| to host. */
+/* Run only the filter kernel: bitmaps (k x ceil(n/32) uint32) and |C(u)| to host.
+ * filter_mode 0 = signatures (isomorphism encoding), 1 = label only, 2 = signatures with the
+ * homomorphism (distinct-key) query encoding. */
 gsi_status gsi_debug_filter(const gsi_graph *g, int32_t k, const int32_t *q_vlabels, int32_t qm,
                             const int32_t *q_src, const int32_t *q_dst, const int32_t *q_elabels,
                             int32_t filter_mode, uint32_t *bitmaps, int64_t *counts);
-/* Host query signatures (k x 16 uint32) as encoded by the library. */
+/* Host query signatures (k x 16 uint32) as encoded by the library; distinct = 1 gives the
+ * homomorphism encoding (each (edge label, neighbour label) key counted once). */
 gsi_status gsi_debug_query_signatures(int32_t k, const int32_t *q_vlabels, int32_t qm,
                                       const int32_t *q_src, const int32_t *q_dst,
-                                      const int32_t *q_elabels, uint32_t *qsig);
+                                      const int32_t *q_elabels, int32_t distinct, uint32_t *qsig);
 
 /* ------------------------------------------------------------------ misc ------------ */
 const char *gsi_last_error(void);

@@ -59,7 +59,7 @@ def lib():
         L.og_degree.restype = I64
         L.og_degree.argtypes = [P, I32]
         L.og_signatures.argtypes = [P, P]
-        L.og_query_signatures.argtypes = [I32, P, I32, P, P, P, P]
+        L.og_query_signatures.argtypes = [I32, P, I32, P, P, P, I32, P]
         L.og_filter.argtypes = [P, P, I32, P, P, P]
         L.og_fingerprint_rows.argtypes = [P, I64, I32, P]
         L.og_sig_group_of.restype = I32
@@ -159,11 +159,12 @@ def signatures(og: OracleGraph) -> np.ndarray:
     return planes
 
 
-def query_signatures(q) -> np.ndarray:
-    """Query signatures, shape (k, 16) uint32 (PAPER.md L545 'same encoding strategy')."""
+def query_signatures(q, distinct: bool = False) -> np.ndarray:
+    """Query signatures, shape (k, 16) uint32 (PAPER.md L545 'same encoding strategy');
+    distinct=True is the homomorphism encoding (each pair counted once)."""
     out = np.zeros((q.n, 16), np.uint32)
     lib().og_query_signatures(q.n, _p(_i32(q.vlabels)), len(q.src), _p(_i32(q.src)), _p(_i32(q.dst)),
-                              _p(_i32(q.elabels)), _p(out))
+                              _p(_i32(q.elabels)), int(distinct), _p(out))
     return out
 
 

@@ -407,15 +407,25 @@ void og_signatures(const og_graph *g, uint32_t *planes) {
     }
 }
 
-/* Query signatures: qsig[u * 16 + w] over the query edges incident to u. */
+/* Query signatures: qsig[u * 16 + w] over the query edges incident to u.  distinct != 0:
+ * each (edge label, neighbour label) pair counted once — under homomorphism two query
+ * neighbours with the same pair may map to one data neighbour, so
+ * only the set of pairs is necessary. */
 void og_query_signatures(int32_t k, const int32_t *qvl, int32_t qm, const int32_t *qs, const int32_t *qd,
-                         const int32_t *qe, uint32_t *qsig) {
+                         const int32_t *qe, int32_t distinct, uint32_t *qsig) {
     int32_t pe[4 * OG_MAXK * OG_MAXK], pn[4 * OG_MAXK * OG_MAXK];
     for (int32_t u = 0; u < k; u++) {
         int64_t c = 0;
         for (int32_t e = 0; e < qm; e++) {
-            if (qs[e] == u) { pe[c] = qe[e]; pn[c] = qvl[qd[e]]; c++; }
-            else if (qd[e] == u) { pe[c] = qe[e]; pn[c] = qvl[qs[e]]; c++; }
+            int32_t l, nl;
+            if (qs[e] == u) { l = qe[e]; nl = qvl[qd[e]]; }
+            else if (qd[e] == u) { l = qe[e]; nl = qvl[qs[e]]; }
+            else continue;
+            int dup = 0;
+            if (distinct)
+                for (int64_t i = 0; i < c; i++) if (pe[i] == l && pn[i] == nl) dup = 1;
+            if (dup) continue;
+            pe[c] = l; pn[c] = nl; c++;
         }
         og_encode(qvl[u], c, pe, pn, qsig + (int64_t)u * OG_SIG_PLANES);
     }

@@ -239,7 +239,7 @@ gsi_status gsi_query(const gsi_graph *g, int32_t k, const int32_t *qvl, int32_t 
     GSI_TRY(prepare_impl(g, k, qvl, qm, qs, qd, qe, &p));
     std::unique_ptr<gsi_prepared> guard(p);
     gsi_status rc = run_impl(g, p, opts, out);
-    if (rc == GSI_OK) (*out)->stats.h2d_bytes += 4ull * p->qsig.size();   // encoded Q signatures
+    if (rc == GSI_OK) (*out)->stats.h2d_bytes += 4ull * p->qsig.size();   // encoded Q signatures (iso + hom)
     return rc;
 }
 
@@ -337,12 +337,12 @@ gsi_status gsi_debug_filter(const gsi_graph *g, int32_t k, const int32_t *qvl, i
 }
 
 gsi_status gsi_debug_query_signatures(int32_t k, const int32_t *qvl, int32_t qm, const int32_t *qs, const int32_t *qd,
-                                      const int32_t *qe, uint32_t *qsig) {
+                                      const int32_t *qe, int32_t distinct, uint32_t *qsig) {
     if (k < 1 || k > GSI_MAX_K || !qvl || !qsig || (qm && (!qs || !qd || !qe))) {
         set_error("invalid argument");
         return GSI_ERR_INVALID_ARG;
     }
-    encode_query_signatures(k, qvl, qm, qs, qd, qe, qsig);
+    encode_query_signatures(k, qvl, qm, qs, qd, qe, qsig, distinct ? 1 : 0);
     return GSI_OK;
 }
 

@@ -335,7 +335,7 @@ gsi_status cuda_fail(cudaError_t e, const char *what);
 
 // Encode the query signatures on the host (same spec as the data side).
 void encode_query_signatures(int32_t k, const int32_t *qvl, int32_t qm, const int32_t *qs, const int32_t *qd,
-                             const int32_t *qe, uint32_t *qsig /* k*16 */);
+                             const int32_t *qe, uint32_t *qsig /* k*16 */, int distinct);
 
 }  // namespace gsi
 
@@ -367,7 +367,7 @@ struct gsi_prepared {
     int k = 0;
     std::vector<int32_t> qvl, qs, qd, qe;
     std::vector<int> qe_dense;       // -1: label absent from G
-    std::vector<uint32_t> qsig;      // k * 16
+    std::vector<uint32_t> qsig;      // 2 * k * 16: iso signatures, then homomorphism signatures
     uint32_t *d_qsig = nullptr;
     bool absent_label = false;
     ~gsi_prepared() {

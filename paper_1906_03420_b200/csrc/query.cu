@@ -235,6 +235,32 @@ __device__ __forceinline__ void probe_row(const int32_t *__restrict__ row, int t
     }
 }
 
+// The buffer bound of a candidate new row without writing anything (used to drop rows whose
+// next-step buffer is empty before they are stored).
+__device__ __forceinline__ void probe_row_local(const int32_t *__restrict__ row, int t_parent, uint32_t newv,
+                                                const StepParams &P, const uint2 *__restrict__ groups, int gpn,
+                                                Loc *L, unsigned long long &len0, unsigned long long &elems) {
+    unsigned long long best = ~0ull, sum = 0, first = 0;
+    bool anyzero = false;
+    for (int e = 0; e < P.E; e++) {
+        const int c = P.col[e];
+        const uint32_t v = c < t_parent ? (uint32_t)__ldg(row + c) : newv;
+        const Loc r = pcsr_lookup(groups, gpn, P.gbase[e], P.ngroups[e], P.lab[e], v, nullptr);
+        if (e == 0) first = r.len;
+        best = r.len < best ? r.len : best;
+        anyzero |= r.len == 0;
+        sum += r.len;
+    }
+    (void)L;
+    if (P.per_row_e0) {
+        len0 = anyzero ? 0ull : best;
+        elems = anyzero ? 0ull : sum;
+    } else {
+        len0 = first;
+        elems = sum;
+    }
+}
+
 // Level 1: F[i] = sum_{i'<i} |N(v'_{i'}, l0)|, F[|M|] = |GBA|, by decoupled look-back.
 __global__ void __launch_bounds__(kThreads) k_probe(const int32_t *__restrict__ M, long long nM, StepParams P,
                                                     const uint2 *__restrict__ groups, int gpn,
@@ -267,26 +293,6 @@ __global__ void __launch_bounds__(kThreads) k_probe(const int32_t *__restrict__ 
 }
 
 // ---------------------------------------------------------------------- join --------
-// Warp-cooperative 32-ary search (all lanes): largest i in [lo, hi) with F[i] <= s, given
-// F[lo] <= s.  log32 steps of one coalesced-ish probe each instead of log2 dependent loads.
-__device__ __forceinline__ long long warp_upper_row(const unsigned long long *__restrict__ F, long long lo,
-                                                    long long hi, unsigned long long s) {
-    const int lane = threadIdx.x & 31;
-    while (hi - lo > 32) {
-        const long long step = (hi - lo + 31) / 32;
-        const long long idx = lo + lane * step;
-        const bool le = idx < hi && __ldg(F + idx) <= s;
-        const unsigned m = __ballot_sync(0xffffffffu, le);
-        const int last = 31 - __clz(m);
-        lo = lo + last * step;
-        hi = min(hi, lo + step);
-    }
-    const long long idx = lo + lane;
-    const bool le = idx < hi && __ldg(F + idx) <= s;
-    const unsigned m = __ballot_sync(0xffffffffu, le);
-    return lo + (31 - __clz(m));
-}
-
 __device__ __forceinline__ bool in_sorted(const int32_t *__restrict__ a, uint32_t n, int32_t x) {
     uint32_t lo = 0, hi = n;
     while (lo < hi) {
@@ -312,6 +318,22 @@ __device__ __forceinline__ void row_hash(const int32_t *__restrict__ row, uint32
 
 enum JoinMode { J_COUNT = 0, J_TABLE = 1, J_NEXT = 2 };
 
+// rowmap[j] = the row holding slot s0 + j*kJoinTile (j < ntiles), rowmap[ntiles] = the row
+// holding slot s1-1: the first/last row of every join tile, found by one thread per tile so
+// that no CTA of the join waits on a dependent search of F.
+__global__ void k_tile_rows(const unsigned long long *__restrict__ F, long long nM, unsigned long long s0,
+                            unsigned long long s1, unsigned ntiles, uint32_t *__restrict__ rowmap) {
+    const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (j > ntiles) return;
+    const unsigned long long s = j < ntiles ? s0 + (unsigned long long)j * kJoinTile : s1 - 1;
+    long long lo = 0, hi = nM + 1;   // largest i with F[i] <= s
+    while (hi - lo > 1) {
+        const long long mid = (lo + hi) >> 1;
+        if (__ldg(F + mid) <= s) lo = mid; else hi = mid;
+    }
+    rowmap[j] = (uint32_t)lo;
+}
+
 // The fused level kernel.  Slots [s0, s1) of the Prealloc space (GBA) of this level are cut
 // into 2048-slot tiles.  Per slot: the candidate x = N(v', l0)[s - F_i] of row i is kept iff
 // x in C(u) (bitset, L1150), x not in m_i (Alg. 3 line 10) and x in every other linking list
@@ -319,16 +341,18 @@ enum JoinMode { J_COUNT = 0, J_TABLE = 1, J_NEXT = 2 };
 // cache, L1155-1158), their output offset comes from a decoupled look-back (the Combine scan
 // of Alg. 3 line 14), and the CTA writes its contiguous block of new rows m_i || x with
 // coalesced stores (Alg. 3 lines 15-21).
-//   J_COUNT : final level, count + fingerprint only (no table).
-//   J_TABLE : final level, rows written in query-id order + fingerprint.
-//   J_NEXT  : rows of M_{t+1} written, and the NEXT step's Prealloc probe runs on each new
-//             row while it is in registers (loc2, and F2 by a second look-back chain), so the
-//             next level never re-reads M_{t+1} just to size its buffers.
+//   J_COUNT : final level, count (+ fingerprint) only.
+//   J_TABLE : final level, rows written in query-id order (+ fingerprint).
+//   J_NEXT  : rows of M_{t+1}.  The NEXT step's Prealloc probe runs on every survivor before
+//             the compaction, so a survivor with an empty next buffer (it can never be
+//             extended) is counted but not stored, and the stored rows' loc / F (second
+//             look-back chain) are written here: the next level never re-reads M_{t+1} to
+//             size its buffers.
 template <int MODE>
-__global__ void __launch_bounds__(kThreads) k_join(const int32_t *__restrict__ M, long long nM,
+__global__ void __launch_bounds__(kThreads, MODE == J_NEXT ? 3 : 4) k_join(const int32_t *__restrict__ M, long long nM,
                                                    const unsigned long long *__restrict__ F,
-                                                   const Loc *__restrict__ loc, StepParams P, StepParams P2,
-                                                   const int32_t *__restrict__ ci,
+                                                   const Loc *__restrict__ loc, const uint32_t *__restrict__ rowmap,
+                                                   StepParams P, StepParams P2, const int32_t *__restrict__ ci,
                                                    const uint32_t *__restrict__ cu_bitmap,
                                                    const uint2 *__restrict__ groups, int gpn,
                                                    unsigned long long s0, unsigned long long s1,
@@ -336,32 +360,23 @@ __global__ void __launch_bounds__(kThreads) k_join(const int32_t *__restrict__ M
                                                    unsigned long long *__restrict__ F2,
                                                    unsigned long long *status, unsigned long long *status2,
                                                    unsigned *tile_ctr, Counters *ctr) {
-    __shared__ int sR[kJoinTile];                       // row offset (from rlo) of every tile slot
-    __shared__ uint32_t sl[MODE == J_NEXT ? kJoinTile : 1];   // len0' of the new rows
-    __shared__ uint32_t sx[MODE == J_COUNT ? 1 : kJoinTile];
-    __shared__ uint32_t si[MODE == J_COUNT ? 1 : kJoinTile];
+    __shared__ int sR[kJoinTile];                                   // row offset (from rlo) per tile slot
+    __shared__ uint32_t sx[MODE == J_COUNT ? 1 : kJoinTile];        // write cache: new vertex
+    __shared__ uint32_t si[MODE == J_COUNT ? 1 : kJoinTile];        //              parent row
+    __shared__ Loc sloc[MODE == J_NEXT ? kJoinTile : 1];            //              next buffer (E' = 1)
     __shared__ unsigned wcnt[kJoinItems][kThreads / 32];
     __shared__ unsigned wbase[kJoinItems][kThreads / 32];
     __shared__ unsigned long long sm[33];
     __shared__ unsigned tile_s, agg_s;
-    __shared__ long long rlo_s, rhi_s;
     __shared__ unsigned long long base_s, base2_s;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) tile_s = atomicAdd(tile_ctr, 1u);
+    for (int j = tid; j < kJoinTile; j += kThreads) sR[j] = 0;
     __syncthreads();
     const unsigned tile = tile_s;
     const unsigned long long tbase = s0 + (unsigned long long)tile * kJoinTile;
     const unsigned long long tend = min(tbase + (unsigned long long)kJoinTile, s1);
-    if (warp == 0) {
-        const long long r = warp_upper_row(F, 0, nM + 1, tbase);
-        if (lane == 0) rlo_s = r;
-    } else if (warp == 1) {
-        const long long r = warp_upper_row(F, 0, nM + 1, tend - 1);
-        if (lane == 0) rhi_s = r;
-    }
-    for (int j = tid; j < kJoinTile; j += kThreads) sR[j] = 0;
-    __syncthreads();
-    const long long rlo = rlo_s, rhi = rhi_s;
+    const long long rlo = __ldg(rowmap + tile), rhi = __ldg(rowmap + tile + 1);
     // Row of every slot of the tile without a per-slot search (load-balanced search): each row
     // overlapping the tile marks its first tile-local slot, then an inclusive max-scan over the
     // 2048 slots spreads the row offset to all its slots.
@@ -382,23 +397,21 @@ __global__ void __launch_bounds__(kThreads) k_join(const int32_t *__restrict__ M
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) inc = max(inc, __shfl_up_sync(0xffffffffu, inc, o) * (lane >= o));
         if (lane == 31) wcnt[0][warp] = (unsigned)inc;
-        __syncthreads();
-        int carry = 0;
-        for (int w = 0; w < warp; w++) carry = max(carry, (int)wcnt[0][w]);
         int prev = __shfl_up_sync(0xffffffffu, inc, 1);
-        if (lane == 0) prev = 0;
-        carry = max(carry, prev);
+        __syncthreads();
+        int carry = lane == 0 ? 0 : prev;
+        for (int w = 0; w < warp; w++) carry = max(carry, (int)wcnt[0][w]);
 #pragma unroll
         for (int q = 0; q < kJoinItems; q++) sR[tid * kJoinItems + q] = max(v[q], carry);
     }
     __syncthreads();
 
     // Phased over the 8 slots of this thread so that each phase's independent loads are in
-    // flight together (loc -> ci -> C(u) bit -> subtraction -> other lists).
+    // flight together (loc -> ci -> C(u) bit -> subtraction -> other lists -> next probe).
     bool keep[kJoinItems];
     uint32_t xs[kJoinItems];
     uint32_t rows[kJoinItems];
-    unsigned long long fi[kJoinItems];
+    uint32_t pos[kJoinItems];
     Loc L0[kJoinItems];
 #pragma unroll
     for (int it = 0; it < kJoinItems; it++) {
@@ -406,14 +419,12 @@ __global__ void __launch_bounds__(kThreads) k_join(const int32_t *__restrict__ M
         keep[it] = s < tend;
         const long long i = rlo + sR[it * kThreads + tid];
         rows[it] = (uint32_t)i;
-        fi[it] = keep[it] ? s - __ldg(F + i) : 0ull;   // position inside the row's buffer
+        pos[it] = keep[it] ? (uint32_t)(s - __ldg(F + i)) : 0u;   // position inside the row's buffer
     }
 #pragma unroll
-    for (int it = 0; it < kJoinItems; it++)
-        L0[it] = keep[it] ? loc[(long long)rows[it] * P.E] : Loc{0u, 0u};
+    for (int it = 0; it < kJoinItems; it++) L0[it] = keep[it] ? loc[(long long)rows[it] * P.E] : Loc{0u, 0u};
 #pragma unroll
-    for (int it = 0; it < kJoinItems; it++)
-        xs[it] = keep[it] ? (uint32_t)__ldg(ci + L0[it].off + (uint32_t)fi[it]) : 0u;
+    for (int it = 0; it < kJoinItems; it++) xs[it] = keep[it] ? (uint32_t)__ldg(ci + L0[it].off + pos[it]) : 0u;
 #pragma unroll
     for (int it = 0; it < kJoinItems; it++) {                                    // x in C(u)
         const uint32_t x = xs[it];
@@ -445,15 +456,62 @@ __global__ void __launch_bounds__(kThreads) k_join(const int32_t *__restrict__ M
             if (P.fp) row_hash(M + (long long)rows[it] * P.t, xs[it], P, h1, h2);
         }
         c = warp_sum_u64(c);
-        h1 = warp_sum_u64(h1);
+        if (lane == 0 && c) atomicAdd(&ctr->count, c);
+        if (P.fp) {
+            h1 = warp_sum_u64(h1);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) h2 ^= __shfl_xor_sync(0xffffffffu, h2, o);
-        if (lane == 0 && c) {
-            atomicAdd(&ctr->count, c);
-            atomicAdd(&ctr->fp1, h1);
-            atomicXor(&ctr->fp2, h2);
+            for (int o = 16; o > 0; o >>= 1) h2 ^= __shfl_xor_sync(0xffffffffu, h2, o);
+            if (lane == 0 && c) {
+                atomicAdd(&ctr->fp1, h1);
+                atomicXor(&ctr->fp2, h2);
+            }
         }
     } else {
+        // ---- J_NEXT: next-step probe of every survivor, dead rows dropped --------------------
+        Loc N0[kJoinItems];
+        if constexpr (MODE == J_NEXT) {
+            unsigned long long all = 0;
+#pragma unroll
+            for (int it = 0; it < kJoinItems; it++) all += keep[it] ? 1 : 0;
+            all = warp_sum_u64(all);
+            if (lane == 0 && all) atomicAdd(&ctr->count, all);      // |M_{t+1}| including dead rows
+            if (P2.E == 1) {
+                const int c2 = P2.col[0];
+                uint32_t v[kJoinItems];
+#pragma unroll
+                for (int it = 0; it < kJoinItems; it++)
+                    v[it] = keep[it] ? (c2 < P.t ? (uint32_t)__ldg(M + (long long)rows[it] * P.t + c2) : xs[it]) : 0u;
+                // two half-batches of 4 keep the 8 first-sector loads (8 words each) in fewer registers
+                uint32_t va[4], vb[4];
+                bool ka[4], kb[4];
+                Loc na[4], nb[4];
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    va[q] = v[q];
+                    ka[q] = keep[q];
+                    vb[q] = v[q + 4];
+                    kb[q] = keep[q + 4];
+                }
+                pcsr_lookup_batch<4>(groups, gpn, P2.gbase[0], P2.ngroups[0], P2.lab[0], va, ka, na);
+                pcsr_lookup_batch<4>(groups, gpn, P2.gbase[0], P2.ngroups[0], P2.lab[0], vb, kb, nb);
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    N0[q] = na[q];
+                    N0[q + 4] = nb[q];
+                }
+#pragma unroll
+                for (int it = 0; it < kJoinItems; it++) keep[it] = keep[it] && N0[it].len > 0;
+            } else {
+#pragma unroll
+                for (int it = 0; it < kJoinItems; it++) {
+                    if (!keep[it]) continue;
+                    unsigned long long l0, el;
+                    probe_row_local(M + (long long)rows[it] * P.t, P.t, xs[it], P2, groups, gpn, nullptr, l0, el);
+                    keep[it] = l0 > 0;
+                    N0[it] = Loc{0u, (uint32_t)l0};
+                }
+            }
+        }
         // ---- ordered compaction into the shared-memory write cache + look-back ------------
         unsigned ballots[kJoinItems];
 #pragma unroll
@@ -491,6 +549,7 @@ __global__ void __launch_bounds__(kThreads) k_join(const int32_t *__restrict__ M
                 const unsigned lp = wbase[it][warp] + __popc(ballots[it] & lt);
                 sx[lp] = xs[it];
                 si[lp] = rows[it];
+                if constexpr (MODE == J_NEXT) sloc[lp] = N0[it];
             }
         }
         __syncthreads();
@@ -517,52 +576,32 @@ __global__ void __launch_bounds__(kThreads) k_join(const int32_t *__restrict__ M
             }
             if (tile == gridDim.x - 1 && tid == 0) ctr->total = base + cnt;
         } else {
-            // ---- probe-ahead: the next step's Prealloc on the new rows ------------------------
-            unsigned long long elems = 0, act = 0;
+            // ---- next-level loc (E' = 1: from the write cache; else probe again) -----------
+            unsigned long long elems = 0;
             if (P2.E == 1) {
-                // tree-shaped step (one linking edge): batched, phased first-sector probes
-                const int c2 = P2.col[0];
-                uint32_t v[kJoinItems];
-                bool ok[kJoinItems];
-                Loc r[kJoinItems];
-#pragma unroll
-                for (int q = 0; q < kJoinItems; q++) {
-                    const unsigned j = tid + q * kThreads;
-                    ok[q] = j < cnt;
-                    v[q] = 0;
-                    if (ok[q]) v[q] = c2 < P.t ? (uint32_t)__ldg(M + (long long)si[j] * P.t + c2) : sx[j];
-                }
-                pcsr_lookup_batch<kJoinItems>(groups, gpn, P2.gbase[0], P2.ngroups[0], P2.lab[0], v, ok, r);
-#pragma unroll
-                for (int q = 0; q < kJoinItems; q++) {
-                    const unsigned j = tid + q * kThreads;
-                    if (!ok[q]) continue;
-                    loc2[base + j] = r[q];
-                    sl[j] = r[q].len;
-                    elems += r[q].len;
-                    act += r[q].len ? 1 : 0;
+                for (unsigned j = tid; j < cnt; j += kThreads) {
+                    const Loc r = sloc[j];
+                    loc2[base + j] = r;
+                    elems += r.len;
                 }
             } else {
                 for (unsigned j = tid; j < cnt; j += kThreads) {
                     unsigned long long l0, el;
                     probe_row(M + (long long)si[j] * P.t, P.t, sx[j], P2, groups, gpn,
                               loc2 + (base + j) * (unsigned long long)P2.E, l0, el);
-                    sl[j] = (uint32_t)l0;
+                    sloc[j] = Loc{0u, (uint32_t)l0};
                     elems += el;
-                    act += l0 ? 1 : 0;
                 }
+                __syncthreads();
             }
             elems = warp_sum_u64(elems);
-            act = warp_sum_u64(act);
             if (lane == 0 && elems) atomicAdd(&ctr->list_elems, elems);
-            if (lane == 0 && act) atomicAdd(&ctr->active_rows, act);
-            __syncthreads();
-            // scan of len0' over the tile's new rows (thread tid owns rows [8 tid, 8 tid + 8))
+            // scan of len0' over the tile's stored rows (thread tid owns rows [8 tid, 8 tid + 8))
             unsigned long long mine = 0;
 #pragma unroll
             for (int q = 0; q < kJoinItems; q++) {
                 const unsigned j = tid * kJoinItems + q;
-                if (j < cnt) mine += sl[j];
+                if (j < cnt) mine += sloc[j].len;
             }
             unsigned long long agg2;
             const unsigned long long ex2 = block_exclusive_scan(mine, sm, &agg2);
@@ -577,7 +616,7 @@ __global__ void __launch_bounds__(kThreads) k_join(const int32_t *__restrict__ M
                 const unsigned j = tid * kJoinItems + q;
                 if (j < cnt) {
                     F2[base + j] = run;
-                    run += sl[j];
+                    run += sloc[j].len;
                 }
             }
             // ---- coalesced write of the contiguous block of new rows ------------------------
@@ -644,15 +683,25 @@ __global__ void k_shard_bounds(const unsigned long long *F, long long nM, int ra
 
 // ====================================================================== host side =====
 void encode_query_signatures(int32_t k, const int32_t *qvl, int32_t qm, const int32_t *qs, const int32_t *qd,
-                             const int32_t *qe, uint32_t *qsig) {
+                             const int32_t *qe, uint32_t *qsig, int distinct) {
     // Same written specification as the data side: plane 0 = label (L1277),
-    // 240 two-bit groups with multiplicity counting (reading A5).
+    // 240 two-bit groups.  Isomorphism counts (edge label, neighbour label) pairs with
+    // multiplicity (reading A5); homomorphism may map two query neighbours with the same key
+    // onto ONE data neighbour, so its query side counts distinct keys (NEXT-1).
     for (int u = 0; u < k; u++) {
         int cnt[kSigGroups];
         std::memset(cnt, 0, sizeof(cnt));
+        std::vector<unsigned long long> seen;
         for (int e = 0; e < qm; e++) {
             int other = qs[e] == u ? qd[e] : (qd[e] == u ? qs[e] : -1);
             if (other < 0) continue;
+            if (distinct) {
+                const unsigned long long key = ((unsigned long long)(uint32_t)qe[e] << 32) | (uint32_t)qvl[other];
+                bool dup = false;
+                for (auto x : seen) dup |= x == key;
+                if (dup) continue;
+                seen.push_back(key);
+            }
             cnt[sig_group((uint32_t)qe[e], (uint32_t)qvl[other])]++;
         }
         uint32_t *s = qsig + (size_t)u * kPlanes;
@@ -873,8 +922,9 @@ gsi_status prepare_impl(const gsi_graph *g, int32_t k, const int32_t *qvl, int32
         p->qe_dense[e] = g->dense_label(qe[e]);
         if (p->qe_dense[e] < 0) p->absent_label = true;
     }
-    p->qsig.resize((size_t)k * kPlanes);
-    encode_query_signatures(k, qvl, qm, qs, qd, qe, p->qsig.data());
+    p->qsig.resize((size_t)2 * k * kPlanes);   // [iso signatures | homomorphism signatures]
+    encode_query_signatures(k, qvl, qm, qs, qd, qe, p->qsig.data(), 0);
+    encode_query_signatures(k, qvl, qm, qs, qd, qe, p->qsig.data() + (size_t)k * kPlanes, 1);
     GSI_CUDA(cudaSetDevice(g->device));
     // stream-ordered allocation: a plain cudaMalloc here would make the driver trim the
     // stream-ordered pool the join levels keep reserved
@@ -1086,7 +1136,6 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
     if (!last) fill_params(C, C.steps[si + 1], P2);
     else std::memset(&P2, 0, sizeof(P2));
     const int E = P.E;
-    S.rows[t - 1] += nM;
     if (S.levels < t) S.levels = t;
     S.gba[t] += gba;
     S.list_elems[t] += elems;
@@ -1141,27 +1190,35 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
             GSI_TRY(A.get(&F2, slots + 1));
             GSI_CUDA(cudaMemsetAsync(F2, 0, 8, st));
         }
+        uint32_t *rowmap = nullptr;
+        GSI_TRY(A.get(&rowmap, (unsigned long long)jt + 1));
+        prof.begin(GSI_K_OTHER);
+        k_tile_rows<<<grid_for((unsigned long long)jt + 1, kThreads), kThreads, 0, st>>>(F, (long long)nM, c0, c1, jt,
+                                                                                       rowmap);
+        prof.end();
         prof.begin(GSI_K_JOIN);
         if (mode == J_COUNT)
-            k_join<J_COUNT><<<jt, kThreads, 0, st>>>(M, (long long)nM, F, loc, P, P2, g->ci, cu, g->groups, g->gpn,
-                                                     c0, c1, out, loc2, F2, st1, st2, tctr, C.ctr);
+            k_join<J_COUNT><<<jt, kThreads, 0, st>>>(M, (long long)nM, F, loc, rowmap, P, P2, g->ci, cu, g->groups,
+                                                     g->gpn, c0, c1, out, loc2, F2, st1, st2, tctr, C.ctr);
         else if (mode == J_TABLE)
-            k_join<J_TABLE><<<jt, kThreads, 0, st>>>(M, (long long)nM, F, loc, P, P2, g->ci, cu, g->groups, g->gpn,
-                                                     c0, c1, out, loc2, F2, st1, st2, tctr, C.ctr);
+            k_join<J_TABLE><<<jt, kThreads, 0, st>>>(M, (long long)nM, F, loc, rowmap, P, P2, g->ci, cu, g->groups,
+                                                     g->gpn, c0, c1, out, loc2, F2, st1, st2, tctr, C.ctr);
         else
-            k_join<J_NEXT><<<jt, kThreads, 0, st>>>(M, (long long)nM, F, loc, P, P2, g->ci, cu, g->groups, g->gpn,
-                                                    c0, c1, out, loc2, F2, st1, st2, tctr, C.ctr);
+            k_join<J_NEXT><<<jt, kThreads, 0, st>>>(M, (long long)nM, F, loc, rowmap, P, P2, g->ci, cu, g->groups,
+                                                    g->gpn, c0, c1, out, loc2, F2, st1, st2, tctr, C.ctr);
         prof.end();
         Counters hc;
         GSI_CUDA(d2h(S, &hc, C.ctr, sizeof(Counters), st));
         GSI_CUDA(cudaStreamSynchronize(st));
         GSI_CUDA(cudaGetLastError());
         A.release(status);
-        const unsigned long long nout = mode == J_COUNT ? hc.count : hc.total;
+        A.release(rowmap);
+        const unsigned long long nout = mode == J_COUNT ? hc.count : hc.total;   // J_NEXT: stored rows
         const double frac = gba ? (double)slots / (double)gba : 0.0;
         double jb = frac * (4.0 * t * active + 4.0 * elems + (8.0 * E + 8.0) * active);
         if (mode == J_TABLE) jb += 4.0 * C.q->k * nout;
         if (mode == J_NEXT) jb += nout * (4.0 * (t + 1) + 16.0 * P2.E + 8.0);
+        if (mode == J_NEXT) S.rows[t] += hc.count;   // |M_{t+1}|: every survivor, stored or not
         S.alg_bytes[GSI_K_JOIN] += jb;
         if (last) {
             C.count += nout;
@@ -1179,7 +1236,7 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
             }
             A.release(out);
         } else if (mode == J_NEXT) {
-            if (nout) rc = level(C, si + 1, out, nout, loc2, F2, hc.total2, hc.active_rows, hc.list_elems);
+            if (nout) rc = level(C, si + 1, out, nout, loc2, F2, hc.total2, nout, hc.list_elems);
             A.release(out);
             A.release(loc2);
             A.release(F2);
@@ -1248,7 +1305,8 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
         unsigned grid = (unsigned)std::min<long long>((words + 31) / 32, (long long)sms * 8);
         if (grid < 1) grid = 1;
         prof.begin(GSI_K_FILTER);
-        k_filter<<<grid, kThreads, 0, st>>>(g->sig, n, k, q->d_qsig, opts.filter_mode == 1, bm, words, d_counts,
+        const uint32_t *qsig = q->d_qsig + (opts.homomorphism ? (size_t)k * kPlanes : 0);
+        k_filter<<<grid, kThreads, 0, st>>>(g->sig, n, k, qsig, opts.filter_mode == 1, bm, words, d_counts,
                                             C.ctr);
         prof.end();
     }
@@ -1387,6 +1445,7 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
         GSI_CUDA(cudaStreamSynchronize(st));
         A.release(status);
         S.alg_bytes[GSI_K_PROBE] += (double)nM * (20.0 * P.E + 8.0);
+        S.rows[0] += nM;
         rc = level(C, 0, M, nM, loc, F, gba, hc.active_rows, hc.list_elems);
         A.release(loc);
         A.release(F);
@@ -1456,7 +1515,8 @@ gsi_status debug_filter_impl(const gsi_graph *g, int32_t k, const int32_t *qvl, 
     GSI_CUDA(cudaMemsetAsync(cnt, 0, 8ull * k, st));
     GSI_CUDA(cudaMemsetAsync(ctr, 0, sizeof(Counters), st));
     unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>((words + 7) / 8, 148 * 8));
-    k_filter<<<grid, kThreads, 0, st>>>(g->sig, n, k, p->d_qsig, mode == 1, bm, words, cnt, ctr);
+    const uint32_t *qsig = p->d_qsig + (mode == 2 ? (size_t)k * kPlanes : 0);   // 2: homomorphism encoding
+    k_filter<<<grid, kThreads, 0, st>>>(g->sig, n, k, qsig, mode == 1, bm, words, cnt, ctr);
     if (bitmaps && words)
         GSI_CUDA(cudaMemcpyAsync(bitmaps, bm, 4ull * words * k, cudaMemcpyDeviceToHost, st));
     std::vector<unsigned long long> hc(k);

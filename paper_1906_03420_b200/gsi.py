@@ -88,7 +88,7 @@ _SIGS = {
     "gsi_debug_lookup": (I32, [P, I64, P, P, P, P, P, I64]),
     "gsi_debug_signatures": (I32, [P, P]),
     "gsi_debug_filter": (I32, [P, I32, P, I32, P, P, P, I32, P, P]),
-    "gsi_debug_query_signatures": (I32, [I32, P, I32, P, P, P, P]),
+    "gsi_debug_query_signatures": (I32, [I32, P, I32, P, P, P, I32, P]),
     "gsi_last_error": (ctypes.c_char_p, []),
     "gsi_version": (ctypes.c_char_p, []),
     "gsi_device_count": (I32, []),
@@ -331,10 +331,11 @@ def gsi_debug_filter(g: GraphHandle, q_vlabels, q_src, q_dst, q_elabels, filter_
     return bm[:, :words], cnt
 
 
-def gsi_debug_query_signatures(q_vlabels, q_src, q_dst, q_elabels) -> np.ndarray:
+def gsi_debug_query_signatures(q_vlabels, q_src, q_dst, q_elabels, distinct: bool = False) -> np.ndarray:
     qv, qs, qd, qe = _i32(q_vlabels), _i32(q_src), _i32(q_dst), _i32(q_elabels)
     out = np.zeros((len(qv), 16), np.uint32)
-    _check(lib.gsi_debug_query_signatures(len(qv), _ptr(qv), len(qs), _ptr(qs), _ptr(qd), _ptr(qe), _ptr(out)),
+    _check(lib.gsi_debug_query_signatures(len(qv), _ptr(qv), len(qs), _ptr(qs), _ptr(qd), _ptr(qe), int(distinct),
+                                          _ptr(out)),
            "gsi_debug_query_signatures")
     return out
 
