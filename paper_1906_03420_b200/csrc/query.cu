@@ -63,7 +63,7 @@ struct Counters {
     unsigned long long active_rows;  // rows with a non-empty prealloc buffer
     unsigned long long count;        // final count (count-only mode) / survivors
     unsigned long long fp1, fp2;
-    unsigned long long plane_loads;  // filter: vertices whose planes 1..15 were read
+    unsigned long long plane_loads;  // filter: signature plane words read (planes 1..15)
     unsigned long long total;        // scan totals written by the last tile
     unsigned long long total2;       // F'[|M'|] of the probe-ahead (J_NEXT)
 };
@@ -75,15 +75,24 @@ __global__ void __launch_bounds__(kThreads) k_filter(const uint32_t *__restrict_
                                                      unsigned long long *__restrict__ counts,
                                                      Counters *__restrict__ ctr) {
     __shared__ uint32_t qs[GSI_MAX_K * kPlanes];
+    __shared__ uint32_t qneed[GSI_MAX_K];            // planes 1..15 where S(u) has a set bit
     __shared__ unsigned long long cnt_s[GSI_MAX_K];
     __shared__ unsigned long long loads_s;
     for (int i = threadIdx.x; i < k * kPlanes; i += blockDim.x) qs[i] = qsig[i];
     if (threadIdx.x < GSI_MAX_K) cnt_s[threadIdx.x] = 0;
     if (threadIdx.x == 0) loads_s = 0;
     __syncthreads();
+    if (threadIdx.x < k) {
+        uint32_t m = 0;
+        for (int pl = 1; pl < kPlanes; pl++)
+            if (qs[threadIdx.x * kPlanes + pl]) m |= 1u << pl;
+        qneed[threadIdx.x] = m;
+    }
+    __syncthreads();
     const int lane = threadIdx.x & 31;
     const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
     constexpr int kFW = 4;   // bitmap words per warp per iteration: 4 coalesced plane-0 loads in flight
+    unsigned long long plane_words = 0;   // plane words this thread read (algorithmic bytes / 4)
     for (long long w0 = (blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5)) * kFW; w0 < words;
          w0 += warps * kFW) {
         uint32_t lab[kFW], mask[kFW];
@@ -99,14 +108,24 @@ __global__ void __launch_bounds__(kThreads) k_filter(const uint32_t *__restrict_
                 if (lab[j] == qs[u * kPlanes]) mask[j] |= 1u << u;   // label field by equality (A4)
         }
         if (!label_only) {
+            // Only the planes where some label-matching u has a set bit can reject v: a plane
+            // whose query word is 0 is contained in anything.  A walk query vertex of degree d
+            // sets <= d of the 15 planes, so most of the column-first table is never read.
 #pragma unroll
             for (int j = 0; j < kFW; j++) {
-                if (!mask[j]) continue;
+                uint32_t need = 0, mm = mask[j];
+                while (mm) {
+                    const int u = __ffs(mm) - 1;
+                    mm &= mm - 1;
+                    need |= qneed[u];
+                }
+                if (!need) continue;
+                plane_words += __popc(need);
                 const long long v = (w0 + j) * 32 + lane;
                 uint32_t p[kPlanes];
 #pragma unroll
-                for (int pl = 1; pl < kPlanes; pl++) p[pl] = __ldcs(sig + (long long)pl * n + v);
-                uint32_t mm = mask[j];
+                for (int pl = 1; pl < kPlanes; pl++) p[pl] = (need >> pl) & 1u ? __ldcs(sig + (long long)pl * n + v) : 0u;
+                mm = mask[j];
                 while (mm) {
                     const int u = __ffs(mm) - 1;
                     mm &= mm - 1;
@@ -121,8 +140,6 @@ __global__ void __launch_bounds__(kThreads) k_filter(const uint32_t *__restrict_
 #pragma unroll
         for (int j = 0; j < kFW; j++) {
             if (w0 + j >= words) break;
-            const unsigned loaded = __ballot_sync(0xffffffffu, !label_only && lab[j] != 0xFFFFFFFFu && mask[j] != 0);
-            if (lane == 0 && loaded) atomicAdd(&loads_s, (unsigned long long)__popc(loaded));
             for (int u = 0; u < k; u++) {
                 const unsigned b = __ballot_sync(0xffffffffu, (mask[j] >> u) & 1u);
                 if (lane == 0) {
@@ -132,6 +149,8 @@ __global__ void __launch_bounds__(kThreads) k_filter(const uint32_t *__restrict_
             }
         }
     }
+    plane_words = warp_sum_u64(plane_words);
+    if (lane == 0 && plane_words) atomicAdd(&loads_s, plane_words);
     __syncthreads();
     if (threadIdx.x < k && cnt_s[threadIdx.x]) atomicAdd(&counts[threadIdx.x], cnt_s[threadIdx.x]);
     if (threadIdx.x == 0 && loads_s) atomicAdd(&ctr->plane_loads, loads_s);
@@ -726,14 +745,35 @@ inline unsigned grid_for(unsigned long long n, int per) {
 }
 
 // Stream-ordered scratch; every allocation is released (stream-ordered) at scope exit.
+// Stream-ordered scratch.  Small buffers come from a per-query bump region (one pool
+// allocation; a level's buffers are released LIFO with mark()/reset(), safe because every
+// kernel of a query runs on one stream); large ones from cudaMallocAsync on the stream.
 struct Arena {
     cudaStream_t st;
     std::vector<void *> ptrs;
+    char *bump = nullptr;
+    size_t cap = 0, off = 0;
     explicit Arena(cudaStream_t s) : st(s) {}
+    gsi_status init_bump(size_t bytes) {
+        if (cudaMallocAsync((void **)&bump, bytes, st) != cudaSuccess) {
+            cudaGetLastError();
+            bump = nullptr;
+            return GSI_OK;   // optional: fall back to per-buffer allocations
+        }
+        cap = bytes;
+        return GSI_OK;
+    }
     template <typename T>
     gsi_status get(T **p, unsigned long long count) {
+        const size_t bytes = (size_t)std::max<unsigned long long>(count, 1) * sizeof(T);
+        const size_t need = (bytes + 255) & ~(size_t)255;
+        if (bump && off + need <= cap) {
+            *p = (T *)(bump + off);
+            off += need;
+            return GSI_OK;
+        }
         void *q = nullptr;
-        cudaError_t e = cudaMallocAsync(&q, std::max<unsigned long long>(count, 1) * sizeof(T), st);
+        cudaError_t e = cudaMallocAsync(&q, bytes, st);
         if (e == cudaErrorMemoryAllocation) {
             cudaGetLastError();
             set_error("device memory exhausted");
@@ -744,7 +784,10 @@ struct Arena {
         *p = (T *)q;
         return GSI_OK;
     }
+    size_t mark() const { return off; }
+    void reset(size_t m) { off = m; }
     void release(void *p) {
+        if (!p || (bump && (char *)p >= bump && (char *)p < bump + cap)) return;   // bump: freed by reset()
         for (auto &q : ptrs)
             if (q == p) {
                 cudaFreeAsync(q, st);
@@ -754,6 +797,7 @@ struct Arena {
     ~Arena() {
         for (void *q : ptrs)
             if (q) cudaFreeAsync(q, st);
+        if (bump) cudaFreeAsync(bump, st);
     }
 };
 
@@ -1171,6 +1215,7 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
             C.capped = true;
             break;
         }
+        const size_t mk = A.mark();
         const unsigned long long c1 = std::min(s1, c0 + chunk), slots = c1 - c0;
         if (c0 != s0 || c1 != s1) S.n_chunks++;
         const unsigned jt = grid_for(slots, kJoinTile);
@@ -1241,6 +1286,7 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
             A.release(loc2);
             A.release(F2);
         }
+        A.reset(mk);
     }
     return rc;
 }
@@ -1289,6 +1335,7 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     C.S = &S;
     C.words = words;
 
+    GSI_TRY(A.init_bump(64ull << 20));
     GSI_TRY(A.get(&C.ctr, 1));
     GSI_CUDA(cudaMemsetAsync(C.ctr, 0, sizeof(Counters), st));
 
@@ -1319,7 +1366,7 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     const double t_filter = now_ms();
     S.ms_filter = (float)(t_filter - t_start);
     for (int u = 0; u < k; u++) S.cand[u] = cand[u];
-    S.alg_bytes[GSI_K_FILTER] = 4.0 * n + 60.0 * hc.plane_loads + 4.0 * words * k;
+    S.alg_bytes[GSI_K_FILTER] = 4.0 * n + 4.0 * hc.plane_loads + 4.0 * words * k;
 
     // ---------------- plan (a4) ----------------
     GSI_TRY(plan_order(q, cand, opts.force_order, C.order));

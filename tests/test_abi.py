@@ -83,9 +83,10 @@ def test_no_device_fails_loudly():
 def test_query_signature_encoding_matches_oracle():
     for s in range(40):
         q = W.random_connected_query(s, 1 + s % 12, nlv=1 + s % 5, nle=1 + s % 7, extra=0.3)
-        a = gsi.gsi_debug_query_signatures(q.vlabels, q.src, q.dst, q.elabels)
-        b = oracle.query_signatures(q)
-        assert np.array_equal(a, b), s
+        for distinct in (False, True):
+            a = gsi.gsi_debug_query_signatures(q.vlabels, q.src, q.dst, q.elabels, distinct=distinct)
+            b = oracle.query_signatures(q, distinct=distinct)
+            assert np.array_equal(a, b), (s, distinct)
 
 
 def test_invalid_arguments_are_errors():

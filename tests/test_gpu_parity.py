@@ -144,7 +144,7 @@ def test_signature_table_bit_exact():
     assert np.array_equal(gsi.gsi_debug_signatures(graph), oracle.signatures(og))
 
 
-@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("mode", [0, 1, 2])
 def test_filter_bitmaps_bit_exact(mode):
     g = W.chung_lu(5000, 30000, 600, nlv=5, nle=7, seed=23)
     graph = gsi.build(g)
@@ -153,8 +153,8 @@ def test_filter_bitmaps_bit_exact(mode):
     for s in range(6):
         q = W.random_walk_query(g, 8, 300 + s)
         bm, cnt = gsi.gsi_debug_filter(graph, q.vlabels, q.src, q.dst, q.elabels, filter_mode=mode)
-        if mode == 0:
-            obm, ocnt = oracle.filter(og, planes, oracle.query_signatures(q))
+        if mode in (0, 2):
+            obm, ocnt = oracle.filter(og, planes, oracle.query_signatures(q, distinct=mode == 2))
         else:
             iso = W.Query(q.n, q.vlabels, np.zeros(0), np.zeros(0), np.zeros(0))   # label-only = no pairs
             obm, ocnt = oracle.filter(og, planes, oracle.query_signatures(iso))
@@ -310,9 +310,10 @@ def test_homomorphism_matches_oracle():
         q = W.random_connected_query(30_000 + s, 2 + s % 4, nlv=1 + s % 2, nle=1 + s % 2)
         graph = gsi.build(g)
         og = oracle.OracleGraph(g)
-        r = gsi.query(graph, q, want_table=True, homomorphism=True, filter_mode=1)
         cnt, fp, otab = oracle.match(og, q, hom=True)
-        assert r.count == cnt and np.array_equal(canon(r.table()), otab), s
+        for fm in (0, 1):   # signature filter with the distinct-key query encoding, and label-only
+            r = gsi.query(graph, q, want_table=True, homomorphism=True, filter_mode=fm)
+            assert r.count == cnt and np.array_equal(canon(r.table()), otab), (s, fm)
 
 
 def test_k1_and_empty_cases():

@@ -318,3 +318,18 @@ def test_fig1_default_filter_sizes():
     assert np.nonzero(bits[0])[0].tolist() == [0]
     assert np.nonzero(bits[1])[0].tolist() == [100]
     assert np.nonzero(bits[2])[0].tolist() == [201]
+
+
+def test_homomorphism_filter_sound_with_distinct_keys():
+    """Under homomorphism two query neighbours with the same (edge label, neighbour label) key
+    may map to one data vertex, so only the distinct-key query encoding is necessary: every
+    f(u) of every homomorphic match passes it (reading A5)."""
+    for s in range(60):
+        g = W.random_tiny_graph(400 + s, nlv=1 + s % 2, nle=1 + s % 2)
+        q = W.random_connected_query(40_000 + s, 2 + s % 4, nlv=1 + s % 2, nle=1 + s % 2, extra=0.5)
+        og = oracle.OracleGraph(g)
+        bm, _ = oracle.filter(og, oracle.signatures(og), oracle.query_signatures(q, distinct=True))
+        bits = np.unpackbits(bm.view(np.uint8), axis=1, bitorder="little")[:, : g.n]
+        for row in oracle.brute_force(g, q, hom=True):
+            for u, v in enumerate(row):
+                assert bits[u, v], (s, row)
