@@ -379,10 +379,17 @@ __global__ void __launch_bounds__(kThreads, MODE == J_NEXT ? 3 : 4) k_join(const
                                                    unsigned long long *__restrict__ F2,
                                                    unsigned long long *status, unsigned long long *status2,
                                                    unsigned *tile_ctr, Counters *ctr) {
-    __shared__ int sR[kJoinTile];                                   // row offset (from rlo) per tile slot
-    __shared__ uint32_t sx[MODE == J_COUNT ? 1 : kJoinTile];        // write cache: new vertex
-    __shared__ uint32_t si[MODE == J_COUNT ? 1 : kJoinTile];        //              parent row
-    __shared__ Loc sloc[MODE == J_NEXT ? kJoinTile : 1];            //              next buffer (E' = 1)
+    // Dynamic shared memory (join_smem_bytes<MODE>()): before the compaction it holds the row
+    // marker / row offset per slot (sR), per tile row off0 - F_i (sBase) and the subtraction
+    // columns (sInj); the write cache (sx, si, sloc) reuses the same bytes afterwards.
+    extern __shared__ __align__(16) unsigned char dsm[];
+    constexpr int kInjStage = MODE == J_COUNT ? 4 : 2;
+    int *sR = reinterpret_cast<int *>(dsm);
+    uint32_t *sBase = reinterpret_cast<uint32_t *>(sR + kJoinTile);
+    int32_t *sInjBase = reinterpret_cast<int32_t *>(sBase + kJoinTile);
+    uint32_t *sx = reinterpret_cast<uint32_t *>(sR);     // write cache: new vertex
+    uint32_t *si = sBase;                                // write cache: parent row
+    Loc *sloc = reinterpret_cast<Loc *>(sInjBase);       // write cache: next buffer (E' = 1)
     __shared__ unsigned wcnt[kJoinItems][kThreads / 32];
     __shared__ unsigned wbase[kJoinItems][kThreads / 32];
     __shared__ unsigned long long sm[33];
@@ -390,18 +397,32 @@ __global__ void __launch_bounds__(kThreads, MODE == J_NEXT ? 3 : 4) k_join(const
     __shared__ unsigned long long base_s, base2_s;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) tile_s = atomicAdd(tile_ctr, 1u);
-    for (int j = tid; j < kJoinTile; j += kThreads) sR[j] = 0;
+    {   // zero the row-marker array with 16 B stores
+        int4 *z = reinterpret_cast<int4 *>(sR);
+        for (int j = tid; j < kJoinTile / 4; j += kThreads) z[j] = make_int4(0, 0, 0, 0);
+    }
     __syncthreads();
     const unsigned tile = tile_s;
     const unsigned long long tbase = s0 + (unsigned long long)tile * kJoinTile;
     const unsigned long long tend = min(tbase + (unsigned long long)kJoinTile, s1);
     const long long rlo = __ldg(rowmap + tile), rhi = __ldg(rowmap + tile + 1);
+    const long long nr = rhi - rlo + 1;
+    // Stage, per row of the tile, base = off0 - F_i (so slot s reads ci[base + s]) and the
+    // columns the subtraction tests, so the per-slot work touches shared memory only.
+    const bool staged = nr <= kJoinTile;
+    const int n_inj_st = staged ? min(P.n_inj, kInjStage) : 0;
     // Row of every slot of the tile without a per-slot search (load-balanced search): each row
     // overlapping the tile marks its first tile-local slot, then an inclusive max-scan over the
     // 2048 slots spreads the row offset to all its slots.
-    for (long long r = tid; r <= rhi - rlo; r += kThreads) {
+    for (long long r = tid; r < nr; r += kThreads) {
         const unsigned long long a = __ldg(F + rlo + r), b = __ldg(F + rlo + r + 1);
         if (a < b && b > tbase && a < tend) sR[a > tbase ? (unsigned)(a - tbase) : 0u] = (int)r;
+        if (staged) {
+            const unsigned long long i = (unsigned long long)(rlo + r);
+            sBase[r] = loc[i * (unsigned)P.E].off - (uint32_t)a;
+            const int32_t *row = M + i * (unsigned)P.t;
+            for (int c = 0; c < n_inj_st; c++) sInjBase[c * kJoinTile + r] = __ldg(row + P.inj_col[c]);
+        }
     }
     __syncthreads();
     {
@@ -418,32 +439,38 @@ __global__ void __launch_bounds__(kThreads, MODE == J_NEXT ? 3 : 4) k_join(const
         if (lane == 31) wcnt[0][warp] = (unsigned)inc;
         int prev = __shfl_up_sync(0xffffffffu, inc, 1);
         __syncthreads();
-        int carry = lane == 0 ? 0 : prev;
-        for (int w = 0; w < warp; w++) carry = max(carry, (int)wcnt[0][w]);
+        const int wm = lane < warp ? (int)wcnt[0][lane] : 0;   // max over the preceding warps
+        int carry = max(lane == 0 ? 0 : prev, 0);
+        int wmax = wm;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+        carry = max(carry, wmax);
 #pragma unroll
         for (int q = 0; q < kJoinItems; q++) sR[tid * kJoinItems + q] = max(v[q], carry);
     }
     __syncthreads();
 
     // Phased over the 8 slots of this thread so that each phase's independent loads are in
-    // flight together (loc -> ci -> C(u) bit -> subtraction -> other lists -> next probe).
+    // flight together (ci -> C(u) bit -> subtraction -> other lists -> next probe).
     bool keep[kJoinItems];
     uint32_t xs[kJoinItems];
-    uint32_t rows[kJoinItems];
-    uint32_t pos[kJoinItems];
-    Loc L0[kJoinItems];
+    uint32_t rows[kJoinItems];   // row offset from rlo
+    uint32_t cio[kJoinItems];
 #pragma unroll
     for (int it = 0; it < kJoinItems; it++) {
         const unsigned long long s = tbase + (unsigned long long)it * kThreads + tid;
         keep[it] = s < tend;
-        const long long i = rlo + sR[it * kThreads + tid];
-        rows[it] = (uint32_t)i;
-        pos[it] = keep[it] ? (uint32_t)(s - __ldg(F + i)) : 0u;   // position inside the row's buffer
+        const int r = sR[it * kThreads + tid];
+        rows[it] = (uint32_t)r;
+        if (staged) {
+            cio[it] = sBase[r] + (uint32_t)s;
+        } else {
+            const unsigned long long i = (unsigned long long)(rlo + r);
+            cio[it] = keep[it] ? loc[i * (unsigned)P.E].off + (uint32_t)(s - __ldg(F + i)) : 0u;
+        }
     }
 #pragma unroll
-    for (int it = 0; it < kJoinItems; it++) L0[it] = keep[it] ? loc[(long long)rows[it] * P.E] : Loc{0u, 0u};
-#pragma unroll
-    for (int it = 0; it < kJoinItems; it++) xs[it] = keep[it] ? (uint32_t)__ldg(ci + L0[it].off + pos[it]) : 0u;
+    for (int it = 0; it < kJoinItems; it++) xs[it] = keep[it] ? (uint32_t)__ldg(ci + cio[it]) : 0u;
 #pragma unroll
     for (int it = 0; it < kJoinItems; it++) {                                    // x in C(u)
         const uint32_t x = xs[it];
@@ -451,14 +478,23 @@ __global__ void __launch_bounds__(kThreads, MODE == J_NEXT ? 3 : 4) k_join(const
     }
     for (int c = 0; c < P.n_inj; c++) {                                         // Alg. 3 line 10
         const int col = P.inj_col[c];
+        if (c < n_inj_st) {
 #pragma unroll
-        for (int it = 0; it < kJoinItems; it++)
-            if (keep[it]) keep[it] = __ldg(M + (long long)rows[it] * P.t + col) != (int32_t)xs[it];
+            for (int it = 0; it < kJoinItems; it++)
+                if (keep[it]) keep[it] = sInjBase[c * kJoinTile + rows[it]] != (int32_t)xs[it];
+        } else {
+#pragma unroll
+            for (int it = 0; it < kJoinItems; it++)
+                if (keep[it])
+                    keep[it] = __ldg(M + (unsigned long long)(rlo + rows[it]) * (unsigned)P.t + col) != (int32_t)xs[it];
+        }
     }
+#pragma unroll
+    for (int it = 0; it < kJoinItems; it++) rows[it] += (uint32_t)rlo;              // absolute row index
     if (P.E > 1) {                                                               // Alg. 3 line 13
 #pragma unroll
         for (int it = 0; it < kJoinItems; it++) {
-            const Loc *L = loc + (long long)rows[it] * P.E;
+            const Loc *L = loc + (unsigned long long)rows[it] * (unsigned)P.E;
             for (int e = 1; e < P.E && keep[it]; e++) {
                 const Loc Le = L[e];
                 keep[it] = in_sorted(ci + Le.off, Le.len, (int32_t)xs[it]);
@@ -532,6 +568,8 @@ __global__ void __launch_bounds__(kThreads, MODE == J_NEXT ? 3 : 4) k_join(const
             }
         }
         // ---- ordered compaction into the shared-memory write cache + look-back ------------
+        // (the __syncthreads below also orders every read of sR / sBase / sInj before the
+        //  write cache, which reuses those bytes, is written)
         unsigned ballots[kJoinItems];
 #pragma unroll
         for (int it = 0; it < kJoinItems; it++) {
@@ -652,6 +690,11 @@ __global__ void __launch_bounds__(kThreads, MODE == J_NEXT ? 3 : 4) k_join(const
             }
         }
     }
+}
+
+template <int MODE>
+constexpr size_t join_smem_bytes() {
+    return (size_t)(2 + (MODE == J_COUNT ? 4 : 2)) * kJoinTile * 4;
 }
 
 // Count + fingerprint of a table whose columns are in pi order (k = 1 queries).
@@ -868,6 +911,10 @@ void ensure_pool(int dev) {
         uint64_t thr = ~0ull;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
+    // the join tiles use > 48 KB of dynamic shared memory (opt-in, per device)
+    cudaFuncSetAttribute(k_join<J_COUNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)join_smem_bytes<J_COUNT>());
+    cudaFuncSetAttribute(k_join<J_TABLE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)join_smem_bytes<J_TABLE>());
+    cudaFuncSetAttribute(k_join<J_NEXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)join_smem_bytes<J_NEXT>());
     cudaGetLastError();
     g_pool_ready[dev] = true;
 }
@@ -1243,13 +1290,13 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         prof.end();
         prof.begin(GSI_K_JOIN);
         if (mode == J_COUNT)
-            k_join<J_COUNT><<<jt, kThreads, 0, st>>>(M, (long long)nM, F, loc, rowmap, P, P2, g->ci, cu, g->groups,
+            k_join<J_COUNT><<<jt, kThreads, join_smem_bytes<J_COUNT>(), st>>>(M, (long long)nM, F, loc, rowmap, P, P2, g->ci, cu, g->groups,
                                                      g->gpn, c0, c1, out, loc2, F2, st1, st2, tctr, C.ctr);
         else if (mode == J_TABLE)
-            k_join<J_TABLE><<<jt, kThreads, 0, st>>>(M, (long long)nM, F, loc, rowmap, P, P2, g->ci, cu, g->groups,
+            k_join<J_TABLE><<<jt, kThreads, join_smem_bytes<J_TABLE>(), st>>>(M, (long long)nM, F, loc, rowmap, P, P2, g->ci, cu, g->groups,
                                                      g->gpn, c0, c1, out, loc2, F2, st1, st2, tctr, C.ctr);
         else
-            k_join<J_NEXT><<<jt, kThreads, 0, st>>>(M, (long long)nM, F, loc, rowmap, P, P2, g->ci, cu, g->groups,
+            k_join<J_NEXT><<<jt, kThreads, join_smem_bytes<J_NEXT>(), st>>>(M, (long long)nM, F, loc, rowmap, P, P2, g->ci, cu, g->groups,
                                                     g->gpn, c0, c1, out, loc2, F2, st1, st2, tctr, C.ctr);
         prof.end();
         Counters hc;

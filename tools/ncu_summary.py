@@ -55,5 +55,63 @@ def full(path):
         print(f"| {name} | " + " | ".join(r[i] for i in idx.values()) + " |")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and sys.argv[1] in ("launches", "full"):
     {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
+
+
+def stalls(path, launch=0, top=15):
+    """Stall-reason breakdown and the hottest SASS lines of one captured launch."""
+    out = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass",
+                          "--launch-skip", str(launch), "--launch-count", "1"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    kname = rows[0][1] if rows and len(rows[0]) > 1 else "?"
+    h = rows[1]
+    S = h.index("Warp Stall Sampling (All Samples)")
+    src = h.index("Source")
+
+    def f(x):
+        try:
+            return float(x)
+        except ValueError:
+            return None
+    data = [r for r in rows[2:] if len(r) > S and f(r[S]) is not None]
+    stall_cols = [i for i, c in enumerate(h) if c.startswith("stall_") and "Not Issued" not in c]
+    tot = sum(f(r[S]) for r in data) or 1.0
+    agg = collections.Counter()
+    for r in data:
+        for i in stall_cols:
+            v = f(r[i])
+            if v:
+                agg[h[i]] += v
+    print(f"kernel: {kname.split('(')[0]}  (launch {launch}; {int(tot)} warp samples)\n")
+    print("| stall reason | share |\n|---|---|")
+    for k_, v in agg.most_common(10):
+        print(f"| {k_[6:]} | {v / tot:.1%} |")
+    print("\n| samples | SASS |\n|---|---|")
+    seen = set()
+    for r in sorted(data, key=lambda r: -f(r[S])):
+        if r[0] in seen:
+            continue
+        seen.add(r[0])
+        print(f"| {int(f(r[S]))} | `{r[src].strip()[:70]}` |")
+        if len(seen) >= top:
+            break
+
+
+def details(path, launch=0):
+    out = subprocess.run(["ncu", "-i", path, "--page", "details", "--csv", "--launch-skip", str(launch),
+                          "--launch-count", "1"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h = rows[0]
+    si, mi, vi, ui = h.index("Section Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("Metric Unit")
+    keep = ("GPU Speed Of Light Throughput", "Memory Workload Analysis", "Compute Workload Analysis",
+            "Occupancy", "Scheduler Statistics", "Warp State Statistics", "Launch Statistics")
+    print("| section | metric | value |\n|---|---|---|")
+    for r in rows[1:]:
+        if r[si] in keep and r[mi]:
+            print(f"| {r[si]} | {r[mi]} | {r[vi]} {r[ui]} |")
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] in ("stalls", "details"):
+    fn = {"stalls": stalls, "details": details}[sys.argv[1]]
+    fn(sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 0)
