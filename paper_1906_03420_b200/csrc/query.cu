@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(kThreads, MODE == J_NEXT ? 3 : 4) k_join(const
     Loc *sloc = reinterpret_cast<Loc *>(sInjBase);       // write cache: next buffer (E' = 1)
     __shared__ unsigned wcnt[kJoinItems][kThreads / 32];
     __shared__ unsigned wbase[kJoinItems][kThreads / 32];
-    __shared__ unsigned long long sm[33];
+    __shared__ unsigned long long sm[34];
     __shared__ unsigned tile_s, agg_s;
     __shared__ unsigned long long base_s, base2_s;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -576,6 +576,15 @@ __global__ void __launch_bounds__(kThreads, MODE == J_NEXT ? 3 : 4) k_join(const
             ballots[it] = __ballot_sync(0xffffffffu, keep[it]);
             if (lane == 0) wcnt[it][warp] = __popc(ballots[it]);
         }
+        if constexpr (MODE == J_NEXT) {
+            // the tile's next-level buffer total is known before the compaction, so both
+            // look-back chains (row offsets and next F) run at the same time (warps 0 and 1)
+            unsigned long long mylen = 0;
+#pragma unroll
+            for (int it = 0; it < kJoinItems; it++) mylen += keep[it] ? N0[it].len : 0u;
+            mylen = warp_sum_u64(mylen);
+            if (lane == 0) sm[warp] = mylen;
+        }
         __syncthreads();
         if (warp == 0) {
             constexpr int NW = kThreads / 32;   // 64 (it, warp) counts in slot order: it * 8 + warp
@@ -596,6 +605,14 @@ __global__ void __launch_bounds__(kThreads, MODE == J_NEXT ? 3 : 4) k_join(const
             if (lane == 0) {
                 base_s = pre;
                 agg_s = total;
+            }
+        } else if (MODE == J_NEXT && warp == 1) {
+            unsigned long long tl = lane < kThreads / 32 ? sm[lane] : 0ull;
+            tl = warp_sum_u64(tl);
+            const unsigned long long pre2 = lookback_exclusive(status2, tile, tl);
+            if (lane == 0) {
+                base2_s = pre2;
+                sm[32] = tl;
             }
         }
         __syncthreads();
@@ -653,21 +670,19 @@ __global__ void __launch_bounds__(kThreads, MODE == J_NEXT ? 3 : 4) k_join(const
             }
             elems = warp_sum_u64(elems);
             if (lane == 0 && elems) atomicAdd(&ctr->list_elems, elems);
-            // scan of len0' over the tile's stored rows (thread tid owns rows [8 tid, 8 tid + 8))
+            // next F over the tile's stored rows (thread tid owns rows [8 tid, 8 tid + 8));
+            // the tile's offset base2_s came from the second look-back chain above
             unsigned long long mine = 0;
 #pragma unroll
             for (int q = 0; q < kJoinItems; q++) {
                 const unsigned j = tid * kJoinItems + q;
                 if (j < cnt) mine += sloc[j].len;
             }
-            unsigned long long agg2;
-            const unsigned long long ex2 = block_exclusive_scan(mine, sm, &agg2);
-            if (warp == 0) {
-                const unsigned long long pre2 = lookback_exclusive(status2, tile, agg2);
-                if (lane == 0) base2_s = pre2;
-            }
-            __syncthreads();
-            unsigned long long run = base2_s + ex2;
+            const unsigned long long agg2 = sm[32];
+            const unsigned long long pre2 = base2_s;
+            unsigned long long dummy;
+            const unsigned long long ex2 = block_exclusive_scan(mine, sm, &dummy);
+            unsigned long long run = pre2 + ex2;
 #pragma unroll
             for (int q = 0; q < kJoinItems; q++) {
                 const unsigned j = tid * kJoinItems + q;
@@ -685,8 +700,8 @@ __global__ void __launch_bounds__(kThreads, MODE == J_NEXT ? 3 : 4) k_join(const
             }
             if (tile == gridDim.x - 1 && tid == 0) {
                 ctr->total = base + cnt;
-                ctr->total2 = base2_s + agg2;
-                F2[base + cnt] = base2_s + agg2;
+                ctr->total2 = pre2 + agg2;
+                F2[base + cnt] = pre2 + agg2;
             }
         }
     }
