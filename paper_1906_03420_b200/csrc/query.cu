@@ -443,7 +443,7 @@ __global__ void __launch_bounds__(kThreads, MODE == J_NEXT ? 3 : 4) k_join(const
         int carry = max(lane == 0 ? 0 : prev, 0);
         int wmax = wm;
 #pragma unroll
-        for (int o = 1; o < 8; o <<= 1) wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+        for (int o = 1; o < 32; o <<= 1) wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
         carry = max(carry, wmax);
 #pragma unroll
         for (int q = 0; q < kJoinItems; q++) sR[tid * kJoinItems + q] = max(v[q], carry);
