@@ -28,14 +28,22 @@ def needs_build() -> bool:
     return any(os.path.getmtime(s) > t for s in sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str = None, defines=()) -> str:
+    """Compile the library (to `out` with extra -D `defines` for A/B variants)."""
+    if out is not None:
+        return _build_to(out, defines, verbose)
     if not force and not needs_build():
         return LIB
+    return _build_to(LIB, defines, verbose)
+
+
+def _build_to(lib_path: str, defines=(), verbose: bool = False) -> str:
+    LIB = lib_path
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
     objs = []
     for src in sorted(glob.glob(os.path.join(CSRC, "*.cu"))):
         obj = os.path.join(os.path.dirname(LIB), os.path.basename(src) + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd))
         subprocess.check_call(cmd)

@@ -39,6 +39,9 @@ namespace gsi {
 namespace {
 
 constexpr int kThreads = 256;
+#ifndef GSI_STAGE_DIV
+#define GSI_STAGE_DIV 4   // stage a tile's rows when it has >= GSI_STAGE_DIV slots per row
+#endif
 constexpr int kJoinItems = 8;
 constexpr int kJoinTile = kThreads * kJoinItems;   // 2048 GBA slots per CTA
 
@@ -93,6 +96,7 @@ __global__ void __launch_bounds__(kThreads) k_filter(const uint32_t *__restrict_
     const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
     constexpr int kFW = 4;   // bitmap words per warp per iteration: 4 coalesced plane-0 loads in flight
     unsigned long long plane_words = 0;   // plane words this thread read (algorithmic bytes / 4)
+    unsigned long long my_count = 0;      // |C(u)| partial for u = lane
     for (long long w0 = (blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5)) * kFW; w0 < words;
          w0 += warps * kFW) {
         uint32_t lab[kFW], mask[kFW];
@@ -140,15 +144,20 @@ __global__ void __launch_bounds__(kThreads) k_filter(const uint32_t *__restrict_
 #pragma unroll
         for (int j = 0; j < kFW; j++) {
             if (w0 + j >= words) break;
+            // lane u collects the bitmap word of query vertex u: one store instruction per word
+            // and a register count per lane instead of k single-lane stores and shared atomics
+            uint32_t mine = 0;
             for (int u = 0; u < k; u++) {
                 const unsigned b = __ballot_sync(0xffffffffu, (mask[j] >> u) & 1u);
-                if (lane == 0) {
-                    bitmaps[(long long)u * words + w0 + j] = b;
-                    if (b) atomicAdd(&cnt_s[u], (unsigned long long)__popc(b));
-                }
+                if (lane == u) mine = b;
+            }
+            if (lane < k) {
+                bitmaps[(long long)lane * words + w0 + j] = mine;
+                my_count += __popc(mine);
             }
         }
     }
+    if (lane < k && my_count) atomicAdd(&cnt_s[lane], my_count);
     plane_words = warp_sum_u64(plane_words);
     if (lane == 0 && plane_words) atomicAdd(&loads_s, plane_words);
     __syncthreads();
@@ -336,15 +345,18 @@ __device__ __forceinline__ void row_hash(const int32_t *__restrict__ row, uint32
 }
 
 enum JoinMode { J_COUNT = 0, J_TABLE = 1, J_NEXT = 2 };
+// Slots per thread: J_NEXT carries the next-step probe state of every slot in registers, so
+// it runs 1024-slot tiles; the others 2048.
+__host__ __device__ constexpr int join_items(int mode) { return mode == J_NEXT ? 4 : 8; }
 
-// rowmap[j] = the row holding slot s0 + j*kJoinTile (j < ntiles), rowmap[ntiles] = the row
+// rowmap[j] = the row holding slot s0 + j*tile (j < ntiles), rowmap[ntiles] = the row
 // holding slot s1-1: the first/last row of every join tile, found by one thread per tile so
 // that no CTA of the join waits on a dependent search of F.
 __global__ void k_tile_rows(const unsigned long long *__restrict__ F, long long nM, unsigned long long s0,
-                            unsigned long long s1, unsigned ntiles, uint32_t *__restrict__ rowmap) {
+                            unsigned long long s1, unsigned ntiles, unsigned tile, uint32_t *__restrict__ rowmap) {
     const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (j > ntiles) return;
-    const unsigned long long s = j < ntiles ? s0 + (unsigned long long)j * kJoinTile : s1 - 1;
+    const unsigned long long s = j < ntiles ? s0 + (unsigned long long)j * tile : s1 - 1;
     long long lo = 0, hi = nM + 1;   // largest i with F[i] <= s
     while (hi - lo > 1) {
         const long long mid = (lo + hi) >> 1;
@@ -368,7 +380,7 @@ __global__ void k_tile_rows(const unsigned long long *__restrict__ F, long long 
 //             look-back chain) are written here: the next level never re-reads M_{t+1} to
 //             size its buffers.
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, MODE == J_NEXT ? 3 : 4) k_join(const int32_t *__restrict__ M, long long nM,
+__global__ void __launch_bounds__(kThreads, 4) k_join(const int32_t *__restrict__ M, long long nM,
                                                    const unsigned long long *__restrict__ F,
                                                    const Loc *__restrict__ loc, const uint32_t *__restrict__ rowmap,
                                                    StepParams P, StepParams P2, const int32_t *__restrict__ ci,
@@ -379,19 +391,21 @@ __global__ void __launch_bounds__(kThreads, MODE == J_NEXT ? 3 : 4) k_join(const
                                                    unsigned long long *__restrict__ F2,
                                                    unsigned long long *status, unsigned long long *status2,
                                                    unsigned *tile_ctr, Counters *ctr) {
+    constexpr int IT = join_items(MODE);   // slots per thread
+    constexpr int TILE = IT * kThreads;    // slots per CTA
     // Dynamic shared memory (join_smem_bytes<MODE>()): before the compaction it holds the row
     // marker / row offset per slot (sR), per tile row off0 - F_i (sBase) and the subtraction
     // columns (sInj); the write cache (sx, si, sloc) reuses the same bytes afterwards.
     extern __shared__ __align__(16) unsigned char dsm[];
     constexpr int kInjStage = MODE == J_COUNT ? 4 : 2;
     int *sR = reinterpret_cast<int *>(dsm);
-    uint32_t *sBase = reinterpret_cast<uint32_t *>(sR + kJoinTile);
-    int32_t *sInjBase = reinterpret_cast<int32_t *>(sBase + kJoinTile);
+    uint32_t *sBase = reinterpret_cast<uint32_t *>(sR + TILE);
+    int32_t *sInjBase = reinterpret_cast<int32_t *>(sBase + TILE);
     uint32_t *sx = reinterpret_cast<uint32_t *>(sR);     // write cache: new vertex
     uint32_t *si = sBase;                                // write cache: parent row
     Loc *sloc = reinterpret_cast<Loc *>(sInjBase);       // write cache: next buffer (E' = 1)
-    __shared__ unsigned wcnt[kJoinItems][kThreads / 32];
-    __shared__ unsigned wbase[kJoinItems][kThreads / 32];
+    __shared__ unsigned wcnt[IT][kThreads / 32];
+    __shared__ unsigned wbase[IT][kThreads / 32];
     __shared__ unsigned long long sm[34];
     __shared__ unsigned tile_s, agg_s;
     __shared__ unsigned long long base_s, base2_s;
@@ -399,17 +413,19 @@ __global__ void __launch_bounds__(kThreads, MODE == J_NEXT ? 3 : 4) k_join(const
     if (tid == 0) tile_s = atomicAdd(tile_ctr, 1u);
     {   // zero the row-marker array with 16 B stores
         int4 *z = reinterpret_cast<int4 *>(sR);
-        for (int j = tid; j < kJoinTile / 4; j += kThreads) z[j] = make_int4(0, 0, 0, 0);
+        for (int j = tid; j < TILE / 4; j += kThreads) z[j] = make_int4(0, 0, 0, 0);
     }
     __syncthreads();
     const unsigned tile = tile_s;
-    const unsigned long long tbase = s0 + (unsigned long long)tile * kJoinTile;
-    const unsigned long long tend = min(tbase + (unsigned long long)kJoinTile, s1);
+    const unsigned long long tbase = s0 + (unsigned long long)tile * TILE;
+    const unsigned long long tend = min(tbase + (unsigned long long)TILE, s1);
     const long long rlo = __ldg(rowmap + tile), rhi = __ldg(rowmap + tile + 1);
     const long long nr = rhi - rlo + 1;
     // Stage, per row of the tile, base = off0 - F_i (so slot s reads ci[base + s]) and the
     // columns the subtraction tests, so the per-slot work touches shared memory only.
-    const bool staged = nr <= kJoinTile;
+    // Staging pays when rows are long (many slots per staged row); with short rows the per-row
+    // loads would sit in the serial prologue, so those tiles read the row data per slot.
+    const bool staged = nr * GSI_STAGE_DIV <= TILE;
     const int n_inj_st = staged ? min(P.n_inj, kInjStage) : 0;
     // Row of every slot of the tile without a per-slot search (load-balanced search): each row
     // overlapping the tile marks its first tile-local slot, then an inclusive max-scan over the
@@ -421,15 +437,15 @@ __global__ void __launch_bounds__(kThreads, MODE == J_NEXT ? 3 : 4) k_join(const
             const unsigned long long i = (unsigned long long)(rlo + r);
             sBase[r] = loc[i * (unsigned)P.E].off - (uint32_t)a;
             const int32_t *row = M + i * (unsigned)P.t;
-            for (int c = 0; c < n_inj_st; c++) sInjBase[c * kJoinTile + r] = __ldg(row + P.inj_col[c]);
+            for (int c = 0; c < n_inj_st; c++) sInjBase[c * TILE + r] = __ldg(row + P.inj_col[c]);
         }
     }
     __syncthreads();
     {
-        int v[kJoinItems], m = 0;
+        int v[IT], m = 0;
 #pragma unroll
-        for (int q = 0; q < kJoinItems; q++) {
-            v[q] = sR[tid * kJoinItems + q];
+        for (int q = 0; q < IT; q++) {
+            v[q] = sR[tid * IT + q];
             m = max(m, v[q]);
             v[q] = m;
         }
@@ -446,18 +462,18 @@ __global__ void __launch_bounds__(kThreads, MODE == J_NEXT ? 3 : 4) k_join(const
         for (int o = 1; o < 32; o <<= 1) wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
         carry = max(carry, wmax);
 #pragma unroll
-        for (int q = 0; q < kJoinItems; q++) sR[tid * kJoinItems + q] = max(v[q], carry);
+        for (int q = 0; q < IT; q++) sR[tid * IT + q] = max(v[q], carry);
     }
     __syncthreads();
 
     // Phased over the 8 slots of this thread so that each phase's independent loads are in
     // flight together (ci -> C(u) bit -> subtraction -> other lists -> next probe).
-    bool keep[kJoinItems];
-    uint32_t xs[kJoinItems];
-    uint32_t rows[kJoinItems];   // row offset from rlo
-    uint32_t cio[kJoinItems];
+    bool keep[IT];
+    uint32_t xs[IT];
+    uint32_t rows[IT];   // row offset from rlo
+    uint32_t cio[IT];
 #pragma unroll
-    for (int it = 0; it < kJoinItems; it++) {
+    for (int it = 0; it < IT; it++) {
         const unsigned long long s = tbase + (unsigned long long)it * kThreads + tid;
         keep[it] = s < tend;
         const int r = sR[it * kThreads + tid];
@@ -470,9 +486,9 @@ __global__ void __launch_bounds__(kThreads, MODE == J_NEXT ? 3 : 4) k_join(const
         }
     }
 #pragma unroll
-    for (int it = 0; it < kJoinItems; it++) xs[it] = keep[it] ? (uint32_t)__ldg(ci + cio[it]) : 0u;
+    for (int it = 0; it < IT; it++) xs[it] = keep[it] ? (uint32_t)__ldg(ci + cio[it]) : 0u;
 #pragma unroll
-    for (int it = 0; it < kJoinItems; it++) {                                    // x in C(u)
+    for (int it = 0; it < IT; it++) {                                    // x in C(u)
         const uint32_t x = xs[it];
         if (keep[it]) keep[it] = (__ldg(cu_bitmap + (x >> 5)) >> (x & 31)) & 1u;
     }
@@ -480,20 +496,20 @@ __global__ void __launch_bounds__(kThreads, MODE == J_NEXT ? 3 : 4) k_join(const
         const int col = P.inj_col[c];
         if (c < n_inj_st) {
 #pragma unroll
-            for (int it = 0; it < kJoinItems; it++)
-                if (keep[it]) keep[it] = sInjBase[c * kJoinTile + rows[it]] != (int32_t)xs[it];
+            for (int it = 0; it < IT; it++)
+                if (keep[it]) keep[it] = sInjBase[c * TILE + rows[it]] != (int32_t)xs[it];
         } else {
 #pragma unroll
-            for (int it = 0; it < kJoinItems; it++)
+            for (int it = 0; it < IT; it++)
                 if (keep[it])
                     keep[it] = __ldg(M + (unsigned long long)(rlo + rows[it]) * (unsigned)P.t + col) != (int32_t)xs[it];
         }
     }
 #pragma unroll
-    for (int it = 0; it < kJoinItems; it++) rows[it] += (uint32_t)rlo;              // absolute row index
+    for (int it = 0; it < IT; it++) rows[it] += (uint32_t)rlo;              // absolute row index
     if (P.E > 1) {                                                               // Alg. 3 line 13
 #pragma unroll
-        for (int it = 0; it < kJoinItems; it++) {
+        for (int it = 0; it < IT; it++) {
             const Loc *L = loc + (unsigned long long)rows[it] * (unsigned)P.E;
             for (int e = 1; e < P.E && keep[it]; e++) {
                 const Loc Le = L[e];
@@ -505,7 +521,7 @@ __global__ void __launch_bounds__(kThreads, MODE == J_NEXT ? 3 : 4) k_join(const
     if constexpr (MODE == J_COUNT) {
         unsigned long long c = 0, h1 = 0, h2 = 0;
 #pragma unroll
-        for (int it = 0; it < kJoinItems; it++) {
+        for (int it = 0; it < IT; it++) {
             if (!keep[it]) continue;
             c++;
             if (P.fp) row_hash(M + (long long)rows[it] * P.t, xs[it], P, h1, h2);
@@ -523,42 +539,39 @@ __global__ void __launch_bounds__(kThreads, MODE == J_NEXT ? 3 : 4) k_join(const
         }
     } else {
         // ---- J_NEXT: next-step probe of every survivor, dead rows dropped --------------------
-        Loc N0[kJoinItems];
+        Loc N0[IT];
         if constexpr (MODE == J_NEXT) {
             unsigned long long all = 0;
 #pragma unroll
-            for (int it = 0; it < kJoinItems; it++) all += keep[it] ? 1 : 0;
+            for (int it = 0; it < IT; it++) all += keep[it] ? 1 : 0;
             all = warp_sum_u64(all);
             if (lane == 0 && all) atomicAdd(&ctr->count, all);      // |M_{t+1}| including dead rows
             if (P2.E == 1) {
                 const int c2 = P2.col[0];
-                uint32_t v[kJoinItems];
+                uint32_t v[IT];
 #pragma unroll
-                for (int it = 0; it < kJoinItems; it++)
+                for (int it = 0; it < IT; it++)
                     v[it] = keep[it] ? (c2 < P.t ? (uint32_t)__ldg(M + (long long)rows[it] * P.t + c2) : xs[it]) : 0u;
-                // two half-batches of 4 keep the 8 first-sector loads (8 words each) in fewer registers
-                uint32_t va[4], vb[4];
-                bool ka[4], kb[4];
-                Loc na[4], nb[4];
+                // batches of 4 keep the first-sector loads (8 words each) in fewer registers
 #pragma unroll
-                for (int q = 0; q < 4; q++) {
-                    va[q] = v[q];
-                    ka[q] = keep[q];
-                    vb[q] = v[q + 4];
-                    kb[q] = keep[q + 4];
-                }
-                pcsr_lookup_batch<4>(groups, gpn, P2.gbase[0], P2.ngroups[0], P2.lab[0], va, ka, na);
-                pcsr_lookup_batch<4>(groups, gpn, P2.gbase[0], P2.ngroups[0], P2.lab[0], vb, kb, nb);
+                for (int h = 0; h < IT; h += 4) {
+                    uint32_t vb[4];
+                    bool kb[4];
+                    Loc nb[4];
 #pragma unroll
-                for (int q = 0; q < 4; q++) {
-                    N0[q] = na[q];
-                    N0[q + 4] = nb[q];
+                    for (int q = 0; q < 4; q++) {
+                        vb[q] = v[h + q];
+                        kb[q] = keep[h + q];
+                    }
+                    pcsr_lookup_batch<4>(groups, gpn, P2.gbase[0], P2.ngroups[0], P2.lab[0], vb, kb, nb);
+#pragma unroll
+                    for (int q = 0; q < 4; q++) N0[h + q] = nb[q];
                 }
 #pragma unroll
-                for (int it = 0; it < kJoinItems; it++) keep[it] = keep[it] && N0[it].len > 0;
+                for (int it = 0; it < IT; it++) keep[it] = keep[it] && N0[it].len > 0;
             } else {
 #pragma unroll
-                for (int it = 0; it < kJoinItems; it++) {
+                for (int it = 0; it < IT; it++) {
                     if (!keep[it]) continue;
                     unsigned long long l0, el;
                     probe_row_local(M + (long long)rows[it] * P.t, P.t, xs[it], P2, groups, gpn, nullptr, l0, el);
@@ -570,9 +583,9 @@ __global__ void __launch_bounds__(kThreads, MODE == J_NEXT ? 3 : 4) k_join(const
         // ---- ordered compaction into the shared-memory write cache + look-back ------------
         // (the __syncthreads below also orders every read of sR / sBase / sInj before the
         //  write cache, which reuses those bytes, is written)
-        unsigned ballots[kJoinItems];
+        unsigned ballots[IT];
 #pragma unroll
-        for (int it = 0; it < kJoinItems; it++) {
+        for (int it = 0; it < IT; it++) {
             ballots[it] = __ballot_sync(0xffffffffu, keep[it]);
             if (lane == 0) wcnt[it][warp] = __popc(ballots[it]);
         }
@@ -581,25 +594,34 @@ __global__ void __launch_bounds__(kThreads, MODE == J_NEXT ? 3 : 4) k_join(const
             // look-back chains (row offsets and next F) run at the same time (warps 0 and 1)
             unsigned long long mylen = 0;
 #pragma unroll
-            for (int it = 0; it < kJoinItems; it++) mylen += keep[it] ? N0[it].len : 0u;
+            for (int it = 0; it < IT; it++) mylen += keep[it] ? N0[it].len : 0u;
             mylen = warp_sum_u64(mylen);
             if (lane == 0) sm[warp] = mylen;
         }
         __syncthreads();
         if (warp == 0) {
-            constexpr int NW = kThreads / 32;   // 64 (it, warp) counts in slot order: it * 8 + warp
-            const unsigned a = wcnt[(2 * lane) / NW][(2 * lane) % NW];
-            const unsigned b = wcnt[(2 * lane + 1) / NW][(2 * lane + 1) % NW];
-            const unsigned pair = a + b;
+            constexpr int NW = kThreads / 32;   // IT * NW (it, warp) counts in slot order: it * NW + warp
+            constexpr int PER = IT * NW / 32;   // entries per lane (1 or 2)
+            unsigned e[PER], pair = 0;
+#pragma unroll
+            for (int q = 0; q < PER; q++) {
+                const int idx = PER * lane + q;
+                e[q] = wcnt[idx / NW][idx % NW];
+                pair += e[q];
+            }
             unsigned inc = pair;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
                 if (lane >= o) inc += y;
             }
-            const unsigned ex = inc - pair;
-            wbase[(2 * lane) / NW][(2 * lane) % NW] = ex;
-            wbase[(2 * lane + 1) / NW][(2 * lane + 1) % NW] = ex + a;
+            unsigned ex = inc - pair;
+#pragma unroll
+            for (int q = 0; q < PER; q++) {
+                const int idx = PER * lane + q;
+                wbase[idx / NW][idx % NW] = ex;
+                ex += e[q];
+            }
             const unsigned total = __shfl_sync(0xffffffffu, inc, 31);
             const unsigned long long pre = lookback_exclusive(status, tile, total);
             if (lane == 0) {
@@ -618,7 +640,7 @@ __global__ void __launch_bounds__(kThreads, MODE == J_NEXT ? 3 : 4) k_join(const
         __syncthreads();
         const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
-        for (int it = 0; it < kJoinItems; it++) {
+        for (int it = 0; it < IT; it++) {
             if (keep[it]) {
                 const unsigned lp = wbase[it][warp] + __popc(ballots[it] & lt);
                 sx[lp] = xs[it];
@@ -674,8 +696,8 @@ __global__ void __launch_bounds__(kThreads, MODE == J_NEXT ? 3 : 4) k_join(const
             // the tile's offset base2_s came from the second look-back chain above
             unsigned long long mine = 0;
 #pragma unroll
-            for (int q = 0; q < kJoinItems; q++) {
-                const unsigned j = tid * kJoinItems + q;
+            for (int q = 0; q < IT; q++) {
+                const unsigned j = tid * IT + q;
                 if (j < cnt) mine += sloc[j].len;
             }
             const unsigned long long agg2 = sm[32];
@@ -684,8 +706,8 @@ __global__ void __launch_bounds__(kThreads, MODE == J_NEXT ? 3 : 4) k_join(const
             const unsigned long long ex2 = block_exclusive_scan(mine, sm, &dummy);
             unsigned long long run = pre2 + ex2;
 #pragma unroll
-            for (int q = 0; q < kJoinItems; q++) {
-                const unsigned j = tid * kJoinItems + q;
+            for (int q = 0; q < IT; q++) {
+                const unsigned j = tid * IT + q;
                 if (j < cnt) {
                     F2[base + j] = run;
                     run += sloc[j].len;
@@ -709,7 +731,7 @@ __global__ void __launch_bounds__(kThreads, MODE == J_NEXT ? 3 : 4) k_join(const
 
 template <int MODE>
 constexpr size_t join_smem_bytes() {
-    return (size_t)(2 + (MODE == J_COUNT ? 4 : 2)) * kJoinTile * 4;
+    return (size_t)(2 + (MODE == J_COUNT ? 4 : 2)) * join_items(MODE) * kThreads * 4;
 }
 
 // Count + fingerprint of a table whose columns are in pi order (k = 1 queries).
@@ -1280,7 +1302,8 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         const size_t mk = A.mark();
         const unsigned long long c1 = std::min(s1, c0 + chunk), slots = c1 - c0;
         if (c0 != s0 || c1 != s1) S.n_chunks++;
-        const unsigned jt = grid_for(slots, kJoinTile);
+        const unsigned tile_slots = (unsigned)(join_items(mode) * kThreads);
+        const unsigned jt = grid_for(slots, tile_slots);
         unsigned long long *status = nullptr;
         GSI_TRY(A.get(&status, 2ull * jt + 2));
         GSI_CUDA(cudaMemsetAsync(status, 0, 8ull * (2ull * jt + 2), st));
@@ -1301,7 +1324,7 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         GSI_TRY(A.get(&rowmap, (unsigned long long)jt + 1));
         prof.begin(GSI_K_OTHER);
         k_tile_rows<<<grid_for((unsigned long long)jt + 1, kThreads), kThreads, 0, st>>>(F, (long long)nM, c0, c1, jt,
-                                                                                       rowmap);
+                                                                                       tile_slots, rowmap);
         prof.end();
         prof.begin(GSI_K_JOIN);
         if (mode == J_COUNT)

@@ -18,7 +18,7 @@ from typing import Dict, List, Optional, Sequence, Tuple
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libgsi_b200.so")
+LIB_PATH = os.environ.get("GSI_LIB") or os.path.join(_PKG, "lib", "libgsi_b200.so")   # GSI_LIB: A/B builds
 HEADER = os.path.join(os.path.dirname(_PKG), "include", "gsi.h")
 
 GSI_MAX_K = 32
