@@ -39,6 +39,12 @@ namespace gsi {
 namespace {
 
 constexpr int kThreads = 256;
+#ifndef GSI_STAGE_BASE
+#define GSI_STAGE_BASE 1  // stage per-row ci bases in the join tile
+#endif
+#ifndef GSI_STAGE_INJ
+#define GSI_STAGE_INJ 1   // stage up to this many subtraction columns per row
+#endif
 #ifndef GSI_STAGE_DIV
 #define GSI_STAGE_DIV 4   // stage a tile's rows when it has >= GSI_STAGE_DIV slots per row
 #endif
@@ -58,6 +64,8 @@ struct StepParams {
     int inj_col[GSI_MAX_K];      // columns the subtraction must test (same vertex label as u)
     int pos_of_q[GSI_MAX_K];     // final level: column (0..t) holding query vertex q
     int fp;                      // final level: accumulate the set fingerprint
+    int stage_base;              // join tile stages per-row ci bases in shared memory
+    int stage_inj;               // ... and up to this many subtraction columns
 };
 
 // Counters shared by the kernels of one query (device).
@@ -397,13 +405,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_join(const int32_t *__restrict_
     // marker / row offset per slot (sR), per tile row off0 - F_i (sBase) and the subtraction
     // columns (sInj); the write cache (sx, si, sloc) reuses the same bytes afterwards.
     extern __shared__ __align__(16) unsigned char dsm[];
-    constexpr int kInjStage = MODE == J_COUNT ? 4 : 2;
+    // staging region (before the compaction)     | write cache (after), same bytes
+    //   sR[TILE] | sBase[TILE] | sInj[P.stage_inj][TILE] | sx[TILE] | si[TILE] | sloc[TILE] (J_NEXT)
     int *sR = reinterpret_cast<int *>(dsm);
     uint32_t *sBase = reinterpret_cast<uint32_t *>(sR + TILE);
     int32_t *sInjBase = reinterpret_cast<int32_t *>(sBase + TILE);
-    uint32_t *sx = reinterpret_cast<uint32_t *>(sR);     // write cache: new vertex
-    uint32_t *si = sBase;                                // write cache: parent row
-    Loc *sloc = reinterpret_cast<Loc *>(sInjBase);       // write cache: next buffer (E' = 1)
+    uint32_t *sx = reinterpret_cast<uint32_t *>(dsm);
+    uint32_t *si = sx + TILE;
+    Loc *sloc = reinterpret_cast<Loc *>(si + TILE);
     __shared__ unsigned wcnt[IT][kThreads / 32];
     __shared__ unsigned wbase[IT][kThreads / 32];
     __shared__ unsigned long long sm[34];
@@ -425,8 +434,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_join(const int32_t *__restrict_
     // columns the subtraction tests, so the per-slot work touches shared memory only.
     // Staging pays when rows are long (many slots per staged row); with short rows the per-row
     // loads would sit in the serial prologue, so those tiles read the row data per slot.
-    const bool staged = nr * GSI_STAGE_DIV <= TILE;
-    const int n_inj_st = staged ? min(P.n_inj, kInjStage) : 0;
+    const bool staged = P.stage_base && nr * GSI_STAGE_DIV <= TILE;
+    const int n_inj_st = staged ? min(P.n_inj, P.stage_inj) : 0;
     // Row of every slot of the tile without a per-slot search (load-balanced search): each row
     // overlapping the tile marks its first tile-local slot, then an inclusive max-scan over the
     // 2048 slots spreads the row offset to all its slots.
@@ -729,10 +738,16 @@ __global__ void __launch_bounds__(kThreads, 4) k_join(const int32_t *__restrict_
     }
 }
 
-template <int MODE>
-constexpr size_t join_smem_bytes() {
-    return (size_t)(2 + (MODE == J_COUNT ? 4 : 2)) * join_items(MODE) * kThreads * 4;
+// Dynamic shared memory of a join launch: the larger of the staging region (row markers,
+// optional ci bases and subtraction columns) and the write cache.  Kept to what the step
+// uses: the rest of the 228 KB SM memory stays L1 cache for the ci / bitmap / row reads.
+inline size_t join_smem_bytes(int mode, const StepParams &P) {
+    const size_t tile = (size_t)join_items(mode) * kThreads;
+    const size_t staging = tile * 4 * (1 + (P.stage_base ? 1 : 0) + (size_t)P.stage_inj);
+    const size_t cache = mode == J_COUNT ? 0 : tile * 4 * 2 + (mode == J_NEXT ? tile * 8 : 0);
+    return std::max(staging, cache);
 }
+constexpr int kMaxJoinSmem = 6 * 2048 * 4;
 
 // Count + fingerprint of a table whose columns are in pi order (k = 1 queries).
 __global__ void k_fp_rows(const int32_t *__restrict__ T, long long nrows, StepParams P, Counters *ctr) {
@@ -949,9 +964,9 @@ void ensure_pool(int dev) {
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     // the join tiles use > 48 KB of dynamic shared memory (opt-in, per device)
-    cudaFuncSetAttribute(k_join<J_COUNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)join_smem_bytes<J_COUNT>());
-    cudaFuncSetAttribute(k_join<J_TABLE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)join_smem_bytes<J_TABLE>());
-    cudaFuncSetAttribute(k_join<J_NEXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)join_smem_bytes<J_NEXT>());
+    cudaFuncSetAttribute(k_join<J_COUNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxJoinSmem);
+    cudaFuncSetAttribute(k_join<J_TABLE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxJoinSmem);
+    cudaFuncSetAttribute(k_join<J_NEXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxJoinSmem);
     cudaGetLastError();
     g_pool_ready[dev] = true;
 }
@@ -1226,6 +1241,7 @@ void fill_params(QueryCtx &C, const Step &s, StepParams &P) {
     P.per_row_e0 = C.opts.e0_mode == 0 ? 1 : 0;
     for (int qv = 0; qv < C.q->k; qv++) P.pos_of_q[qv] = C.pos_of_q[qv];
     P.fp = C.opts.fingerprint != 0;
+    P.stage_base = GSI_STAGE_BASE;
     std::vector<int> eorder(E);
     for (int e = 0; e < E; e++) eorder[e] = e;
     std::swap(eorder[0], eorder[s.paper_e0]);   // paper mode: e0 first (Alg. 3 line 9)
@@ -1245,6 +1261,7 @@ void fill_params(QueryCtx &C, const Step &s, StepParams &P) {
             if (!linked) P.inj_col[P.n_inj++] = c;
         }
     }
+    P.stage_inj = P.stage_base ? std::min(P.n_inj, GSI_STAGE_INJ) : 0;
 }
 
 // Level t = steps[si].t: M (nM x t) with its Prealloc (loc, F, |GBA| = gba) already computed
@@ -1328,13 +1345,13 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         prof.end();
         prof.begin(GSI_K_JOIN);
         if (mode == J_COUNT)
-            k_join<J_COUNT><<<jt, kThreads, join_smem_bytes<J_COUNT>(), st>>>(M, (long long)nM, F, loc, rowmap, P, P2, g->ci, cu, g->groups,
+            k_join<J_COUNT><<<jt, kThreads, join_smem_bytes(J_COUNT, P), st>>>(M, (long long)nM, F, loc, rowmap, P, P2, g->ci, cu, g->groups,
                                                      g->gpn, c0, c1, out, loc2, F2, st1, st2, tctr, C.ctr);
         else if (mode == J_TABLE)
-            k_join<J_TABLE><<<jt, kThreads, join_smem_bytes<J_TABLE>(), st>>>(M, (long long)nM, F, loc, rowmap, P, P2, g->ci, cu, g->groups,
+            k_join<J_TABLE><<<jt, kThreads, join_smem_bytes(J_TABLE, P), st>>>(M, (long long)nM, F, loc, rowmap, P, P2, g->ci, cu, g->groups,
                                                      g->gpn, c0, c1, out, loc2, F2, st1, st2, tctr, C.ctr);
         else
-            k_join<J_NEXT><<<jt, kThreads, join_smem_bytes<J_NEXT>(), st>>>(M, (long long)nM, F, loc, rowmap, P, P2, g->ci, cu, g->groups,
+            k_join<J_NEXT><<<jt, kThreads, join_smem_bytes(J_NEXT, P), st>>>(M, (long long)nM, F, loc, rowmap, P, P2, g->ci, cu, g->groups,
                                                     g->gpn, c0, c1, out, loc2, F2, st1, st2, tctr, C.ctr);
         prof.end();
         Counters hc;
@@ -1420,7 +1437,10 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     C.S = &S;
     C.words = words;
 
-    GSI_TRY(A.init_bump(64ull << 20));
+#ifndef GSI_BUMP_MB
+#define GSI_BUMP_MB 64
+#endif
+    if (GSI_BUMP_MB > 0) GSI_TRY(A.init_bump((size_t)GSI_BUMP_MB << 20));
     GSI_TRY(A.get(&C.ctr, 1));
     GSI_CUDA(cudaMemsetAsync(C.ctr, 0, sizeof(Counters), st));
 
