@@ -355,7 +355,10 @@ __device__ __forceinline__ void row_hash(const int32_t *__restrict__ row, uint32
 enum JoinMode { J_COUNT = 0, J_TABLE = 1, J_NEXT = 2 };
 // Slots per thread: J_NEXT carries the next-step probe state of every slot in registers, so
 // it runs 1024-slot tiles; the others 2048.
-__host__ __device__ constexpr int join_items(int mode) { return mode == J_NEXT ? 4 : 8; }
+#ifndef GSI_NEXT_ITEMS
+#define GSI_NEXT_ITEMS 4
+#endif
+__host__ __device__ constexpr int join_items(int mode) { return mode == J_NEXT ? GSI_NEXT_ITEMS : 8; }
 
 // rowmap[j] = the row holding slot s0 + j*tile (j < ntiles), rowmap[ntiles] = the row
 // holding slot s1-1: the first/last row of every join tile, found by one thread per tile so
@@ -388,7 +391,7 @@ __global__ void k_tile_rows(const unsigned long long *__restrict__ F, long long 
 //             look-back chain) are written here: the next level never re-reads M_{t+1} to
 //             size its buffers.
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, 4) k_join(const int32_t *__restrict__ M, long long nM,
+__global__ void __launch_bounds__(kThreads, (MODE == J_NEXT && GSI_NEXT_ITEMS > 4) ? 3 : 4) k_join(const int32_t *__restrict__ M, long long nM,
                                                    const unsigned long long *__restrict__ F,
                                                    const Loc *__restrict__ loc, const uint32_t *__restrict__ rowmap,
                                                    StepParams P, StepParams P2, const int32_t *__restrict__ ci,
@@ -481,17 +484,26 @@ __global__ void __launch_bounds__(kThreads, 4) k_join(const int32_t *__restrict_
     uint32_t xs[IT];
     uint32_t rows[IT];   // row offset from rlo
     uint32_t cio[IT];
+    const uint32_t tlen = (uint32_t)(tend - tbase);   // slots in this tile (<= TILE)
+    if (staged) {        // tile-uniform branch: 32-bit slot arithmetic against shared memory only
+        const uint32_t tb32 = (uint32_t)tbase;
 #pragma unroll
-    for (int it = 0; it < IT; it++) {
-        const unsigned long long s = tbase + (unsigned long long)it * kThreads + tid;
-        keep[it] = s < tend;
-        const int r = sR[it * kThreads + tid];
-        rows[it] = (uint32_t)r;
-        if (staged) {
-            cio[it] = sBase[r] + (uint32_t)s;
-        } else {
+        for (int it = 0; it < IT; it++) {
+            const uint32_t ls = (uint32_t)(it * kThreads + tid);
+            keep[it] = ls < tlen;
+            const int r = sR[ls];
+            rows[it] = (uint32_t)r;
+            cio[it] = sBase[r] + tb32 + ls;
+        }
+    } else {
+#pragma unroll
+        for (int it = 0; it < IT; it++) {
+            const uint32_t ls = (uint32_t)(it * kThreads + tid);
+            keep[it] = ls < tlen;
+            const int r = sR[ls];
+            rows[it] = (uint32_t)r;
             const unsigned long long i = (unsigned long long)(rlo + r);
-            cio[it] = keep[it] ? loc[i * (unsigned)P.E].off + (uint32_t)(s - __ldg(F + i)) : 0u;
+            cio[it] = keep[it] ? loc[i * (unsigned)P.E].off + (uint32_t)(tbase + ls - __ldg(F + i)) : 0u;
         }
     }
 #pragma unroll
