@@ -356,9 +356,14 @@ enum JoinMode { J_COUNT = 0, J_TABLE = 1, J_NEXT = 2 };
 // Slots per thread: J_NEXT carries the next-step probe state of every slot in registers, so
 // it runs 1024-slot tiles; the others 2048.
 #ifndef GSI_NEXT_ITEMS
-#define GSI_NEXT_ITEMS 4
+#define GSI_NEXT_ITEMS 8
 #endif
-__host__ __device__ constexpr int join_items(int mode) { return mode == J_NEXT ? GSI_NEXT_ITEMS : 8; }
+#ifndef GSI_COUNT_ITEMS
+#define GSI_COUNT_ITEMS 8
+#endif
+__host__ __device__ constexpr int join_items(int mode) {
+    return mode == J_NEXT ? GSI_NEXT_ITEMS : (mode == J_COUNT ? GSI_COUNT_ITEMS : 8);
+}
 
 // rowmap[j] = the row holding slot s0 + j*tile (j < ntiles), rowmap[ntiles] = the row
 // holding slot s1-1: the first/last row of every join tile, found by one thread per tile so
@@ -391,7 +396,10 @@ __global__ void k_tile_rows(const unsigned long long *__restrict__ F, long long 
 //             look-back chain) are written here: the next level never re-reads M_{t+1} to
 //             size its buffers.
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, (MODE == J_NEXT && GSI_NEXT_ITEMS > 4) ? 3 : 4) k_join(const int32_t *__restrict__ M, long long nM,
+#ifndef GSI_NEXT_MINB
+#define GSI_NEXT_MINB 3
+#endif
+__global__ void __launch_bounds__(kThreads, join_items(MODE) > 8 ? 2 : ((MODE == J_NEXT && GSI_NEXT_ITEMS > 4) ? GSI_NEXT_MINB : 4)) k_join(const int32_t *__restrict__ M, long long nM,
                                                    const unsigned long long *__restrict__ F,
                                                    const Loc *__restrict__ loc, const uint32_t *__restrict__ rowmap,
                                                    StepParams P, StepParams P2, const int32_t *__restrict__ ci,
@@ -759,7 +767,7 @@ inline size_t join_smem_bytes(int mode, const StepParams &P) {
     const size_t cache = mode == J_COUNT ? 0 : tile * 4 * 2 + (mode == J_NEXT ? tile * 8 : 0);
     return std::max(staging, cache);
 }
-constexpr int kMaxJoinSmem = 6 * 2048 * 4;
+constexpr int kMaxJoinSmem = 6 * 4096 * 4;
 
 // Count + fingerprint of a table whose columns are in pi order (k = 1 queries).
 __global__ void k_fp_rows(const int32_t *__restrict__ T, long long nrows, StepParams P, Counters *ctr) {
