@@ -347,14 +347,19 @@ def run_gsi(args):
     dom = int(np.argmax(ms_k))
     peak, peak_src = load_peaks()
     achieved = (bytes_k[dom] / (ms_k[dom] / 1e3)) / 1e9 if ms_k[dom] > 0 else 0.0
-    traffic = None
+    # DRAM traffic of the dominant kernel from the committed `ncu --set full` capture of this
+    # workload (dram__bytes_read.sum + dram__bytes_write.sum per launch, averaged over the
+    # captured launches; profiles/ncu_traffic.json names the capture)
+    traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         tt = json.load(open(tp)).get(args.config, {}).get(gsi.KCLASS[dom])
         if tt is not None:
-            traffic = tt
+            traffic, traffic_src = tt.get("dram_bytes_per_launch"), tt.get("source")
     roofline = {"bound": "hbm", "kernel": f"k_{gsi.KCLASS[dom]}", "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                "alg_bytes_per_launch": float(bytes_k[dom] / max(launches_k[dom], 1)),
+                "ms_per_launch": float(ms_k[dom] / max(launches_k[dom], 1)), "peak_source": peak_src,
                 "share_of_step": float(ms_k[dom] / max(ms_k.sum(), 1e-9)),
                 "per_kernel_ms": {gsi.KCLASS[i]: float(ms_k[i]) for i in range(6)},
                 "per_kernel_alg_GBps": {gsi.KCLASS[i]: float(bytes_k[i] / (ms_k[i] / 1e3) / 1e9) if ms_k[i] else 0.0

@@ -1341,12 +1341,14 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         if (c0 != s0 || c1 != s1) S.n_chunks++;
         const unsigned tile_slots = (unsigned)(join_items(mode) * kThreads);
         const unsigned jt = grid_for(slots, tile_slots);
+        // one zeroed scratch region per launch: [Counters | tile counter + status 1 | status 2]
+        constexpr unsigned kCtrWords = sizeof(Counters) / 8;
         unsigned long long *status = nullptr;
-        GSI_TRY(A.get(&status, 2ull * jt + 2));
-        GSI_CUDA(cudaMemsetAsync(status, 0, 8ull * (2ull * jt + 2), st));
-        unsigned *tctr = (unsigned *)status;
-        unsigned long long *st1 = status + 1, *st2 = status + 2 + jt;
-        GSI_CUDA(cudaMemsetAsync(C.ctr, 0, sizeof(Counters), st));
+        GSI_TRY(A.get(&status, kCtrWords + 2ull * jt + 2));
+        GSI_CUDA(cudaMemsetAsync(status, 0, 8ull * (kCtrWords + 2ull * jt + 2), st));
+        Counters *lctr = reinterpret_cast<Counters *>(status);
+        unsigned *tctr = (unsigned *)(status + kCtrWords);
+        unsigned long long *st1 = status + kCtrWords + 1, *st2 = status + kCtrWords + 2 + jt;
         int32_t *out = nullptr;
         Loc *loc2 = nullptr;
         unsigned long long *F2 = nullptr;
@@ -1354,8 +1356,7 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         if (mode == J_NEXT) {
             GSI_TRY(A.get(&out, slots * (unsigned long long)(t + 1)));
             GSI_TRY(A.get(&loc2, slots * (unsigned long long)P2.E));
-            GSI_TRY(A.get(&F2, slots + 1));
-            GSI_CUDA(cudaMemsetAsync(F2, 0, 8, st));
+            GSI_TRY(A.get(&F2, slots + 1));   // F2[0..nout] written by the kernel
         }
         uint32_t *rowmap = nullptr;
         GSI_TRY(A.get(&rowmap, (unsigned long long)jt + 1));
@@ -1366,16 +1367,16 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         prof.begin(GSI_K_JOIN);
         if (mode == J_COUNT)
             k_join<J_COUNT><<<jt, kThreads, join_smem_bytes(J_COUNT, P), st>>>(M, (long long)nM, F, loc, rowmap, P, P2, g->ci, cu, g->groups,
-                                                     g->gpn, c0, c1, out, loc2, F2, st1, st2, tctr, C.ctr);
+                                                     g->gpn, c0, c1, out, loc2, F2, st1, st2, tctr, lctr);
         else if (mode == J_TABLE)
             k_join<J_TABLE><<<jt, kThreads, join_smem_bytes(J_TABLE, P), st>>>(M, (long long)nM, F, loc, rowmap, P, P2, g->ci, cu, g->groups,
-                                                     g->gpn, c0, c1, out, loc2, F2, st1, st2, tctr, C.ctr);
+                                                     g->gpn, c0, c1, out, loc2, F2, st1, st2, tctr, lctr);
         else
             k_join<J_NEXT><<<jt, kThreads, join_smem_bytes(J_NEXT, P), st>>>(M, (long long)nM, F, loc, rowmap, P, P2, g->ci, cu, g->groups,
-                                                    g->gpn, c0, c1, out, loc2, F2, st1, st2, tctr, C.ctr);
+                                                    g->gpn, c0, c1, out, loc2, F2, st1, st2, tctr, lctr);
         prof.end();
         Counters hc;
-        GSI_CUDA(d2h(S, &hc, C.ctr, sizeof(Counters), st));
+        GSI_CUDA(d2h(S, &hc, lctr, sizeof(Counters), st));
         GSI_CUDA(cudaStreamSynchronize(st));
         GSI_CUDA(cudaGetLastError());
         A.release(status);
