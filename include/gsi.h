@@ -146,6 +146,7 @@ typedef struct {
                                     exact count of the completed chunk prefix                  */
     int32_t fingerprint;         /* 1: compute the set fingerprint of the final rows (costs ~2k
                                     hash rounds per match); 0: fingerprint = (count, 0, 0)      */
+    int32_t no_shared_lists;     /* 1: never switch a level to shared N(v,l0) ∩ C(u) lists      */
 } gsi_query_opts;
 
 void gsi_query_opts_default(gsi_query_opts *opts);
@@ -192,6 +193,7 @@ typedef struct {
     uint32_t n_chunks;                /* slot-range chunks executed below the memory budget   */
     int32_t capped;                   /* 1: timed out with partial_on_timeout                 */
     uint64_t h2d_bytes, d2h_bytes;    /* host<->device bytes this query copied                */
+    uint32_t n_shared_lists;          /* levels that enumerated shared N(v,l0) ∩ C(u) lists   */
 } gsi_stats;
 
 gsi_status gsi_result_count(const gsi_result *r, uint64_t *count);

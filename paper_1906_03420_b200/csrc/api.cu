@@ -123,7 +123,7 @@ gsi_status gsi_graph_buffers(const gsi_graph *g, gsi_buffer_desc *descs, int32_t
         return GSI_ERR_INVALID_ARG;
     }
     const int nl = g->n_labels;
-    const uint64_t need = sizeof(MetaHeader) + (uint64_t)nl * (4 + 8 + 8 + 4);
+    const uint64_t need = sizeof(MetaHeader) + (uint64_t)nl * (4 + 8 + 8 + 4) + 4ull * (nl + 1);
     if (descs) {
         descs[0] = {"sig", g->sig, (uint64_t)g->n * kPlanes * 4};
         descs[1] = {"groups", g->groups, (uint64_t)g->n_groups * g->gpn * 8};
@@ -135,7 +135,7 @@ gsi_status gsi_graph_buffers(const gsi_graph *g, gsi_buffer_desc *descs, int32_t
             set_error("meta buffer too small");
             return GSI_ERR_INVALID_ARG;
         }
-        MetaHeader h{kMetaMagic, g->n, g->m, g->n_groups, g->overflow_groups, nl, g->gpn, g->max_chain, 1};
+        MetaHeader h{kMetaMagic, g->n, g->m, g->n_groups, g->overflow_groups, nl, g->gpn, g->max_chain, 2};
         char *p = (char *)meta;
         std::memcpy(p, &h, sizeof(h));
         p += sizeof(h);
@@ -146,6 +146,8 @@ gsi_status gsi_graph_buffers(const gsi_graph *g, gsi_buffer_desc *descs, int32_t
         std::memcpy(p, g->gbase.data(), 8ull * nl);
         p += 8ull * nl;
         std::memcpy(p, g->ngroups.data(), 4ull * nl);
+        p += 4ull * nl;
+        std::memcpy(p, g->ci_lo.data(), 4ull * (nl + 1));
     }
     *meta_bytes = need;
     return GSI_OK;
@@ -162,7 +164,7 @@ gsi_status gsi_graph_alloc_like(const void *meta, uint64_t meta_bytes, const gsi
     MetaHeader h;
     std::memcpy(&h, meta, sizeof(h));
     const int nl = h.n_labels;
-    if (h.magic != kMetaMagic || meta_bytes < sizeof(MetaHeader) + (uint64_t)nl * 24) {
+    if (h.magic != kMetaMagic || h.version != 2 || meta_bytes < sizeof(MetaHeader) + (uint64_t)nl * 24 + 4ull * (nl + 1)) {
         set_error("metadata blob is not a gsi graph description");
         return GSI_ERR_INVALID_ARG;
     }
@@ -189,6 +191,9 @@ gsi_status gsi_graph_alloc_like(const void *meta, uint64_t meta_bytes, const gsi
     std::memcpy(g->gbase.data(), p, 8ull * nl);
     p += 8ull * nl;
     std::memcpy(g->ngroups.data(), p, 4ull * nl);
+    p += 4ull * nl;
+    g->ci_lo.resize(nl + 1);
+    std::memcpy(g->ci_lo.data(), p, 4ull * (nl + 1));
     GSI_CUDA(cudaMalloc(&g->sig, std::max<uint64_t>(16, (uint64_t)g->n * kPlanes * 4)));
     GSI_CUDA(cudaMalloc(&g->groups, std::max<uint64_t>(16, (uint64_t)g->n_groups * g->gpn * 8)));
     GSI_CUDA(cudaMalloc(&g->ci, std::max<uint64_t>(16, (uint64_t)g->m * 8)));

@@ -358,6 +358,7 @@ struct gsi_graph {
     std::vector<int64_t> freq;      // |E(P(G,l))|
     std::vector<int64_t> gbase;     // first group of partition l
     std::vector<uint32_t> ngroups;  // |V(D_l)|
+    std::vector<uint32_t> ci_lo;    // [nl+1]: P(G,l)'s runs are ci[ci_lo[l], ci_lo[l+1])
     int dense_label(int32_t raw) const;   // -1 if absent
 };
 

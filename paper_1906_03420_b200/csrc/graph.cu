@@ -266,9 +266,14 @@ __global__ void k_signatures(int64_t E, int64_t n, const unsigned long long *key
     }
 }
 
-__global__ void k_label_tables(int nl, const uint32_t *lstart, const uint32_t *ustart, long long *freq) {
-    for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < nl; l += gridDim.x * blockDim.x)
-        freq[l] = (long long)(ustart[lstart[l + 1]] - ustart[lstart[l]]) / 2;
+// freq(l) and the ci range of partition l: its groups are contiguous and ci is laid out in
+// group order, so P(G,l)'s neighbour runs are ci[gci[lstart[l]], gci[lstart[l+1]]).
+__global__ void k_label_tables(int nl, const uint32_t *lstart, const uint32_t *ustart, const uint32_t *gci,
+                               long long *freq, uint32_t *cilo) {
+    for (int l = blockIdx.x * blockDim.x + threadIdx.x; l <= nl; l += gridDim.x * blockDim.x) {
+        if (l < nl) freq[l] = (long long)(ustart[lstart[l + 1]] - ustart[lstart[l]]) / 2;
+        cilo[l] = gci[lstart[l]];
+    }
 }
 
 inline int bits_for(uint64_t x) {
@@ -377,6 +382,7 @@ gsi_status build_graph_impl(int64_t n, const int32_t *h_vl, int64_t m, const int
     if (n) GSI_CUDA(cudaMemcpyAsync(g->sig, d_vl.p, 4 * n, cudaMemcpyDeviceToDevice, st));   // L1277
 
     if (m == 0) {
+        g->ci_lo.assign(1, 0u);
         GSI_CUDA(cudaMalloc(&g->groups, 16));
         GSI_CUDA(cudaMalloc(&g->ci, 16));
         GSI_CUDA(cudaStreamSynchronize(st));
@@ -491,8 +497,12 @@ gsi_status build_graph_impl(int64_t n, const int32_t *h_vl, int64_t m, const int
 
     // ---- host label tables ----------------------------------------------------------
     DevBuf<long long> d_freq;
+    DevBuf<uint32_t> d_cilo;
     GSI_CUDA(d_freq.alloc(nl, st));
-    k_label_tables<<<blocks_for(nl), kB, 0, st>>>(nl, lstart.p, ustart.p, d_freq.p);
+    GSI_CUDA(d_cilo.alloc(nl + 1, st));
+    k_label_tables<<<blocks_for(nl + 1), kB, 0, st>>>(nl, lstart.p, ustart.p, gci.p, d_freq.p, d_cilo.p);
+    g->ci_lo.resize(nl + 1);
+    GSI_CUDA(cudaMemcpyAsync(g->ci_lo.data(), d_cilo.p, 4ull * (nl + 1), cudaMemcpyDeviceToHost, st));
     std::vector<uint32_t> h_lstart(nl + 1);
     g->freq.resize(nl);
     uint32_t h_maxchain = 0, h_spilled = 0;

@@ -39,6 +39,9 @@ namespace gsi {
 namespace {
 
 constexpr int kThreads = 256;
+#ifndef GSI_PREFILTER_RATIO
+#define GSI_PREFILTER_RATIO 2   // share N(v,l0) ∩ C(u) when |GBA| >= ratio x |ci of P(G,l0)| (0: off)
+#endif
 #ifndef GSI_STAGE_BASE
 #define GSI_STAGE_BASE 1  // stage per-row ci bases in the join tile
 #endif
@@ -64,6 +67,7 @@ struct StepParams {
     int inj_col[GSI_MAX_K];      // columns the subtraction must test (same vertex label as u)
     int pos_of_q[GSI_MAX_K];     // final level: column (0..t) holding query vertex q
     int fp;                      // final level: accumulate the set fingerprint
+    int prefiltered;             // loc / ci point at N(v,l0) ∩ C(u) (k_filter_partition): no bitmap test
     int stage_base;              // join tile stages per-row ci bases in shared memory
     int stage_inj;               // ... and up to this many subtraction columns
 };
@@ -516,10 +520,12 @@ __global__ void __launch_bounds__(kThreads, join_items(MODE) > 8 ? 2 : ((MODE ==
     }
 #pragma unroll
     for (int it = 0; it < IT; it++) xs[it] = keep[it] ? (uint32_t)__ldg(ci + cio[it]) : 0u;
+    if (!P.prefiltered) {
 #pragma unroll
-    for (int it = 0; it < IT; it++) {                                    // x in C(u)
-        const uint32_t x = xs[it];
-        if (keep[it]) keep[it] = (__ldg(cu_bitmap + (x >> 5)) >> (x & 31)) & 1u;
+        for (int it = 0; it < IT; it++) {                                // x in C(u)
+            const uint32_t x = xs[it];
+            if (keep[it]) keep[it] = (__ldg(cu_bitmap + (x >> 5)) >> (x & 31)) & 1u;
+        }
     }
     for (int c = 0; c < P.n_inj; c++) {                                         // Alg. 3 line 10
         const int col = P.inj_col[c];
@@ -769,6 +775,126 @@ inline size_t join_smem_bytes(int mode, const StepParams &P) {
 }
 constexpr int kMaxJoinSmem = 6 * 4096 * 4;
 
+// ------------------------------------------------------- shared candidate lists -----
+// Duplicate removal (§VI-B, Alg. 5) taken one step further for B200: at a
+// level whose rows re-scan the same neighbour lists many times (|GBA| >> |ci of P(G,l0)|),
+// N(v,l0) ∩ C(u) is computed ONCE per partition run (one pass over P(G,l0)'s ci) and the
+// rows then enumerate only those candidates.  fpos[o - lo] = number of kept entries of the
+// partition before offset o, fci = the kept entries in ci order (runs stay sorted).
+__global__ void __launch_bounds__(kThreads) k_filter_partition(const int32_t *__restrict__ ci, uint32_t lo,
+                                                               uint32_t hi, const uint32_t *__restrict__ cu_bitmap,
+                                                               uint32_t *__restrict__ fpos,
+                                                               int32_t *__restrict__ fci,
+                                                               unsigned long long *status, unsigned *tile_ctr) {
+    constexpr int IT = 8, TILE = IT * kThreads;
+    __shared__ unsigned wcnt[IT][kThreads / 32];
+    __shared__ unsigned wbase[IT][kThreads / 32];
+    __shared__ unsigned tile_s, agg_s;
+    __shared__ unsigned long long base_s;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) tile_s = atomicAdd(tile_ctr, 1u);
+    __syncthreads();
+    const unsigned tile = tile_s;
+    const uint32_t tb = lo + tile * (uint32_t)TILE;
+    bool keep[IT];
+    int32_t xs[IT];
+    unsigned ballots[IT];
+#pragma unroll
+    for (int it = 0; it < IT; it++) {
+        const uint32_t o = tb + it * kThreads + tid;
+        keep[it] = o < hi;
+        xs[it] = keep[it] ? __ldg(ci + o) : 0;
+    }
+#pragma unroll
+    for (int it = 0; it < IT; it++)
+        if (keep[it]) keep[it] = (__ldg(cu_bitmap + ((uint32_t)xs[it] >> 5)) >> (xs[it] & 31)) & 1u;
+#pragma unroll
+    for (int it = 0; it < IT; it++) {
+        ballots[it] = __ballot_sync(0xffffffffu, keep[it]);
+        if (lane == 0) wcnt[it][warp] = __popc(ballots[it]);
+    }
+    __syncthreads();
+    if (warp == 0) {
+        constexpr int NW = kThreads / 32, PER = IT * NW / 32;
+        unsigned e[PER], pair = 0;
+#pragma unroll
+        for (int q = 0; q < PER; q++) {
+            const int idx = PER * lane + q;
+            e[q] = wcnt[idx / NW][idx % NW];
+            pair += e[q];
+        }
+        unsigned inc = pair;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        unsigned ex = inc - pair;
+#pragma unroll
+        for (int q = 0; q < PER; q++) {
+            const int idx = PER * lane + q;
+            wbase[idx / NW][idx % NW] = ex;
+            ex += e[q];
+        }
+        const unsigned total = __shfl_sync(0xffffffffu, inc, 31);
+        const unsigned long long pre = lookback_exclusive(status, tile, total);
+        if (lane == 0) {
+            base_s = pre;
+            agg_s = total;
+        }
+    }
+    __syncthreads();
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int it = 0; it < IT; it++) {
+        const uint32_t o = tb + it * kThreads + tid;
+        const uint32_t pos = (uint32_t)base_s + wbase[it][warp] + __popc(ballots[it] & lt);
+        if (o < hi) fpos[o - lo] = pos;
+        if (keep[it]) fci[pos] = xs[it];
+    }
+    if (tile == gridDim.x - 1 && tid == 0) fpos[hi - lo] = (uint32_t)(base_s + agg_s);
+}
+
+// Re-point the rows of a level (one linking edge) at their filtered runs and rebuild F.
+__global__ void __launch_bounds__(kThreads) k_refilter(Loc *__restrict__ loc, long long nM,
+                                                       const uint32_t *__restrict__ fpos, uint32_t lo, uint32_t hi,
+                                                       unsigned long long *__restrict__ F,
+                                                       unsigned long long *status, unsigned *tile_ctr,
+                                                       Counters *ctr) {
+    __shared__ unsigned long long sm[33];
+    __shared__ unsigned tile_s;
+    __shared__ unsigned long long base_s;
+    if (threadIdx.x == 0) tile_s = atomicAdd(tile_ctr, 1u);
+    __syncthreads();
+    const unsigned tile = tile_s;
+    const long long i = (long long)tile * kThreads + threadIdx.x;
+    unsigned long long len0 = 0;
+    if (i < nM) {
+        const Loc L = loc[i];
+        Loc R{0u, 0u};
+        if (L.len && L.off >= lo && L.off + L.len <= hi) {
+            const uint32_t a = __ldg(fpos + (L.off - lo)), b = __ldg(fpos + (L.off + L.len - lo));
+            R = Loc{a, b - a};
+        }
+        loc[i] = R;
+        len0 = R.len;
+    }
+    unsigned long long agg;
+    const unsigned long long ex = block_exclusive_scan(len0, sm, &agg);
+    if (threadIdx.x < 32) {
+        const unsigned long long pre = lookback_exclusive(status, tile, agg);
+        if (threadIdx.x == 0) base_s = pre;
+    }
+    __syncthreads();
+    if (i < nM) F[i] = base_s + ex;
+    if (tile == gridDim.x - 1 && threadIdx.x == kThreads - 1) F[nM] = base_s + agg;
+    const unsigned long long a1 = warp_sum_u64(len0 ? 1ull : 0ull), e1 = warp_sum_u64(len0);
+    if ((threadIdx.x & 31) == 0) {
+        if (a1) atomicAdd(&ctr->active_rows, a1);
+        if (e1) atomicAdd(&ctr->list_elems, e1);
+    }
+}
+
 // Count + fingerprint of a table whose columns are in pi order (k = 1 queries).
 __global__ void k_fp_rows(const int32_t *__restrict__ T, long long nrows, StepParams P, Counters *ctr) {
     unsigned long long h1 = 0, h2 = 0;
@@ -889,6 +1015,20 @@ struct Arena {
         }
         void *q = nullptr;
         cudaError_t e = cudaMallocAsync(&q, bytes, st);
+        if (e == cudaErrorMemoryAllocation) {
+            cudaGetLastError();
+            set_error("device memory exhausted");
+            return GSI_ERR_OOM;
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+        ptrs.push_back(q);
+        *p = (T *)q;
+        return GSI_OK;
+    }
+    template <typename T>
+    gsi_status get_big(T **p, unsigned long long count) {   // never from the bump region
+        void *q = nullptr;
+        cudaError_t e = cudaMallocAsync(&q, (size_t)std::max<unsigned long long>(count, 1) * sizeof(T), st);
         if (e == cudaErrorMemoryAllocation) {
             cudaGetLastError();
             set_error("device memory exhausted");
@@ -1249,6 +1389,7 @@ struct QueryCtx {
     bool capped = false;
     unsigned long long count = 0, fp1 = 0, fp2 = 0;
     std::vector<std::pair<int32_t *, unsigned long long>> pieces;   // final table pieces (device)
+    std::vector<std::pair<uint32_t *, int32_t *>> filt;             // per step: (fpos, fci) or null
 };
 
 void fill_params(QueryCtx &C, const Step &s, StepParams &P) {
@@ -1288,6 +1429,7 @@ void fill_params(QueryCtx &C, const Step &s, StepParams &P) {
 // (by k_probe for level 1, by the previous level's fused kernel otherwise).
 gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc *loc, unsigned long long *F,
                  unsigned long long gba, unsigned long long active, unsigned long long elems) {
+    // (gba / active / elems are updated below if this level switches to shared candidate lists)
     const Step &s = C.steps[si];
     const int t = s.t;
     const bool last = si + 1 == C.steps.size();
@@ -1305,6 +1447,50 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
     S.gba[t] += gba;
     S.list_elems[t] += elems;
     if (nM == 0 || gba == 0) return GSI_OK;
+
+    // ---- shared candidate lists: N(v,l0) ∩ C(u) once per partition run ----
+    const int32_t *cip = g->ci;
+    if (GSI_PREFILTER_RATIO > 0 && !C.opts.no_shared_lists && C.opts.e0_mode == 0 && E == 1) {
+        const uint32_t lo = g->ci_lo[P.lab[0]], hi = g->ci_lo[P.lab[0] + 1];
+        if (hi > lo && gba >= (unsigned long long)GSI_PREFILTER_RATIO * (hi - lo)) {
+            if (C.filt.size() < C.steps.size()) C.filt.assign(C.steps.size(), {nullptr, nullptr});
+            const uint32_t *cu0 = C.bm + (long long)s.u * C.words;
+            if (!C.filt[si].first) {
+                uint32_t *fpos = nullptr;
+                int32_t *fci = nullptr;
+                GSI_TRY(A.get_big(&fpos, (unsigned long long)(hi - lo) + 1));
+                GSI_TRY(A.get_big(&fci, (unsigned long long)(hi - lo)));
+                const unsigned ft = grid_for(hi - lo, 8 * kThreads);
+                unsigned long long *fst = nullptr;
+                GSI_TRY(A.get(&fst, (unsigned long long)ft + 1));
+                GSI_CUDA(cudaMemsetAsync(fst, 0, 8ull * (ft + 1), st));
+                prof.begin(GSI_K_OTHER);
+                k_filter_partition<<<ft, kThreads, 0, st>>>(g->ci, lo, hi, cu0, fpos, fci, fst + 1, (unsigned *)fst);
+                prof.end();
+                S.alg_bytes[GSI_K_OTHER] += 12.0 * (hi - lo);
+                C.filt[si] = {fpos, fci};
+            }
+            const unsigned rt = grid_for(nM, kThreads);
+            unsigned long long *rst = nullptr;
+            GSI_TRY(A.get(&rst, (unsigned long long)rt + 1 + sizeof(Counters) / 8));
+            GSI_CUDA(cudaMemsetAsync(rst, 0, 8ull * (rt + 1) + sizeof(Counters), st));
+            Counters *rctr = reinterpret_cast<Counters *>(rst + rt + 1);
+            prof.begin(GSI_K_OTHER);
+            k_refilter<<<rt, kThreads, 0, st>>>(loc, (long long)nM, C.filt[si].first, lo, hi, F, rst + 1,
+                                                (unsigned *)rst, rctr);
+            prof.end();
+            Counters hc0;
+            GSI_CUDA(d2h(S, &gba, F + nM, 8, st));
+            GSI_CUDA(d2h(S, &hc0, rctr, sizeof(Counters), st));
+            GSI_CUDA(cudaStreamSynchronize(st));
+            active = hc0.active_rows;
+            elems = hc0.list_elems;
+            P.prefiltered = 1;
+            cip = C.filt[si].second;
+            S.n_shared_lists++;
+            if (gba == 0) return GSI_OK;
+        }
+    }
 
     // ---- shard this level's slot range ----
     unsigned long long s0 = 0, s1 = gba;
@@ -1366,13 +1552,13 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         prof.end();
         prof.begin(GSI_K_JOIN);
         if (mode == J_COUNT)
-            k_join<J_COUNT><<<jt, kThreads, join_smem_bytes(J_COUNT, P), st>>>(M, (long long)nM, F, loc, rowmap, P, P2, g->ci, cu, g->groups,
+            k_join<J_COUNT><<<jt, kThreads, join_smem_bytes(J_COUNT, P), st>>>(M, (long long)nM, F, loc, rowmap, P, P2, cip, cu, g->groups,
                                                      g->gpn, c0, c1, out, loc2, F2, st1, st2, tctr, lctr);
         else if (mode == J_TABLE)
-            k_join<J_TABLE><<<jt, kThreads, join_smem_bytes(J_TABLE, P), st>>>(M, (long long)nM, F, loc, rowmap, P, P2, g->ci, cu, g->groups,
+            k_join<J_TABLE><<<jt, kThreads, join_smem_bytes(J_TABLE, P), st>>>(M, (long long)nM, F, loc, rowmap, P, P2, cip, cu, g->groups,
                                                      g->gpn, c0, c1, out, loc2, F2, st1, st2, tctr, lctr);
         else
-            k_join<J_NEXT><<<jt, kThreads, join_smem_bytes(J_NEXT, P), st>>>(M, (long long)nM, F, loc, rowmap, P, P2, g->ci, cu, g->groups,
+            k_join<J_NEXT><<<jt, kThreads, join_smem_bytes(J_NEXT, P), st>>>(M, (long long)nM, F, loc, rowmap, P, P2, cip, cu, g->groups,
                                                     g->gpn, c0, c1, out, loc2, F2, st1, st2, tctr, lctr);
         prof.end();
         Counters hc;

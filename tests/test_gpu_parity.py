@@ -227,12 +227,16 @@ def test_large_counts_fingerprint():
     g = W.chung_lu(4000, 30000, 500, nlv=3, nle=4, seed=31)
     graph = gsi.build(g)
     og = oracle.OracleGraph(g)
+    shared = 0
     for s in (700, 703, 705):
         q = W.random_walk_query(g, 6, s)
         cnt, fp, _ = oracle.match(og, q, table=False)
-        r = gsi.query(graph, q)
-        assert r.count == cnt and r.fingerprint() == fp
+        for sl in (True, False):   # with and without shared N(v,l0) ∩ C(u) lists
+            r = gsi.query(graph, q, shared_lists=sl)
+            assert r.count == cnt and r.fingerprint() == fp, (s, sl)
+            shared += r.stats()["n_shared_lists"] if sl else 0
         assert cnt > 10_000_000 or s == 703
+    assert shared > 0
 
 
 def test_enron_shaped_config():
@@ -383,6 +387,8 @@ def test_chunked_execution_invariance():
         assert full.count == cnt and np.array_equal(canon(full.table()), otab)
         for cs in (2048, 4096 + 17, 50_000):
             r = gsi.query(graph, q, want_table=True, chunk_slots=cs)
+            assert np.array_equal(r.table(), full.table())
+            r = gsi.query(graph, q, want_table=True, chunk_slots=cs, shared_lists=False)
             assert np.array_equal(r.table(), full.table())
             assert r.fingerprint() == full.fingerprint()
             c = gsi.query(graph, q, chunk_slots=cs)              # count-only path
