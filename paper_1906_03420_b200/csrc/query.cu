@@ -42,6 +42,9 @@ constexpr int kThreads = 256;
 #ifndef GSI_PREFILTER_RATIO
 #define GSI_PREFILTER_RATIO 2   // share N(v,l0) ∩ C(u) when |GBA| >= ratio x |ci of P(G,l0)| (0: off)
 #endif
+#ifndef GSI_PREFILTER_AHEAD
+#define GSI_PREFILTER_AHEAD 4   // ... and produce a level's rows pre-pointed when 4x its parent's slots exceed it
+#endif
 #ifndef GSI_STAGE_BASE
 #define GSI_STAGE_BASE 1  // stage per-row ci bases in the join tile
 #endif
@@ -68,6 +71,8 @@ struct StepParams {
     int pos_of_q[GSI_MAX_K];     // final level: column (0..t) holding query vertex q
     int fp;                      // final level: accumulate the set fingerprint
     int prefiltered;             // loc / ci point at N(v,l0) ∩ C(u) (k_filter_partition): no bitmap test
+    const uint32_t *fpos;        // (as the NEXT step of J_NEXT) filtered positions of P(G,l0)'s ci
+    uint32_t flo, fhi;           //   ... and the partition's ci range
     int stage_base;              // join tile stages per-row ci bases in shared memory
     int stage_inj;               // ... and up to this many subtraction columns
 };
@@ -601,6 +606,15 @@ __global__ void __launch_bounds__(kThreads, join_items(MODE) > 8 ? 2 : ((MODE ==
                     pcsr_lookup_batch<4>(groups, gpn, P2.gbase[0], P2.ngroups[0], P2.lab[0], vb, kb, nb);
 #pragma unroll
                     for (int q = 0; q < 4; q++) N0[h + q] = nb[q];
+                }
+                if (P2.prefiltered) {   // re-point at the shared N(v,l0) ∩ C(u) run of the next step
+#pragma unroll
+                    for (int it = 0; it < IT; it++) {
+                        if (!keep[it] || !N0[it].len) continue;
+                        const uint32_t a = __ldg(P2.fpos + (N0[it].off - P2.flo));
+                        const uint32_t b = __ldg(P2.fpos + (N0[it].off + N0[it].len - P2.flo));
+                        N0[it] = Loc{a, b - a};
+                    }
                 }
 #pragma unroll
                 for (int it = 0; it < IT; it++) keep[it] = keep[it] && N0[it].len > 0;
@@ -1425,10 +1439,39 @@ void fill_params(QueryCtx &C, const Step &s, StepParams &P) {
     P.stage_inj = P.stage_base ? std::min(P.n_inj, GSI_STAGE_INJ) : 0;
 }
 
+// Build (once per query step) N(v,l0) ∩ C(u) for every run of P(G,l0): fpos + fci.
+gsi_status ensure_filtered(QueryCtx &C, size_t si, uint32_t lab) {
+    if (C.filt.size() < C.steps.size()) C.filt.assign(C.steps.size(), {nullptr, nullptr});
+    if (C.filt[si].first) return GSI_OK;
+    const gsi_graph *g = C.g;
+    Arena &A = *C.A;
+    cudaStream_t st = C.st;
+    const uint32_t lo = g->ci_lo[lab], hi = g->ci_lo[lab + 1];
+    uint32_t *fpos = nullptr;
+    int32_t *fci = nullptr;
+    GSI_TRY(A.get_big(&fpos, (unsigned long long)(hi - lo) + 1));
+    GSI_TRY(A.get_big(&fci, (unsigned long long)(hi - lo)));
+    const unsigned ft = grid_for(hi - lo, 8 * kThreads);
+    unsigned long long *fst = nullptr;
+    GSI_TRY(A.get_big(&fst, (unsigned long long)ft + 1));
+    GSI_CUDA(cudaMemsetAsync(fst, 0, 8ull * (ft + 1), st));
+    const uint32_t *cu0 = C.bm + (long long)C.steps[si].u * C.words;
+    C.prof->begin(GSI_K_OTHER);
+    k_filter_partition<<<ft, kThreads, 0, st>>>(g->ci, lo, hi, cu0, fpos, fci, fst + 1, (unsigned *)fst);
+    C.prof->end();
+    C.S->alg_bytes[GSI_K_OTHER] += 12.0 * (hi - lo);
+    C.filt[si] = {fpos, fci};
+    return GSI_OK;
+}
+
+bool shared_lists_allowed(const QueryCtx &C, const StepParams &P) {
+    return GSI_PREFILTER_RATIO > 0 && !C.opts.no_shared_lists && C.opts.e0_mode == 0 && P.E == 1;
+}
+
 // Level t = steps[si].t: M (nM x t) with its Prealloc (loc, F, |GBA| = gba) already computed
 // (by k_probe for level 1, by the previous level's fused kernel otherwise).
 gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc *loc, unsigned long long *F,
-                 unsigned long long gba, unsigned long long active, unsigned long long elems) {
+                 unsigned long long gba, unsigned long long active, unsigned long long elems, bool filtered_in) {
     // (gba / active / elems are updated below if this level switches to shared candidate lists)
     const Step &s = C.steps[si];
     const int t = s.t;
@@ -1450,26 +1493,13 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
 
     // ---- shared candidate lists: N(v,l0) ∩ C(u) once per partition run ----
     const int32_t *cip = g->ci;
-    if (GSI_PREFILTER_RATIO > 0 && !C.opts.no_shared_lists && C.opts.e0_mode == 0 && E == 1) {
+    if (filtered_in) {   // the previous level's probe-ahead already pointed the rows at them
+        P.prefiltered = 1;
+        cip = C.filt[si].second;
+    } else if (shared_lists_allowed(C, P)) {
         const uint32_t lo = g->ci_lo[P.lab[0]], hi = g->ci_lo[P.lab[0] + 1];
         if (hi > lo && gba >= (unsigned long long)GSI_PREFILTER_RATIO * (hi - lo)) {
-            if (C.filt.size() < C.steps.size()) C.filt.assign(C.steps.size(), {nullptr, nullptr});
-            const uint32_t *cu0 = C.bm + (long long)s.u * C.words;
-            if (!C.filt[si].first) {
-                uint32_t *fpos = nullptr;
-                int32_t *fci = nullptr;
-                GSI_TRY(A.get_big(&fpos, (unsigned long long)(hi - lo) + 1));
-                GSI_TRY(A.get_big(&fci, (unsigned long long)(hi - lo)));
-                const unsigned ft = grid_for(hi - lo, 8 * kThreads);
-                unsigned long long *fst = nullptr;
-                GSI_TRY(A.get(&fst, (unsigned long long)ft + 1));
-                GSI_CUDA(cudaMemsetAsync(fst, 0, 8ull * (ft + 1), st));
-                prof.begin(GSI_K_OTHER);
-                k_filter_partition<<<ft, kThreads, 0, st>>>(g->ci, lo, hi, cu0, fpos, fci, fst + 1, (unsigned *)fst);
-                prof.end();
-                S.alg_bytes[GSI_K_OTHER] += 12.0 * (hi - lo);
-                C.filt[si] = {fpos, fci};
-            }
+            GSI_TRY(ensure_filtered(C, si, P.lab[0]));
             const unsigned rt = grid_for(nM, kThreads);
             unsigned long long *rst = nullptr;
             GSI_TRY(A.get(&rst, (unsigned long long)rt + 1 + sizeof(Counters) / 8));
@@ -1487,10 +1517,10 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
             elems = hc0.list_elems;
             P.prefiltered = 1;
             cip = C.filt[si].second;
-            S.n_shared_lists++;
             if (gba == 0) return GSI_OK;
         }
     }
+    if (P.prefiltered) S.n_shared_lists++;
 
     // ---- shard this level's slot range ----
     unsigned long long s0 = 0, s1 = gba;
@@ -1544,6 +1574,23 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
             GSI_TRY(A.get(&loc2, slots * (unsigned long long)P2.E));
             GSI_TRY(A.get(&F2, slots + 1));   // F2[0..nout] written by the kernel
         }
+        // next step on shared lists? (its rows are produced here, so the probe-ahead can point
+        // them at N(v,l0') ∩ C(u') directly and drop rows whose filtered run is empty)
+        bool pf_next = false;
+        if (mode == J_NEXT && shared_lists_allowed(C, P2)) {
+            const uint32_t lo2 = g->ci_lo[P2.lab[0]], hi2 = g->ci_lo[P2.lab[0] + 1];
+            if (hi2 > lo2 && (C.filt.size() > si + 1 && C.filt[si + 1].first ||
+                              slots * (unsigned long long)GSI_PREFILTER_AHEAD >= (unsigned long long)(hi2 - lo2))) {
+                GSI_TRY(ensure_filtered(C, si + 1, P2.lab[0]));
+                P2.prefiltered = 1;
+                P2.fpos = C.filt[si + 1].first;
+                P2.flo = lo2;
+                P2.fhi = hi2;
+                pf_next = true;
+            } else {
+                P2.prefiltered = 0;
+            }
+        }
         uint32_t *rowmap = nullptr;
         GSI_TRY(A.get(&rowmap, (unsigned long long)jt + 1));
         prof.begin(GSI_K_OTHER);
@@ -1590,7 +1637,7 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
             }
             A.release(out);
         } else if (mode == J_NEXT) {
-            if (nout) rc = level(C, si + 1, out, nout, loc2, F2, hc.total2, nout, hc.list_elems);
+            if (nout) rc = level(C, si + 1, out, nout, loc2, F2, hc.total2, nout, hc.list_elems, pf_next);
             A.release(out);
             A.release(loc2);
             A.release(F2);
@@ -1805,7 +1852,7 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
         A.release(status);
         S.alg_bytes[GSI_K_PROBE] += (double)nM * (20.0 * P.E + 8.0);
         S.rows[0] += nM;
-        rc = level(C, 0, M, nM, loc, F, gba, hc.active_rows, hc.list_elems);
+        rc = level(C, 0, M, nM, loc, F, gba, hc.active_rows, hc.list_elems, false);
         A.release(loc);
         A.release(F);
     }
