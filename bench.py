@@ -142,14 +142,11 @@ def oracle_sample(og, qs, budget_s: float, per_query_timeout: float, threads: in
     while secs < budget_s and done < len(qs):
         q = qs[i % len(qs)]
         t = time.perf_counter()
-        try:
-            c, fp, _ = oracle.match(og, q, table=False, threads=threads, timeout=per_query_timeout)
-        except oracle.OracleError as e:
-            if e.code != -9:
-                raise
-            c = 0
+        c, fp, _ = oracle.match(og, q, table=False, threads=threads, timeout=per_query_timeout, partial=True)
+        el = time.perf_counter() - t
+        if per_query_timeout > 0 and el >= per_query_timeout:
             touts += 1
-        secs += time.perf_counter() - t
+        secs += el
         matches += c
         done += 1
         i += 1

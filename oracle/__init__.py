@@ -117,9 +117,10 @@ class OracleGraph:
 
 def match(og: OracleGraph, q, root: int = 0, roots: Optional[Sequence[int]] = None, threads: int = 0,
           hom: bool = False, table: bool = True, cap: Optional[int] = None,
-          timeout: float = 0.0) -> Tuple[int, Tuple[int, int, int], Optional[np.ndarray]]:
+          timeout: float = 0.0, partial: bool = False) -> Tuple[int, Tuple[int, int, int], Optional[np.ndarray]]:
     """Enumerate R(Q,G).  Returns (count, fingerprint (count, sum, xor), table or None);
-    the table is k int32 per row in query-id order, sorted lexicographically."""
+    the table is k int32 per row in query-id order, sorted lexicographically.
+    partial=True (count-only): on timeout return the matches found so far instead of raising."""
     qv, qs, qd, qe = _i32(q.vlabels), _i32(q.src), _i32(q.dst), _i32(q.elabels)
     r = None if roots is None else _i32(roots)
     fp = np.zeros(3, np.uint64)
@@ -138,7 +139,9 @@ def match(og: OracleGraph, q, root: int = 0, roots: Optional[Sequence[int]] = No
     cnt = lib().og_match(og._h, k, _p(qv), len(qs), _p(qs), _p(qd), _p(qe), root,
                          None if r is None else _p(r), 0 if r is None else len(r), threads, int(hom),
                          None if out is None else _p(out), 0 if out is None else cap, _p(fp), timeout)
-    if cnt < 0:
+    if cnt == -9 and partial and out is None:
+        cnt = int(fp[0])
+    elif cnt < 0:
         raise OracleError(int(cnt))
     fpt = (int(fp[0]), int(fp[1]), int(fp[2]))
     return int(cnt), fpt, (None if out is None else out[: min(cnt, cap)])

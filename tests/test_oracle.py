@@ -333,3 +333,14 @@ def test_homomorphism_filter_sound_with_distinct_keys():
         for row in oracle.brute_force(g, q, hom=True):
             for u, v in enumerate(row):
                 assert bits[u, v], (s, row)
+
+
+def test_partial_count_on_timeout():
+    """Timed-out count-only runs report the matches found so far (a prefix of the search)."""
+    g = W.chung_lu(4000, 30000, 500, nlv=1, nle=1, seed=31)
+    og = oracle.OracleGraph(g)
+    q = W.path_query(6)
+    with pytest.raises(oracle.OracleError):
+        oracle.match(og, q, table=False, timeout=1e-3)
+    c, fp, _ = oracle.match(og, q, table=False, timeout=1e-3, partial=True)
+    assert 0 <= c == fp[0]
