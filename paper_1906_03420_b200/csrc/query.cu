@@ -45,6 +45,9 @@ constexpr int kThreads = 256;
 #ifndef GSI_PREFILTER_AHEAD
 #define GSI_PREFILTER_AHEAD 4   // ... and produce a level's rows pre-pointed when 4x its parent's slots exceed it
 #endif
+#ifndef GSI_FAST_ITEMS
+#define GSI_FAST_ITEMS 16   // slots per thread of the lean count-only kernel (0: never use it)
+#endif
 #ifndef GSI_STAGE_BASE
 #define GSI_STAGE_BASE 1  // stage per-row ci bases in the join tile
 #endif
@@ -778,6 +781,115 @@ __global__ void __launch_bounds__(kThreads, join_items(MODE) > 8 ? 2 : ((MODE ==
     }
 }
 
+// Lean count-only final level for the common case: one linking edge, rows on shared
+// N(v,l0) ∩ C(u) runs (so every candidate already passed C(u)), no fingerprint.  Per slot the
+// only work left is reading the candidate and testing the subtraction columns, so the tile
+// is larger (CIT slots per thread) and the per-slot state is two registers.
+template <int CIT>
+__global__ void __launch_bounds__(kThreads, 4) k_count_fast(const int32_t *__restrict__ M, long long nM,
+                                                            const unsigned long long *__restrict__ F,
+                                                            const Loc *__restrict__ loc,
+                                                            const uint32_t *__restrict__ rowmap, StepParams P,
+                                                            const int32_t *__restrict__ fci, unsigned long long s0,
+                                                            unsigned long long s1, Counters *ctr) {
+    constexpr int TILE = CIT * kThreads;
+    extern __shared__ __align__(16) unsigned char dsm[];
+    int *sR = reinterpret_cast<int *>(dsm);                              // row offset per slot
+    uint32_t *sBase = reinterpret_cast<uint32_t *>(sR + TILE);           // off0 - F_i per row
+    int32_t *sInj = reinterpret_cast<int32_t *>(sBase + TILE);           // subtraction columns
+    __shared__ unsigned wmax_s[kThreads / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned tile = blockIdx.x;
+    const unsigned long long tbase = s0 + (unsigned long long)tile * TILE;
+    const unsigned long long tend = min(tbase + (unsigned long long)TILE, s1);
+    {
+        int4 *z = reinterpret_cast<int4 *>(sR);
+        for (int j = tid; j < TILE / 4; j += kThreads) z[j] = make_int4(0, 0, 0, 0);
+    }
+    __syncthreads();
+    const long long rlo = __ldg(rowmap + tile), rhi = __ldg(rowmap + tile + 1);
+    const long long nr = rhi - rlo + 1;
+    const bool staged = nr <= TILE;
+    const int ninj = P.n_inj, nst = staged ? min(ninj, P.stage_inj) : 0;
+    for (long long r = tid; r < nr; r += kThreads) {
+        const unsigned long long a = __ldg(F + rlo + r), b = __ldg(F + rlo + r + 1);
+        if (a < b && b > tbase && a < tend) sR[a > tbase ? (unsigned)(a - tbase) : 0u] = (int)r;
+        if (staged) {
+            const unsigned long long i = (unsigned long long)(rlo + r);
+            sBase[r] = loc[i].off - (uint32_t)a;
+            const int32_t *row = M + i * (unsigned)P.t;
+            for (int c = 0; c < nst; c++) sInj[c * TILE + r] = __ldg(row + P.inj_col[c]);
+        }
+    }
+    __syncthreads();
+    {   // inclusive max-scan of the row markers over the tile (thread owns CIT consecutive slots)
+        int v[CIT], m = 0;
+#pragma unroll
+        for (int q = 0; q < CIT; q++) {
+            v[q] = sR[tid * CIT + q];
+            m = max(m, v[q]);
+            v[q] = m;
+        }
+        int inc = m;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) inc = max(inc, __shfl_up_sync(0xffffffffu, inc, o) * (lane >= o));
+        if (lane == 31) wmax_s[warp] = (unsigned)inc;
+        int prev = __shfl_up_sync(0xffffffffu, inc, 1);
+        __syncthreads();
+        int wm = lane < warp ? (int)wmax_s[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) wm = max(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+        const int carry = max(lane == 0 ? 0 : prev, wm);
+#pragma unroll
+        for (int q = 0; q < CIT; q++) sR[tid * CIT + q] = max(v[q], carry);
+    }
+    __syncthreads();
+    const uint32_t tlen = (uint32_t)(tend - tbase), tb32 = (uint32_t)tbase;
+    int32_t xs[CIT];
+    uint32_t cnt = 0;
+    if (staged) {
+#pragma unroll
+        for (int it = 0; it < CIT; it++) {
+            const uint32_t ls = (uint32_t)(it * kThreads + tid);
+            xs[it] = ls < tlen ? __ldg(fci + (sBase[sR[ls]] + tb32 + ls)) : -1;
+        }
+        unsigned dead = 0;   // bit it: slot it failed (or is past the tile end)
+#pragma unroll
+        for (int it = 0; it < CIT; it++)
+            if (xs[it] < 0) dead |= 1u << it;
+        for (int c = 0; c < ninj; c++) {
+            if (c < nst) {
+#pragma unroll
+                for (int it = 0; it < CIT; it++)
+                    if (sInj[c * TILE + sR[it * kThreads + tid]] == xs[it]) dead |= 1u << it;
+            } else {
+#pragma unroll
+                for (int it = 0; it < CIT; it++) {
+                    const uint32_t ls = (uint32_t)(it * kThreads + tid);
+                    const unsigned long long i = (unsigned long long)(rlo + sR[ls]);
+                    if (!((dead >> it) & 1u) && __ldg(M + i * (unsigned)P.t + P.inj_col[c]) == xs[it]) dead |= 1u << it;
+                }
+            }
+        }
+        cnt = CIT - __popc(dead);
+    } else {
+#pragma unroll
+        for (int it = 0; it < CIT; it++) {
+            const uint32_t ls = (uint32_t)(it * kThreads + tid);
+            if (ls >= tlen) continue;
+            const unsigned long long i = (unsigned long long)(rlo + sR[ls]);
+            const int32_t x = __ldg(fci + loc[i].off + (uint32_t)(tbase + ls - __ldg(F + i)));
+            bool k = true;
+            for (int c = 0; c < ninj && k; c++) k = __ldg(M + i * (unsigned)P.t + P.inj_col[c]) != x;
+            cnt += k ? 1u : 0u;
+        }
+    }
+    unsigned long long c64 = warp_sum_u64(cnt);
+    if (lane == 0 && c64) atomicAdd(&ctr->count, c64);
+}
+
+constexpr int kFastItems = GSI_FAST_ITEMS > 0 ? GSI_FAST_ITEMS : 8;
+
 // Dynamic shared memory of a join launch: the larger of the staging region (row markers,
 // optional ci bases and subtraction columns) and the write cache.  Kept to what the step
 // uses: the rest of the 228 KB SM memory stays L1 cache for the ci / bitmap / row reads.
@@ -1141,6 +1253,7 @@ void ensure_pool(int dev) {
     cudaFuncSetAttribute(k_join<J_COUNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxJoinSmem);
     cudaFuncSetAttribute(k_join<J_TABLE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxJoinSmem);
     cudaFuncSetAttribute(k_join<J_NEXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxJoinSmem);
+    cudaFuncSetAttribute(k_count_fast<kFastItems>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxJoinSmem);
     cudaGetLastError();
     g_pool_ready[dev] = true;
 }
@@ -1555,7 +1668,8 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         const size_t mk = A.mark();
         const unsigned long long c1 = std::min(s1, c0 + chunk), slots = c1 - c0;
         if (c0 != s0 || c1 != s1) S.n_chunks++;
-        const unsigned tile_slots = (unsigned)(join_items(mode) * kThreads);
+        const bool fast = GSI_FAST_ITEMS > 0 && mode == J_COUNT && P.prefiltered && !P.fp && P.E == 1;
+        const unsigned tile_slots = (unsigned)((fast ? kFastItems : join_items(mode)) * kThreads);
         const unsigned jt = grid_for(slots, tile_slots);
         // one zeroed scratch region per launch: [Counters | tile counter + status 1 | status 2]
         constexpr unsigned kCtrWords = sizeof(Counters) / 8;
@@ -1598,7 +1712,11 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
                                                                                        tile_slots, rowmap);
         prof.end();
         prof.begin(GSI_K_JOIN);
-        if (mode == J_COUNT)
+        if (fast) {
+            const size_t fsm = (size_t)tile_slots * 4 * (2 + (size_t)std::min(P.n_inj, P.stage_inj));
+            k_count_fast<kFastItems><<<jt, kThreads, fsm, st>>>(M, (long long)nM, F, loc, rowmap, P, cip, c0, c1,
+                                                                    lctr);
+        } else if (mode == J_COUNT)
             k_join<J_COUNT><<<jt, kThreads, join_smem_bytes(J_COUNT, P), st>>>(M, (long long)nM, F, loc, rowmap, P, P2, cip, cu, g->groups,
                                                      g->gpn, c0, c1, out, loc2, F2, st1, st2, tctr, lctr);
         else if (mode == J_TABLE)
