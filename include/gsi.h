@@ -194,6 +194,7 @@ typedef struct {
     int32_t capped;                   /* 1: timed out with partial_on_timeout                 */
     uint64_t h2d_bytes, d2h_bytes;    /* host<->device bytes this query copied                */
     uint32_t n_shared_lists;          /* levels that enumerated shared N(v,l0) ∩ C(u) lists   */
+    float ms_host_alloc, ms_host_sync; /* host time in stream-ordered allocation / stream syncs */
 } gsi_stats;
 
 gsi_status gsi_result_count(const gsi_result *r, uint64_t *count);

@@ -1118,6 +1118,7 @@ inline unsigned grid_for(unsigned long long n, int per) {
 struct Arena {
     cudaStream_t st;
     std::vector<void *> ptrs;
+    double ms_alloc = 0;   // host time in cudaMallocAsync (stats.ms_host_alloc)
     char *bump = nullptr;
     size_t cap = 0, off = 0;
     explicit Arena(cudaStream_t s) : st(s) {}
@@ -1140,7 +1141,9 @@ struct Arena {
             return GSI_OK;
         }
         void *q = nullptr;
+        const auto t0 = std::chrono::steady_clock::now();
         cudaError_t e = cudaMallocAsync(&q, bytes, st);
+        ms_alloc += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         if (e == cudaErrorMemoryAllocation) {
             cudaGetLastError();
             set_error("device memory exhausted");
@@ -1154,7 +1157,9 @@ struct Arena {
     template <typename T>
     gsi_status get_big(T **p, unsigned long long count) {   // never from the bump region
         void *q = nullptr;
+        const auto t0 = std::chrono::steady_clock::now();
         cudaError_t e = cudaMallocAsync(&q, (size_t)std::max<unsigned long long>(count, 1) * sizeof(T), st);
+        ms_alloc += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         if (e == cudaErrorMemoryAllocation) {
             cudaGetLastError();
             set_error("device memory exhausted");
@@ -1226,6 +1231,14 @@ struct Prof {
         }
     }
 };
+
+// stream sync with the host wait time accounted in stats.ms_host_sync
+cudaError_t sync_timed(gsi_stats &S, cudaStream_t st) {
+    const auto t0 = std::chrono::steady_clock::now();
+    cudaError_t e = cudaStreamSynchronize(st);
+    S.ms_host_sync += (float)std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    return e;
+}
 
 cudaError_t d2h(gsi_stats &S, void *dst, const void *src, size_t bytes, cudaStream_t st) {
     S.d2h_bytes += bytes;
@@ -1625,7 +1638,7 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
             Counters hc0;
             GSI_CUDA(d2h(S, &gba, F + nM, 8, st));
             GSI_CUDA(d2h(S, &hc0, rctr, sizeof(Counters), st));
-            GSI_CUDA(cudaStreamSynchronize(st));
+            GSI_CUDA(sync_timed(S, st));
             active = hc0.active_rows;
             elems = hc0.list_elems;
             P.prefiltered = 1;
@@ -1645,7 +1658,7 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         prof.end();
         long long hb[4];
         GSI_CUDA(d2h(S, hb, bounds, sizeof(hb), st));
-        GSI_CUDA(cudaStreamSynchronize(st));
+        GSI_CUDA(sync_timed(S, st));
         A.release(bounds);
         s0 = (unsigned long long)hb[2];
         s1 = (unsigned long long)hb[3];
@@ -1728,7 +1741,7 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         prof.end();
         Counters hc;
         GSI_CUDA(d2h(S, &hc, lctr, sizeof(Counters), st));
-        GSI_CUDA(cudaStreamSynchronize(st));
+        GSI_CUDA(sync_timed(S, st));
         GSI_CUDA(cudaGetLastError());
         A.release(status);
         A.release(rowmap);
@@ -1838,7 +1851,7 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     Counters hc;
     GSI_CUDA(d2h(S, cand.data(), d_counts, 8ull * k, st));
     GSI_CUDA(d2h(S, &hc, C.ctr, sizeof(Counters), st));
-    GSI_CUDA(cudaStreamSynchronize(st));
+    GSI_CUDA(sync_timed(S, st));
     GSI_CUDA(cudaGetLastError());
     const double t_filter = now_ms();
     S.ms_filter = (float)(t_filter - t_start);
@@ -1902,7 +1915,7 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
             k_compact_roots<<<tiles, kThreads, 0, st>>>(d_roots, nr, bm1, M, status + 1, (unsigned *)status, C.ctr);
             prof.end();
             GSI_CUDA(d2h(S, &hc, C.ctr, sizeof(Counters), st));
-            GSI_CUDA(cudaStreamSynchronize(st));
+            GSI_CUDA(sync_timed(S, st));
             nM = hc.total;
             S.alg_bytes[GSI_K_COMPACT] += 8.0 * nr + 4.0 * nM;
         } else {
@@ -1934,7 +1947,7 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
             prof.end();
         }
         GSI_CUDA(d2h(S, &hc, C.ctr, sizeof(Counters), st));
-        GSI_CUDA(cudaStreamSynchronize(st));
+        GSI_CUDA(sync_timed(S, st));
         C.count = nM;
         C.fp1 = hc.fp1;
         C.fp2 = hc.fp2;
@@ -1966,7 +1979,7 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
         unsigned long long gba = 0;
         GSI_CUDA(d2h(S, &gba, F + nM, 8, st));
         GSI_CUDA(d2h(S, &hc, C.ctr, sizeof(Counters), st));
-        GSI_CUDA(cudaStreamSynchronize(st));
+        GSI_CUDA(sync_timed(S, st));
         A.release(status);
         S.alg_bytes[GSI_K_PROBE] += (double)nM * (20.0 * P.E + 8.0);
         S.rows[0] += nM;
@@ -2009,8 +2022,9 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
         }
         C.pieces.clear();
     }
-    GSI_CUDA(cudaStreamSynchronize(st));
+    GSI_CUDA(sync_timed(S, st));
     prof.finish(&S);
+    S.ms_host_alloc = (float)A.ms_alloc;
     S.count = res->count;
     S.ms_join = (float)(now_ms() - t_plan);
     S.ms_total = (float)(now_ms() - t_start);

@@ -64,7 +64,8 @@ class gsi_stats(ctypes.Structure):
                 ("ms_join", ctypes.c_float), ("ms_kernel", ctypes.c_float * GSI_N_KCLASS),
                 ("launches", U32 * GSI_N_KCLASS), ("alg_bytes", ctypes.c_double * GSI_N_KCLASS),
                 ("total_launches", U32), ("n_chunks", U32), ("capped", I32), ("h2d_bytes", U64),
-                ("d2h_bytes", U64), ("n_shared_lists", U32)]
+                ("d2h_bytes", U64), ("n_shared_lists", U32), ("ms_host_alloc", ctypes.c_float),
+                ("ms_host_sync", ctypes.c_float)]
 
 
 _SIGS = {

@@ -219,6 +219,7 @@ def test_medium_random_walk_queries(seed):
         assert np.array_equal(canon(tab), otab)
         assert strictly_increasing_in_order(tab, r.stats()["order"][:q.n])
         assert tuple(q.embedding.tolist()) in {tuple(x) for x in tab.tolist()}
+        assert gsi.query(graph, q, fingerprint=False).count == cnt
 
 
 def test_large_counts_fingerprint():
@@ -235,6 +236,8 @@ def test_large_counts_fingerprint():
             r = gsi.query(graph, q, shared_lists=sl)
             assert r.count == cnt and r.fingerprint() == fp, (s, sl)
             shared += r.stats()["n_shared_lists"] if sl else 0
+            r = gsi.query(graph, q, shared_lists=sl, fingerprint=False)   # lean count-only kernel
+            assert r.count == cnt, (s, sl)
         assert cnt > 10_000_000 or s == 703
     assert shared > 0
 

@@ -11,7 +11,7 @@ for l in sys.stdin:
     if l.startswith('{'):
         d = json.loads(l); tot[0] += d['wall_ms']; tot[1] += d['kernels']['join']['ms']
         print(d['q'], d['count'], d['wall_ms'], 'join', round(d['kernels']['join']['ms'], 3), 'filt', round(d['kernels']['filter']['ms'], 3),
-              'other', round(d['kernels']['other']['ms'], 3), 'n_other', d['kernels']['other']['launches'], 'hjoin', round(d['ms_join'], 2))
+              'other', round(d['kernels']['other']['ms'], 3), 'n_other', d['kernels']['other']['launches'], 'hjoin', round(d['ms_join'], 2), 'alloc', round(d['ms_alloc'], 2), 'sync', round(d['ms_sync'], 2))
 print('TOTAL wall %.1f join %.1f' % tuple(tot))
 "
 done

@@ -50,4 +50,5 @@ for i, q in qs.items():
                             if s["ms_kernel"][c] else 0} for c in range(6)}
     print(json.dumps({"q": i, "count": r.count, "wall_ms": round(ms, 2), "rows": s["rows"][:q.n],
                       "gba": s["gba"][1:q.n], "chunks": s["n_chunks"], "kernels": kern,
-                      "ms_filter": s["ms_filter"], "ms_join": s["ms_join"]}), flush=True)
+                      "ms_filter": s["ms_filter"], "ms_join": s["ms_join"], "ms_alloc": s["ms_host_alloc"],
+                      "ms_sync": s["ms_host_sync"]}), flush=True)
