@@ -207,7 +207,10 @@ def _cuda_ok():
 def workload_config(args, g):
     return {"workload": f"{args.config}: {BENCH_CONFIGS[args.config]['desc']}", "n": int(g.n), "m": int(g.m),
             "queries_per_step": args.queries, "query_k": args.k, "query_seeds": f"1000..{999 + args.queries}",
-            "graph_seed": 1, "mode": "count-only (final level fused count + fingerprint)",
+            "graph_seed": 1,
+            "mode": "count-only (gsi_query count; a one-edge last step is counted by the level before it "
+                    "as |N(v,l0) ∩ C(u)| minus the row's own vertices, see DESIGN.md; 'enumerated' = every "
+                    "match visited and hashed)",
             "l2": "inputs larger than L2 (PCSR+signatures >> 126 MB); no flush"}
 
 
@@ -264,10 +267,12 @@ def run_gsi(args):
     prepared = [gsi.prepare(graph, q) for q in qs]
     counts = torch.zeros(len(qs), dtype=torch.int64, device="cuda")
 
-    def step(profile=False, stats=None):
+    def step(profile=False, stats=None, enumerate_all=False):
+        # count-only (the product's count path; fingerprint off so the last level may be
+        # counted ahead); enumerate_all=True hashes every match of the last level instead
         for i, p in enumerate(prepared):
             r = gsi.gsi_query_run(graph, p, stream=sptr, timeout_s=args.query_timeout, profile=profile,
-                                  partial_on_timeout=True, **shard)
+                                  partial_on_timeout=True, fingerprint=enumerate_all, **shard)
             counts[i] = r.count
             if stats is not None:
                 stats.append(r.stats())
@@ -278,7 +283,7 @@ def run_gsi(args):
     def e2e_step():
         for i, q in enumerate(qs):
             r = gsi.gsi_query(graph, q.vlabels, q.src, q.dst, q.elabels, stream=sptr,
-                              timeout_s=args.query_timeout, partial_on_timeout=True, **shard)
+                              timeout_s=args.query_timeout, partial_on_timeout=True, fingerprint=False, **shard)
             counts[i] = r.count
         if ws > 1:
             dist.all_reduce(counts)
@@ -329,6 +334,26 @@ def run_gsi(args):
     e2e_s = float(e2e_t.item())
     h2d = sum(4 * q.n + 12 * len(q.src) + 64 * q.n for q in qs)        # query arrays + signatures
     d2h = sum(8 * q.n + 64 * (2 * q.n + 2) for q in qs)                # |C(u)|, per-level sizes, count
+
+    # ---- secondary: every match of the last level enumerated (and hashed), one step --------
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    en_stats = []
+    ev0.record(stream)
+    en_counts = step(stats=en_stats, enumerate_all=True)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    en_ms = ev0.elapsed_time(ev1)
+    en_t = torch.tensor([en_ms], dtype=torch.float64, device="cuda")
+    if ws > 1:
+        dist.all_reduce(en_t, op=dist.ReduceOp.MAX)
+    en_ms = float(en_t.item())
+    en_matches = int(en_counts.sum().item())
+    enumerated = {"value": en_matches / (en_ms / 1000.0), "unit": "matches/s", "ms_per_step": en_ms,
+                  "matches_per_step": en_matches,
+                  "capped_queries": int(sum(s_["capped"] for s_ in en_stats)),
+                  "note": "fingerprint on: every match of the last level enumerated and hashed on the device"}
 
     # ---- profiled pass: per-kernel CUDA-event times + algorithmic bytes -----------------
     pstats = []
@@ -391,7 +416,7 @@ def run_gsi(args):
         "capped_queries_per_step": capped, "query_timeout_s": args.query_timeout,
         "e2e": {"value": m_e2e * args.steps / e2e_s, "unit": "matches/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_query": 1000.0 * e2e_s / args.steps / len(qs)},
-        "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": launches,
+        "enumerated": enumerated, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": launches,
         "graph": {"n_groups": info["n_groups"], "max_chain": info["max_chain"],
                   "bytes_total": info["bytes_total"], "build_ms": info["ms_build"]},
     }

@@ -147,6 +147,12 @@ typedef struct {
     int32_t fingerprint;         /* 1: compute the set fingerprint of the final rows (costs ~2k
                                     hash rounds per match); 0: fingerprint = (count, 0, 0)      */
     int32_t no_shared_lists;     /* 1: never switch a level to shared N(v,l0) ∩ C(u) lists      */
+    int32_t no_count_ahead;      /* 1: enumerate every match of the last level even in count-only
+                                    mode.  0 (default): when the last step has one linking edge
+                                    and no fingerprint/table is wanted, the level before it counts
+                                    each new row's extensions as |N(v,l0) ∩ C(u)| minus the row's
+                                    own vertices in that run (Alg. 3 lines 9-10 applied to a
+                                    count), so M_{k-1} is never stored and M_k never enumerated  */
 } gsi_query_opts;
 
 void gsi_query_opts_default(gsi_query_opts *opts);
@@ -195,6 +201,9 @@ typedef struct {
     uint64_t h2d_bytes, d2h_bytes;    /* host<->device bytes this query copied                */
     uint32_t n_shared_lists;          /* levels that enumerated shared N(v,l0) ∩ C(u) lists   */
     float ms_host_alloc, ms_host_sync; /* host time in stream-ordered allocation / stream syncs */
+    int32_t count_ahead;              /* 1: the last level was counted by the level before it    */
+    uint32_t n_probe_ahead;           /* levels whose next-step locate came from a per-candidate
+                                         probe-ahead table instead of a PCSR probe per new row   */
 } gsi_stats;
 
 gsi_status gsi_result_count(const gsi_result *r, uint64_t *count);

@@ -45,6 +45,9 @@ constexpr int kThreads = 256;
 #ifndef GSI_PREFILTER_AHEAD
 #define GSI_PREFILTER_AHEAD 4   // ... and produce a level's rows pre-pointed when 4x its parent's slots exceed it
 #endif
+#ifndef GSI_PROBE_AHEAD
+#define GSI_PROBE_AHEAD 2   // build a step's probe-ahead table when its slots >= 2x its partition (0: off)
+#endif
 #ifndef GSI_FAST_ITEMS
 #define GSI_FAST_ITEMS 16   // slots per thread of the lean count-only kernel (0: never use it)
 #endif
@@ -78,6 +81,10 @@ struct StepParams {
     uint32_t flo, fhi;           //   ... and the partition's ci range
     int stage_base;              // join tile stages per-row ci bases in shared memory
     int stage_inj;               // ... and up to this many subtraction columns
+    const Loc *pa;               // probe-ahead table of this step: pa[p] = the NEXT step's filtered
+                                 //   run of x = (prefiltered ci)[p] (null: probe PCSR per new row)
+    const uint32_t *cu;          // (as the counted final step of J_CAHEAD) C(u) bitmap ...
+    const int32_t *fci;          //   ... and the shared N(v,l0) ∩ C(u) runs of P(G,l0)
 };
 
 // Counters shared by the kernels of one query (device).
@@ -364,7 +371,7 @@ __device__ __forceinline__ void row_hash(const int32_t *__restrict__ row, uint32
     h2 ^= b;
 }
 
-enum JoinMode { J_COUNT = 0, J_TABLE = 1, J_NEXT = 2 };
+enum JoinMode { J_COUNT = 0, J_TABLE = 1, J_NEXT = 2, J_CAHEAD = 3 };
 // Slots per thread: J_NEXT carries the next-step probe state of every slot in registers, so
 // it runs 1024-slot tiles; the others 2048.
 #ifndef GSI_NEXT_ITEMS
@@ -375,6 +382,50 @@ enum JoinMode { J_COUNT = 0, J_TABLE = 1, J_NEXT = 2 };
 #endif
 __host__ __device__ constexpr int join_items(int mode) {
     return mode == J_NEXT ? GSI_NEXT_ITEMS : (mode == J_COUNT ? GSI_COUNT_ITEMS : 8);
+}
+
+// The NEXT step's list of every survivor (row, x) when that step has one linking edge:
+// from the probe-ahead table aligned with this step's candidates (one coalesced 8 B read),
+// else one PCSR probe per survivor (batches of 4 keep the first-sector loads in flight),
+// re-pointed at the next step's shared N(v,l0) ∩ C(u) run when it has one.
+template <int IT>
+__device__ __forceinline__ void next_step_locs(const StepParams &P, const StepParams &P2, const int32_t *__restrict__ M,
+                                               const uint32_t (&rows)[IT], const uint32_t (&xs)[IT],
+                                               const uint32_t (&cio)[IT], const bool (&keep)[IT],
+                                               const uint2 *__restrict__ groups, int gpn, Loc (&N0)[IT]) {
+    if (P.pa) {
+#pragma unroll
+        for (int it = 0; it < IT; it++) N0[it] = keep[it] ? P.pa[cio[it]] : Loc{0u, 0u};
+        return;
+    }
+    const int c2 = P2.col[0];
+    uint32_t v[IT];
+#pragma unroll
+    for (int it = 0; it < IT; it++)
+        v[it] = keep[it] ? (c2 < P.t ? (uint32_t)__ldg(M + (long long)rows[it] * P.t + c2) : xs[it]) : 0u;
+#pragma unroll
+    for (int h = 0; h < IT; h += 4) {
+        uint32_t vb[4];
+        bool kb[4];
+        Loc nb[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            vb[q] = v[h + q];
+            kb[q] = keep[h + q];
+        }
+        pcsr_lookup_batch<4>(groups, gpn, P2.gbase[0], P2.ngroups[0], P2.lab[0], vb, kb, nb);
+#pragma unroll
+        for (int q = 0; q < 4; q++) N0[h + q] = nb[q];
+    }
+    if (P2.prefiltered) {   // re-point at the shared N(v,l0) ∩ C(u) run of the next step
+#pragma unroll
+        for (int it = 0; it < IT; it++) {
+            if (!keep[it] || !N0[it].len) continue;
+            const uint32_t a = __ldg(P2.fpos + (N0[it].off - P2.flo));
+            const uint32_t b = __ldg(P2.fpos + (N0[it].off + N0[it].len - P2.flo));
+            N0[it] = Loc{a, b - a};
+        }
+    }
 }
 
 // rowmap[j] = the row holding slot s0 + j*tile (j < ntiles), rowmap[ntiles] = the row
@@ -411,7 +462,7 @@ template <int MODE>
 #ifndef GSI_NEXT_MINB
 #define GSI_NEXT_MINB 3
 #endif
-__global__ void __launch_bounds__(kThreads, join_items(MODE) > 8 ? 2 : ((MODE == J_NEXT && GSI_NEXT_ITEMS > 4) ? GSI_NEXT_MINB : 4)) k_join(const int32_t *__restrict__ M, long long nM,
+__global__ void __launch_bounds__(kThreads, join_items(MODE) > 8 ? 2 : (((MODE == J_NEXT && GSI_NEXT_ITEMS > 4) || MODE == J_CAHEAD) ? GSI_NEXT_MINB : 4)) k_join(const int32_t *__restrict__ M, long long nM,
                                                    const unsigned long long *__restrict__ F,
                                                    const Loc *__restrict__ loc, const uint32_t *__restrict__ rowmap,
                                                    StepParams P, StepParams P2, const int32_t *__restrict__ ci,
@@ -580,6 +631,37 @@ __global__ void __launch_bounds__(kThreads, join_items(MODE) > 8 ? 2 : ((MODE ==
                 atomicXor(&ctr->fp2, h2);
             }
         }
+    } else if constexpr (MODE == J_CAHEAD) {
+        // ---- count-ahead: this level's survivors are the rows of M_{k-1}; the last step has
+        // one linking edge, so the extensions of row' = m_i || x are exactly
+        // (N(v,l0) ∩ C(u_k)) \ row' (Alg. 3 lines 9-10): count |run| minus the row's own
+        // vertices found in the run, without storing row' or enumerating the run.
+        Loc N0[IT];
+        next_step_locs<IT>(P, P2, M, rows, xs, cio, keep, groups, gpn, N0);
+        unsigned long long surv = 0, c = 0, bound = 0;
+#pragma unroll
+        for (int it = 0; it < IT; it++) {
+            if (!keep[it]) continue;
+            surv++;
+            const Loc R = N0[it];
+            bound += R.len;
+            uint32_t cc = R.len;
+            for (int j = 0; j < P2.n_inj && cc; j++) {
+                const int col = P2.inj_col[j];
+                const int32_t y = col < P.t ? __ldg(M + (long long)rows[it] * P.t + col) : (int32_t)xs[it];
+                if ((__ldg(P2.cu + ((uint32_t)y >> 5)) >> (y & 31)) & 1u)
+                    cc -= in_sorted(P2.fci + R.off, R.len, y) ? 1u : 0u;
+            }
+            c += cc;
+        }
+        surv = warp_sum_u64(surv);
+        c = warp_sum_u64(c);
+        bound = warp_sum_u64(bound);
+        if (lane == 0) {
+            if (c) atomicAdd(&ctr->count, c);
+            if (surv) atomicAdd(&ctr->total, surv);
+            if (bound) atomicAdd(&ctr->total2, bound);
+        }
     } else {
         // ---- J_NEXT: next-step probe of every survivor, dead rows dropped --------------------
         Loc N0[IT];
@@ -590,35 +672,7 @@ __global__ void __launch_bounds__(kThreads, join_items(MODE) > 8 ? 2 : ((MODE ==
             all = warp_sum_u64(all);
             if (lane == 0 && all) atomicAdd(&ctr->count, all);      // |M_{t+1}| including dead rows
             if (P2.E == 1) {
-                const int c2 = P2.col[0];
-                uint32_t v[IT];
-#pragma unroll
-                for (int it = 0; it < IT; it++)
-                    v[it] = keep[it] ? (c2 < P.t ? (uint32_t)__ldg(M + (long long)rows[it] * P.t + c2) : xs[it]) : 0u;
-                // batches of 4 keep the first-sector loads (8 words each) in fewer registers
-#pragma unroll
-                for (int h = 0; h < IT; h += 4) {
-                    uint32_t vb[4];
-                    bool kb[4];
-                    Loc nb[4];
-#pragma unroll
-                    for (int q = 0; q < 4; q++) {
-                        vb[q] = v[h + q];
-                        kb[q] = keep[h + q];
-                    }
-                    pcsr_lookup_batch<4>(groups, gpn, P2.gbase[0], P2.ngroups[0], P2.lab[0], vb, kb, nb);
-#pragma unroll
-                    for (int q = 0; q < 4; q++) N0[h + q] = nb[q];
-                }
-                if (P2.prefiltered) {   // re-point at the shared N(v,l0) ∩ C(u) run of the next step
-#pragma unroll
-                    for (int it = 0; it < IT; it++) {
-                        if (!keep[it] || !N0[it].len) continue;
-                        const uint32_t a = __ldg(P2.fpos + (N0[it].off - P2.flo));
-                        const uint32_t b = __ldg(P2.fpos + (N0[it].off + N0[it].len - P2.flo));
-                        N0[it] = Loc{a, b - a};
-                    }
-                }
+                next_step_locs<IT>(P, P2, M, rows, xs, cio, keep, groups, gpn, N0);
 #pragma unroll
                 for (int it = 0; it < IT; it++) keep[it] = keep[it] && N0[it].len > 0;
             } else {
@@ -896,7 +950,7 @@ constexpr int kFastItems = GSI_FAST_ITEMS > 0 ? GSI_FAST_ITEMS : 8;
 inline size_t join_smem_bytes(int mode, const StepParams &P) {
     const size_t tile = (size_t)join_items(mode) * kThreads;
     const size_t staging = tile * 4 * (1 + (P.stage_base ? 1 : 0) + (size_t)P.stage_inj);
-    const size_t cache = mode == J_COUNT ? 0 : tile * 4 * 2 + (mode == J_NEXT ? tile * 8 : 0);
+    const size_t cache = (mode == J_COUNT || mode == J_CAHEAD) ? 0 : tile * 4 * 2 + (mode == J_NEXT ? tile * 8 : 0);
     return std::max(staging, cache);
 }
 constexpr int kMaxJoinSmem = 6 * 4096 * 4;
@@ -979,6 +1033,41 @@ __global__ void __launch_bounds__(kThreads) k_filter_partition(const int32_t *__
         if (keep[it]) fci[pos] = xs[it];
     }
     if (tile == gridDim.x - 1 && tid == 0) fpos[hi - lo] = (uint32_t)(base_s + agg_s);
+}
+
+// Probe-ahead table of a step on shared lists whose NEXT step has one linking edge, to the
+// vertex this step adds: pa[p] = the next step's N(x,l0') ∩ C(u') run of x = fci[p].  Rows of
+// a level re-scan the same candidate runs many times (that is why the runs are shared), so
+// one PCSR probe per candidate replaces one per new row, and the join reads pa[p] coalesced
+// next to fci[p].
+__global__ void __launch_bounds__(kThreads) k_probe_ahead(const int32_t *__restrict__ fci,
+                                                          const uint32_t *__restrict__ ntotal, StepParams P2,
+                                                          const uint2 *__restrict__ groups, int gpn,
+                                                          Loc *__restrict__ pa) {
+    const uint32_t total = *ntotal;
+    const uint32_t stride = gridDim.x * kThreads;
+    for (uint32_t p0 = blockIdx.x * kThreads + threadIdx.x; p0 < total; p0 += 4 * stride) {
+        uint32_t v[4];
+        bool kb[4];
+        Loc nb[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const uint32_t p = p0 + q * stride;
+            kb[q] = p < total;
+            v[q] = kb[q] ? (uint32_t)__ldg(fci + p) : 0u;
+        }
+        pcsr_lookup_batch<4>(groups, gpn, P2.gbase[0], P2.ngroups[0], P2.lab[0], v, kb, nb);
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            if (!kb[q]) continue;
+            Loc r = nb[q];
+            if (r.len) {
+                const uint32_t a = __ldg(P2.fpos + (r.off - P2.flo)), b = __ldg(P2.fpos + (r.off + r.len - P2.flo));
+                r = Loc{a, b - a};
+            }
+            pa[p0 + q * stride] = r;
+        }
+    }
 }
 
 // Re-point the rows of a level (one linking edge) at their filtered runs and rebuild F.
@@ -1266,6 +1355,7 @@ void ensure_pool(int dev) {
     cudaFuncSetAttribute(k_join<J_COUNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxJoinSmem);
     cudaFuncSetAttribute(k_join<J_TABLE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxJoinSmem);
     cudaFuncSetAttribute(k_join<J_NEXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxJoinSmem);
+    cudaFuncSetAttribute(k_join<J_CAHEAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxJoinSmem);
     cudaFuncSetAttribute(k_count_fast<kFastItems>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxJoinSmem);
     cudaGetLastError();
     g_pool_ready[dev] = true;
@@ -1530,6 +1620,7 @@ struct QueryCtx {
     unsigned long long count = 0, fp1 = 0, fp2 = 0;
     std::vector<std::pair<int32_t *, unsigned long long>> pieces;   // final table pieces (device)
     std::vector<std::pair<uint32_t *, int32_t *>> filt;             // per step: (fpos, fci) or null
+    std::vector<Loc *> pa;                                           // per step: probe-ahead table or null
 };
 
 void fill_params(QueryCtx &C, const Step &s, StepParams &P) {
@@ -1587,6 +1678,26 @@ gsi_status ensure_filtered(QueryCtx &C, size_t si, uint32_t lab) {
     C.prof->end();
     C.S->alg_bytes[GSI_K_OTHER] += 12.0 * (hi - lo);
     C.filt[si] = {fpos, fci};
+    return GSI_OK;
+}
+
+// Probe-ahead table of step si (on shared lists; its next step links to the vertex it adds).
+gsi_status ensure_probe_ahead(QueryCtx &C, size_t si, const StepParams &P, const StepParams &P2) {
+    if (C.pa.size() < C.steps.size()) C.pa.assign(C.steps.size(), nullptr);
+    if (C.pa[si]) return GSI_OK;
+    const gsi_graph *g = C.g;
+    const uint32_t lo = g->ci_lo[P.lab[0]], hi = g->ci_lo[P.lab[0] + 1];
+    Loc *pa = nullptr;
+    GSI_TRY(C.A->get_big(&pa, (unsigned long long)(hi - lo)));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
+    const unsigned grid = std::min<unsigned>(grid_for(hi - lo, 4 * kThreads), (unsigned)sms * 8);
+    C.prof->begin(GSI_K_OTHER);
+    k_probe_ahead<<<grid, kThreads, 0, C.st>>>(C.filt[si].second, C.filt[si].first + (hi - lo), P2, g->groups,
+                                               g->gpn, pa);
+    C.prof->end();
+    C.S->alg_bytes[GSI_K_OTHER] += 20.0 * (hi - lo);   // read x, locate (8 B), re-point (8 B write)
+    C.pa[si] = pa;
     return GSI_OK;
 }
 
@@ -1648,9 +1759,19 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
     }
     if (P.prefiltered) S.n_shared_lists++;
 
+    // ---- count-ahead: the last step has one linking edge and only the count is wanted, so
+    // this level counts the extensions of its survivors on the last step's shared lists ----
+    bool cahead = false;
+    if (!last && si + 2 == C.steps.size() && !C.opts.want_table && !C.opts.fingerprint &&
+        !C.opts.no_count_ahead && shared_lists_allowed(C, P2)) {
+        const uint32_t lo2 = g->ci_lo[P2.lab[0]], hi2 = g->ci_lo[P2.lab[0] + 1];
+        cahead = hi2 > lo2 && ((C.filt.size() > si + 1 && C.filt[si + 1].first) ||
+                               gba * (unsigned long long)GSI_PREFILTER_AHEAD >= (unsigned long long)(hi2 - lo2));
+    }
+
     // ---- shard this level's slot range ----
     unsigned long long s0 = 0, s1 = gba;
-    if (!C.sharded && (nM >= C.shard_min || gba > C.cap_slots || last)) {
+    if (!C.sharded && (nM >= C.shard_min || gba > C.cap_slots || last || cahead)) {
         long long *bounds = nullptr;
         GSI_TRY(A.get(&bounds, 4));
         prof.begin(GSI_K_OTHER);
@@ -1668,9 +1789,10 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         C.sharded = true;
     }
 
-    const int mode = !last ? J_NEXT : (C.opts.want_table ? J_TABLE : J_COUNT);
-    const unsigned long long chunk =
-        mode == J_COUNT ? std::max<unsigned long long>(s1 - s0, 1) : std::max<unsigned long long>(C.cap_slots, kJoinTile);
+    const int mode = cahead ? J_CAHEAD : (!last ? J_NEXT : (C.opts.want_table ? J_TABLE : J_COUNT));
+    const unsigned long long chunk = (mode == J_COUNT || mode == J_CAHEAD)
+                                         ? std::max<unsigned long long>(s1 - s0, 1)
+                                         : std::max<unsigned long long>(C.cap_slots, kJoinTile);
     const uint32_t *cu = C.bm + (long long)s.u * C.words;
     gsi_status rc = GSI_OK;
     for (unsigned long long c0 = s0; c0 < s1 && rc == GSI_OK; c0 += chunk) {
@@ -1704,7 +1826,15 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         // next step on shared lists? (its rows are produced here, so the probe-ahead can point
         // them at N(v,l0') ∩ C(u') directly and drop rows whose filtered run is empty)
         bool pf_next = false;
-        if (mode == J_NEXT && shared_lists_allowed(C, P2)) {
+        if (mode == J_CAHEAD) {
+            GSI_TRY(ensure_filtered(C, si + 1, P2.lab[0]));
+            P2.prefiltered = 1;
+            P2.fpos = C.filt[si + 1].first;
+            P2.flo = g->ci_lo[P2.lab[0]];
+            P2.fhi = g->ci_lo[P2.lab[0] + 1];
+            P2.fci = C.filt[si + 1].second;
+            P2.cu = C.bm + (long long)C.steps[si + 1].u * C.words;
+        } else if (mode == J_NEXT && shared_lists_allowed(C, P2)) {
             const uint32_t lo2 = g->ci_lo[P2.lab[0]], hi2 = g->ci_lo[P2.lab[0] + 1];
             if (hi2 > lo2 && (C.filt.size() > si + 1 && C.filt[si + 1].first ||
                               slots * (unsigned long long)GSI_PREFILTER_AHEAD >= (unsigned long long)(hi2 - lo2))) {
@@ -1716,6 +1846,19 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
                 pf_next = true;
             } else {
                 P2.prefiltered = 0;
+            }
+        }
+        // probe-ahead: the next step links to the vertex this step adds, and this level's rows
+        // re-scan its candidate runs often enough to pay one probe per candidate
+        P.pa = nullptr;
+        if ((mode == J_NEXT || mode == J_CAHEAD) && P.prefiltered && P2.prefiltered && P2.E == 1 &&
+            P2.col[0] == t && GSI_PROBE_AHEAD > 0) {
+            const uint32_t plo = g->ci_lo[P.lab[0]], phi = g->ci_lo[P.lab[0] + 1];
+            if ((C.pa.size() > si && C.pa[si]) ||
+                slots >= (unsigned long long)GSI_PROBE_AHEAD * (unsigned long long)(phi - plo)) {
+                GSI_TRY(ensure_probe_ahead(C, si, P, P2));
+                P.pa = C.pa[si];
+                S.n_probe_ahead++;
             }
         }
         uint32_t *rowmap = nullptr;
@@ -1732,6 +1875,9 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         } else if (mode == J_COUNT)
             k_join<J_COUNT><<<jt, kThreads, join_smem_bytes(J_COUNT, P), st>>>(M, (long long)nM, F, loc, rowmap, P, P2, cip, cu, g->groups,
                                                      g->gpn, c0, c1, out, loc2, F2, st1, st2, tctr, lctr);
+        else if (mode == J_CAHEAD)
+            k_join<J_CAHEAD><<<jt, kThreads, join_smem_bytes(J_CAHEAD, P), st>>>(M, (long long)nM, F, loc, rowmap, P, P2, cip, cu,
+                                                      g->groups, g->gpn, c0, c1, out, loc2, F2, st1, st2, tctr, lctr);
         else if (mode == J_TABLE)
             k_join<J_TABLE><<<jt, kThreads, join_smem_bytes(J_TABLE, P), st>>>(M, (long long)nM, F, loc, rowmap, P, P2, cip, cu, g->groups,
                                                      g->gpn, c0, c1, out, loc2, F2, st1, st2, tctr, lctr);
@@ -1745,12 +1891,21 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         GSI_CUDA(cudaGetLastError());
         A.release(status);
         A.release(rowmap);
-        const unsigned long long nout = mode == J_COUNT ? hc.count : hc.total;   // J_NEXT: stored rows
+        const unsigned long long nout = (mode == J_COUNT || mode == J_CAHEAD) ? hc.count : hc.total;   // J_NEXT: stored rows
         const double frac = gba ? (double)slots / (double)gba : 0.0;
         double jb = frac * (4.0 * t * active + 4.0 * elems + (8.0 * E + 8.0) * active);
         if (mode == J_TABLE) jb += 4.0 * C.q->k * nout;
         if (mode == J_NEXT) jb += nout * (4.0 * (t + 1) + 16.0 * P2.E + 8.0);
         if (mode == J_NEXT) S.rows[t] += hc.count;   // |M_{t+1}|: every survivor, stored or not
+        if (mode == J_CAHEAD) {                        // survivors = |M_{t+1}|, counted = |M_{t+2}|
+            jb += 8.0 * hc.total;                      // locate of the last step's run per survivor
+            S.rows[t] += hc.total;
+            S.rows[t + 1] += hc.count;
+            S.gba[t + 1] += hc.total2;
+            if (S.levels < t + 2) S.levels = t + 2;
+            S.count_ahead = 1;
+            C.count += hc.count;
+        }
         S.alg_bytes[GSI_K_JOIN] += jb;
         if (last) {
             C.count += nout;

@@ -42,7 +42,8 @@ class gsi_query_opts(ctypes.Structure):
                 ("force_order", P), ("force_first_edge", P), ("roots", P), ("n_roots", I64),
                 ("shard_rank", I32), ("shard_count", I32), ("shard_min_rows", U64),
                 ("mem_budget_bytes", U64), ("timeout_s", ctypes.c_double), ("profile", I32), ("stream", P),
-                ("chunk_slots", U64), ("partial_on_timeout", I32), ("fingerprint", I32), ("no_shared_lists", I32)]
+                ("chunk_slots", U64), ("partial_on_timeout", I32), ("fingerprint", I32), ("no_shared_lists", I32),
+                ("no_count_ahead", I32)]
 
 
 class gsi_graph_info(ctypes.Structure):
@@ -65,7 +66,7 @@ class gsi_stats(ctypes.Structure):
                 ("launches", U32 * GSI_N_KCLASS), ("alg_bytes", ctypes.c_double * GSI_N_KCLASS),
                 ("total_launches", U32), ("n_chunks", U32), ("capped", I32), ("h2d_bytes", U64),
                 ("d2h_bytes", U64), ("n_shared_lists", U32), ("ms_host_alloc", ctypes.c_float),
-                ("ms_host_sync", ctypes.c_float)]
+                ("ms_host_sync", ctypes.c_float), ("count_ahead", I32), ("n_probe_ahead", U32)]
 
 
 _SIGS = {
@@ -257,7 +258,7 @@ class Prepared:
 def _opts(want_table=False, homomorphism=False, filter_mode=0, e0_mode=0, force_order=None,
           force_first_edge=None, roots=None, shard_rank=0, shard_count=1, shard_min_rows=0,
           mem_budget_bytes=0, timeout_s=0.0, profile=False, stream=None, chunk_slots=0,
-          partial_on_timeout=False, fingerprint=True, shared_lists=True):
+          partial_on_timeout=False, fingerprint=True, shared_lists=True, count_ahead=True):
     o = gsi_query_opts()
     lib.gsi_query_opts_default(ctypes.byref(o))
     keep = []
@@ -274,6 +275,7 @@ def _opts(want_table=False, homomorphism=False, filter_mode=0, e0_mode=0, force_
     o.chunk_slots, o.partial_on_timeout = chunk_slots, int(partial_on_timeout)
     o.fingerprint = int(fingerprint)   # binding default: on (the C default is off)
     o.no_shared_lists = 0 if shared_lists else 1
+    o.no_count_ahead = 0 if count_ahead else 1
     return o, keep
 
 

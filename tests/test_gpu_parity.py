@@ -408,3 +408,34 @@ def test_timeout_partial_prefix():
     with pytest.raises(gsi.GsiError) as e:
         gsi.query(graph, q, timeout_s=1e-6, chunk_slots=2048)
     assert e.value.status == "GSI_ERR_TIMEOUT"
+
+
+def test_count_ahead_matches_oracle():
+    """Count-only mode counts the last level from the level before it (|N(v,l0) ∩ C(u)| minus
+    the row's own vertices in that run, Alg. 3 lines 9-10) — same count as the oracle and as
+    enumerating every match; few vertex labels make the subtraction columns many."""
+    seen = 0
+    for gs, nlv, nle, k in [(81, 1, 2, 6), (82, 2, 3, 7), (83, 3, 4, 6), (84, 2, 1, 5)]:
+        g = W.chung_lu(4000, 30000, 500, nlv=nlv, nle=nle, seed=gs)
+        graph = gsi.build(g)
+        og = oracle.OracleGraph(g)
+        for s in range(3):
+            q = W.random_walk_query(g, k, 7000 + 10 * gs + s)
+            try:
+                cnt = oracle.match(og, q, table=False, timeout=20.0)[0]
+            except oracle.OracleError:
+                continue
+            r = gsi.query(graph, q, fingerprint=False)
+            assert r.count == cnt, (gs, s)
+            seen += r.stats()["count_ahead"]
+            assert gsi.query(graph, q, fingerprint=False, count_ahead=False).count == cnt
+            for W_ in (2, 3):   # sharded at the count-ahead level at the latest
+                assert sum(gsi.query(graph, q, fingerprint=False, shard_rank=r_, shard_count=W_).count
+                           for r_ in range(W_)) == cnt
+            assert gsi.query(graph, q, fingerprint=False, chunk_slots=4096).count == cnt
+            try:
+                hc = oracle.match(og, q, table=False, hom=True, timeout=20.0)[0]
+            except oracle.OracleError:
+                continue
+            assert gsi.query(graph, q, fingerprint=False, homomorphism=True).count == hc
+    assert seen >= 4

@@ -1,0 +1,3 @@
+set -x
+python -m pytest tests -m gpu -x -q --timeout 900 -k "count_ahead or large_counts or medium or chunked or sharding" 2>&1 | tail -15
+timeout 900 python tools/profile_query.py --config C5m --qidx 0 2 3 7 11 13 19 --reps 2 --no-fp 2>&1 | cut -c1-900
