@@ -26,6 +26,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -85,6 +87,8 @@ struct StepParams {
                                  //   run of x = (prefiltered ci)[p] (null: probe PCSR per new row)
     const uint32_t *cu;          // (as the counted final step of J_CAHEAD) C(u) bitmap ...
     const int32_t *fci;          //   ... and the shared N(v,l0) ∩ C(u) runs of P(G,l0)
+    int out_w;                   // J_NEXT: stored columns of a new row (count-only: live ones)
+    int out_src[GSI_MAX_K];      //   ... column j = parent column out_src[j], or x if < 0
 };
 
 // Counters shared by the kernels of one query (device).
@@ -820,11 +824,12 @@ __global__ void __launch_bounds__(kThreads, join_items(MODE) > 8 ? 2 : (((MODE =
                 }
             }
             // ---- coalesced write of the contiguous block of new rows ------------------------
-            const int W = P.t + 1;
+            const int W = P.out_w;
             int32_t *o = out + base * (unsigned long long)W;
             for (unsigned e = tid; e < cnt * (unsigned)W; e += kThreads) {
                 const unsigned r = e / W, c = e - r * W;
-                o[e] = (int)c < P.t ? __ldg(M + (long long)si[r] * P.t + c) : (int32_t)sx[r];
+                const int src = P.out_src[c];
+                o[e] = src >= 0 ? __ldg(M + (long long)si[r] * P.t + src) : (int32_t)sx[r];
             }
             if (tile == gridDim.x - 1 && tid == 0) {
                 ctr->total = base + cnt;
@@ -1291,6 +1296,7 @@ struct Prof {
         launches[cls]++;
         if (!on) return;
         Rec r{cls, nullptr, nullptr};
+        host_t.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count() - host_base);
         cudaEventCreate(&r.a);
         cudaEventCreate(&r.b);
         cudaEventRecord(r.a, st);
@@ -1299,12 +1305,34 @@ struct Prof {
     void end() {
         if (on && !recs.empty()) cudaEventRecord(recs.back().b, st);
     }
+    cudaEvent_t base = nullptr;
+    double host_base = 0;
+    std::vector<double> host_t;   // host time (ms since base) of every begin(), GSI_TRACE
+    void start() {
+        if (!on) return;
+        cudaEventCreate(&base);
+        cudaEventRecord(base, st);
+        host_base = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    }
     void finish(gsi_stats *s) {
         for (int c = 0; c < GSI_N_KCLASS; c++) {
             s->launches[c] = launches[c];
             s->ms_kernel[c] = 0.f;
         }
         s->total_launches = total;
+        if (on && base && getenv("GSI_TRACE")) {   // GPU timeline: kernel class, start, end, gap (ms)
+            float prev_end = 0.f;
+            for (size_t i = 0; i < recs.size(); i++) {
+                float a = 0.f, b = 0.f;
+                cudaEventElapsedTime(&a, base, recs[i].a);
+                cudaEventElapsedTime(&b, base, recs[i].b);
+                fprintf(stderr, "[trace] %3zu cls %d host %.3f start %.3f end %.3f dur %.3f gap %.3f\n", i,
+                        recs[i].cls, i < host_t.size() ? host_t[i] : -1.0, a, b, b - a, a - prev_end);
+                prev_end = b;
+            }
+        }
+        if (base) cudaEventDestroy(base);
+        base = nullptr;
         for (auto &r : recs) {
             float ms = 0.f;
             if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) s->ms_kernel[r.cls] += ms;
@@ -1621,9 +1649,51 @@ struct QueryCtx {
     std::vector<std::pair<int32_t *, unsigned long long>> pieces;   // final table pieces (device)
     std::vector<std::pair<uint32_t *, int32_t *>> filt;             // per step: (fpos, fci) or null
     std::vector<Loc *> pa;                                           // per step: probe-ahead table or null
+    // Stored columns.  Count-only mode stores in M_t only the columns a later step reads (its
+    // linking columns and subtraction columns); phys[t][c] = position of logical column c in
+    // a row of M_t (-1: dropped), width[t] = stored columns.  Table / fingerprint: all.
+    std::vector<std::vector<int>> phys;
+    std::vector<int> width;
 };
 
-void fill_params(QueryCtx &C, const Step &s, StepParams &P) {
+// Columns of M a step reads: linking columns and (isomorphism) the subtraction columns, i.e.
+// the earlier columns with u's vertex label that are not linked (x in N(m[c],l) => x != m[c]).
+static void step_reads(const QueryCtx &C, const Step &s, std::vector<int> &cols) {
+    cols.assign(s.col.begin(), s.col.end());
+    if (C.opts.homomorphism) return;
+    for (int c = 0; c < s.t; c++) {
+        if (C.q->qvl[C.order[c]] != C.q->qvl[s.u]) continue;
+        bool linked = false;
+        for (int lc : s.col) linked |= lc == c;
+        if (!linked) cols.push_back(c);
+    }
+}
+
+void plan_layout(QueryCtx &C, bool project) {
+    const int k = C.q->k;
+    C.phys.assign(k + 1, std::vector<int>(k + 1, -1));
+    C.width.assign(k + 1, 0);
+    std::vector<int> need(k + 1, 0);   // need[c] = largest step t (columns before it) reading c
+    std::vector<int> cols;
+    for (auto &s : C.steps) {
+        step_reads(C, s, cols);
+        for (int c : cols) need[c] = std::max(need[c], s.t);
+    }
+    for (int t = 1; t <= k; t++) {
+        int w = 0;
+        for (int c = 0; c < t; c++)
+            if (!project || need[c] >= t) C.phys[t][c] = w++;
+        C.width[t] = w;
+    }
+}
+
+// Logical column c of a row of M_{lt+1} = m ‖ x read through M_lt's layout: x (c == lt) is
+// the sentinel width[lt] ("the vertex being added"), others their stored position.
+static int to_phys(const QueryCtx &C, int lt, int c) {
+    return c == lt ? C.width[lt] : C.phys[lt][c];
+}
+
+void fill_params(QueryCtx &C, const Step &s, StepParams &P, int lt) {
     const gsi_graph *g = C.g;
     std::memset(&P, 0, sizeof(P));
     const int E = (int)s.col.size();
@@ -1654,6 +1724,17 @@ void fill_params(QueryCtx &C, const Step &s, StepParams &P) {
         }
     }
     P.stage_inj = P.stage_base ? std::min(P.n_inj, GSI_STAGE_INJ) : 0;
+    // columns in the layout of M_lt (lt = s.t: this step's own level; lt = s.t - 1: the step
+    // seen from the level before it, where its column s.t - 1 is that level's new vertex)
+    P.t = C.width[lt];
+    for (int e = 0; e < E; e++) P.col[e] = to_phys(C, lt, P.col[e]);
+    for (int c = 0; c < P.n_inj; c++) P.inj_col[c] = to_phys(C, lt, P.inj_col[c]);
+    // the row this step produces (J_NEXT): the columns M_{s.t+1} stores
+    P.out_w = 0;
+    if (lt == s.t && s.t + 1 <= C.q->k) {
+        for (int c = 0; c <= s.t; c++)
+            if (C.phys[s.t + 1][c] >= 0) P.out_src[P.out_w++] = c < s.t ? C.phys[s.t][c] : -1;
+    }
 }
 
 // Build (once per query step) N(v,l0) ∩ C(u) for every run of P(G,l0): fpos + fci.
@@ -1719,8 +1800,8 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
     cudaStream_t st = C.st;
     const gsi_graph *g = C.g;
     StepParams P, P2;
-    fill_params(C, s, P);
-    if (!last) fill_params(C, C.steps[si + 1], P2);
+    fill_params(C, s, P, t);
+    if (!last) fill_params(C, C.steps[si + 1], P2, t);
     else std::memset(&P2, 0, sizeof(P2));
     const int E = P.E;
     if (S.levels < t) S.levels = t;
@@ -1819,7 +1900,7 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         unsigned long long *F2 = nullptr;
         if (mode == J_TABLE) GSI_TRY(A.get(&out, slots * (unsigned long long)C.q->k));
         if (mode == J_NEXT) {
-            GSI_TRY(A.get(&out, slots * (unsigned long long)(t + 1)));
+            GSI_TRY(A.get(&out, slots * (unsigned long long)std::max(P.out_w, 1)));
             GSI_TRY(A.get(&loc2, slots * (unsigned long long)P2.E));
             GSI_TRY(A.get(&F2, slots + 1));   // F2[0..nout] written by the kernel
         }
@@ -1852,7 +1933,7 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         // re-scan its candidate runs often enough to pay one probe per candidate
         P.pa = nullptr;
         if ((mode == J_NEXT || mode == J_CAHEAD) && P.prefiltered && P2.prefiltered && P2.E == 1 &&
-            P2.col[0] == t && GSI_PROBE_AHEAD > 0) {
+            P2.col[0] == P.t && GSI_PROBE_AHEAD > 0) {
             const uint32_t plo = g->ci_lo[P.lab[0]], phi = g->ci_lo[P.lab[0] + 1];
             if ((C.pa.size() > si && C.pa[si]) ||
                 slots >= (unsigned long long)GSI_PROBE_AHEAD * (unsigned long long)(phi - plo)) {
@@ -1893,9 +1974,9 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         A.release(rowmap);
         const unsigned long long nout = (mode == J_COUNT || mode == J_CAHEAD) ? hc.count : hc.total;   // J_NEXT: stored rows
         const double frac = gba ? (double)slots / (double)gba : 0.0;
-        double jb = frac * (4.0 * t * active + 4.0 * elems + (8.0 * E + 8.0) * active);
+        double jb = frac * (4.0 * P.t * active + 4.0 * elems + (8.0 * E + 8.0) * active);
         if (mode == J_TABLE) jb += 4.0 * C.q->k * nout;
-        if (mode == J_NEXT) jb += nout * (4.0 * (t + 1) + 16.0 * P2.E + 8.0);
+        if (mode == J_NEXT) jb += nout * (4.0 * P.out_w + 16.0 * P2.E + 8.0);
         if (mode == J_NEXT) S.rows[t] += hc.count;   // |M_{t+1}|: every survivor, stored or not
         if (mode == J_CAHEAD) {                        // survivors = |M_{t+1}|, counted = |M_{t+2}|
             jb += 8.0 * hc.total;                      // locate of the last step's run per survivor
@@ -1969,6 +2050,7 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     Prof prof;
     prof.on = opts.profile != 0;
     prof.st = st;
+    prof.start();
     C.g = g;
     C.q = q;
     C.st = st;
@@ -2023,6 +2105,7 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     }
     C.pos_of_q.assign(k, 0);
     for (int j = 0; j < k; j++) C.pos_of_q[C.order[j]] = j;
+    plan_layout(C, !opts.want_table && !opts.fingerprint);
     const double t_plan = now_ms();
     S.ms_plan = (float)(t_plan - t_filter);
 
@@ -2115,7 +2198,7 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     } else if (!empty) {
         // level-1 Prealloc (Alg. 4) on M_1 = C(pi_1)
         StepParams P;
-        fill_params(C, C.steps[0], P);
+        fill_params(C, C.steps[0], P, 1);
         Loc *loc = nullptr;
         unsigned long long *F = nullptr, *status = nullptr;
         GSI_TRY(A.get(&loc, std::max<unsigned long long>(nM, 1) * (unsigned long long)P.E));

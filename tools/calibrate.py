@@ -22,6 +22,7 @@ ap.add_argument("--nle", type=int, default=None)
 ap.add_argument("--queries", type=int, default=20)
 ap.add_argument("--k", type=int, default=12)
 ap.add_argument("--timeout", type=float, default=10.0)
+ap.add_argument("--fp", action="store_true", help="fingerprint on: enumerate every match")
 a = ap.parse_args()
 over = {}
 if a.scale:
@@ -42,7 +43,7 @@ print(f"build {time.time() - t:.2f}s {graph.info()}", flush=True)
 tot_c, tot_ms = 0, 0.0
 for i, q in enumerate(qs):
     t = time.time()
-    r = gsi.query(graph, q, timeout_s=a.timeout, partial_on_timeout=True)
+    r = gsi.query(graph, q, timeout_s=a.timeout, partial_on_timeout=True, fingerprint=a.fp)
     torch.cuda.synchronize()
     ms = 1000 * (time.time() - t)
     s = r.stats()
