@@ -50,6 +50,9 @@ constexpr int kThreads = 256;
 #ifndef GSI_PROBE_AHEAD
 #define GSI_PROBE_AHEAD 2   // build a step's probe-ahead table when its slots >= 2x its partition (0: off)
 #endif
+#ifndef GSI_CAHEAD_WARP
+#define GSI_CAHEAD_WARP 1   // count-ahead on shared lists: warp-centric kernel (0: slot tiles)
+#endif
 #ifndef GSI_FAST_ITEMS
 #define GSI_FAST_ITEMS 16   // slots per thread of the lean count-only kernel (0: never use it)
 #endif
@@ -947,6 +950,154 @@ __global__ void __launch_bounds__(kThreads, 4) k_count_fast(const int32_t *__res
     if (lane == 0 && c64) atomicAdd(&ctr->count, c64);
 }
 
+// Count-ahead, warp-centric (rows on shared candidate runs, which are short): a warp takes 32
+// consecutive rows, scans their buffer lengths with shuffles and walks the concatenated slots
+// 32 at a time; the owner of slot j is the first lane whose inclusive length exceeds j (a
+// 5-step shuffle search), and the owner's row data (run offset, subtraction columns, the last
+// step's row-constant subtraction vertices) travel by shuffle.  No shared memory, no block
+// barriers, no F reads: per row only loc and the needed columns, per slot the candidate,
+// its probe-ahead entry and the tests.  Same arithmetic as k_join<J_CAHEAD>.
+constexpr int kCaReg = 4;   // subtraction columns held in registers (more are read from M)
+__device__ __forceinline__ bool in_bitmap(const uint32_t *__restrict__ bm, int32_t v) {
+    return (__ldg(bm + ((uint32_t)v >> 5)) >> (v & 31)) & 1u;
+}
+__global__ void __launch_bounds__(kThreads, 4) k_cahead_warp(const int32_t *__restrict__ M, long long r0, long long r1,
+                                                             const Loc *__restrict__ loc, StepParams P, StepParams P2,
+                                                             const int32_t *__restrict__ cip,
+                                                             const uint32_t *__restrict__ cu_bitmap,
+                                                             const uint2 *__restrict__ groups, int gpn, Counters *ctr) {
+    const int lane = threadIdx.x & 31;
+    const long long gw = (blockIdx.x * (long long)kThreads + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * kThreads) >> 5;
+    const unsigned E = (unsigned)P.E;
+    const int ninj = P.n_inj, ninj2 = P2.n_inj;
+    // The last step links to a column of the parent row (not to the vertex this step adds):
+    // its run R and every row-column subtraction hit are constant per row, so a survivor x
+    // only costs the test "x in R" (when x itself is a subtraction column of the last step).
+    const bool rowR = P2.col[0] < P.t;
+    bool xinj = false;
+    for (int c = 0; c < ninj2; c++) xinj |= P2.inj_col[c] >= P.t;
+    unsigned long long cnt = 0, surv = 0, bound = 0;
+    for (long long base = r0 + gw * 32; base < r1; base += nw * 32) {
+        const long long i = base + lane;
+        const bool valid = i < r1;
+        const Loc L = valid ? loc[(unsigned long long)i * E] : Loc{0u, 0u};
+        const int32_t *row = M + (unsigned long long)(valid ? i : r0) * (unsigned)P.t;
+        int32_t inj[kCaReg], y2[kCaReg];
+#pragma unroll
+        for (int c = 0; c < kCaReg; c++) inj[c] = (valid && c < ninj) ? __ldg(row + P.inj_col[c]) : -1;
+        Loc RR{0u, 0u};
+        uint32_t rbase = 0;
+#pragma unroll
+        for (int c = 0; c < kCaReg; c++) y2[c] = -1;
+        if (rowR) {
+            if (valid && L.len) {
+                RR = pcsr_lookup(groups, gpn, P2.gbase[0], P2.ngroups[0], P2.lab[0], (uint32_t)__ldg(row + P2.col[0]), nullptr);
+                if (RR.len) {
+                    const uint32_t a = __ldg(P2.fpos + (RR.off - P2.flo)), b = __ldg(P2.fpos + (RR.off + RR.len - P2.flo));
+                    RR = Loc{a, b - a};
+                }
+                rbase = RR.len;
+                for (int c = 0; c < ninj2 && rbase; c++) {
+                    if (P2.inj_col[c] >= P.t) continue;
+                    const int32_t y = __ldg(row + P2.inj_col[c]);
+                    if (in_bitmap(P2.cu, y) && in_sorted(P2.fci + RR.off, RR.len, y)) rbase--;
+                }
+            }
+        } else {
+            // the last step's subtraction vertices that are columns of this row: their C(u_k)
+            // bit is tested once here (-1: cannot be in any candidate run)
+#pragma unroll
+            for (int c = 0; c < kCaReg; c++) {
+                if (valid && c < ninj2 && P2.inj_col[c] < P.t) {
+                    const int32_t y = __ldg(row + P2.inj_col[c]);
+                    if (in_bitmap(P2.cu, y)) y2[c] = y;
+                }
+            }
+        }
+        uint32_t inc = L.len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        const uint32_t excl = inc - L.len;
+        const uint32_t T = __shfl_sync(0xffffffffu, inc, 31);
+        for (uint32_t j0 = 0; j0 < T; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            int o = 0;   // owner = number of lanes whose inclusive length is <= j
+#pragma unroll
+            for (int st = 16; st > 0; st >>= 1) {
+                const uint32_t v = __shfl_sync(0xffffffffu, inc, o + st - 1);
+                if (v <= j) o += st;
+            }
+            o &= 31;
+            const uint32_t off = __shfl_sync(0xffffffffu, L.off, o);
+            const uint32_t ex = __shfl_sync(0xffffffffu, excl, o);
+            int32_t ri[kCaReg], ry[kCaReg];
+#pragma unroll
+            for (int c = 0; c < kCaReg; c++) {
+                ri[c] = __shfl_sync(0xffffffffu, inj[c], o);
+                ry[c] = __shfl_sync(0xffffffffu, y2[c], o);
+            }
+            const uint32_t roff = __shfl_sync(0xffffffffu, RR.off, o), rlen = __shfl_sync(0xffffffffu, RR.len, o);
+            const uint32_t rb = __shfl_sync(0xffffffffu, rbase, o);
+            if (j >= T) continue;
+            const unsigned long long ri_row = (unsigned long long)(base + o);
+            const uint32_t pos = off + (j - ex);
+            const int32_t x = __ldg(cip + pos);
+            bool keep = true;
+            if (!P.prefiltered) keep = in_bitmap(cu_bitmap, x);
+#pragma unroll
+            for (int c = 0; c < kCaReg; c++) keep &= ri[c] != x;
+            for (int c = kCaReg; c < ninj && keep; c++) keep = __ldg(M + ri_row * (unsigned)P.t + P.inj_col[c]) != x;
+            for (unsigned e = 1; e < E && keep; e++) {
+                const Loc Le = loc[ri_row * E + e];
+                keep = in_sorted(cip + Le.off, Le.len, x);
+            }
+            if (!keep) continue;
+            surv++;
+            if (rowR) {
+                bound += rlen;
+                uint32_t cc = rb;
+                if (xinj && cc && in_bitmap(P2.cu, x) && in_sorted(P2.fci + roff, rlen, x)) cc--;
+                cnt += cc;
+                continue;
+            }
+            Loc R;
+            if (P.pa) {
+                R = P.pa[pos];
+            } else {
+                R = pcsr_lookup(groups, gpn, P2.gbase[0], P2.ngroups[0], P2.lab[0], (uint32_t)x, nullptr);
+                if (R.len) {
+                    const uint32_t a = __ldg(P2.fpos + (R.off - P2.flo)), b = __ldg(P2.fpos + (R.off + R.len - P2.flo));
+                    R = Loc{a, b - a};
+                }
+            }
+            bound += R.len;
+            uint32_t cc = R.len;
+#pragma unroll
+            for (int c = 0; c < kCaReg; c++) {
+                if (c >= ninj2 || !cc) break;
+                if (ry[c] >= 0 && in_sorted(P2.fci + R.off, R.len, ry[c])) cc--;
+            }
+            for (int c = kCaReg; c < ninj2 && cc; c++) {
+                const int32_t y = __ldg(M + ri_row * (unsigned)P.t + P2.inj_col[c]);
+                if (in_bitmap(P2.cu, y) && in_sorted(P2.fci + R.off, R.len, y)) cc--;
+            }
+            cnt += cc;
+        }
+    }
+    cnt = warp_sum_u64(cnt);
+    surv = warp_sum_u64(surv);
+    bound = warp_sum_u64(bound);
+    if (lane == 0) {
+        if (cnt) atomicAdd(&ctr->count, cnt);
+        if (surv) atomicAdd(&ctr->total, surv);
+        if (bound) atomicAdd(&ctr->total2, bound);
+    }
+}
+
 constexpr int kFastItems = GSI_FAST_ITEMS > 0 ? GSI_FAST_ITEMS : 8;
 
 // Dynamic shared memory of a join launch: the larger of the staging region (row markers,
@@ -1401,6 +1552,12 @@ unsigned long long available_bytes(int dev) {
     return (unsigned long long)fr + (reserved > used ? reserved - used : 0);
 }
 
+// Test / A-B switches read per query (never needed in production).
+bool env_flag(const char *name) {
+    const char *e = getenv(name);
+    return e && e[0] == '1';
+}
+
 double now_ms() {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -1852,6 +2009,7 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
 
     // ---- shard this level's slot range ----
     unsigned long long s0 = 0, s1 = gba;
+    long long r_lo = 0, r_hi = (long long)nM;   // rows of this level that are ours
     if (!C.sharded && (nM >= C.shard_min || gba > C.cap_slots || last || cahead)) {
         long long *bounds = nullptr;
         GSI_TRY(A.get(&bounds, 4));
@@ -1864,6 +2022,8 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         A.release(bounds);
         s0 = (unsigned long long)hb[2];
         s1 = (unsigned long long)hb[3];
+        r_lo = hb[0];
+        r_hi = hb[1];
         S.shard_level = t;
         S.shard_row_begin = (uint64_t)hb[0];
         S.shard_row_end = (uint64_t)hb[1];
@@ -1949,7 +2109,14 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
                                                                                        tile_slots, rowmap);
         prof.end();
         prof.begin(GSI_K_JOIN);
-        if (fast) {
+        if (mode == J_CAHEAD && P.prefiltered && GSI_CAHEAD_WARP && !env_flag("GSI_CAHEAD_TILE")) {
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
+            const unsigned long long units = ((unsigned long long)(r_hi - r_lo) + 31) / 32;
+            const unsigned wg = (unsigned)std::max<unsigned long long>(
+                1, std::min<unsigned long long>((units + 7) / 8, (unsigned long long)sms * 8));
+            k_cahead_warp<<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, P2, cip, cu, g->groups, g->gpn, lctr);
+        } else if (fast) {
             const size_t fsm = (size_t)tile_slots * 4 * (2 + (size_t)std::min(P.n_inj, P.stage_inj));
             k_count_fast<kFastItems><<<jt, kThreads, fsm, st>>>(M, (long long)nM, F, loc, rowmap, P, cip, c0, c1,
                                                                     lctr);

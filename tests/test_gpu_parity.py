@@ -410,10 +410,13 @@ def test_timeout_partial_prefix():
     assert e.value.status == "GSI_ERR_TIMEOUT"
 
 
-def test_count_ahead_matches_oracle():
+@pytest.mark.parametrize("tile", [False, True])
+def test_count_ahead_matches_oracle(tile, monkeypatch):
     """Count-only mode counts the last level from the level before it (|N(v,l0) ∩ C(u)| minus
     the row's own vertices in that run, Alg. 3 lines 9-10) — same count as the oracle and as
-    enumerating every match; few vertex labels make the subtraction columns many."""
+    enumerating every match; few vertex labels make the subtraction columns many.  Both
+    count-ahead kernels: warp-centric (default on shared runs) and the slot-tiled k_join."""
+    monkeypatch.setenv("GSI_CAHEAD_TILE", "1" if tile else "0")
     seen = 0
     for gs, nlv, nle, k in [(81, 1, 2, 6), (82, 2, 3, 7), (83, 3, 4, 6), (84, 2, 1, 5)]:
         g = W.chung_lu(4000, 30000, 500, nlv=nlv, nle=nle, seed=gs)
