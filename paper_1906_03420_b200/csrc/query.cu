@@ -53,6 +53,9 @@ constexpr int kThreads = 256;
 #ifndef GSI_CAHEAD_WARP
 #define GSI_CAHEAD_WARP 1   // count-ahead on shared lists: warp-centric kernel (0: slot tiles)
 #endif
+#ifndef GSI_STAGE_NEXT
+#define GSI_STAGE_NEXT 1    // J_NEXT: stage a row-constant next-step run per tile row
+#endif
 #ifndef GSI_FAST_ITEMS
 #define GSI_FAST_ITEMS 16   // slots per thread of the lean count-only kernel (0: never use it)
 #endif
@@ -90,6 +93,10 @@ struct StepParams {
                                  //   run of x = (prefiltered ci)[p] (null: probe PCSR per new row)
     const uint32_t *cu;          // (as the counted final step of J_CAHEAD) C(u) bitmap ...
     const int32_t *fci;          //   ... and the shared N(v,l0) ∩ C(u) runs of P(G,l0)
+    int stage_next;              // J_NEXT: the next step's run is row-constant (links to a parent
+                                 //   column): located once per tile row into shared memory
+    int no_f2;                   // J_NEXT: the next level walks rows without F (warp count-ahead):
+                                 //   skip F' and its look-back chain, only total them
     int out_w;                   // J_NEXT: stored columns of a new row (count-only: live ones)
     int out_src[GSI_MAX_K];      //   ... column j = parent column out_src[j], or x if < 0
 };
@@ -399,7 +406,13 @@ template <int IT>
 __device__ __forceinline__ void next_step_locs(const StepParams &P, const StepParams &P2, const int32_t *__restrict__ M,
                                                const uint32_t (&rows)[IT], const uint32_t (&xs)[IT],
                                                const uint32_t (&cio)[IT], const bool (&keep)[IT],
-                                               const uint2 *__restrict__ groups, int gpn, Loc (&N0)[IT]) {
+                                               const uint2 *__restrict__ groups, int gpn, Loc (&N0)[IT],
+                                               const Loc *sNext = nullptr, long long rlo = 0) {
+    if (sNext) {   // row-constant: staged per tile row
+#pragma unroll
+        for (int it = 0; it < IT; it++) N0[it] = keep[it] ? sNext[rows[it] - rlo] : Loc{0u, 0u};
+        return;
+    }
     if (P.pa) {
 #pragma unroll
         for (int it = 0; it < IT; it++) N0[it] = keep[it] ? P.pa[cio[it]] : Loc{0u, 0u};
@@ -491,6 +504,7 @@ __global__ void __launch_bounds__(kThreads, join_items(MODE) > 8 ? 2 : (((MODE =
     int *sR = reinterpret_cast<int *>(dsm);
     uint32_t *sBase = reinterpret_cast<uint32_t *>(sR + TILE);
     int32_t *sInjBase = reinterpret_cast<int32_t *>(sBase + TILE);
+    Loc *sNext = reinterpret_cast<Loc *>(sInjBase + (size_t)P.stage_inj * TILE);   // [TILE / GSI_STAGE_DIV]
     uint32_t *sx = reinterpret_cast<uint32_t *>(dsm);
     uint32_t *si = sx + TILE;
     Loc *sloc = reinterpret_cast<Loc *>(si + TILE);
@@ -528,6 +542,19 @@ __global__ void __launch_bounds__(kThreads, join_items(MODE) > 8 ? 2 : (((MODE =
             sBase[r] = loc[i * (unsigned)P.E].off - (uint32_t)a;
             const int32_t *row = M + i * (unsigned)P.t;
             for (int c = 0; c < n_inj_st; c++) sInjBase[c * TILE + r] = __ldg(row + P.inj_col[c]);
+            if (MODE == J_NEXT && P.stage_next) {
+                Loc R = Loc{0u, 0u};
+                if (a < b) {
+                    R = pcsr_lookup(groups, gpn, P2.gbase[0], P2.ngroups[0], P2.lab[0], (uint32_t)__ldg(row + P2.col[0]),
+                                    nullptr);
+                    if (P2.prefiltered && R.len) {
+                        const uint32_t fa = __ldg(P2.fpos + (R.off - P2.flo));
+                        const uint32_t fb = __ldg(P2.fpos + (R.off + R.len - P2.flo));
+                        R = Loc{fa, fb - fa};
+                    }
+                }
+                sNext[r] = R;
+            }
         }
     }
     __syncthreads();
@@ -679,7 +706,8 @@ __global__ void __launch_bounds__(kThreads, join_items(MODE) > 8 ? 2 : (((MODE =
             all = warp_sum_u64(all);
             if (lane == 0 && all) atomicAdd(&ctr->count, all);      // |M_{t+1}| including dead rows
             if (P2.E == 1) {
-                next_step_locs<IT>(P, P2, M, rows, xs, cio, keep, groups, gpn, N0);
+                next_step_locs<IT>(P, P2, M, rows, xs, cio, keep, groups, gpn, N0,
+                                   (P.stage_next && staged) ? sNext : nullptr, rlo);
 #pragma unroll
                 for (int it = 0; it < IT; it++) keep[it] = keep[it] && N0[it].len > 0;
             } else {
@@ -744,10 +772,14 @@ __global__ void __launch_bounds__(kThreads, join_items(MODE) > 8 ? 2 : (((MODE =
         } else if (MODE == J_NEXT && warp == 1) {
             unsigned long long tl = lane < kThreads / 32 ? sm[lane] : 0ull;
             tl = warp_sum_u64(tl);
-            const unsigned long long pre2 = lookback_exclusive(status2, tile, tl);
-            if (lane == 0) {
-                base2_s = pre2;
-                sm[32] = tl;
+            if (P.no_f2) {
+                if (lane == 0 && tl) atomicAdd(&ctr->total2, tl);
+            } else {
+                const unsigned long long pre2 = lookback_exclusive(status2, tile, tl);
+                if (lane == 0) {
+                    base2_s = pre2;
+                    sm[32] = tl;
+                }
             }
         }
         __syncthreads();
@@ -807,23 +839,29 @@ __global__ void __launch_bounds__(kThreads, join_items(MODE) > 8 ? 2 : (((MODE =
             if (lane == 0 && elems) atomicAdd(&ctr->list_elems, elems);
             // next F over the tile's stored rows (thread tid owns rows [8 tid, 8 tid + 8));
             // the tile's offset base2_s came from the second look-back chain above
-            unsigned long long mine = 0;
+            if (!P.no_f2) {
+                unsigned long long mine = 0;
 #pragma unroll
-            for (int q = 0; q < IT; q++) {
-                const unsigned j = tid * IT + q;
-                if (j < cnt) mine += sloc[j].len;
-            }
-            const unsigned long long agg2 = sm[32];
-            const unsigned long long pre2 = base2_s;
-            unsigned long long dummy;
-            const unsigned long long ex2 = block_exclusive_scan(mine, sm, &dummy);
-            unsigned long long run = pre2 + ex2;
+                for (int q = 0; q < IT; q++) {
+                    const unsigned j = tid * IT + q;
+                    if (j < cnt) mine += sloc[j].len;
+                }
+                const unsigned long long agg2 = sm[32];
+                const unsigned long long pre2 = base2_s;
+                unsigned long long dummy;
+                const unsigned long long ex2 = block_exclusive_scan(mine, sm, &dummy);
+                unsigned long long run = pre2 + ex2;
 #pragma unroll
-            for (int q = 0; q < IT; q++) {
-                const unsigned j = tid * IT + q;
-                if (j < cnt) {
-                    F2[base + j] = run;
-                    run += sloc[j].len;
+                for (int q = 0; q < IT; q++) {
+                    const unsigned j = tid * IT + q;
+                    if (j < cnt) {
+                        F2[base + j] = run;
+                        run += sloc[j].len;
+                    }
+                }
+                if (tile == gridDim.x - 1 && tid == 0) {
+                    ctr->total2 = pre2 + agg2;
+                    F2[base + cnt] = pre2 + agg2;
                 }
             }
             // ---- coalesced write of the contiguous block of new rows ------------------------
@@ -834,11 +872,7 @@ __global__ void __launch_bounds__(kThreads, join_items(MODE) > 8 ? 2 : (((MODE =
                 const int src = P.out_src[c];
                 o[e] = src >= 0 ? __ldg(M + (long long)si[r] * P.t + src) : (int32_t)sx[r];
             }
-            if (tile == gridDim.x - 1 && tid == 0) {
-                ctr->total = base + cnt;
-                ctr->total2 = pre2 + agg2;
-                F2[base + cnt] = pre2 + agg2;
-            }
+            if (tile == gridDim.x - 1 && tid == 0) ctr->total = base + cnt;
         }
     }
 }
@@ -1105,7 +1139,8 @@ constexpr int kFastItems = GSI_FAST_ITEMS > 0 ? GSI_FAST_ITEMS : 8;
 // uses: the rest of the 228 KB SM memory stays L1 cache for the ci / bitmap / row reads.
 inline size_t join_smem_bytes(int mode, const StepParams &P) {
     const size_t tile = (size_t)join_items(mode) * kThreads;
-    const size_t staging = tile * 4 * (1 + (P.stage_base ? 1 : 0) + (size_t)P.stage_inj);
+    const size_t staging = tile * 4 * (1 + (P.stage_base ? 1 : 0) + (size_t)P.stage_inj) +
+                           (P.stage_next ? tile / GSI_STAGE_DIV * sizeof(Loc) : 0);
     const size_t cache = (mode == J_COUNT || mode == J_CAHEAD) ? 0 : tile * 4 * 2 + (mode == J_NEXT ? tile * 8 : 0);
     return std::max(staging, cache);
 }
@@ -1264,6 +1299,29 @@ __global__ void __launch_bounds__(kThreads) k_refilter(Loc *__restrict__ loc, lo
         if (a1) atomicAdd(&ctr->active_rows, a1);
         if (e1) atomicAdd(&ctr->list_elems, e1);
     }
+}
+
+// F = exclusive scan of the buffer bounds loc[i*E].len (rows that arrived without F).
+__global__ void __launch_bounds__(kThreads) k_lens_scan(const Loc *__restrict__ loc, long long nM, int E,
+                                                        unsigned long long *__restrict__ F,
+                                                        unsigned long long *status, unsigned *tile_ctr) {
+    __shared__ unsigned long long sm[33];
+    __shared__ unsigned tile_s;
+    __shared__ unsigned long long base_s;
+    if (threadIdx.x == 0) tile_s = atomicAdd(tile_ctr, 1u);
+    __syncthreads();
+    const unsigned tile = tile_s;
+    const long long i = (long long)tile * kThreads + threadIdx.x;
+    const unsigned long long len0 = i < nM ? loc[(unsigned long long)i * E].len : 0ull;
+    unsigned long long agg;
+    const unsigned long long ex = block_exclusive_scan(len0, sm, &agg);
+    if (threadIdx.x < 32) {
+        const unsigned long long pre = lookback_exclusive(status, tile, agg);
+        if (threadIdx.x == 0) base_s = pre;
+    }
+    __syncthreads();
+    if (i < nM) F[i] = base_s + ex;
+    if (tile == gridDim.x - 1 && threadIdx.x == kThreads - 1) F[nM] = base_s + agg;
 }
 
 // Count + fingerprint of a table whose columns are in pi order (k = 1 queries).
@@ -1943,6 +2001,22 @@ bool shared_lists_allowed(const QueryCtx &C, const StepParams &P) {
     return GSI_PREFILTER_RATIO > 0 && !C.opts.no_shared_lists && C.opts.e0_mode == 0 && P.E == 1;
 }
 
+// F for rows whose producer skipped it (it expected the warp count-ahead, which needs none).
+gsi_status build_F(QueryCtx &C, const Loc *loc, unsigned long long nM, int E, unsigned long long **F) {
+    const unsigned rt = grid_for(nM, kThreads);
+    unsigned long long *rst = nullptr;
+    GSI_TRY(C.A->get(F, nM + 1));
+    GSI_TRY(C.A->get(&rst, (unsigned long long)rt + 1));
+    GSI_CUDA(cudaMemsetAsync(rst, 0, 8ull * (rt + 1), C.st));
+    C.prof->begin(GSI_K_OTHER);
+    k_lens_scan<<<rt, kThreads, 0, C.st>>>(loc, (long long)nM, E, *F, rst + 1, (unsigned *)rst);
+    C.prof->end();
+    C.S->alg_bytes[GSI_K_OTHER] += 16.0 * nM;
+    return GSI_OK;
+}
+
+bool cahead_warp_enabled() { return GSI_CAHEAD_WARP && !env_flag("GSI_CAHEAD_TILE"); }
+
 // Level t = steps[si].t: M (nM x t) with its Prealloc (loc, F, |GBA| = gba) already computed
 // (by k_probe for level 1, by the previous level's fused kernel otherwise).
 gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc *loc, unsigned long long *F,
@@ -2007,6 +2081,9 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
                                gba * (unsigned long long)GSI_PREFILTER_AHEAD >= (unsigned long long)(hi2 - lo2));
     }
 
+    // rows without F (see no_f2): build it unless the warp count-ahead consumes them as they are
+    if (!F && (!(cahead && P.prefiltered && cahead_warp_enabled()) || !C.sharded)) GSI_TRY(build_F(C, loc, nM, E, &F));
+
     // ---- shard this level's slot range ----
     unsigned long long s0 = 0, s1 = gba;
     long long r_lo = 0, r_hi = (long long)nM;   // rows of this level that are ours
@@ -2062,7 +2139,7 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         if (mode == J_NEXT) {
             GSI_TRY(A.get(&out, slots * (unsigned long long)std::max(P.out_w, 1)));
             GSI_TRY(A.get(&loc2, slots * (unsigned long long)P2.E));
-            GSI_TRY(A.get(&F2, slots + 1));   // F2[0..nout] written by the kernel
+            // F2[0..nout] written by the kernel (allocated below unless skipped)
         }
         // next step on shared lists? (its rows are produced here, so the probe-ahead can point
         // them at N(v,l0') ∩ C(u') directly and drop rows whose filtered run is empty)
@@ -2102,14 +2179,27 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
                 S.n_probe_ahead++;
             }
         }
+        // the next step's run is row-constant: locate it once per tile row
+        P.stage_next = mode == J_NEXT && P2.E == 1 && P2.col[0] < P.t && GSI_STAGE_NEXT;
+        // the next level is the count-ahead level on shared lists, walked by the warp kernel
+        // (no F needed): skip F' and its look-back chain
+        P.no_f2 = 0;
+        if (mode == J_NEXT && pf_next && si + 3 == C.steps.size() && !C.opts.want_table && !C.opts.fingerprint &&
+            !C.opts.no_count_ahead && !C.opts.no_shared_lists && C.opts.e0_mode == 0 &&
+            C.steps[si + 2].col.size() == 1 && cahead_warp_enabled() && C.sharded)
+            P.no_f2 = 1;
+        const bool warp_ca = mode == J_CAHEAD && P.prefiltered && cahead_warp_enabled();
         uint32_t *rowmap = nullptr;
-        GSI_TRY(A.get(&rowmap, (unsigned long long)jt + 1));
-        prof.begin(GSI_K_OTHER);
-        k_tile_rows<<<grid_for((unsigned long long)jt + 1, kThreads), kThreads, 0, st>>>(F, (long long)nM, c0, c1, jt,
-                                                                                       tile_slots, rowmap);
-        prof.end();
+        if (!warp_ca) {   // first/last row of every slot tile (the warp count-ahead walks rows)
+            GSI_TRY(A.get(&rowmap, (unsigned long long)jt + 1));
+            prof.begin(GSI_K_OTHER);
+            k_tile_rows<<<grid_for((unsigned long long)jt + 1, kThreads), kThreads, 0, st>>>(F, (long long)nM, c0, c1, jt,
+                                                                                           tile_slots, rowmap);
+            prof.end();
+        }
+        if (mode == J_NEXT && !P.no_f2) GSI_TRY(A.get(&F2, slots + 1));
         prof.begin(GSI_K_JOIN);
-        if (mode == J_CAHEAD && P.prefiltered && GSI_CAHEAD_WARP && !env_flag("GSI_CAHEAD_TILE")) {
+        if (warp_ca) {
             int sms = 148;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
             const unsigned long long units = ((unsigned long long)(r_hi - r_lo) + 31) / 32;
