@@ -238,6 +238,12 @@ gsi_status gsi_debug_query_signatures(int32_t k, const int32_t *q_vlabels, int32
                                       const int32_t *q_src, const int32_t *q_dst,
                                       const int32_t *q_elabels, int32_t distinct, uint32_t *qsig);
 
+/* ------------------------------------------------------------------ memory ---------- */
+/* Queries keep one device workspace per device between calls (a double-ended stack the
+ * level recursion carves; re-allocating it per level cost more than the kernels).  Free an
+ * idle workspace now (device -1 = current).  Graph builds do this themselves.  Never fails. */
+void gsi_trim_workspace(int32_t device);
+
 /* ------------------------------------------------------------------ misc ------------ */
 const char *gsi_last_error(void);
 const char *gsi_version(void);

@@ -73,6 +73,15 @@ void gsi_build_opts_default(gsi_build_opts *o) {
     o->stream = nullptr;
 }
 
+void gsi_trim_workspace(int32_t device) {
+    int dev = device;
+    if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    gsi::workspace_trim(dev);
+}
+
 void gsi_query_opts_default(gsi_query_opts *o) {
     if (!o) return;
     std::memset(o, 0, sizeof(*o));
@@ -194,6 +203,11 @@ gsi_status gsi_graph_alloc_like(const void *meta, uint64_t meta_bytes, const gsi
     p += 4ull * nl;
     g->ci_lo.resize(nl + 1);
     std::memcpy(g->ci_lo.data(), p, 4ull * (nl + 1));
+    {
+        int dev = 0;
+        GSI_CUDA(cudaGetDevice(&dev));
+        workspace_trim(dev);
+    }
     GSI_CUDA(cudaMalloc(&g->sig, std::max<uint64_t>(16, (uint64_t)g->n * kPlanes * 4)));
     GSI_CUDA(cudaMalloc(&g->groups, std::max<uint64_t>(16, (uint64_t)g->n_groups * g->gpn * 8)));
     GSI_CUDA(cudaMalloc(&g->ci, std::max<uint64_t>(16, (uint64_t)g->m * 8)));

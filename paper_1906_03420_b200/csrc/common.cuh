@@ -333,6 +333,9 @@ gsi_status cuda_fail(cudaError_t e, const char *what);
         if (_s != GSI_OK) return _s;         \
     } while (0)
 
+// Free the device's idle query workspace (query.cu); called before graph allocations.
+void workspace_trim(int dev);
+
 // Encode the query signatures on the host (same spec as the data side).
 void encode_query_signatures(int32_t k, const int32_t *qvl, int32_t qm, const int32_t *qs, const int32_t *qd,
                              const int32_t *qe, uint32_t *qsig /* k*16 */, int distinct);

@@ -313,6 +313,7 @@ gsi_status build_graph_impl(int64_t n, const int32_t *h_vl, int64_t m, const int
     int dev = opts && opts->device >= 0 ? opts->device : -1;
     if (dev >= 0) GSI_CUDA(cudaSetDevice(dev));
     GSI_CUDA(cudaGetDevice(&dev));
+    workspace_trim(dev);   // an idle query workspace must not starve the build
     cudaStream_t st = opts && opts->stream ? (cudaStream_t)opts->stream : cudaStreamPerThread;
 
     const int64_t E = 2 * m;

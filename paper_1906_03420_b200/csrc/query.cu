@@ -1414,39 +1414,87 @@ inline unsigned grid_for(unsigned long long n, int per) {
     return (unsigned)std::min<unsigned long long>(b, 0x7FFFFFFFull);
 }
 
-// Stream-ordered scratch; every allocation is released (stream-ordered) at scope exit.
-// Stream-ordered scratch.  Small buffers come from a per-query bump region (one pool
-// allocation; a level's buffers are released LIFO with mark()/reset(), safe because every
-// kernel of a query runs on one stream); large ones from cudaMallocAsync on the stream.
+// Per-device workspace: one plain allocation kept across queries and carved as a
+// double-ended stack.  The depth-first level recursion allocates LIFO (mark()/reset() per
+// chunk) from the bottom; query-lifetime buffers (shared candidate runs, probe-ahead tables)
+// come from the top.  Growing the stream-ordered pool by ~1 GB per level chunk cost 7-20 ms
+// of host time per allocation (physical mapping) — more than the kernels of a chunk.  A
+// query owns the workspace exclusively; a concurrent query on the same device falls back to
+// stream-ordered allocations.  Graph builds trim an idle workspace first.
+struct Workspace {
+    std::mutex mu;
+    char *base = nullptr;
+    size_t cap = 0;
+    size_t want = 64ull << 20;   // high-water demand of the queries so far (next size)
+    bool busy = false;
+};
+Workspace g_ws[64];
+
+}  // namespace
+
+void workspace_trim(int dev) {
+    if (dev < 0 || dev >= 64) return;
+    std::lock_guard<std::mutex> lk(g_ws[dev].mu);
+    if (g_ws[dev].busy || !g_ws[dev].base) return;
+    cudaFree(g_ws[dev].base);
+    g_ws[dev].base = nullptr;
+    g_ws[dev].cap = 0;
+    g_ws[dev].want = 64ull << 20;   // a new graph: learn its queries' demand afresh
+}
+
+namespace {
+
 struct Arena {
     cudaStream_t st;
     std::vector<void *> ptrs;
-    double ms_alloc = 0;   // host time in cudaMallocAsync (stats.ms_host_alloc)
+    double ms_alloc = 0;   // host time in allocation calls (stats.ms_host_alloc)
     char *bump = nullptr;
-    size_t cap = 0, off = 0;
+    size_t cap = 0, off = 0, top = 0;
+    int ws_dev = -1;       // >= 0: bump is that device's workspace
+    size_t live_fb = 0, demand = 0;   // live fallback bytes; high-water mark of all scratch
     explicit Arena(cudaStream_t s) : st(s) {}
-    gsi_status init_bump(size_t bytes) {
-        if (cudaMallocAsync((void **)&bump, bytes, st) != cudaSuccess) {
-            cudaGetLastError();
-            bump = nullptr;
-            return GSI_OK;   // optional: fall back to per-buffer allocations
+    void note() { demand = std::max(demand, off + (cap - top) + live_fb); }
+    // Take the device workspace, (re)sized to at least `bytes`; on any failure keep going
+    // with stream-ordered allocations only.
+    void init_workspace(int dev, size_t budget) {
+        if (dev < 0 || dev >= 64) return;
+        Workspace &W = g_ws[dev];
+        std::lock_guard<std::mutex> lk(W.mu);
+        if (W.busy) return;
+        const size_t bytes = std::min(budget, std::max(W.want, (size_t)64 << 20));
+        const auto t0 = std::chrono::steady_clock::now();
+        if (W.cap < bytes) {
+            if (W.base) cudaFree(W.base);
+            W.base = nullptr;
+            W.cap = 0;
+            cudaMemPool_t pool;   // hand pool-cached memory back to the driver first
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                cudaDeviceSynchronize();
+                cudaMemPoolTrimTo(pool, 0);
+            }
+            if (cudaMalloc((void **)&W.base, bytes) != cudaSuccess) {
+                cudaGetLastError();
+                W.base = nullptr;
+                return;
+            }
+            W.cap = bytes;
         }
-        cap = bytes;
-        return GSI_OK;
+        ms_alloc += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        W.busy = true;
+        ws_dev = dev;
+        bump = W.base;
+        cap = W.cap;
+        off = 0;
+        top = cap & ~(size_t)255;   // both stack ends stay 256 B aligned
     }
     template <typename T>
-    gsi_status get(T **p, unsigned long long count) {
-        const size_t bytes = (size_t)std::max<unsigned long long>(count, 1) * sizeof(T);
-        const size_t need = (bytes + 255) & ~(size_t)255;
-        if (bump && off + need <= cap) {
-            *p = (T *)(bump + off);
-            off += need;
-            return GSI_OK;
-        }
+    gsi_status fallback(T **p, size_t bytes) {
         void *q = nullptr;
         const auto t0 = std::chrono::steady_clock::now();
         cudaError_t e = cudaMallocAsync(&q, bytes, st);
-        ms_alloc += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        const double dt = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        ms_alloc += dt;
+        if (dt > 1.0 && getenv("GSI_TRACE")) fprintf(stderr, "[alloc] pool %zu bytes %.3f ms\n", bytes, dt);
         if (e == cudaErrorMemoryAllocation) {
             cudaGetLastError();
             set_error("device memory exhausted");
@@ -1454,39 +1502,60 @@ struct Arena {
         }
         if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
         ptrs.push_back(q);
+        sizes.push_back(bytes);
+        live_fb += bytes;
+        note();
         *p = (T *)q;
         return GSI_OK;
+    }
+    std::vector<size_t> sizes;
+    template <typename T>
+    gsi_status get(T **p, unsigned long long count) {   // scoped: freed by reset() / at exit
+        const size_t bytes = (size_t)std::max<unsigned long long>(count, 1) * sizeof(T);
+        const size_t need = (bytes + 255) & ~(size_t)255;
+        if (bump && off + need <= top) {
+            *p = (T *)(bump + off);
+            off += need;
+            note();
+            return GSI_OK;
+        }
+        if (bump) demand = std::max(demand, off + need + (cap - top) + live_fb);
+        return fallback(p, bytes);
     }
     template <typename T>
-    gsi_status get_big(T **p, unsigned long long count) {   // never from the bump region
-        void *q = nullptr;
-        const auto t0 = std::chrono::steady_clock::now();
-        cudaError_t e = cudaMallocAsync(&q, (size_t)std::max<unsigned long long>(count, 1) * sizeof(T), st);
-        ms_alloc += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-        if (e == cudaErrorMemoryAllocation) {
-            cudaGetLastError();
-            set_error("device memory exhausted");
-            return GSI_ERR_OOM;
+    gsi_status get_big(T **p, unsigned long long count) {   // query lifetime
+        const size_t bytes = (size_t)std::max<unsigned long long>(count, 1) * sizeof(T);
+        const size_t need = (bytes + 255) & ~(size_t)255;
+        if (bump && top >= off + need) {
+            top -= need;
+            *p = (T *)(bump + top);
+            note();
+            return GSI_OK;
         }
-        if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
-        ptrs.push_back(q);
-        *p = (T *)q;
-        return GSI_OK;
+        if (bump) demand = std::max(demand, off + need + (cap - top) + live_fb);
+        return fallback(p, bytes);
     }
+    size_t free_bytes() const { return bump ? top - off : 0; }
     size_t mark() const { return off; }
     void reset(size_t m) { off = m; }
     void release(void *p) {
-        if (!p || (bump && (char *)p >= bump && (char *)p < bump + cap)) return;   // bump: freed by reset()
-        for (auto &q : ptrs)
-            if (q == p) {
-                cudaFreeAsync(q, st);
-                q = nullptr;
+        if (!p || (bump && (char *)p >= bump && (char *)p < bump + cap)) return;   // workspace: reset()
+        for (size_t i = 0; i < ptrs.size(); i++)
+            if (ptrs[i] == p) {
+                cudaFreeAsync(ptrs[i], st);
+                ptrs[i] = nullptr;
+                live_fb -= sizes[i];
             }
     }
     ~Arena() {
         for (void *q : ptrs)
             if (q) cudaFreeAsync(q, st);
-        if (bump) cudaFreeAsync(bump, st);
+        if (ws_dev >= 0) {
+            cudaStreamSynchronize(st);   // nothing in flight may still use the workspace
+            std::lock_guard<std::mutex> lk(g_ws[ws_dev].mu);
+            g_ws[ws_dev].busy = false;
+            g_ws[ws_dev].want = std::max(g_ws[ws_dev].want, demand + demand / 8);
+        }
     }
 };
 
@@ -2316,10 +2385,17 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     C.S = &S;
     C.words = words;
 
-#ifndef GSI_BUMP_MB
-#define GSI_BUMP_MB 64
-#endif
-    if (GSI_BUMP_MB > 0) GSI_TRY(A.init_bump((size_t)GSI_BUMP_MB << 20));
+    // device memory the query may use; the workspace grows to the demand seen so far
+    unsigned long long budget = opts.mem_budget_bytes;
+    if (!budget) {
+        size_t idle = 0;
+        {
+            std::lock_guard<std::mutex> lk(g_ws[g->device].mu);
+            if (!g_ws[g->device].busy) idle = g_ws[g->device].cap;
+        }
+        budget = (unsigned long long)(0.85 * (double)(available_bytes(g->device) + idle));
+    }
+    A.init_workspace(g->device, budget);
     GSI_TRY(A.get(&C.ctr, 1));
     GSI_CUDA(cudaMemsetAsync(C.ctr, 0, sizeof(Counters), st));
 
@@ -2369,8 +2445,8 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     // memory budget -> chunk capacity in GBA slots (bytes per slot per level: S,R 8 B,
     // M' 4(t+1) B, the child level's loc/F 8E+8 B), over the k-1 levels that may nest.
     {
-        unsigned long long budget =
-            opts.mem_budget_bytes ? opts.mem_budget_bytes : (unsigned long long)(0.85 * available_bytes(g->device));
+        // (the chunk capacity depends on the budget only, never on the workspace size, so the
+        // chunking of a query is reproducible)
         int maxE = 1;
         for (auto &s : C.steps) maxE = std::max(maxE, (int)s.col.size());
         const double per_slot = 8.0 + 4.0 * (k + 1) + 8.0 * maxE + 8.0;

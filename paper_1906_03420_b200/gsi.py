@@ -83,6 +83,7 @@ _SIGS = {
     "gsi_prepared_free": (None, [P]),
     "gsi_result_count": (I32, [P, P]),
     "gsi_result_fingerprint": (I32, [P, P]),
+    "gsi_trim_workspace": (None, [I32]),
     "gsi_result_table": (I32, [P, P, P]),
     "gsi_result_copy_table": (I32, [P, P, U64]),
     "gsi_result_stats": (I32, [P, P]),
@@ -342,6 +343,10 @@ def gsi_debug_query_signatures(q_vlabels, q_src, q_dst, q_elabels, distinct: boo
                                           _ptr(out)),
            "gsi_debug_query_signatures")
     return out
+
+
+def gsi_trim_workspace(device: int = -1) -> None:
+    lib.gsi_trim_workspace(device)
 
 
 def gsi_last_error() -> str:
