@@ -53,6 +53,15 @@ constexpr int kThreads = 256;
 #ifndef GSI_CAHEAD_WARP
 #define GSI_CAHEAD_WARP 1   // count-ahead on shared lists: warp-centric kernel (0: slot tiles)
 #endif
+#ifndef GSI_CAHEAD_MINB
+#define GSI_CAHEAD_MINB 4   // k_cahead_warp: resident blocks per SM the registers are sized for
+#endif
+#ifndef GSI_CAHEAD_U
+#define GSI_CAHEAD_U 1      // k_cahead_warp: slots per lane per pass
+#endif
+#ifndef GSI_STAGE_ROWS
+#define GSI_STAGE_ROWS 1    // join tile staging: rows per thread per pass (loads phased together)
+#endif
 #ifndef GSI_STAGE_NEXT
 #define GSI_STAGE_NEXT 1    // J_NEXT: stage a row-constant next-step run per tile row
 #endif
@@ -534,27 +543,53 @@ __global__ void __launch_bounds__(kThreads, join_items(MODE) > 8 ? 2 : (((MODE =
     // Row of every slot of the tile without a per-slot search (load-balanced search): each row
     // overlapping the tile marks its first tile-local slot, then an inclusive max-scan over the
     // 2048 slots spreads the row offset to all its slots.
-    for (long long r = tid; r < nr; r += kThreads) {
-        const unsigned long long a = __ldg(F + rlo + r), b = __ldg(F + rlo + r + 1);
-        if (a < b && b > tbase && a < tend) sR[a > tbase ? (unsigned)(a - tbase) : 0u] = (int)r;
+    // two rows per thread per pass, phased so that both rows' dependent loads (F -> loc / row
+    // columns -> PCSR sector -> fpos) are in flight together
+    constexpr int RS = GSI_STAGE_ROWS;
+    for (long long r0 = tid; r0 < nr; r0 += RS * kThreads) {
+        long long rr[RS];
+        bool ok[RS];
+        unsigned long long a[RS], b[RS];
+#pragma unroll
+        for (int q = 0; q < RS; q++) {
+            rr[q] = r0 + q * kThreads;
+            ok[q] = rr[q] < nr;
+            a[q] = ok[q] ? __ldg(F + rlo + rr[q]) : 0ull;
+            b[q] = ok[q] ? __ldg(F + rlo + rr[q] + 1) : 0ull;
+        }
+#pragma unroll
+        for (int q = 0; q < RS; q++)
+            if (ok[q] && a[q] < b[q] && b[q] > tbase && a[q] < tend)
+                sR[a[q] > tbase ? (unsigned)(a[q] - tbase) : 0u] = (int)rr[q];
         if (staged) {
-            const unsigned long long i = (unsigned long long)(rlo + r);
-            sBase[r] = loc[i * (unsigned)P.E].off - (uint32_t)a;
-            const int32_t *row = M + i * (unsigned)P.t;
-            for (int c = 0; c < n_inj_st; c++) sInjBase[c * TILE + r] = __ldg(row + P.inj_col[c]);
-            if (MODE == J_NEXT && P.stage_next) {
-                Loc R = Loc{0u, 0u};
-                if (a < b) {
-                    R = pcsr_lookup(groups, gpn, P2.gbase[0], P2.ngroups[0], P2.lab[0], (uint32_t)__ldg(row + P2.col[0]),
-                                    nullptr);
-                    if (P2.prefiltered && R.len) {
-                        const uint32_t fa = __ldg(P2.fpos + (R.off - P2.flo));
-                        const uint32_t fb = __ldg(P2.fpos + (R.off + R.len - P2.flo));
-                        R = Loc{fa, fb - fa};
-                    }
-                }
-                sNext[r] = R;
+            uint32_t off[RS], vn[RS];
+            bool kn[RS];
+#pragma unroll
+            for (int q = 0; q < RS; q++) {
+                const unsigned long long i = (unsigned long long)(rlo + (ok[q] ? rr[q] : 0));
+                const int32_t *row = M + i * (unsigned)P.t;
+                off[q] = ok[q] ? loc[i * (unsigned)P.E].off : 0u;
+                for (int c = 0; c < n_inj_st; c++)
+                    if (ok[q]) sInjBase[c * TILE + rr[q]] = __ldg(row + P.inj_col[c]);
+                kn[q] = MODE == J_NEXT && P.stage_next && ok[q] && a[q] < b[q];
+                vn[q] = kn[q] ? (uint32_t)__ldg(row + P2.col[0]) : 0u;
             }
+            if (MODE == J_NEXT && P.stage_next) {
+                Loc R[RS];
+                pcsr_lookup_batch<RS>(groups, gpn, P2.gbase[0], P2.ngroups[0], P2.lab[0], vn, kn, R);
+#pragma unroll
+                for (int q = 0; q < RS; q++) {
+                    if (kn[q] && P2.prefiltered && R[q].len) {
+                        const uint32_t fa = __ldg(P2.fpos + (R[q].off - P2.flo));
+                        const uint32_t fb = __ldg(P2.fpos + (R[q].off + R[q].len - P2.flo));
+                        R[q] = Loc{fa, fb - fa};
+                    }
+                    if (ok[q]) sNext[rr[q]] = kn[q] ? R[q] : Loc{0u, 0u};
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < RS; q++)
+                if (ok[q]) sBase[rr[q]] = off[q] - (uint32_t)a[q];
         }
     }
     __syncthreads();
@@ -995,7 +1030,7 @@ constexpr int kCaReg = 4;   // subtraction columns held in registers (more are r
 __device__ __forceinline__ bool in_bitmap(const uint32_t *__restrict__ bm, int32_t v) {
     return (__ldg(bm + ((uint32_t)v >> 5)) >> (v & 31)) & 1u;
 }
-__global__ void __launch_bounds__(kThreads, 4) k_cahead_warp(const int32_t *__restrict__ M, long long r0, long long r1,
+__global__ void __launch_bounds__(kThreads, GSI_CAHEAD_MINB) k_cahead_warp(const int32_t *__restrict__ M, long long r0, long long r1,
                                                              const Loc *__restrict__ loc, StepParams P, StepParams P2,
                                                              const int32_t *__restrict__ cip,
                                                              const uint32_t *__restrict__ cu_bitmap,
@@ -1057,69 +1092,93 @@ __global__ void __launch_bounds__(kThreads, 4) k_cahead_warp(const int32_t *__re
         }
         const uint32_t excl = inc - L.len;
         const uint32_t T = __shfl_sync(0xffffffffu, inc, 31);
-        for (uint32_t j0 = 0; j0 < T; j0 += 32) {
-            const uint32_t j = j0 + lane;
-            int o = 0;   // owner = number of lanes whose inclusive length is <= j
+        // two slots per lane per pass (j and j + 32): their owner searches, candidate and
+        // probe-ahead loads are issued together
+        constexpr int U = GSI_CAHEAD_U;
+        for (uint32_t j0 = 0; j0 < T; j0 += 32 * U) {
+            uint32_t jj[U], pos[U], roff[U], rlen[U], rb[U];
+            int oo[U];
+            int32_t ri[U][kCaReg], ry[U][kCaReg];
 #pragma unroll
-            for (int st = 16; st > 0; st >>= 1) {
-                const uint32_t v = __shfl_sync(0xffffffffu, inc, o + st - 1);
-                if (v <= j) o += st;
-            }
-            o &= 31;
-            const uint32_t off = __shfl_sync(0xffffffffu, L.off, o);
-            const uint32_t ex = __shfl_sync(0xffffffffu, excl, o);
-            int32_t ri[kCaReg], ry[kCaReg];
+            for (int u = 0; u < U; u++) {
+                const uint32_t j = j0 + 32 * u + lane;
+                int o = 0;   // owner = number of lanes whose inclusive length is <= j
 #pragma unroll
-            for (int c = 0; c < kCaReg; c++) {
-                ri[c] = __shfl_sync(0xffffffffu, inj[c], o);
-                ry[c] = __shfl_sync(0xffffffffu, y2[c], o);
-            }
-            const uint32_t roff = __shfl_sync(0xffffffffu, RR.off, o), rlen = __shfl_sync(0xffffffffu, RR.len, o);
-            const uint32_t rb = __shfl_sync(0xffffffffu, rbase, o);
-            if (j >= T) continue;
-            const unsigned long long ri_row = (unsigned long long)(base + o);
-            const uint32_t pos = off + (j - ex);
-            const int32_t x = __ldg(cip + pos);
-            bool keep = true;
-            if (!P.prefiltered) keep = in_bitmap(cu_bitmap, x);
+                for (int st = 16; st > 0; st >>= 1) {
+                    const uint32_t v = __shfl_sync(0xffffffffu, inc, o + st - 1);
+                    if (v <= j) o += st;
+                }
+                o &= 31;
+                oo[u] = o;
+                jj[u] = j;
+                pos[u] = __shfl_sync(0xffffffffu, L.off, o) + (j - __shfl_sync(0xffffffffu, excl, o));
+                // (warp-uniform branches: only the row data this step needs travels)
 #pragma unroll
-            for (int c = 0; c < kCaReg; c++) keep &= ri[c] != x;
-            for (int c = kCaReg; c < ninj && keep; c++) keep = __ldg(M + ri_row * (unsigned)P.t + P.inj_col[c]) != x;
-            for (unsigned e = 1; e < E && keep; e++) {
-                const Loc Le = loc[ri_row * E + e];
-                keep = in_sorted(cip + Le.off, Le.len, x);
-            }
-            if (!keep) continue;
-            surv++;
-            if (rowR) {
-                bound += rlen;
-                uint32_t cc = rb;
-                if (xinj && cc && in_bitmap(P2.cu, x) && in_sorted(P2.fci + roff, rlen, x)) cc--;
-                cnt += cc;
-                continue;
-            }
-            Loc R;
-            if (P.pa) {
-                R = P.pa[pos];
-            } else {
-                R = pcsr_lookup(groups, gpn, P2.gbase[0], P2.ngroups[0], P2.lab[0], (uint32_t)x, nullptr);
-                if (R.len) {
-                    const uint32_t a = __ldg(P2.fpos + (R.off - P2.flo)), b = __ldg(P2.fpos + (R.off + R.len - P2.flo));
-                    R = Loc{a, b - a};
+                for (int c = 0; c < kCaReg; c++) {
+                    ri[u][c] = -1;
+                    ry[u][c] = -1;
+                    if (c < ninj) ri[u][c] = __shfl_sync(0xffffffffu, inj[c], o);
+                    if (!rowR && c < ninj2) ry[u][c] = __shfl_sync(0xffffffffu, y2[c], o);
+                }
+                roff[u] = rlen[u] = rb[u] = 0u;
+                if (rowR) {
+                    rb[u] = __shfl_sync(0xffffffffu, rbase, o);
+                    rlen[u] = __shfl_sync(0xffffffffu, RR.len, o);
+                    if (xinj) roff[u] = __shfl_sync(0xffffffffu, RR.off, o);
                 }
             }
-            bound += R.len;
-            uint32_t cc = R.len;
+            int32_t x[U];
+            Loc R[U];
 #pragma unroll
-            for (int c = 0; c < kCaReg; c++) {
-                if (c >= ninj2 || !cc) break;
-                if (ry[c] >= 0 && in_sorted(P2.fci + R.off, R.len, ry[c])) cc--;
+            for (int u = 0; u < U; u++) {
+                x[u] = jj[u] < T ? __ldg(cip + pos[u]) : -1;
+                R[u] = (!rowR && P.pa && jj[u] < T) ? P.pa[pos[u]] : Loc{0u, 0u};
             }
-            for (int c = kCaReg; c < ninj2 && cc; c++) {
-                const int32_t y = __ldg(M + ri_row * (unsigned)P.t + P2.inj_col[c]);
-                if (in_bitmap(P2.cu, y) && in_sorted(P2.fci + R.off, R.len, y)) cc--;
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                if (jj[u] >= T) continue;
+                const unsigned long long ri_row = (unsigned long long)(base + oo[u]);
+                const int32_t xv = x[u];
+                bool keep = true;
+                if (!P.prefiltered) keep = in_bitmap(cu_bitmap, xv);
+#pragma unroll
+                for (int c = 0; c < kCaReg; c++) keep &= ri[u][c] != xv;
+                for (int c = kCaReg; c < ninj && keep; c++) keep = __ldg(M + ri_row * (unsigned)P.t + P.inj_col[c]) != xv;
+                for (unsigned e = 1; e < E && keep; e++) {
+                    const Loc Le = loc[ri_row * E + e];
+                    keep = in_sorted(cip + Le.off, Le.len, xv);
+                }
+                if (!keep) continue;
+                surv++;
+                if (rowR) {
+                    bound += rlen[u];
+                    uint32_t cc = rb[u];
+                    if (xinj && cc && in_bitmap(P2.cu, xv) && in_sorted(P2.fci + roff[u], rlen[u], xv)) cc--;
+                    cnt += cc;
+                    continue;
+                }
+                Loc Rv = R[u];
+                if (!P.pa) {
+                    Rv = pcsr_lookup(groups, gpn, P2.gbase[0], P2.ngroups[0], P2.lab[0], (uint32_t)xv, nullptr);
+                    if (Rv.len) {
+                        const uint32_t fa = __ldg(P2.fpos + (Rv.off - P2.flo));
+                        const uint32_t fb = __ldg(P2.fpos + (Rv.off + Rv.len - P2.flo));
+                        Rv = Loc{fa, fb - fa};
+                    }
+                }
+                bound += Rv.len;
+                uint32_t cc = Rv.len;
+#pragma unroll
+                for (int c = 0; c < kCaReg; c++) {
+                    if (c >= ninj2 || !cc) break;
+                    if (ry[u][c] >= 0 && in_sorted(P2.fci + Rv.off, Rv.len, ry[u][c])) cc--;
+                }
+                for (int c = kCaReg; c < ninj2 && cc; c++) {
+                    const int32_t y = __ldg(M + ri_row * (unsigned)P.t + P2.inj_col[c]);
+                    if (in_bitmap(P2.cu, y) && in_sorted(P2.fci + Rv.off, Rv.len, y)) cc--;
+                }
+                cnt += cc;
             }
-            cnt += cc;
         }
     }
     cnt = warp_sum_u64(cnt);
@@ -1535,7 +1594,6 @@ struct Arena {
         if (bump) demand = std::max(demand, off + need + (cap - top) + live_fb);
         return fallback(p, bytes);
     }
-    size_t free_bytes() const { return bump ? top - off : 0; }
     size_t mark() const { return off; }
     void reset(size_t m) { off = m; }
     void release(void *p) {

@@ -442,3 +442,37 @@ def test_count_ahead_matches_oracle(tile, monkeypatch):
                 continue
             assert gsi.query(graph, q, fingerprint=False, homomorphism=True).count == hc
     assert seen >= 4
+
+
+def test_bench_scale_root_restricted():
+    """Parity at the bench's full size (C5m: R-MAT scale 25, 264 M edges) in the bench's
+    launch configuration (count-only: count-ahead, projection, shared runs, probe-ahead;
+    and the enumerated fingerprint pass), through the root-restricted protocol of SURVEY.md
+    §8(c): both sides restricted to f(pi_1) in S for a sample S of pi_1's label class; the
+    sample shrinks until the oracle finishes in seconds."""
+    import torch
+    g = W.make_config("C5m", device="cuda")
+    adj = W._Adj(g, device="cuda")
+    qs = [W.random_walk_query(g, 12, 1000 + i, adj) for i in (0, 2, 7, 11, 13)]
+    del adj
+    torch.cuda.empty_cache()
+    graph = gsi.build(g)
+    og = oracle.OracleGraph(g)
+    rng = np.random.default_rng(5)
+    checked = 0
+    for q in qs:
+        root = gsi.query(graph, q, fingerprint=False).stats()["order"][0]
+        cls = np.nonzero(g.vlabels == q.vlabels[root])[0]
+        for ns in (256, 32, 4):
+            roots = np.sort(rng.choice(cls, min(ns, len(cls)), replace=False))
+            try:
+                cnt, fp, _ = oracle.match(og, q, root=root, roots=roots, table=False, timeout=15.0)
+            except oracle.OracleError:
+                continue
+            r = gsi.query(graph, q, roots=roots, fingerprint=False)
+            assert r.count == cnt, (q.seed if hasattr(q, "seed") else None, ns)
+            r = gsi.query(graph, q, roots=roots)
+            assert r.count == cnt and r.fingerprint() == fp
+            checked += cnt > 0
+            break
+    assert checked >= 3

@@ -24,6 +24,7 @@ ap.add_argument("--k", type=int, default=12)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--no-fp", action="store_true")
 ap.add_argument("--table", action="store_true")
+ap.add_argument("--enum", action="store_true", help="count_ahead off: enumerate every match of the last level")
 a = ap.parse_args()
 over = {}
 if a.scale:
@@ -40,7 +41,7 @@ for i, q in qs.items():
         prof = rep == a.reps - 1
         torch.cuda.synchronize()
         t = time.time()
-        r = gsi.query(graph, q, profile=prof, fingerprint=not a.no_fp, want_table=a.table)
+        r = gsi.query(graph, q, profile=prof, fingerprint=not a.no_fp, want_table=a.table, count_ahead=not a.enum)
         torch.cuda.synchronize()
         ms = 1000 * (time.time() - t)
     s = r.stats()
