@@ -211,7 +211,8 @@ def workload_config(args, g):
             "mode": "count-only (gsi_query count; a one-edge last step is counted by the level before it "
                     "as |N(v,l0) ∩ C(u)| minus the row's own vertices, see DESIGN.md; 'enumerated' = every "
                     "match of the last level visited and checked)",
-            "l2": "inputs larger than L2 (PCSR+signatures >> 126 MB); no flush"}
+            "l2": "inputs larger than L2 (PCSR+signatures >> 126 MB); no flush",
+            "concurrency": args.concurrency}
 
 
 # ------------------------------------------------------------------------ GPU arm --------
@@ -269,23 +270,26 @@ def run_gsi(args):
 
     def step(profile=False, stats=None, enumerate_all=False):
         # count-only (the product's count path: the last level may be counted ahead);
-        # enumerate_all=True visits and checks every match of the last level instead
-        for i, p in enumerate(prepared):
-            r = gsi.gsi_query_run(graph, p, stream=sptr, timeout_s=args.query_timeout, profile=profile,
-                                  partial_on_timeout=True, fingerprint=False, count_ahead=not enumerate_all,
-                                  **shard)
-            counts[i] = r.count
-            if stats is not None:
-                stats.append(r.stats())
+        # enumerate_all=True visits and checks every match of the last level instead.  The
+        # batch runs its queries concurrently (--concurrency host workers / streams); the
+        # profiled pass runs them one at a time so per-kernel event times are not shared.
+        rs = gsi.gsi_query_run_batch(graph, prepared, concurrency=1 if profile else args.concurrency,
+                                     timeout_s=args.query_timeout, profile=profile, partial_on_timeout=True,
+                                     fingerprint=False, count_ahead=not enumerate_all, **shard)
+        counts.copy_(torch.tensor([r.count for r in rs], dtype=torch.int64))
+        if stats is not None:
+            stats.extend(r.stats() for r in rs)
         if ws > 1:
             dist.all_reduce(counts)
         return counts
 
     def e2e_step():
-        for i, q in enumerate(qs):
-            r = gsi.gsi_query(graph, q.vlabels, q.src, q.dst, q.elabels, stream=sptr,
-                              timeout_s=args.query_timeout, partial_on_timeout=True, fingerprint=False, **shard)
-            counts[i] = r.count
+        # the public API from host arrays: validate + encode + H2D of every query, the
+        # concurrent batch run, and the counts back on the host
+        ps = [gsi.prepare(graph, q) for q in qs]
+        rs = gsi.gsi_query_run_batch(graph, ps, concurrency=args.concurrency, timeout_s=args.query_timeout,
+                                     partial_on_timeout=True, fingerprint=False, **shard)
+        counts.copy_(torch.tensor([r.count for r in rs], dtype=torch.int64))
         if ws > 1:
             dist.all_reduce(counts)
         return int(counts.sum().item())
@@ -449,6 +453,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-enumerated", action="store_true", help="skip the secondary enumerated pass")
+    ap.add_argument("--concurrency", type=int, default=2, help="queries in flight (host workers / streams)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -178,6 +178,18 @@ gsi_status gsi_query_run(const gsi_graph *g, const gsi_prepared *q, const gsi_qu
                          gsi_result **out);
 void gsi_prepared_free(gsi_prepared *q);
 
+/*
+ * gsi_query_run_batch — run nq prepared queries of one graph concurrently (inter-query
+ * parallelism, SURVEY.md §8(e) "tiny queries"): `concurrency` (1..8) host workers, each with
+ * its own CUDA stream and query workspace, take the queries in order; their kernels
+ * interleave on the device.  opts applies to every query (opts->stream is ignored; a zero
+ * mem_budget_bytes becomes the device budget / concurrency).  out receives nq result
+ * handles in query order; on any error all are freed, out[] is NULL and the status of the
+ * first failing query is returned (gsi_last_error names it).
+ */
+gsi_status gsi_query_run_batch(const gsi_graph *g, int32_t nq, const gsi_prepared *const *qs,
+                               const gsi_query_opts *opts, int32_t concurrency, gsi_result **out);
+
 typedef struct {
     int32_t k, levels;                /* levels = number of join levels executed            */
     int32_t order[GSI_MAX_K];         /* join order pi (query ids)                          */

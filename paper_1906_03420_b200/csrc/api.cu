@@ -13,6 +13,7 @@ namespace gsi {
 static thread_local std::string g_last_error;
 
 void set_error(const std::string &msg) { g_last_error = msg; }
+std::string gsi_last_error_str() { return g_last_error; }
 
 gsi_status cuda_fail(cudaError_t e, const char *what) {
     g_last_error = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
@@ -27,6 +28,8 @@ gsi_status debug_lookup_impl(const gsi_graph *g, int64_t nq, const int32_t *v, c
 gsi_status prepare_impl(const gsi_graph *g, int32_t k, const int32_t *qvl, int32_t qm, const int32_t *qs,
                         const int32_t *qd, const int32_t *qe, gsi_prepared **out);
 gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_opts *opts, gsi_result **out);
+gsi_status run_batch_impl(const gsi_graph *g, int32_t nq, const gsi_prepared *const *qs, const gsi_query_opts *opts,
+                          int32_t conc, gsi_result **out);
 gsi_status debug_filter_impl(const gsi_graph *g, int32_t k, const int32_t *qvl, int32_t qm, const int32_t *qs,
                              const int32_t *qd, const int32_t *qe, int32_t mode, uint32_t *bitmaps, int64_t *counts);
 
@@ -245,6 +248,21 @@ gsi_status gsi_query_run(const gsi_graph *g, const gsi_prepared *q, const gsi_qu
 }
 
 void gsi_prepared_free(gsi_prepared *q) { delete q; }
+
+gsi_status gsi_query_run_batch(const gsi_graph *g, int32_t nq, const gsi_prepared *const *qs,
+                               const gsi_query_opts *opts, int32_t concurrency, gsi_result **out) {
+    if (nq > 0 && !out) {
+        set_error("out is NULL");
+        return GSI_ERR_INVALID_ARG;
+    }
+    GSI_TRY(need_device());
+    for (int i = 0; i < nq; i++)
+        if (!qs || !qs[i] || qs[i]->g != g) {
+            set_error("batch entry " + std::to_string(i) + " is not a query prepared for this graph");
+            return GSI_ERR_INVALID_ARG;
+        }
+    return run_batch_impl(g, nq, qs, opts, concurrency, out);
+}
 
 gsi_status gsi_query(const gsi_graph *g, int32_t k, const int32_t *qvl, int32_t qm, const int32_t *qs,
                      const int32_t *qd, const int32_t *qe, const gsi_query_opts *opts, gsi_result **out) {

@@ -319,6 +319,8 @@ __device__ __forceinline__ unsigned long long block_exclusive_scan(unsigned long
 namespace gsi {
 
 void set_error(const std::string &msg);
+std::string gsi_last_error_str();   // this thread's last error message
+size_t workspace_idle_bytes(int dev);
 gsi_status cuda_fail(cudaError_t e, const char *what);
 
 #define GSI_CUDA(call)                                            \

@@ -30,7 +30,10 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <atomic>
 #include <mutex>
+#include <string>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -1487,18 +1490,33 @@ struct Workspace {
     size_t want = 64ull << 20;   // high-water demand of the queries so far (next size)
     bool busy = false;
 };
-Workspace g_ws[64];
+constexpr int kWsSlots = 8;        // concurrent queries per device with their own workspace
+Workspace g_ws[64][kWsSlots];
 
 }  // namespace
 
 void workspace_trim(int dev) {
     if (dev < 0 || dev >= 64) return;
-    std::lock_guard<std::mutex> lk(g_ws[dev].mu);
-    if (g_ws[dev].busy || !g_ws[dev].base) return;
-    cudaFree(g_ws[dev].base);
-    g_ws[dev].base = nullptr;
-    g_ws[dev].cap = 0;
-    g_ws[dev].want = 64ull << 20;   // a new graph: learn its queries' demand afresh
+    for (int k = 0; k < kWsSlots; k++) {
+        Workspace &W = g_ws[dev][k];
+        std::lock_guard<std::mutex> lk(W.mu);
+        if (W.busy) continue;
+        if (W.base) cudaFree(W.base);
+        W.base = nullptr;
+        W.cap = 0;
+        W.want = 64ull << 20;   // a new graph: learn its queries' demand afresh
+    }
+}
+
+// Bytes held by the device's idle workspaces (they count as available to a new query).
+size_t workspace_idle_bytes(int dev) {
+    size_t idle = 0;
+    if (dev < 0 || dev >= 64) return 0;
+    for (int k = 0; k < kWsSlots; k++) {
+        std::lock_guard<std::mutex> lk(g_ws[dev][k].mu);
+        if (!g_ws[dev][k].busy) idle += g_ws[dev][k].cap;
+    }
+    return idle;
 }
 
 namespace {
@@ -1509,7 +1527,7 @@ struct Arena {
     double ms_alloc = 0;   // host time in allocation calls (stats.ms_host_alloc)
     char *bump = nullptr;
     size_t cap = 0, off = 0, top = 0;
-    int ws_dev = -1;       // >= 0: bump is that device's workspace
+    int ws_dev = -1, ws_slot = -1;   // >= 0: bump is that device's workspace slot
     size_t live_fb = 0, demand = 0;   // live fallback bytes; high-water mark of all scratch
     explicit Arena(cudaStream_t s) : st(s) {}
     void note() { demand = std::max(demand, off + (cap - top) + live_fb); }
@@ -1517,7 +1535,10 @@ struct Arena {
     // with stream-ordered allocations only.
     void init_workspace(int dev, size_t budget) {
         if (dev < 0 || dev >= 64) return;
-        Workspace &W = g_ws[dev];
+        for (int k = 0; k < kWsSlots && ws_dev < 0; k++) take_slot(dev, k, budget);
+    }
+    void take_slot(int dev, int slot, size_t budget) {
+        Workspace &W = g_ws[dev][slot];
         std::lock_guard<std::mutex> lk(W.mu);
         if (W.busy) return;
         const size_t bytes = std::min(budget, std::max(W.want, (size_t)64 << 20));
@@ -1541,6 +1562,7 @@ struct Arena {
         ms_alloc += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         W.busy = true;
         ws_dev = dev;
+        ws_slot = slot;
         bump = W.base;
         cap = W.cap;
         off = 0;
@@ -1610,9 +1632,10 @@ struct Arena {
             if (q) cudaFreeAsync(q, st);
         if (ws_dev >= 0) {
             cudaStreamSynchronize(st);   // nothing in flight may still use the workspace
-            std::lock_guard<std::mutex> lk(g_ws[ws_dev].mu);
-            g_ws[ws_dev].busy = false;
-            g_ws[ws_dev].want = std::max(g_ws[ws_dev].want, demand + demand / 8);
+            Workspace &W = g_ws[ws_dev][ws_slot];
+            std::lock_guard<std::mutex> lk(W.mu);
+            W.busy = false;
+            W.want = std::max(W.want, demand + demand / 8);
         }
     }
 };
@@ -2446,12 +2469,7 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     // device memory the query may use; the workspace grows to the demand seen so far
     unsigned long long budget = opts.mem_budget_bytes;
     if (!budget) {
-        size_t idle = 0;
-        {
-            std::lock_guard<std::mutex> lk(g_ws[g->device].mu);
-            if (!g_ws[g->device].busy) idle = g_ws[g->device].cap;
-        }
-        budget = (unsigned long long)(0.85 * (double)(available_bytes(g->device) + idle));
+        budget = (unsigned long long)(0.85 * (double)(available_bytes(g->device) + workspace_idle_bytes(g->device)));
     }
     A.init_workspace(g->device, budget);
     GSI_TRY(A.get(&C.ctr, 1));
@@ -2661,6 +2679,71 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     return GSI_OK;
 }
 
+}  // namespace gsi
+
+// ====================================================================== batch ==========
+// Independent queries run concurrently: `conc` host workers, each with its own stream and
+// workspace slot, pull queries in order; the device interleaves their kernels, so one
+// query's host round trips (a count read back per level) and tiny levels overlap with
+// another's large ones.  Each query's memory budget is the device budget / conc.
+namespace gsi {
+gsi_status run_batch_impl(const gsi_graph *g, int32_t nq, const gsi_prepared *const *qs,
+                          const gsi_query_opts *opts_in, int32_t conc, gsi_result **out) {
+    if (!g || nq < 0 || (nq > 0 && (!qs || !out))) {
+        set_error("invalid batch arguments");
+        return GSI_ERR_INVALID_ARG;
+    }
+    for (int i = 0; i < nq; i++) out[i] = nullptr;
+    if (nq == 0) return GSI_OK;
+    gsi_query_opts base;
+    gsi_query_opts_default(&base);
+    if (opts_in) base = *opts_in;
+    const int T = std::max(1, std::min<int>(std::min(conc, nq), kWsSlots));
+    GSI_CUDA(cudaSetDevice(g->device));
+    if (!base.mem_budget_bytes)
+        base.mem_budget_bytes = (unsigned long long)(0.85 * (double)(available_bytes(g->device) +
+                                                                     workspace_idle_bytes(g->device)) / T);
+    std::vector<gsi_status> rc(nq, GSI_OK);
+    std::vector<std::string> err(nq);
+    std::atomic<int> next{0};
+    auto worker = [&]() {
+        cudaSetDevice(g->device);
+        cudaStream_t s = nullptr;
+        if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
+            cudaGetLastError();
+            s = nullptr;
+        }
+        gsi_query_opts o = base;
+        if (s) o.stream = s;
+        for (;;) {
+            const int i = next.fetch_add(1);
+            if (i >= nq) break;
+            rc[i] = run_impl(g, qs[i], &o, &out[i]);
+            if (rc[i] != GSI_OK) err[i] = gsi_last_error_str();
+        }
+        if (s) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+        }
+    };
+    if (T == 1) {
+        worker();
+    } else {
+        std::vector<std::thread> th;
+        for (int w = 0; w < T; w++) th.emplace_back(worker);
+        for (auto &t : th) t.join();
+    }
+    for (int i = 0; i < nq; i++)
+        if (rc[i] != GSI_OK) {
+            for (int j = 0; j < nq; j++) {
+                delete out[j];
+                out[j] = nullptr;
+            }
+            set_error("query " + std::to_string(i) + " of the batch: " + err[i]);
+            return rc[i];
+        }
+    return GSI_OK;
+}
 }  // namespace gsi
 
 // ====================================================================== debug filter ===

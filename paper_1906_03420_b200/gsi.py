@@ -84,6 +84,7 @@ _SIGS = {
     "gsi_result_count": (I32, [P, P]),
     "gsi_result_fingerprint": (I32, [P, P]),
     "gsi_trim_workspace": (None, [I32]),
+    "gsi_query_run_batch": (I32, [P, I32, P, P, I32, P]),
     "gsi_result_table": (I32, [P, P, P]),
     "gsi_result_copy_table": (I32, [P, P, U64]),
     "gsi_result_stats": (I32, [P, P]),
@@ -302,6 +303,16 @@ def gsi_query_run(g: GraphHandle, p: Prepared, **opts) -> Result:
     out = P()
     _check(lib.gsi_query_run(g.h, p.h, ctypes.byref(o), ctypes.byref(out)), "gsi_query_run")
     return Result(out.value, p.k)
+
+
+def gsi_query_run_batch(g: GraphHandle, prepared: Sequence["Prepared"], concurrency: int = 4, **opts) -> List[Result]:
+    """Run prepared queries concurrently (`concurrency` host workers / streams)."""
+    n = len(prepared)
+    o, keep = _opts(**opts)
+    arr = (P * max(n, 1))(*[p.h for p in prepared])
+    outs = (P * max(n, 1))()
+    _check(lib.gsi_query_run_batch(g.h, n, arr, ctypes.byref(o), int(concurrency), outs), "gsi_query_run_batch")
+    return [Result(outs[i], prepared[i].k) for i in range(n)]
 
 
 # ---------------------------------------------------------------------------- debug --

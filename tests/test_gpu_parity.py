@@ -476,3 +476,27 @@ def test_bench_scale_root_restricted():
             checked += cnt > 0
             break
     assert checked >= 3
+
+
+def test_query_batch_concurrent():
+    """gsi_query_run_batch: concurrent queries (own streams and workspaces) give exactly the
+    per-query results, in query order, for every concurrency; errors free the whole batch."""
+    g = W.chung_lu(20_000, 120_000, 2_000, nlv=8, nle=6, seed=91)
+    graph = gsi.build(g)
+    og = oracle.OracleGraph(g)
+    qs = bounded_queries(g, og, lambda s: 4 + s % 7, range(9100, 9160), hi=3_000_000, want=10)
+    assert len(qs) >= 6
+    prepared = [gsi.prepare(graph, q) for q in qs]
+    single = [gsi.gsi_query_run(graph, p, want_table=True) for p in prepared]
+    for conc in (1, 3, 8):
+        rs = gsi.gsi_query_run_batch(graph, prepared, concurrency=conc, want_table=True)
+        for a, b in zip(rs, single):
+            assert a.count == b.count and a.fingerprint() == b.fingerprint()
+            assert np.array_equal(a.table(), b.table())
+        rs = gsi.gsi_query_run_batch(graph, prepared, concurrency=conc, fingerprint=False)
+        assert [r.count for r in rs] == [b.count for b in single]
+    for q, b in zip(qs, single):
+        assert b.count == oracle.match(og, q, table=False)[0]
+    other = gsi.build(W.cycle_graph(5))
+    with pytest.raises(gsi.GsiError):
+        gsi.gsi_query_run_batch(other, prepared, concurrency=2)
