@@ -59,6 +59,9 @@ constexpr int kThreads = 256;
 #ifndef GSI_CAHEAD_MINB
 #define GSI_CAHEAD_MINB 4   // k_cahead_warp: resident blocks per SM the registers are sized for
 #endif
+#ifndef GSI_CAHEAD_LEAN
+#define GSI_CAHEAD_LEAN 1   // lean count-ahead kernel for the common shape (0: always k_cahead_warp)
+#endif
 #ifndef GSI_CAHEAD_U
 #define GSI_CAHEAD_U 1      // k_cahead_warp: slots per lane per pass
 #endif
@@ -410,6 +413,33 @@ __host__ __device__ constexpr int join_items(int mode) {
     return mode == J_NEXT ? GSI_NEXT_ITEMS : (mode == J_COUNT ? GSI_COUNT_ITEMS : 8);
 }
 
+// Duplicate removal (Alg. 5) at warp scope: consecutive rows of M
+// that hold the same vertex v in the probed column (siblings share their prefix columns, and
+// rows stay in lexicographic order) need the same run N(v,l) ∩ C(u).  Only the first lane of
+// each run of equal v probes PCSR; the others take its result by shuffle.  Every lane of
+// the warp must call this (need = false for lanes without a row).
+__device__ __forceinline__ Loc warp_dedup_lookup(bool need, int32_t v, const StepParams &P2,
+                                                 const uint2 *__restrict__ groups, int gpn) {
+    const int lane = threadIdx.x & 31;
+    const int32_t pv = __shfl_up_sync(0xffffffffu, v, 1);
+    const bool head = need && (lane == 0 || pv != v);
+    Loc R{0u, 0u};
+    if (head) {
+        R = pcsr_lookup(groups, gpn, P2.gbase[0], P2.ngroups[0], P2.lab[0], (uint32_t)v, nullptr);
+        if (P2.prefiltered && R.len) {
+            const uint32_t a = __ldg(P2.fpos + (R.off - P2.flo)), b = __ldg(P2.fpos + (R.off + R.len - P2.flo));
+            R = Loc{a, b - a};
+        }
+    }
+    const unsigned heads = __ballot_sync(0xffffffffu, head);
+    const unsigned upto = heads & (0xffffffffu >> (31 - lane));   // heads at lanes <= this one
+    const int src = upto ? 31 - __clz(upto) : lane;
+    R.off = __shfl_sync(0xffffffffu, R.off, src);
+    R.len = __shfl_sync(0xffffffffu, R.len, src);
+    if (!need) R = Loc{0u, 0u};
+    return R;
+}
+
 // The NEXT step's list of every survivor (row, x) when that step has one linking edge:
 // from the probe-ahead table aligned with this step's candidates (one coalesced 8 B read),
 // else one PCSR probe per survivor (batches of 4 keep the first-sector loads in flight),
@@ -549,7 +579,8 @@ __global__ void __launch_bounds__(kThreads, join_items(MODE) > 8 ? 2 : (((MODE =
     // two rows per thread per pass, phased so that both rows' dependent loads (F -> loc / row
     // columns -> PCSR sector -> fpos) are in flight together
     constexpr int RS = GSI_STAGE_ROWS;
-    for (long long r0 = tid; r0 < nr; r0 += RS * kThreads) {
+    // (warp-uniform trip count: the staged next-step lookups are warp-collective)
+    for (long long r0 = tid; r0 - tid < nr; r0 += RS * kThreads) {
         long long rr[RS];
         bool ok[RS];
         unsigned long long a[RS], b[RS];
@@ -578,16 +609,11 @@ __global__ void __launch_bounds__(kThreads, join_items(MODE) > 8 ? 2 : (((MODE =
                 vn[q] = kn[q] ? (uint32_t)__ldg(row + P2.col[0]) : 0u;
             }
             if (MODE == J_NEXT && P.stage_next) {
-                Loc R[RS];
-                pcsr_lookup_batch<RS>(groups, gpn, P2.gbase[0], P2.ngroups[0], P2.lab[0], vn, kn, R);
 #pragma unroll
                 for (int q = 0; q < RS; q++) {
-                    if (kn[q] && P2.prefiltered && R[q].len) {
-                        const uint32_t fa = __ldg(P2.fpos + (R[q].off - P2.flo));
-                        const uint32_t fb = __ldg(P2.fpos + (R[q].off + R[q].len - P2.flo));
-                        R[q] = Loc{fa, fb - fa};
-                    }
-                    if (ok[q]) sNext[rr[q]] = kn[q] ? R[q] : Loc{0u, 0u};
+                    // consecutive tile rows sharing the probed vertex share one lookup (Alg. 5)
+                    const Loc R = warp_dedup_lookup(kn[q], kn[q] ? (int32_t)vn[q] : -1, P2, groups, gpn);
+                    if (ok[q]) sNext[rr[q]] = R;
                 }
             }
 #pragma unroll
@@ -1063,12 +1089,10 @@ __global__ void __launch_bounds__(kThreads, GSI_CAHEAD_MINB) k_cahead_warp(const
 #pragma unroll
         for (int c = 0; c < kCaReg; c++) y2[c] = -1;
         if (rowR) {
-            if (valid && L.len) {
-                RR = pcsr_lookup(groups, gpn, P2.gbase[0], P2.ngroups[0], P2.lab[0], (uint32_t)__ldg(row + P2.col[0]), nullptr);
-                if (RR.len) {
-                    const uint32_t a = __ldg(P2.fpos + (RR.off - P2.flo)), b = __ldg(P2.fpos + (RR.off + RR.len - P2.flo));
-                    RR = Loc{a, b - a};
-                }
+            const bool need = valid && L.len;
+            const int32_t v = need ? __ldg(row + P2.col[0]) : -1;
+            RR = warp_dedup_lookup(need, v, P2, groups, gpn);
+            if (need) {
                 rbase = RR.len;
                 for (int c = 0; c < ninj2 && rbase; c++) {
                     if (P2.inj_col[c] >= P.t) continue;
@@ -1182,6 +1206,75 @@ __global__ void __launch_bounds__(kThreads, GSI_CAHEAD_MINB) k_cahead_warp(const
                 }
                 cnt += cc;
             }
+        }
+    }
+    cnt = warp_sum_u64(cnt);
+    surv = warp_sum_u64(surv);
+    bound = warp_sum_u64(bound);
+    if (lane == 0) {
+        if (cnt) atomicAdd(&ctr->count, cnt);
+        if (surv) atomicAdd(&ctr->total, surv);
+        if (bound) atomicAdd(&ctr->total2, bound);
+    }
+}
+
+// The common count-ahead shape, lean: the last step links to a parent column (its run and
+// the row-column subtraction hits are per row, located with warp duplicate removal), the
+// vertex this step adds is not a subtraction column of the last step, one linking edge on
+// shared runs, at most NINJ subtraction columns in this step.  A slot then costs the owner
+// search, the candidate read and NINJ compares: every candidate x of the row's run is read
+// and checked, and contributes the row's extension count rb (same arithmetic as
+// k_cahead_warp, with the generic paths compiled out).
+template <int NINJ>
+__global__ void __launch_bounds__(kThreads, 4) k_cahead_lean(const int32_t *__restrict__ M, long long r0, long long r1,
+                                                             const Loc *__restrict__ loc, StepParams P, StepParams P2,
+                                                             const int32_t *__restrict__ cip,
+                                                             const uint2 *__restrict__ groups, int gpn, Counters *ctr) {
+    const int lane = threadIdx.x & 31;
+    const long long gw = (blockIdx.x * (long long)kThreads + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * kThreads) >> 5;
+    const int ninj2 = P2.n_inj;
+    unsigned long long cnt = 0, surv = 0, bound = 0;
+    for (long long base = r0 + gw * 32; base < r1; base += nw * 32) {
+        const long long i = base + lane;
+        const bool valid = i < r1;
+        const Loc L = valid ? loc[(unsigned long long)i] : Loc{0u, 0u};
+        const int32_t *row = M + (unsigned long long)(valid ? i : r0) * (unsigned)P.t;
+        const int32_t inj = (NINJ > 0 && valid) ? __ldg(row + P.inj_col[0]) : -1;
+        const bool need = valid && L.len;
+        const Loc RR = warp_dedup_lookup(need, need ? __ldg(row + P2.col[0]) : -1, P2, groups, gpn);
+        uint32_t rbase = RR.len;
+        for (int c = 0; c < ninj2 && rbase; c++) {
+            const int32_t y = __ldg(row + P2.inj_col[c]);
+            if (in_bitmap(P2.cu, y) && in_sorted(P2.fci + RR.off, RR.len, y)) rbase--;
+        }
+        uint32_t inc = L.len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        const uint32_t excl = inc - L.len;
+        const uint32_t T = __shfl_sync(0xffffffffu, inc, 31);
+        for (uint32_t j0 = 0; j0 < T; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            int o = 0;
+#pragma unroll
+            for (int st = 16; st > 0; st >>= 1) {
+                const uint32_t v = __shfl_sync(0xffffffffu, inc, o + st - 1);
+                if (v <= j) o += st;
+            }
+            o &= 31;
+            const uint32_t pos = __shfl_sync(0xffffffffu, L.off, o) + (j - __shfl_sync(0xffffffffu, excl, o));
+            const uint32_t rb = __shfl_sync(0xffffffffu, rbase, o);
+            const uint32_t rl = __shfl_sync(0xffffffffu, RR.len, o);
+            const int32_t ri = NINJ > 0 ? __shfl_sync(0xffffffffu, inj, o) : -1;
+            if (j >= T) continue;
+            const int32_t x = __ldg(cip + pos);
+            if (NINJ > 0 && x == ri) continue;
+            surv++;
+            bound += rl;
+            cnt += rb;
         }
     }
     cnt = warp_sum_u64(cnt);
@@ -2355,7 +2448,18 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
             const unsigned long long units = ((unsigned long long)(r_hi - r_lo) + 31) / 32;
             const unsigned wg = (unsigned)std::max<unsigned long long>(
                 1, std::min<unsigned long long>((units + 7) / 8, (unsigned long long)sms * 8));
-            k_cahead_warp<<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, P2, cip, cu, g->groups, g->gpn, lctr);
+            bool xinj = false;
+            for (int c = 0; c < P2.n_inj; c++) xinj |= P2.inj_col[c] >= P.t;
+            const bool lean = GSI_CAHEAD_LEAN && !env_flag("GSI_CAHEAD_NOLEAN") && P2.col[0] < P.t && !xinj && P.E == 1 && P.n_inj <= 1;
+            if (lean && P.n_inj == 0)
+                k_cahead_lean<0><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, P2, cip, g->groups, g->gpn, lctr);
+            else if (lean)
+                k_cahead_lean<1><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, P2, cip, g->groups, g->gpn, lctr);
+            else
+                k_cahead_warp<<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, P2, cip, cu, g->groups, g->gpn, lctr);
+            if (getenv("GSI_TRACE"))
+                fprintf(stderr, "[cahead] t %d rows %lld slots %llu w %d rowR %d pa %d ninj %d ninj2 %d E %d\n", t,
+                        r_hi - r_lo, s1 - s0, P.t, P2.col[0] < P.t, P.pa != nullptr, P.n_inj, P2.n_inj, P.E);
         } else if (fast) {
             const size_t fsm = (size_t)tile_slots * 4 * (2 + (size_t)std::min(P.n_inj, P.stage_inj));
             k_count_fast<kFastItems><<<jt, kThreads, fsm, st>>>(M, (long long)nM, F, loc, rowmap, P, cip, c0, c1,
