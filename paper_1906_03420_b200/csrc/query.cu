@@ -62,6 +62,9 @@ constexpr int kThreads = 256;
 #ifndef GSI_CAHEAD_LEAN
 #define GSI_CAHEAD_LEAN 1   // lean count-ahead kernel for the common shape (0: always k_cahead_warp)
 #endif
+#ifndef GSI_NEXT_LEAN
+#define GSI_NEXT_LEAN 1     // lean warp-centric J_NEXT writing rows at their Prealloc slots (0: off)
+#endif
 #ifndef GSI_CAHEAD_U
 #define GSI_CAHEAD_U 1      // k_cahead_warp: slots per lane per pass
 #endif
@@ -1287,6 +1290,121 @@ __global__ void __launch_bounds__(kThreads, 4) k_cahead_lean(const int32_t *__re
     }
 }
 
+// Lean J_NEXT (count-only mode, one linking edge on shared runs in this step and the next):
+// warp-centric like k_cahead_lean, and the new rows go straight to their Prealloc slots —
+// row i's buffer is GBA[F_i, F_i + |N(v,l0)|) (Alg. 4), so candidate j of row i
+// writes row m_i || x at slot F_i + j with no scan, and a slot whose candidate fails leaves a
+// hole: its loc entry is {0, 0}, i.e. a row with an empty next buffer that the next level
+// skips like any other.  The Combine compaction (Alg. 3 lines 14-21) is dropped: count-only
+// levels tolerate holes, and rows stay in lexicographic order.  Slots [c0, c1) of the level
+// (a chunk may cut a row); rowmap[0..1] = the rows holding slots c0 and c1 - 1.
+template <int NINJ>
+__global__ void __launch_bounds__(kThreads, 4) k_next_lean(const int32_t *__restrict__ M, const uint32_t *__restrict__ rowmap,
+                                                           const Loc *__restrict__ loc,
+                                                           const unsigned long long *__restrict__ F,
+                                                           unsigned long long c0, unsigned long long c1, StepParams P,
+                                                           StepParams P2, const int32_t *__restrict__ cip,
+                                                           const uint32_t *__restrict__ cu_bitmap,
+                                                           const uint2 *__restrict__ groups, int gpn,
+                                                           int32_t *__restrict__ out, Loc *__restrict__ loc2,
+                                                           Counters *ctr) {
+    const int lane = threadIdx.x & 31;
+    const long long gw = (blockIdx.x * (long long)kThreads + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * kThreads) >> 5;
+    const long long r0 = rowmap[0], r1 = (long long)rowmap[1] + 1;
+    const int W = P.out_w;
+    const bool rowN = P2.col[0] < P.t;   // the next step's run is per row
+    unsigned long long surv = 0, kept = 0, nlen = 0;
+    for (long long base = r0 + gw * 32; base < r1; base += nw * 32) {
+        const long long i = base + lane;
+        const bool valid = i < r1;
+        Loc L = valid ? loc[(unsigned long long)i] : Loc{0u, 0u};
+        unsigned long long a = valid ? F[i] : 0ull;   // first slot of the row (clipped to the chunk)
+        if (valid) {
+            const unsigned long long b = min(a + L.len, c1);
+            const unsigned long long a2 = max(a, c0);
+            L.off += (uint32_t)(a2 - a);
+            L.len = b > a2 ? (uint32_t)(b - a2) : 0u;
+            a = a2;
+        }
+        const int32_t *row = M + (unsigned long long)(valid ? i : r0) * (unsigned)P.t;
+        const int32_t inj = (NINJ > 0 && valid) ? __ldg(row + P.inj_col[0]) : -1;
+        Loc RN{0u, 0u};
+        if (rowN) {
+            const bool need = valid && L.len;
+            RN = warp_dedup_lookup(need, need ? __ldg(row + P2.col[0]) : -1, P2, groups, gpn);
+        }
+        uint32_t inc = L.len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        const uint32_t excl = inc - L.len;
+        const uint32_t T = __shfl_sync(0xffffffffu, inc, 31);
+        for (uint32_t j0 = 0; j0 < T; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            int o = 0;
+#pragma unroll
+            for (int st = 16; st > 0; st >>= 1) {
+                const uint32_t v = __shfl_sync(0xffffffffu, inc, o + st - 1);
+                if (v <= j) o += st;
+            }
+            o &= 31;
+            const uint32_t k = j - __shfl_sync(0xffffffffu, excl, o);
+            const uint32_t pos = __shfl_sync(0xffffffffu, L.off, o) + k;
+            const unsigned long long slot = __shfl_sync(0xffffffffu, a, o) + k;
+            const int32_t ri = NINJ > 0 ? __shfl_sync(0xffffffffu, inj, o) : -1;
+            Loc N0;
+            N0.off = rowN ? __shfl_sync(0xffffffffu, RN.off, o) : 0u;
+            N0.len = rowN ? __shfl_sync(0xffffffffu, RN.len, o) : 0u;
+            if (j >= T) continue;
+            const unsigned long long ro = (unsigned long long)(base + o);
+            const int32_t x = __ldg(cip + pos);
+            bool keep = P.prefiltered || in_bitmap(cu_bitmap, x);
+            if (NINJ > 0) keep &= x != ri;
+            if (keep) {
+                surv++;
+                if (!rowN) {
+                    if (P.pa) {
+                        N0 = P.pa[pos];
+                    } else {
+                        N0 = pcsr_lookup(groups, gpn, P2.gbase[0], P2.ngroups[0], P2.lab[0], (uint32_t)x, nullptr);
+                        if (N0.len) {
+                            const uint32_t fa = __ldg(P2.fpos + (N0.off - P2.flo));
+                            const uint32_t fb = __ldg(P2.fpos + (N0.off + N0.len - P2.flo));
+                            N0 = Loc{fa, fb - fa};
+                        }
+                    }
+                }
+                keep = N0.len > 0;   // a row with an empty next buffer is counted, never stored
+            }
+            const unsigned long long lo = slot - c0;
+            loc2[lo] = keep ? N0 : Loc{0u, 0u};
+            if (keep) {
+                kept++;
+                nlen += N0.len;
+                int32_t *orow = out + lo * (unsigned)W;
+                for (int c = 0; c < W; c++) {
+                    const int src = P.out_src[c];
+                    orow[c] = src >= 0 ? __ldg(M + ro * (unsigned)P.t + src) : x;
+                }
+            }
+        }
+    }
+    surv = warp_sum_u64(surv);
+    kept = warp_sum_u64(kept);
+    nlen = warp_sum_u64(nlen);
+    if (lane == 0) {
+        if (surv) atomicAdd(&ctr->count, surv);
+        if (kept) atomicAdd(&ctr->active_rows, kept);
+        if (nlen) {
+            atomicAdd(&ctr->total2, nlen);
+            atomicAdd(&ctr->list_elems, nlen);
+        }
+    }
+}
+
 constexpr int kFastItems = GSI_FAST_ITEMS > 0 ? GSI_FAST_ITEMS : 8;
 
 // Dynamic shared memory of a join launch: the larger of the staging region (row markers,
@@ -2107,6 +2225,7 @@ struct QueryCtx {
     std::vector<std::pair<int32_t *, unsigned long long>> pieces;   // final table pieces (device)
     std::vector<std::pair<uint32_t *, int32_t *>> filt;             // per step: (fpos, fci) or null
     std::vector<Loc *> pa;                                           // per step: probe-ahead table or null
+    std::vector<char> lean_off;                                      // per step: lean J_NEXT left too many holes
     // Stored columns.  Count-only mode stores in M_t only the columns a later step reads (its
     // linking columns and subtraction columns); phys[t][c] = position of logical column c in
     // a row of M_t (-1: dropped), width[t] = stored columns.  Table / fingerprint: all.
@@ -2431,18 +2550,42 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
             !C.opts.no_count_ahead && !C.opts.no_shared_lists && C.opts.e0_mode == 0 &&
             C.steps[si + 2].col.size() == 1 && cahead_warp_enabled() && C.sharded)
             P.no_f2 = 1;
+        // lean J_NEXT: count-only, one linking edge here and in the next step (on shared runs),
+        // and the next level is the warp count-ahead, which walks rows with holes at no cost
+        // (a deeper level would pay for them: more rows, and an F to build)
+        if (C.lean_off.size() < C.steps.size()) C.lean_off.assign(C.steps.size(), 0);
+        const bool lean_next = P.no_f2 && GSI_NEXT_LEAN && !env_flag("GSI_NEXT_NOLEAN") && P.E == 1 && P2.E == 1 &&
+                               P.n_inj <= 1 && !C.lean_off[si];
         const bool warp_ca = mode == J_CAHEAD && P.prefiltered && cahead_warp_enabled();
         uint32_t *rowmap = nullptr;
-        if (!warp_ca) {   // first/last row of every slot tile (the warp count-ahead walks rows)
+        if (!warp_ca && !lean_next) {   // first/last row of every slot tile (the warp count-ahead walks rows)
             GSI_TRY(A.get(&rowmap, (unsigned long long)jt + 1));
             prof.begin(GSI_K_OTHER);
             k_tile_rows<<<grid_for((unsigned long long)jt + 1, kThreads), kThreads, 0, st>>>(F, (long long)nM, c0, c1, jt,
                                                                                            tile_slots, rowmap);
             prof.end();
         }
-        if (mode == J_NEXT && !P.no_f2) GSI_TRY(A.get(&F2, slots + 1));
+        if (mode == J_NEXT && !P.no_f2 && !lean_next) GSI_TRY(A.get(&F2, slots + 1));
+        uint32_t *rows2 = nullptr;
+        if (lean_next) {   // the rows holding slots c0 and c1 - 1
+            GSI_TRY(A.get(&rows2, 2));
+            prof.begin(GSI_K_OTHER);
+            k_tile_rows<<<1, 32, 0, st>>>(F, (long long)nM, c0, c1, 1, (unsigned)std::min<unsigned long long>(slots, 0xFFFFFFFFull), rows2);
+            prof.end();
+        }
         prof.begin(GSI_K_JOIN);
-        if (warp_ca) {
+        if (lean_next) {
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
+            const unsigned wg = (unsigned)std::max<unsigned long long>(
+                1, std::min<unsigned long long>((slots + kThreads - 1) / kThreads, (unsigned long long)sms * 4));
+            if (P.n_inj == 0)
+                k_next_lean<0><<<wg, kThreads, 0, st>>>(M, rows2, loc, F, c0, c1, P, P2, cip, cu, g->groups, g->gpn, out,
+                                                        loc2, lctr);
+            else
+                k_next_lean<1><<<wg, kThreads, 0, st>>>(M, rows2, loc, F, c0, c1, P, P2, cip, cu, g->groups, g->gpn, out,
+                                                        loc2, lctr);
+        } else if (warp_ca) {
             int sms = 148;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
             const unsigned long long units = ((unsigned long long)(r_hi - r_lo) + 31) / 32;
@@ -2483,11 +2626,16 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         GSI_CUDA(cudaGetLastError());
         A.release(status);
         A.release(rowmap);
-        const unsigned long long nout = (mode == J_COUNT || mode == J_CAHEAD) ? hc.count : hc.total;   // J_NEXT: stored rows
+        // J_NEXT: stored rows (lean: every slot of the chunk, holes included)
+        const unsigned long long nout = (mode == J_COUNT || mode == J_CAHEAD) ? hc.count : (lean_next ? slots : hc.total);
+        const unsigned long long kept = lean_next ? hc.active_rows : nout;   // rows with a next buffer
+        // holes cost the next level a row each: below 60 % kept, this level's later chunks
+        // go back to the compacting tile kernel
+        if (lean_next && kept * 5 < slots * 3) C.lean_off[si] = 1;
         const double frac = gba ? (double)slots / (double)gba : 0.0;
         double jb = frac * (4.0 * P.t * active + 4.0 * elems + (8.0 * E + 8.0) * active);
         if (mode == J_TABLE) jb += 4.0 * C.q->k * nout;
-        if (mode == J_NEXT) jb += nout * (4.0 * P.out_w + 16.0 * P2.E + 8.0);
+        if (mode == J_NEXT) jb += kept * (4.0 * P.out_w + 16.0 * P2.E + 8.0);
         if (mode == J_NEXT) S.rows[t] += hc.count;   // |M_{t+1}|: every survivor, stored or not
         if (mode == J_CAHEAD) {                        // survivors = |M_{t+1}|, counted = |M_{t+2}|
             jb += 8.0 * hc.total;                      // locate of the last step's run per survivor
@@ -2515,7 +2663,7 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
             }
             A.release(out);
         } else if (mode == J_NEXT) {
-            if (nout) rc = level(C, si + 1, out, nout, loc2, F2, hc.total2, nout, hc.list_elems, pf_next);
+            if (nout && hc.total2) rc = level(C, si + 1, out, nout, loc2, F2, hc.total2, kept, hc.list_elems, pf_next);
             A.release(out);
             A.release(loc2);
             A.release(F2);
