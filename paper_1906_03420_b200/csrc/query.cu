@@ -62,6 +62,12 @@ constexpr int kThreads = 256;
 #ifndef GSI_CAHEAD_LEAN
 #define GSI_CAHEAD_LEAN 1   // lean count-ahead kernel for the common shape (0: always k_cahead_warp)
 #endif
+#ifndef GSI_FILTER_MINB
+#define GSI_FILTER_MINB 1   // k_filter: resident blocks per SM the registers are sized for
+#endif
+#ifndef GSI_FILTER_FW
+#define GSI_FILTER_FW 4     // k_filter: bitmap words per warp per iteration
+#endif
 #ifndef GSI_NEXT_LEAN
 #define GSI_NEXT_LEAN 1     // lean warp-centric J_NEXT writing rows at their Prealloc slots (0: off)
 #endif
@@ -131,7 +137,7 @@ struct Counters {
 };
 
 // ---------------------------------------------------------------------- filter ------
-__global__ void __launch_bounds__(kThreads) k_filter(const uint32_t *__restrict__ sig, long long n, int k,
+__global__ void __launch_bounds__(kThreads, GSI_FILTER_MINB) k_filter(const uint32_t *__restrict__ sig, long long n, int k,
                                                      const uint32_t *__restrict__ qsig, int label_only,
                                                      uint32_t *__restrict__ bitmaps, long long words,
                                                      unsigned long long *__restrict__ counts,
@@ -153,7 +159,7 @@ __global__ void __launch_bounds__(kThreads) k_filter(const uint32_t *__restrict_
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-    constexpr int kFW = 4;   // bitmap words per warp per iteration: 4 coalesced plane-0 loads in flight
+    constexpr int kFW = GSI_FILTER_FW;   // bitmap words per warp per iteration (coalesced plane-0 loads in flight)
     unsigned long long plane_words = 0;   // plane words this thread read (algorithmic bytes / 4)
     unsigned long long my_count = 0;      // |C(u)| partial for u = lane
     for (long long w0 = (blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5)) * kFW; w0 < words;
@@ -1108,7 +1114,7 @@ __global__ void __launch_bounds__(kThreads, GSI_CAHEAD_MINB) k_cahead_warp(const
             // bit is tested once here (-1: cannot be in any candidate run)
 #pragma unroll
             for (int c = 0; c < kCaReg; c++) {
-                if (valid && c < ninj2 && P2.inj_col[c] < P.t) {
+                if (valid && L.len && c < ninj2 && P2.inj_col[c] < P.t) {   // (a hole row holds no vertices)
                     const int32_t y = __ldg(row + P2.inj_col[c]);
                     if (in_bitmap(P2.cu, y)) y2[c] = y;
                 }

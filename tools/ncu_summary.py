@@ -50,6 +50,7 @@ def full(path):
     ki = hdr.index("Kernel Name")
     print("| kernel | " + " | ".join(idx) + " |")
     print("|---" * (len(idx) + 1) + "|")
+    print("| (unit) | " + " | ".join(rows[1][i] for i in idx.values()) + " |")
     for r in rows[2:]:
         name = r[ki].split("(")[0].replace("void ", "").split("<")[0].split("::")[-1]
         print(f"| {name} | " + " | ".join(r[i] for i in idx.values()) + " |")

@@ -10,7 +10,7 @@ python tools/ncu_summary.py launches $src/launches_$tag.csv > $dst/${tag}_launch
 gzip -c $src/launches_$tag.csv > $dst/${tag}_launches.csv.gz
 if [ -f $src/join_full_$tag.ncu-rep ]; then
   python tools/ncu_summary.py full $src/join_full_$tag.ncu-rep > $dst/${tag}_join_metrics.md
-  n=$(($(wc -l < $dst/${tag}_join_metrics.md) - 2))
+  n=$(($(wc -l < $dst/${tag}_join_metrics.md) - 3))
   for i in $(seq 0 $((n - 1))); do
     python tools/ncu_summary.py details $src/join_full_$tag.ncu-rep $i > $dst/${tag}_join_details_launch$i.md
     python tools/ncu_summary.py stalls $src/join_full_$tag.ncu-rep $i > $dst/${tag}_join_stalls_launch$i.md
