@@ -63,7 +63,7 @@ constexpr int kThreads = 256;
 #define GSI_CAHEAD_LEAN 1   // lean count-ahead kernel for the common shape (0: always k_cahead_warp)
 #endif
 #ifndef GSI_FILTER_MINB
-#define GSI_FILTER_MINB 1   // k_filter: resident blocks per SM the registers are sized for
+#define GSI_FILTER_MINB 4   // k_filter: resident blocks per SM the registers are sized for
 #endif
 #ifndef GSI_FILTER_FW
 #define GSI_FILTER_FW 4     // k_filter: bitmap words per warp per iteration
@@ -142,12 +142,19 @@ __global__ void __launch_bounds__(kThreads, GSI_FILTER_MINB) k_filter(const uint
                                                      uint32_t *__restrict__ bitmaps, long long words,
                                                      unsigned long long *__restrict__ counts,
                                                      Counters *__restrict__ ctr) {
+    static_assert(GSI_FILTER_FW == 4, "the bitmap store is one 16 B vector per query vertex");
+    constexpr int kHT = 64;                          // label -> query-vertex mask, open addressing
     __shared__ uint32_t qs[GSI_MAX_K * kPlanes];
     __shared__ uint32_t qneed[GSI_MAX_K];            // planes 1..15 where S(u) has a set bit
+    __shared__ uint32_t ht_lab[kHT], ht_mask[kHT];
     __shared__ unsigned long long cnt_s[GSI_MAX_K];
     __shared__ unsigned long long loads_s;
     for (int i = threadIdx.x; i < k * kPlanes; i += blockDim.x) qs[i] = qsig[i];
     if (threadIdx.x < GSI_MAX_K) cnt_s[threadIdx.x] = 0;
+    if (threadIdx.x < kHT) {
+        ht_lab[threadIdx.x] = 0xFFFFFFFFu;           // empty (labels are < 2^31)
+        ht_mask[threadIdx.x] = 0u;
+    }
     if (threadIdx.x == 0) loads_s = 0;
     __syncthreads();
     if (threadIdx.x < k) {
@@ -156,6 +163,14 @@ __global__ void __launch_bounds__(kThreads, GSI_FILTER_MINB) k_filter(const uint
             if (qs[threadIdx.x * kPlanes + pl]) m |= 1u << pl;
         qneed[threadIdx.x] = m;
     }
+    if (threadIdx.x == 0)
+        for (int u = 0; u < k; u++) {
+            const uint32_t L = qs[u * kPlanes];
+            uint32_t h = (L * 0x9E3779B1u) >> 26;
+            while (ht_lab[h] != 0xFFFFFFFFu && ht_lab[h] != L) h = (h + 1) & (kHT - 1);
+            ht_lab[h] = L;
+            ht_mask[h] |= 1u << u;
+        }
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
@@ -168,13 +183,13 @@ __global__ void __launch_bounds__(kThreads, GSI_FILTER_MINB) k_filter(const uint
 #pragma unroll
         for (int j = 0; j < kFW; j++) {
             const long long v = (w0 + j) * 32 + lane;
-            lab[j] = (w0 + j < words && v < n) ? __ldcs(sig + v) : 0xFFFFFFFFu;   // labels are < 2^31
+            lab[j] = (w0 + j < words && v < n) ? __ldcs(sig + v) : 0xFFFFFFFEu;   // matches no query label
         }
 #pragma unroll
-        for (int j = 0; j < kFW; j++) {
-            mask[j] = 0;
-            for (int u = 0; u < k; u++)
-                if (lab[j] == qs[u * kPlanes]) mask[j] |= 1u << u;   // label field by equality (A4)
+        for (int j = 0; j < kFW; j++) {   // label field by equality (A4): one hash probe, not k compares
+            uint32_t h = (lab[j] * 0x9E3779B1u) >> 26, e;
+            while ((e = ht_lab[h]) != lab[j] && e != 0xFFFFFFFFu) h = (h + 1) & (kHT - 1);
+            mask[j] = e == lab[j] ? ht_mask[h] : 0u;
         }
         if (!label_only) {
             // Only the planes where some label-matching u has a set bit can reject v: a plane
@@ -206,20 +221,31 @@ __global__ void __launch_bounds__(kThreads, GSI_FILTER_MINB) k_filter(const uint
                 }
             }
         }
+        // lane u collects the kFW bitmap words of query vertex u (ballots only for the query
+        // vertices some lane matched) and stores them as one 16 B vector
+        uint32_t mine[kFW];
 #pragma unroll
         for (int j = 0; j < kFW; j++) {
-            if (w0 + j >= words) break;
-            // lane u collects the bitmap word of query vertex u: one store instruction per word
-            // and a register count per lane instead of k single-lane stores and shared atomics
-            uint32_t mine = 0;
-            for (int u = 0; u < k; u++) {
+            mine[j] = 0u;
+            uint32_t present = __reduce_or_sync(0xffffffffu, mask[j]);
+            while (present) {
+                const int u = __ffs(present) - 1;
+                present &= present - 1;
                 const unsigned b = __ballot_sync(0xffffffffu, (mask[j] >> u) & 1u);
-                if (lane == u) mine = b;
+                if (lane == u) mine[j] = b;
             }
-            if (lane < k) {
-                bitmaps[(long long)lane * words + w0 + j] = mine;
-                my_count += __popc(mine);
+        }
+        if (lane < k) {
+            uint32_t *dst = bitmaps + (long long)lane * words + w0;
+            if (w0 + kFW <= words && ((words & 3) == 0)) {
+                *reinterpret_cast<uint4 *>(dst) = make_uint4(mine[0], mine[1], mine[2], mine[3]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < kFW; j++)
+                    if (w0 + j < words) dst[j] = mine[j];
             }
+#pragma unroll
+            for (int j = 0; j < kFW; j++) my_count += __popc(mine[j]);
         }
     }
     if (lane < k && my_count) atomicAdd(&cnt_s[lane], my_count);
