@@ -71,6 +71,9 @@ constexpr int kThreads = 256;
 #ifndef GSI_NEXT_LEAN
 #define GSI_NEXT_LEAN 1     // lean warp-centric J_NEXT writing rows at their Prealloc slots (0: off)
 #endif
+#ifndef GSI_COUNT_LEAN
+#define GSI_COUNT_LEAN 1    // enumerating last level on shared runs: lean warp walk (0: slot tiles)
+#endif
 #ifndef GSI_CAHEAD_U
 #define GSI_CAHEAD_U 1      // k_cahead_warp: slots per lane per pass
 #endif
@@ -1260,7 +1263,9 @@ __global__ void __launch_bounds__(kThreads, GSI_CAHEAD_MINB) k_cahead_warp(const
 // search, the candidate read and NINJ compares: every candidate x of the row's run is read
 // and checked, and contributes the row's extension count rb (same arithmetic as
 // k_cahead_warp, with the generic paths compiled out).
-template <int NINJ>
+// FINAL: the same walk as the last level of an enumerating count (count-ahead off): every
+// candidate x of a row's run that passes the subtraction is one match, counted once.
+template <int NINJ, bool FINAL>
 __global__ void __launch_bounds__(kThreads, 4) k_cahead_lean(const int32_t *__restrict__ M, long long r0, long long r1,
                                                              const Loc *__restrict__ loc, StepParams P, StepParams P2,
                                                              const int32_t *__restrict__ cip,
@@ -1277,9 +1282,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_cahead_lean(const int32_t *__re
         const int32_t *row = M + (unsigned long long)(valid ? i : r0) * (unsigned)P.t;
         const int32_t inj = (NINJ > 0 && valid) ? __ldg(row + P.inj_col[0]) : -1;
         const bool need = valid && L.len;
-        const Loc RR = warp_dedup_lookup(need, need ? __ldg(row + P2.col[0]) : -1, P2, groups, gpn);
+        Loc RR{1u, 1u};   // FINAL: each surviving candidate is one match
+        if (!FINAL) RR = warp_dedup_lookup(need, need ? __ldg(row + P2.col[0]) : -1, P2, groups, gpn);
         uint32_t rbase = RR.len;
-        for (int c = 0; c < ninj2 && rbase; c++) {
+        for (int c = 0; c < ninj2 && rbase && !FINAL; c++) {
             const int32_t y = __ldg(row + P2.inj_col[c]);
             if (in_bitmap(P2.cu, y) && in_sorted(P2.fci + RR.off, RR.len, y)) rbase--;
         }
@@ -2411,6 +2417,25 @@ gsi_status build_F(QueryCtx &C, const Loc *loc, unsigned long long nM, int E, un
 
 bool cahead_warp_enabled() { return GSI_CAHEAD_WARP && !env_flag("GSI_CAHEAD_TILE"); }
 
+// The last level of an enumerating count on shared runs is walked row-wise by the lean warp
+// kernel (no F, holes allowed).
+bool final_walks_rows(const QueryCtx &C, const StepParams &P, int mode) {
+    return mode == J_COUNT && GSI_COUNT_LEAN && !env_flag("GSI_COUNT_NOLEAN") && P.prefiltered && !P.fp && P.E == 1 &&
+           P.n_inj <= 1 && cahead_warp_enabled();
+}
+
+// The level after step si will walk its rows without F (the warp count-ahead, or the lean last
+// level), so step si may skip F' and write its rows at their Prealloc slots.
+bool next_walks_rows(const QueryCtx &C, size_t si, bool pf_next) {
+    if (!pf_next || !C.sharded || C.opts.want_table || C.opts.fingerprint || C.opts.e0_mode != 0 ||
+        C.opts.no_shared_lists || !cahead_warp_enabled())
+        return false;
+    const size_t nl = si + 1;
+    if (nl + 2 == C.steps.size()) return !C.opts.no_count_ahead && C.steps[nl + 1].col.size() == 1;
+    if (nl + 1 == C.steps.size()) return GSI_COUNT_LEAN && !env_flag("GSI_COUNT_NOLEAN") && C.steps[nl].col.size() == 1;
+    return false;
+}
+
 // Level t = steps[si].t: M (nM x t) with its Prealloc (loc, F, |GBA| = gba) already computed
 // (by k_probe for level 1, by the previous level's fused kernel otherwise).
 gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc *loc, unsigned long long *F,
@@ -2476,7 +2501,12 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
     }
 
     // rows without F (see no_f2): build it unless the warp count-ahead consumes them as they are
-    if (!F && (!(cahead && P.prefiltered && cahead_warp_enabled()) || !C.sharded)) GSI_TRY(build_F(C, loc, nM, E, &F));
+    {
+        StepParams Pl = P;   // (the last level's lean walk needs no F either)
+        const bool walker = (cahead && P.prefiltered && cahead_warp_enabled()) ||
+                            (last && !C.opts.want_table && final_walks_rows(C, Pl, J_COUNT));
+        if (!F && (!walker || !C.sharded)) GSI_TRY(build_F(C, loc, nM, E, &F));
+    }
 
     // ---- shard this level's slot range ----
     unsigned long long s0 = 0, s1 = gba;
@@ -2577,11 +2607,7 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         P.stage_next = mode == J_NEXT && P2.E == 1 && P2.col[0] < P.t && GSI_STAGE_NEXT;
         // the next level is the count-ahead level on shared lists, walked by the warp kernel
         // (no F needed): skip F' and its look-back chain
-        P.no_f2 = 0;
-        if (mode == J_NEXT && pf_next && si + 3 == C.steps.size() && !C.opts.want_table && !C.opts.fingerprint &&
-            !C.opts.no_count_ahead && !C.opts.no_shared_lists && C.opts.e0_mode == 0 &&
-            C.steps[si + 2].col.size() == 1 && cahead_warp_enabled() && C.sharded)
-            P.no_f2 = 1;
+        P.no_f2 = mode == J_NEXT && next_walks_rows(C, si, pf_next) ? 1 : 0;
         // lean J_NEXT: count-only, one linking edge here and in the next step (on shared runs),
         // and the next level is the warp count-ahead, which walks rows with holes at no cost
         // (a deeper level would pay for them: more rows, and an F to build)
@@ -2589,8 +2615,9 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         const bool lean_next = P.no_f2 && GSI_NEXT_LEAN && !env_flag("GSI_NEXT_NOLEAN") && P.E == 1 && P2.E == 1 &&
                                P.n_inj <= 1 && !C.lean_off[si];
         const bool warp_ca = mode == J_CAHEAD && P.prefiltered && cahead_warp_enabled();
+        const bool final_lean = final_walks_rows(C, P, mode);
         uint32_t *rowmap = nullptr;
-        if (!warp_ca && !lean_next) {   // first/last row of every slot tile (the warp count-ahead walks rows)
+        if (!warp_ca && !lean_next && !final_lean) {   // first/last row of every slot tile (the warp count-ahead walks rows)
             GSI_TRY(A.get(&rowmap, (unsigned long long)jt + 1));
             prof.begin(GSI_K_OTHER);
             k_tile_rows<<<grid_for((unsigned long long)jt + 1, kThreads), kThreads, 0, st>>>(F, (long long)nM, c0, c1, jt,
@@ -2627,14 +2654,24 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
             for (int c = 0; c < P2.n_inj; c++) xinj |= P2.inj_col[c] >= P.t;
             const bool lean = GSI_CAHEAD_LEAN && !env_flag("GSI_CAHEAD_NOLEAN") && P2.col[0] < P.t && !xinj && P.E == 1 && P.n_inj <= 1;
             if (lean && P.n_inj == 0)
-                k_cahead_lean<0><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, P2, cip, g->groups, g->gpn, lctr);
+                k_cahead_lean<0, false><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, P2, cip, g->groups, g->gpn, lctr);
             else if (lean)
-                k_cahead_lean<1><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, P2, cip, g->groups, g->gpn, lctr);
+                k_cahead_lean<1, false><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, P2, cip, g->groups, g->gpn, lctr);
             else
                 k_cahead_warp<<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, P2, cip, cu, g->groups, g->gpn, lctr);
             if (getenv("GSI_TRACE"))
                 fprintf(stderr, "[cahead] t %d rows %lld slots %llu w %d rowR %d pa %d ninj %d ninj2 %d E %d\n", t,
                         r_hi - r_lo, s1 - s0, P.t, P2.col[0] < P.t, P.pa != nullptr, P.n_inj, P2.n_inj, P.E);
+        } else if (final_lean) {
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
+            const unsigned long long units = ((unsigned long long)(r_hi - r_lo) + 31) / 32;
+            const unsigned wg = (unsigned)std::max<unsigned long long>(
+                1, std::min<unsigned long long>((units + 7) / 8, (unsigned long long)sms * 8));
+            if (P.n_inj == 0)
+                k_cahead_lean<0, true><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, P2, cip, g->groups, g->gpn, lctr);
+            else
+                k_cahead_lean<1, true><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, P2, cip, g->groups, g->gpn, lctr);
         } else if (fast) {
             const size_t fsm = (size_t)tile_slots * 4 * (2 + (size_t)std::min(P.n_inj, P.stage_inj));
             k_count_fast<kFastItems><<<jt, kThreads, fsm, st>>>(M, (long long)nM, F, loc, rowmap, P, cip, c0, c1,

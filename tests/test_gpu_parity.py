@@ -420,6 +420,7 @@ def test_count_ahead_matches_oracle(kernel, monkeypatch):
     monkeypatch.setenv("GSI_CAHEAD_TILE", "1" if kernel == "tile" else "0")
     monkeypatch.setenv("GSI_CAHEAD_NOLEAN", "1" if kernel != "lean" else "0")
     monkeypatch.setenv("GSI_NEXT_NOLEAN", "1" if kernel != "lean" else "0")   # lean J_NEXT (holes) too
+    monkeypatch.setenv("GSI_COUNT_NOLEAN", "1" if kernel != "lean" else "0")  # and the enumerating last level
     seen = 0
     for gs, nlv, nle, k in [(81, 1, 2, 6), (82, 2, 3, 7), (83, 3, 4, 6), (84, 2, 1, 5)]:
         g = W.chung_lu(4000, 30000, 500, nlv=nlv, nle=nle, seed=gs)
