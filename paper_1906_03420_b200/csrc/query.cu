@@ -1297,6 +1297,21 @@ __global__ void __launch_bounds__(kThreads, 4) k_cahead_lean(const int32_t *__re
         }
         const uint32_t excl = inc - L.len;
         const uint32_t T = __shfl_sync(0xffffffffu, inc, 31);
+        // Rows of a unit are mostly siblings with runs of similar length: when the longest
+        // run is at most twice the mean, every lane walks its own row (no owner search, no
+        // shuffles; >= 50 % of the lanes busy); otherwise the balanced walk below.
+        const uint32_t maxlen = __reduce_max_sync(0xffffffffu, L.len);
+        if (maxlen * 16 <= T) {
+            for (uint32_t kk = 0; kk < maxlen; kk++) {
+                if (kk >= L.len) break;
+                const int32_t x = __ldg(cip + L.off + kk);
+                if (NINJ > 0 && x == inj) continue;
+                surv++;
+                bound += RR.len;
+                cnt += rbase;
+            }
+            continue;
+        }
         for (uint32_t j0 = 0; j0 < T; j0 += 32) {
             const uint32_t j = j0 + lane;
             int o = 0;
