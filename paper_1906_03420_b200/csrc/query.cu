@@ -607,7 +607,9 @@ __global__ void __launch_bounds__(kThreads, join_items(MODE) > 8 ? 2 : (((MODE =
     const unsigned tile = tile_s;
     const unsigned long long tbase = s0 + (unsigned long long)tile * TILE;
     const unsigned long long tend = min(tbase + (unsigned long long)TILE, s1);
-    const long long rlo = __ldg(rowmap + tile), rhi = __ldg(rowmap + tile + 1);
+    // (no rowmap: a single tile, which may scan every row of the level)
+    const long long rlo = rowmap ? (long long)__ldg(rowmap + tile) : 0ll;
+    const long long rhi = rowmap ? (long long)__ldg(rowmap + tile + 1) : nM - 1;
     const long long nr = rhi - rlo + 1;
     // Stage, per row of the tile, base = off0 - F_i (so slot s reads ci[base + s]) and the
     // columns the subtraction tests, so the per-slot work touches shared memory only.
@@ -1009,7 +1011,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_count_fast(const int32_t *__res
         for (int j = tid; j < TILE / 4; j += kThreads) z[j] = make_int4(0, 0, 0, 0);
     }
     __syncthreads();
-    const long long rlo = __ldg(rowmap + tile), rhi = __ldg(rowmap + tile + 1);
+    // (no rowmap: a single tile, which may scan every row of the level)
+    const long long rlo = rowmap ? (long long)__ldg(rowmap + tile) : 0ll;
+    const long long rhi = rowmap ? (long long)__ldg(rowmap + tile + 1) : nM - 1;
     const long long nr = rhi - rlo + 1;
     const bool staged = nr <= TILE;
     const int ninj = P.n_inj, nst = staged ? min(ninj, P.stage_inj) : 0;
@@ -1760,6 +1764,10 @@ struct Workspace {
 };
 constexpr int kWsSlots = 8;        // concurrent queries per device with their own workspace
 Workspace g_ws[64][kWsSlots];
+// Device-wide high-water demand: every slot grows to the largest query seen on the device,
+// so a heavy query never lands on a slot that only ever ran light ones (concurrent batches
+// assign queries to slots dynamically).
+std::atomic<size_t> g_ws_want[64];
 
 }  // namespace
 
@@ -1774,6 +1782,7 @@ void workspace_trim(int dev) {
         W.cap = 0;
         W.want = 64ull << 20;   // a new graph: learn its queries' demand afresh
     }
+    g_ws_want[dev] = 0;
 }
 
 // Bytes held by the device's idle workspaces (they count as available to a new query).
@@ -1809,7 +1818,7 @@ struct Arena {
         Workspace &W = g_ws[dev][slot];
         std::lock_guard<std::mutex> lk(W.mu);
         if (W.busy) return;
-        const size_t bytes = std::min(budget, std::max(W.want, (size_t)64 << 20));
+        const size_t bytes = std::min(budget, std::max(std::max(W.want, g_ws_want[dev].load()), (size_t)64 << 20));
         const auto t0 = std::chrono::steady_clock::now();
         if (W.cap < bytes) {
             if (W.base) cudaFree(W.base);
@@ -1904,6 +1913,9 @@ struct Arena {
             std::lock_guard<std::mutex> lk(W.mu);
             W.busy = false;
             W.want = std::max(W.want, demand + demand / 8);
+            size_t cur = g_ws_want[ws_dev].load();
+            while (W.want > cur && !g_ws_want[ws_dev].compare_exchange_weak(cur, W.want)) {
+            }
         }
     }
 };
@@ -2636,7 +2648,9 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         const bool warp_ca = mode == J_CAHEAD && P.prefiltered && cahead_warp_enabled();
         const bool final_lean = final_walks_rows(C, P, mode);
         uint32_t *rowmap = nullptr;
-        if (!warp_ca && !lean_next && !final_lean) {   // first/last row of every slot tile (the warp count-ahead walks rows)
+        // first/last row of every slot tile (the warp kernels walk rows; a single tile scans
+        // the level's rows itself, which saves a launch per small level)
+        if (!warp_ca && !lean_next && !final_lean && (jt > 1 || nM > 2048)) {
             GSI_TRY(A.get(&rowmap, (unsigned long long)jt + 1));
             prof.begin(GSI_K_OTHER);
             k_tile_rows<<<grid_for((unsigned long long)jt + 1, kThreads), kThreads, 0, st>>>(F, (long long)nM, c0, c1, jt,
