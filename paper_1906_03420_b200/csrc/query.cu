@@ -74,6 +74,9 @@ constexpr int kThreads = 256;
 #ifndef GSI_COUNT_LEAN
 #define GSI_COUNT_LEAN 1    // enumerating last level on shared runs: lean warp walk (0: slot tiles)
 #endif
+#ifndef GSI_CAHEAD_LONG
+#define GSI_CAHEAD_LONG 1   // k_cahead_lean: rows with >= 32 candidates walked warp-cooperatively
+#endif
 #ifndef GSI_CAHEAD_U
 #define GSI_CAHEAD_U 1      // k_cahead_warp: slots per lane per pass
 #endif
@@ -1320,7 +1323,39 @@ __global__ void __launch_bounds__(kThreads, 4) k_cahead_lean(const int32_t *__re
             }
             continue;
         }
-        for (uint32_t j0 = 0; j0 < T; j0 += 32) {
+#if GSI_CAHEAD_LONG
+        // Rows with >= 32 candidates are walked by the whole warp, one row at a time (the row's
+        // data broadcast once, no owner search); the rest by the balanced walk below.
+        uint32_t longs = __ballot_sync(0xffffffffu, L.len >= 32);
+        while (longs) {
+            const int r = __ffs(longs) - 1;
+            longs &= longs - 1;
+            const uint32_t off = __shfl_sync(0xffffffffu, L.off, r), len = __shfl_sync(0xffffffffu, L.len, r);
+            const uint32_t rb = __shfl_sync(0xffffffffu, rbase, r), rl = __shfl_sync(0xffffffffu, RR.len, r);
+            const int32_t ri = NINJ > 0 ? __shfl_sync(0xffffffffu, inj, r) : -1;
+            for (uint32_t kk = lane; kk < len; kk += 32) {
+                const int32_t x = __ldg(cip + off + kk);
+                if (NINJ > 0 && x == ri) continue;
+                surv++;
+                bound += rl;
+                cnt += rb;
+            }
+        }
+        if (__any_sync(0xffffffffu, L.len >= 32)) {   // the balanced walk over the short rows only
+            const uint32_t sl = L.len >= 32 ? 0u : L.len;
+            inc = sl;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+        }
+        const uint32_t excl2 = inc - (L.len >= 32 ? 0u : L.len);
+        const uint32_t T2 = __shfl_sync(0xffffffffu, inc, 31);
+#else
+        const uint32_t excl2 = excl, T2 = T;
+#endif
+        for (uint32_t j0 = 0; j0 < T2; j0 += 32) {
             const uint32_t j = j0 + lane;
             int o = 0;
 #pragma unroll
@@ -1329,11 +1364,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_cahead_lean(const int32_t *__re
                 if (v <= j) o += st;
             }
             o &= 31;
-            const uint32_t pos = __shfl_sync(0xffffffffu, L.off, o) + (j - __shfl_sync(0xffffffffu, excl, o));
+            const uint32_t pos = __shfl_sync(0xffffffffu, L.off, o) + (j - __shfl_sync(0xffffffffu, excl2, o));
             const uint32_t rb = __shfl_sync(0xffffffffu, rbase, o);
             const uint32_t rl = __shfl_sync(0xffffffffu, RR.len, o);
             const int32_t ri = NINJ > 0 ? __shfl_sync(0xffffffffu, inj, o) : -1;
-            if (j >= T) continue;
+            if (j >= T2) continue;
             const int32_t x = __ldg(cip + pos);
             if (NINJ > 0 && x == ri) continue;
             surv++;
