@@ -2075,6 +2075,21 @@ unsigned long long available_bytes(int dev) {
     return (unsigned long long)fr + (reserved > used ? reserved - used : 0);
 }
 
+// One pinned Counters block per host thread (levels of a query run on one thread, one at a
+// time); nullptr if pinned memory is unavailable.
+Counters *pinned_counters() {
+    thread_local Counters *p = nullptr;
+    thread_local bool tried = false;
+    if (!tried) {
+        tried = true;
+        if (cudaMallocHost((void **)&p, sizeof(Counters)) != cudaSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+        }
+    }
+    return p;
+}
+
 // Test / A-B switches read per query (never needed in production).
 bool env_flag(const char *name) {
     const char *e = getenv(name);
@@ -2700,6 +2715,7 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
             k_tile_rows<<<1, 32, 0, st>>>(F, (long long)nM, c0, c1, 1, (unsigned)std::min<unsigned long long>(slots, 0xFFFFFFFFull), rows2);
             prof.end();
         }
+        Counters hc_local;
         prof.begin(GSI_K_JOIN);
         if (lean_next) {
             int sms = 148;
@@ -2757,10 +2773,13 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
             k_join<J_NEXT><<<jt, kThreads, join_smem_bytes(J_NEXT, P), st>>>(M, (long long)nM, F, loc, rowmap, P, P2, cip, cu, g->groups,
                                                     g->gpn, c0, c1, out, loc2, F2, st1, st2, tctr, lctr);
         prof.end();
-        Counters hc;
-        GSI_CUDA(d2h(S, &hc, lctr, sizeof(Counters), st));
+        // the level's counters come back through pinned memory (a pageable copy stages
+        // through a driver buffer: ~10 us more per level on the small-query critical path)
+        Counters *hp = pinned_counters();
+        GSI_CUDA(d2h(S, hp ? (void *)hp : (void *)&hc_local, lctr, sizeof(Counters), st));
         GSI_CUDA(sync_timed(S, st));
         GSI_CUDA(cudaGetLastError());
+        const Counters hc = hp ? *hp : hc_local;
         A.release(status);
         A.release(rowmap);
         // J_NEXT: stored rows (lean: every slot of the chunk, holes included)
