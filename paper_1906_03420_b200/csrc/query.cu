@@ -2345,6 +2345,10 @@ struct QueryCtx {
     std::vector<std::pair<uint32_t *, int32_t *>> filt;             // per step: (fpos, fci) or null
     std::vector<Loc *> pa;                                           // per step: probe-ahead table or null
     std::vector<char> lean_off;                                      // per step: lean J_NEXT left too many holes
+    // Zeroed once per query; every level launch takes a never-used slice for its counters and
+    // look-back status words (saves a memset per level on the small-query critical path).
+    unsigned long long *zpool = nullptr;
+    unsigned long long zcap = 0, zoff = 0;
     // Stored columns.  Count-only mode stores in M_t only the columns a later step reads (its
     // linking columns and subtraction columns); phys[t][c] = position of logical column c in
     // a row of M_t (-1: dropped), width[t] = stored columns.  Table / fingerprint: all.
@@ -2632,8 +2636,15 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         // one zeroed scratch region per launch: [Counters | tile counter + status 1 | status 2]
         constexpr unsigned kCtrWords = sizeof(Counters) / 8;
         unsigned long long *status = nullptr;
-        GSI_TRY(A.get(&status, kCtrWords + 2ull * jt + 2));
-        GSI_CUDA(cudaMemsetAsync(status, 0, 8ull * (kCtrWords + 2ull * jt + 2), st));
+        const unsigned long long swords = kCtrWords + 2ull * jt + 2;
+        const bool zslice = C.zoff + swords <= C.zcap;
+        if (zslice) {   // a fresh slice of the query's pre-zeroed pool
+            status = C.zpool + C.zoff;
+            C.zoff += (swords + 3) & ~3ull;
+        } else {
+            GSI_TRY(A.get(&status, swords));
+            GSI_CUDA(cudaMemsetAsync(status, 0, 8ull * swords, st));
+        }
         Counters *lctr = reinterpret_cast<Counters *>(status);
         unsigned *tctr = (unsigned *)(status + kCtrWords);
         unsigned long long *st1 = status + kCtrWords + 1, *st2 = status + kCtrWords + 2 + jt;
@@ -2780,7 +2791,7 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         GSI_CUDA(sync_timed(S, st));
         GSI_CUDA(cudaGetLastError());
         const Counters hc = hp ? *hp : hc_local;
-        A.release(status);
+        if (!zslice) A.release(status);
         A.release(rowmap);
         // J_NEXT: stored rows (lean: every slot of the chunk, holes included)
         const unsigned long long nout = (mode == J_COUNT || mode == J_CAHEAD) ? hc.count : (lean_next ? slots : hc.total);
@@ -2881,6 +2892,15 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     }
     A.init_workspace(g->device, budget);
     GSI_TRY(A.get(&C.ctr, 1));
+    {
+        constexpr unsigned long long kZWords = 1ull << 17;   // 1 MB
+        if (A.get_big(&C.zpool, kZWords) == GSI_OK && cudaMemsetAsync(C.zpool, 0, 8ull * kZWords, st) == cudaSuccess) {
+            C.zcap = kZWords;
+        } else {
+            cudaGetLastError();
+            C.zpool = nullptr;
+        }
+    }
     GSI_CUDA(cudaMemsetAsync(C.ctr, 0, sizeof(Counters), st));
 
     // ---------------- filter (a3) ----------------
