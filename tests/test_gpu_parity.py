@@ -505,3 +505,21 @@ def test_query_batch_concurrent():
     other = gsi.build(W.cycle_graph(5))
     with pytest.raises(gsi.GsiError):
         gsi.gsi_query_run_batch(other, prepared, concurrency=2)
+
+
+def test_workspace_trim_and_reuse():
+    """The per-device query workspace is reused across queries, grows with demand and can be
+    freed at any time (gsi_trim_workspace) without changing any result."""
+    g = W.chung_lu(20_000, 120_000, 2_000, nlv=8, nle=6, seed=95)
+    graph = gsi.build(g)
+    og = oracle.OracleGraph(g)
+    qs = bounded_queries(g, og, 7, range(9500, 9540), lo=1000, hi=3_000_000, want=4)
+    assert qs
+    ref = [oracle.match(og, q, table=False)[0] for q in qs]
+    for rep in range(2):
+        for q, c in zip(qs, ref):
+            assert gsi.query(graph, q, fingerprint=False).count == c
+            assert gsi.query(graph, q, fingerprint=False, count_ahead=False).count == c
+        gsi.gsi_trim_workspace()
+        gsi.gsi_trim_workspace(0)
+    assert gsi.query(graph, qs[0], fingerprint=False, mem_budget_bytes=64 << 20).count == ref[0]
