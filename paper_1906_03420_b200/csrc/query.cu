@@ -77,6 +77,9 @@ constexpr int kThreads = 256;
 #ifndef GSI_CAHEAD_LONG
 #define GSI_CAHEAD_LONG 1   // k_cahead_lean: rows with >= 32 candidates walked warp-cooperatively
 #endif
+#ifndef GSI_FP_ITEMS
+#define GSI_FP_ITEMS 8      // k_filter_partition: entries per thread (tile = 256 x this)
+#endif
 #ifndef GSI_CAHEAD_U
 #define GSI_CAHEAD_U 1      // k_cahead_warp: slots per lane per pass
 #endif
@@ -1306,7 +1309,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_cahead_lean(const int32_t *__re
             const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
             if (lane >= o) inc += y;
         }
-        const uint32_t excl = inc - L.len;
         const uint32_t T = __shfl_sync(0xffffffffu, inc, 31);
         // Rows of a unit are mostly siblings with runs of similar length: when the longest
         // run is at most twice the mean, every lane walks its own row (no owner search, no
@@ -1353,7 +1355,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_cahead_lean(const int32_t *__re
         const uint32_t excl2 = inc - (L.len >= 32 ? 0u : L.len);
         const uint32_t T2 = __shfl_sync(0xffffffffu, inc, 31);
 #else
-        const uint32_t excl2 = excl, T2 = T;
+        const uint32_t excl2 = inc - L.len, T2 = T;
 #endif
         for (uint32_t j0 = 0; j0 < T2; j0 += 32) {
             const uint32_t j = j0 + lane;
@@ -1526,7 +1528,7 @@ __global__ void __launch_bounds__(kThreads) k_filter_partition(const int32_t *__
                                                                uint32_t *__restrict__ fpos,
                                                                int32_t *__restrict__ fci,
                                                                unsigned long long *status, unsigned *tile_ctr) {
-    constexpr int IT = 8, TILE = IT * kThreads;
+    constexpr int IT = GSI_FP_ITEMS, TILE = IT * kThreads;
     __shared__ unsigned wcnt[IT][kThreads / 32];
     __shared__ unsigned wbase[IT][kThreads / 32];
     __shared__ unsigned tile_s, agg_s;
@@ -2449,7 +2451,7 @@ gsi_status ensure_filtered(QueryCtx &C, size_t si, uint32_t lab) {
     int32_t *fci = nullptr;
     GSI_TRY(A.get_big(&fpos, (unsigned long long)(hi - lo) + 1));
     GSI_TRY(A.get_big(&fci, (unsigned long long)(hi - lo)));
-    const unsigned ft = grid_for(hi - lo, 8 * kThreads);
+    const unsigned ft = grid_for(hi - lo, GSI_FP_ITEMS * kThreads);
     unsigned long long *fst = nullptr;
     GSI_TRY(A.get_big(&fst, (unsigned long long)ft + 1));
     GSI_CUDA(cudaMemsetAsync(fst, 0, 8ull * (ft + 1), st));
