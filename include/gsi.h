@@ -23,7 +23,7 @@
  *    different host threads on different streams.
  *  - Streams: `stream` fields take a cudaStream_t (NULL = the per-thread default stream).
  *    Calls return after the work they enqueue has completed (counts are host values).
- *  - Limits: |V| < 2^31, 2|E| < 2^32, query k <= 32 vertices, labels are int32 >= 0.
+ *  - Limits: |V| < 2^31 - 1, 2|E| < 2^31 - 1, query k <= 32 vertices, labels are int32 >= 0.
  */
 #ifndef GSI_H
 #define GSI_H
@@ -57,6 +57,26 @@ typedef enum {
 /* Kernel classes reported in gsi_stats (profile mode). */
 enum { GSI_K_FILTER = 0, GSI_K_COMPACT = 1, GSI_K_PROBE = 2, GSI_K_JOIN = 3, GSI_K_LINK = 4,
        GSI_K_OTHER = 5 };
+
+/* Kernel variants: gsi_stats.variant_launches[v] counts the launches of each (always, not only
+ * in profile mode), so a test can prove which code path produced a result. */
+#define GSI_N_KVARIANT 16
+enum { GSI_V_JOIN_NEXT = 0,       /* k_join<J_NEXT>: slot tiles, compacting (Combine) write     */
+       GSI_V_JOIN_COUNT = 1,      /* k_join<J_COUNT>: slot tiles, final level count (+ hash)    */
+       GSI_V_JOIN_TABLE = 2,      /* k_join<J_TABLE>: slot tiles, final table                  */
+       GSI_V_JOIN_CAHEAD = 3,     /* k_join<J_CAHEAD>: slot tiles, count-ahead                 */
+       GSI_V_COUNT_FAST = 4,      /* k_count_fast: slot tiles, final count on shared runs      */
+       GSI_V_NEXT_LEAN = 5,       /* k_next_lean: warp rows, rows at their Prealloc slots      */
+       GSI_V_CAHEAD_WARP = 6,     /* k_cahead_warp: generic warp count-ahead                   */
+       GSI_V_CAHEAD_LEAN = 7,     /* k_cahead_lean<*,false>: closed-form count-ahead           */
+       GSI_V_FINAL_LEAN = 8,      /* k_cahead_lean<*,true>: closed-form final count            */
+       GSI_V_FINAL_FP = 9,        /* k_final_fp: every final match read and hashed             */
+       GSI_V_FILTER_PARTITION = 10, /* k_filter_partition: shared N(v,l0) ∩ C(u) runs          */
+       GSI_V_REFILTER = 11,       /* k_refilter: a level re-pointed at shared runs             */
+       GSI_V_PROBE_AHEAD = 12,    /* k_probe_ahead: per-candidate next-step locate table       */
+       GSI_V_SMALL = 13,          /* k_small_query: whole query in one launch                  */
+       GSI_V_TWO_STEP = 14,       /* ablation: count pass of the two-step output               */
+       GSI_V_RESERVED = 15 };
 
 typedef struct gsi_graph gsi_graph;       /* opaque: PCSR + signature table on one device   */
 typedef struct gsi_result gsi_result;     /* opaque: count, fingerprint, optional table     */
@@ -216,6 +236,7 @@ typedef struct {
     int32_t count_ahead;              /* 1: the last level was counted by the level before it    */
     uint32_t n_probe_ahead;           /* levels whose next-step locate came from a per-candidate
                                          probe-ahead table instead of a PCSR probe per new row   */
+    uint32_t variant_launches[GSI_N_KVARIANT]; /* launches per kernel variant (GSI_V_*)         */
 } gsi_stats;
 
 gsi_status gsi_result_count(const gsi_result *r, uint64_t *count);

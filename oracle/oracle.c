@@ -131,8 +131,9 @@ int64_t og_neighbors(const og_graph *g, int32_t v, int32_t l, int32_t *out, int6
 
 /* ------------------------------------------------------------- fingerprint ------- */
 /* SURVEY.md §8(c) 'Set fingerprint': FP(R) = (|R|, sum_rows h1(row) mod 2^64,
- * xor_rows h2(row)), rows in query-id order.  h(row, seed): h = seed; for each column
- * c: h = splitmix64_finalizer(h ^ (uint32)row[c]).  Commutative, hence order-free.    */
+ * xor_rows h2(row)), rows in query-id order (DESIGN.md §3 'Fingerprint').  A row's hash
+ * with seed s: S = sum over columns c of mix(s ^ (c+1) << 32 ^ (uint32)row[c]) mod 2^64,
+ * h = mix(S), mix = the splitmix64 finaliser.  Sum/xor over rows: order-free.          */
 #define OG_FP_SEED1 0x243F6A8885A308D3ull
 #define OG_FP_SEED2 0x13198A2E03707344ull
 static uint64_t og_mix64(uint64_t z) {
@@ -142,9 +143,10 @@ static uint64_t og_mix64(uint64_t z) {
     return z ^ (z >> 31);
 }
 static uint64_t og_rowhash(const int32_t *row, int32_t k, uint64_t seed) {
-    uint64_t h = seed;
-    for (int32_t c = 0; c < k; c++) h = og_mix64(h ^ (uint64_t)(uint32_t)row[c]);
-    return h;
+    uint64_t S = 0;
+    for (int32_t c = 0; c < k; c++)
+        S += og_mix64(seed ^ ((uint64_t)(uint32_t)(c + 1) << 32) ^ (uint64_t)(uint32_t)row[c]);
+    return og_mix64(S);
 }
 void og_fingerprint_rows(const int32_t *rows, int64_t nrows, int32_t k, uint64_t fp[3]) {
     fp[0] = (uint64_t)nrows; fp[1] = 0; fp[2] = 0;

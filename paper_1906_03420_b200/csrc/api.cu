@@ -247,7 +247,11 @@ gsi_status gsi_query_run(const gsi_graph *g, const gsi_prepared *q, const gsi_qu
     return run_impl(g, q, opts, out);
 }
 
-void gsi_prepared_free(gsi_prepared *q) { delete q; }
+void gsi_prepared_free(gsi_prepared *q) {
+    if (!q) return;
+    cudaSetDevice(q->device);   // its device copy of the signatures lives on the graph's device
+    delete q;
+}
 
 gsi_status gsi_query_run_batch(const gsi_graph *g, int32_t nq, const gsi_prepared *const *qs,
                                const gsi_query_opts *opts, int32_t concurrency, gsi_result **out) {

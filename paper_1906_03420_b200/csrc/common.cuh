@@ -69,6 +69,14 @@ __host__ __device__ __forceinline__ uint64_t fp_mix(uint64_t z) {
     return z ^ (z >> 31);
 }
 
+// Set fingerprint: the hash of a final row (query-id order) is
+// fp_mix(Σ_q fp_term(seed, q, row[q]) mod 2^64) — a per-column keyed term, summed, then
+// finalised, so a row's k-1 parent terms can be summed once and each extension x costs one
+// term and one finaliser.
+__host__ __device__ __forceinline__ uint64_t fp_term(uint64_t seed, int q, uint32_t v) {
+    return fp_mix(seed ^ ((uint64_t)(uint32_t)(q + 1) << 32) ^ (uint64_t)v);
+}
+
 // Home group of v in partition l: multiply-high range reduction of f(v) (reading A7).
 __host__ __device__ __forceinline__ uint32_t pcsr_home(uint32_t v, uint32_t l_dense, uint32_t ngroups) {
     uint32_t h = murmur2_u32(v, kPcsrSeed ^ l_dense);
@@ -370,6 +378,7 @@ struct gsi_graph {
 // A validated, encoded query (opaque to callers).
 struct gsi_prepared {
     const gsi_graph *g = nullptr;
+    int device = 0;                  // g->device at prepare time
     int k = 0;
     std::vector<int32_t> qvl, qs, qd, qe;
     std::vector<int> qe_dense;       // -1: label absent from G

@@ -302,8 +302,9 @@ gsi_status build_graph_impl(int64_t n, const int32_t *h_vl, int64_t m, const int
         set_error("gpn must be in [2,16] (PAPER.md L700-701)");
         return GSI_ERR_INVALID_ARG;
     }
-    if (n < 0 || m < 0 || n >= (1ll << 31) - 1 || 2 * m >= (1ll << 32) - 1) {
-        set_error("need 0 <= n < 2^31-1 and 0 <= 2m < 2^32-1");
+    // 2m < 2^31: the build's CUB sort / unique / scan calls take int item counts
+    if (n < 0 || m < 0 || n >= (1ll << 31) - 1 || 2 * m >= (1ll << 31) - 1) {
+        set_error("need 0 <= n < 2^31-1 and 0 <= 2m < 2^31-1");
         return GSI_ERR_INVALID_ARG;
     }
     if ((n > 0 && !h_vl) || (m > 0 && (!h_src || !h_dst || !h_el))) {
@@ -384,6 +385,9 @@ gsi_status build_graph_impl(int64_t n, const int32_t *h_vl, int64_t m, const int
 
     if (m == 0) {
         g->ci_lo.assign(1, 0u);
+        g->freq.clear();
+        g->gbase.assign(1, 0);
+        g->ngroups.assign(1, 0u);
         GSI_CUDA(cudaMalloc(&g->groups, 16));
         GSI_CUDA(cudaMalloc(&g->ci, 16));
         GSI_CUDA(cudaStreamSynchronize(st));

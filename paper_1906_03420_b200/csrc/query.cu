@@ -435,17 +435,18 @@ __device__ __forceinline__ bool in_sorted(const int32_t *__restrict__ a, uint32_
     return lo < n && __ldg(a + lo) == x;
 }
 
+// Set fingerprint of a final row m || x: h_j = fp_mix(Σ_q fp_term(seed_j, q, row[q])).
 __device__ __forceinline__ void row_hash(const int32_t *__restrict__ row, uint32_t x, const StepParams &P,
                                          unsigned long long &h1, unsigned long long &h2) {
-    unsigned long long a = kFpSeed1, b = kFpSeed2;
+    unsigned long long a = 0, b = 0;
     for (int q = 0; q < P.k; q++) {
         const int col = P.pos_of_q[q];
         const uint32_t val = col < P.t ? (uint32_t)__ldg(row + col) : x;
-        a = fp_mix(a ^ val);
-        b = fp_mix(b ^ val);
+        a += fp_term(kFpSeed1, q, val);
+        b += fp_term(kFpSeed2, q, val);
     }
-    h1 += a;
-    h2 ^= b;
+    h1 += fp_mix(a);
+    h2 ^= fp_mix(b);
 }
 
 enum JoinMode { J_COUNT = 0, J_TABLE = 1, J_NEXT = 2, J_CAHEAD = 3 };
@@ -1270,15 +1271,17 @@ __global__ void __launch_bounds__(kThreads, GSI_CAHEAD_MINB) k_cahead_warp(const
     }
 }
 
-// The common count-ahead shape, lean: the last step links to a parent column (its run and
-// the row-column subtraction hits are per row, located with warp duplicate removal), the
-// vertex this step adds is not a subtraction column of the last step, one linking edge on
-// shared runs, at most NINJ subtraction columns in this step.  A slot then costs the owner
-// search, the candidate read and NINJ compares: every candidate x of the row's run is read
-// and checked, and contributes the row's extension count rb (same arithmetic as
-// k_cahead_warp, with the generic paths compiled out).
-// FINAL: the same walk as the last level of an enumerating count (count-ahead off): every
-// candidate x of a row's run that passes the subtraction is one match, counted once.
+// The common count-ahead shape, lean and in closed form: the last step links to a parent
+// column (its run RR and the row-column subtraction hits against it are per row, located with
+// warp duplicate removal), the vertex this step adds is not a subtraction column of the last
+// step, one linking edge on shared runs (every candidate of the row's run L is already in
+// C(u)), at most NINJ (<= 1) subtraction columns in this step.  Then for row m of M_{k-2}:
+//   survivors  s(m) = |L| - [inj(m) in L]                      (Alg. 3 lines 9-10)
+//   extensions of each survivor m || x = rb(m) = |RR| - |{y in m : y in RR}|  (constant in x)
+// so the row contributes s(m) * rb(m) matches with one binary search for inj in L and one per
+// last-step subtraction column in RR — no walk over the candidates.
+// FINAL: the same row formula as the last level of an enumerating count (count-ahead off):
+// the row's matches are the candidates of L minus the subtraction hit, s(m).
 template <int NINJ, bool FINAL>
 __global__ void __launch_bounds__(kThreads, 4) k_cahead_lean(const int32_t *__restrict__ M, long long r0, long long r1,
                                                              const Loc *__restrict__ loc, StepParams P, StepParams P2,
@@ -1294,7 +1297,6 @@ __global__ void __launch_bounds__(kThreads, 4) k_cahead_lean(const int32_t *__re
         const bool valid = i < r1;
         const Loc L = valid ? loc[(unsigned long long)i] : Loc{0u, 0u};
         const int32_t *row = M + (unsigned long long)(valid ? i : r0) * (unsigned)P.t;
-        const int32_t inj = (NINJ > 0 && valid) ? __ldg(row + P.inj_col[0]) : -1;
         const bool need = valid && L.len;
         Loc RR{1u, 1u};   // FINAL: each surviving candidate is one match
         if (!FINAL) RR = warp_dedup_lookup(need, need ? __ldg(row + P2.col[0]) : -1, P2, groups, gpn);
@@ -1303,80 +1305,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_cahead_lean(const int32_t *__re
             const int32_t y = __ldg(row + P2.inj_col[c]);
             if (in_bitmap(P2.cu, y) && in_sorted(P2.fci + RR.off, RR.len, y)) rbase--;
         }
-        uint32_t inc = L.len;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += y;
+        uint32_t sv = need ? L.len : 0u;
+        if (NINJ > 0 && need) {
+            const int32_t inj = __ldg(row + P.inj_col[0]);
+            if (in_sorted(cip + L.off, L.len, inj)) sv--;
         }
-        const uint32_t T = __shfl_sync(0xffffffffu, inc, 31);
-        // Rows of a unit are mostly siblings with runs of similar length: when the longest
-        // run is at most twice the mean, every lane walks its own row (no owner search, no
-        // shuffles; >= 50 % of the lanes busy); otherwise the balanced walk below.
-        const uint32_t maxlen = __reduce_max_sync(0xffffffffu, L.len);
-        if (maxlen * 16 <= T) {
-            for (uint32_t kk = 0; kk < maxlen; kk++) {
-                if (kk >= L.len) break;
-                const int32_t x = __ldg(cip + L.off + kk);
-                if (NINJ > 0 && x == inj) continue;
-                surv++;
-                bound += RR.len;
-                cnt += rbase;
-            }
-            continue;
-        }
-#if GSI_CAHEAD_LONG
-        // Rows with >= 32 candidates are walked by the whole warp, one row at a time (the row's
-        // data broadcast once, no owner search); the rest by the balanced walk below.
-        uint32_t longs = __ballot_sync(0xffffffffu, L.len >= 32);
-        while (longs) {
-            const int r = __ffs(longs) - 1;
-            longs &= longs - 1;
-            const uint32_t off = __shfl_sync(0xffffffffu, L.off, r), len = __shfl_sync(0xffffffffu, L.len, r);
-            const uint32_t rb = __shfl_sync(0xffffffffu, rbase, r), rl = __shfl_sync(0xffffffffu, RR.len, r);
-            const int32_t ri = NINJ > 0 ? __shfl_sync(0xffffffffu, inj, r) : -1;
-            for (uint32_t kk = lane; kk < len; kk += 32) {
-                const int32_t x = __ldg(cip + off + kk);
-                if (NINJ > 0 && x == ri) continue;
-                surv++;
-                bound += rl;
-                cnt += rb;
-            }
-        }
-        if (__any_sync(0xffffffffu, L.len >= 32)) {   // the balanced walk over the short rows only
-            const uint32_t sl = L.len >= 32 ? 0u : L.len;
-            inc = sl;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-                if (lane >= o) inc += y;
-            }
-        }
-        const uint32_t excl2 = inc - (L.len >= 32 ? 0u : L.len);
-        const uint32_t T2 = __shfl_sync(0xffffffffu, inc, 31);
-#else
-        const uint32_t excl2 = inc - L.len, T2 = T;
-#endif
-        for (uint32_t j0 = 0; j0 < T2; j0 += 32) {
-            const uint32_t j = j0 + lane;
-            int o = 0;
-#pragma unroll
-            for (int st = 16; st > 0; st >>= 1) {
-                const uint32_t v = __shfl_sync(0xffffffffu, inc, o + st - 1);
-                if (v <= j) o += st;
-            }
-            o &= 31;
-            const uint32_t pos = __shfl_sync(0xffffffffu, L.off, o) + (j - __shfl_sync(0xffffffffu, excl2, o));
-            const uint32_t rb = __shfl_sync(0xffffffffu, rbase, o);
-            const uint32_t rl = __shfl_sync(0xffffffffu, RR.len, o);
-            const int32_t ri = NINJ > 0 ? __shfl_sync(0xffffffffu, inj, o) : -1;
-            if (j >= T2) continue;
-            const int32_t x = __ldg(cip + pos);
-            if (NINJ > 0 && x == ri) continue;
-            surv++;
-            bound += rl;
-            cnt += rb;
-        }
+        surv += sv;
+        bound += (unsigned long long)sv * RR.len;
+        cnt += (unsigned long long)sv * rbase;
     }
     cnt = warp_sum_u64(cnt);
     surv = warp_sum_u64(surv);
@@ -1385,6 +1321,111 @@ __global__ void __launch_bounds__(kThreads, 4) k_cahead_lean(const int32_t *__re
         if (cnt) atomicAdd(&ctr->count, cnt);
         if (surv) atomicAdd(&ctr->total, surv);
         if (bound) atomicAdd(&ctr->total2, bound);
+    }
+}
+
+// Fingerprinted last level on shared runs (the enumerating pass: every match is read and
+// hashed).  Same shape as k_cahead_lean<FINAL>: one linking edge, rows on shared
+// N(v,l0) ∩ C(u) runs, at most NINJ subtraction columns.  The set fingerprint of DESIGN.md
+// §3 hashes a row as fp_mix(Σ_q fp_term(seed, q, row[q])), so the k-1 terms of the parent
+// row are summed once per row (by the lane that owns it) and each match x of the row costs
+// its candidate read, the subtraction compare and two terms + two finalisers.  The walk is
+// load-balanced like the count kernels: lane-own rows when the unit's runs are even, long
+// rows (>= 32 candidates) by the whole warp, the rest by a shuffle owner search.
+template <int NINJ>
+__global__ void __launch_bounds__(kThreads, 4) k_final_fp(const int32_t *__restrict__ M, long long r0, long long r1,
+                                                          const Loc *__restrict__ loc, StepParams P, int qx,
+                                                          const int32_t *__restrict__ cip, Counters *ctr) {
+    const int lane = threadIdx.x & 31;
+    const long long gw = (blockIdx.x * (long long)kThreads + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * kThreads) >> 5;
+    unsigned long long cnt = 0, h1 = 0, h2 = 0;
+    for (long long base = r0 + gw * 32; base < r1; base += nw * 32) {
+        const long long i = base + lane;
+        const bool valid = i < r1;
+        const Loc L = valid ? loc[(unsigned long long)i] : Loc{0u, 0u};
+        const int32_t *row = M + (unsigned long long)(valid ? i : r0) * (unsigned)P.t;
+        const int32_t inj = (NINJ > 0 && valid && L.len) ? __ldg(row + P.inj_col[0]) : -1;
+        unsigned long long s1 = 0, s2 = 0;   // the parent row's terms (every column but x)
+        if (valid && L.len) {
+            for (int q = 0; q < P.k; q++) {
+                const int col = P.pos_of_q[q];
+                if (col >= P.t) continue;
+                const uint32_t v = (uint32_t)__ldg(row + col);
+                s1 += fp_term(kFpSeed1, q, v);
+                s2 += fp_term(kFpSeed2, q, v);
+            }
+        }
+        uint32_t inc = L.len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        const uint32_t T = __shfl_sync(0xffffffffu, inc, 31);
+        const uint32_t maxlen = __reduce_max_sync(0xffffffffu, L.len);
+        if (maxlen * 16 <= T) {   // even runs: every lane walks its own row
+            for (uint32_t kk = 0; kk < L.len; kk++) {
+                const int32_t x = __ldg(cip + L.off + kk);
+                if (NINJ > 0 && x == inj) continue;
+                cnt++;
+                h1 += fp_mix(s1 + fp_term(kFpSeed1, qx, (uint32_t)x));
+                h2 ^= fp_mix(s2 + fp_term(kFpSeed2, qx, (uint32_t)x));
+            }
+            continue;
+        }
+        uint32_t longs = __ballot_sync(0xffffffffu, L.len >= 32);
+        while (longs) {   // long rows: the whole warp, one row at a time
+            const int r = __ffs(longs) - 1;
+            longs &= longs - 1;
+            const uint32_t off = __shfl_sync(0xffffffffu, L.off, r), len = __shfl_sync(0xffffffffu, L.len, r);
+            const unsigned long long a1 = __shfl_sync(0xffffffffu, s1, r), a2 = __shfl_sync(0xffffffffu, s2, r);
+            const int32_t ri = NINJ > 0 ? __shfl_sync(0xffffffffu, inj, r) : -1;
+            for (uint32_t kk = lane; kk < len; kk += 32) {
+                const int32_t x = __ldg(cip + off + kk);
+                if (NINJ > 0 && x == ri) continue;
+                cnt++;
+                h1 += fp_mix(a1 + fp_term(kFpSeed1, qx, (uint32_t)x));
+                h2 ^= fp_mix(a2 + fp_term(kFpSeed2, qx, (uint32_t)x));
+            }
+        }
+        const uint32_t sl = L.len >= 32 ? 0u : L.len;   // the short rows: balanced walk
+        inc = sl;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        const uint32_t excl = inc - sl;
+        const uint32_t T2 = __shfl_sync(0xffffffffu, inc, 31);
+        for (uint32_t j0 = 0; j0 < T2; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            int o = 0;   // owner = number of lanes whose inclusive length is <= j
+#pragma unroll
+            for (int st = 16; st > 0; st >>= 1) {
+                const uint32_t v = __shfl_sync(0xffffffffu, inc, o + st - 1);
+                if (v <= j) o += st;
+            }
+            o &= 31;
+            const uint32_t pos = __shfl_sync(0xffffffffu, L.off, o) + (j - __shfl_sync(0xffffffffu, excl, o));
+            const unsigned long long a1 = __shfl_sync(0xffffffffu, s1, o), a2 = __shfl_sync(0xffffffffu, s2, o);
+            const int32_t ri = NINJ > 0 ? __shfl_sync(0xffffffffu, inj, o) : -1;
+            if (j >= T2) continue;
+            const int32_t x = __ldg(cip + pos);
+            if (NINJ > 0 && x == ri) continue;
+            cnt++;
+            h1 += fp_mix(a1 + fp_term(kFpSeed1, qx, (uint32_t)x));
+            h2 ^= fp_mix(a2 + fp_term(kFpSeed2, qx, (uint32_t)x));
+        }
+    }
+    cnt = warp_sum_u64(cnt);
+    h1 = warp_sum_u64(h1);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) h2 ^= __shfl_xor_sync(0xffffffffu, h2, o);
+    if (lane == 0 && cnt) {
+        atomicAdd(&ctr->count, cnt);
+        atomicAdd(&ctr->fp1, h1);
+        atomicXor(&ctr->fp2, h2);
     }
 }
 
@@ -1699,14 +1740,14 @@ __global__ void __launch_bounds__(kThreads) k_lens_scan(const Loc *__restrict__ 
 __global__ void k_fp_rows(const int32_t *__restrict__ T, long long nrows, StepParams P, Counters *ctr) {
     unsigned long long h1 = 0, h2 = 0;
     for (long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x; r < nrows; r += (long long)gridDim.x * blockDim.x) {
-        unsigned long long a = kFpSeed1, b = kFpSeed2;
+        unsigned long long a = 0, b = 0;
         for (int q = 0; q < P.k; q++) {
             uint32_t val = (uint32_t)T[r * P.t + P.pos_of_q[q]];
-            a = fp_mix(a ^ val);
-            b = fp_mix(b ^ val);
+            a += fp_term(kFpSeed1, q, val);
+            b += fp_term(kFpSeed2, q, val);
         }
-        h1 += a;
-        h2 ^= b;
+        h1 += fp_mix(a);
+        h2 ^= fp_mix(b);
     }
     h1 = warp_sum_u64(h1);
 #pragma unroll
@@ -2077,20 +2118,35 @@ unsigned long long available_bytes(int dev) {
     return (unsigned long long)fr + (reserved > used ? reserved - used : 0);
 }
 
-// One pinned Counters block per host thread (levels of a query run on one thread, one at a
-// time); nullptr if pinned memory is unavailable.
-Counters *pinned_counters() {
-    thread_local Counters *p = nullptr;
-    thread_local bool tried = false;
-    if (!tried) {
-        tried = true;
+// Pinned Counters blocks (the per-level counter read-back of a query): a process-wide
+// free list, so host threads that come and go (batch workers) reuse a bounded set instead of
+// leaking one page-locked allocation each.  A query holds one block for its lifetime.
+std::mutex g_pinned_mu;
+std::vector<Counters *> g_pinned_free;
+struct PinnedCounters {
+    Counters *p = nullptr;   // nullptr if pinned memory is unavailable
+    PinnedCounters() {
+        {
+            std::lock_guard<std::mutex> lk(g_pinned_mu);
+            if (!g_pinned_free.empty()) {
+                p = g_pinned_free.back();
+                g_pinned_free.pop_back();
+                return;
+            }
+        }
         if (cudaMallocHost((void **)&p, sizeof(Counters)) != cudaSuccess) {
             cudaGetLastError();
             p = nullptr;
         }
     }
-    return p;
-}
+    ~PinnedCounters() {
+        if (!p) return;
+        std::lock_guard<std::mutex> lk(g_pinned_mu);
+        g_pinned_free.push_back(p);
+    }
+    PinnedCounters(const PinnedCounters &) = delete;
+    PinnedCounters &operator=(const PinnedCounters &) = delete;
+};
 
 // Test / A-B switches read per query (never needed in production).
 bool env_flag(const char *name) {
@@ -2170,6 +2226,7 @@ gsi_status prepare_impl(const gsi_graph *g, int32_t k, const int32_t *qvl, int32
     }
     auto p = std::make_unique<gsi_prepared>();
     p->g = g;
+    p->device = g->device;
     p->k = k;
     p->qvl.assign(qvl, qvl + k);
     p->qs.assign(qs, qs + qm);
@@ -2277,6 +2334,9 @@ static gsi_status build_steps(const gsi_prepared *q, const std::vector<int> &ord
     const int k = q->k, qm = (int)q->qs.size();
     std::vector<int> pos(k, -1);
     for (int j = 0; j < k; j++) pos[order[j]] = j;
+    // a query edge label absent from G (dense label -1) has freq 0 (the query is empty, which
+    // run_impl detects after planning; it must not index freq here)
+    auto freq_of = [&](int lab) -> long long { return lab < 0 ? 0ll : g->freq[lab]; };
     steps.clear();
     for (int j = 1; j < k; j++) {
         Step s;
@@ -2293,7 +2353,7 @@ static gsi_status build_steps(const gsi_prepared *q, const std::vector<int> &ord
         // e0: min freq(l); ties (min raw label id, min column) (reading A9)
         int best = 0;
         for (size_t e = 1; e < s.col.size(); e++) {
-            long long fb = g->freq[s.lab[best]], fe = g->freq[s.lab[e]];
+            long long fb = freq_of(s.lab[best]), fe = freq_of(s.lab[e]);
             if (fe < fb || (fe == fb && (s.rawlab[e] < s.rawlab[best] ||
                                          (s.rawlab[e] == s.rawlab[best] && s.col[e] < s.col[best]))))
                 best = (int)e;
@@ -2301,7 +2361,7 @@ static gsi_status build_steps(const gsi_prepared *q, const std::vector<int> &ord
         if (force_e0 && force_e0[j] >= 0) {
             int f = -1;
             for (size_t e = 0; e < s.col.size(); e++)
-                if (s.other[e] == force_e0[j] && (f < 0 || g->freq[s.lab[e]] < g->freq[s.lab[f]])) f = (int)e;
+                if (s.other[e] == force_e0[j] && (f < 0 || freq_of(s.lab[e]) < freq_of(s.lab[f]))) f = (int)e;
             if (f < 0) {
                 set_error("force_first_edge names a vertex not linked to the joined vertex");
                 return GSI_ERR_INVALID_ARG;
@@ -2331,6 +2391,7 @@ struct QueryCtx {
     Arena *A = nullptr;
     Prof *prof = nullptr;
     Counters *ctr = nullptr;
+    Counters *pinned = nullptr;   // host read-back block of this query (nullptr: pageable)
     gsi_stats *S = nullptr;
     const uint32_t *bm = nullptr;
     long long words = 0;
@@ -2457,6 +2518,7 @@ gsi_status ensure_filtered(QueryCtx &C, size_t si, uint32_t lab) {
     GSI_CUDA(cudaMemsetAsync(fst, 0, 8ull * (ft + 1), st));
     const uint32_t *cu0 = C.bm + (long long)C.steps[si].u * C.words;
     C.prof->begin(GSI_K_OTHER);
+    C.S->variant_launches[GSI_V_FILTER_PARTITION]++;
     k_filter_partition<<<ft, kThreads, 0, st>>>(g->ci, lo, hi, cu0, fpos, fci, fst + 1, (unsigned *)fst);
     C.prof->end();
     C.S->alg_bytes[GSI_K_OTHER] += 12.0 * (hi - lo);
@@ -2476,6 +2538,7 @@ gsi_status ensure_probe_ahead(QueryCtx &C, size_t si, const StepParams &P, const
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
     const unsigned grid = std::min<unsigned>(grid_for(hi - lo, 4 * kThreads), (unsigned)sms * 8);
     C.prof->begin(GSI_K_OTHER);
+    C.S->variant_launches[GSI_V_PROBE_AHEAD]++;
     k_probe_ahead<<<grid, kThreads, 0, C.st>>>(C.filt[si].second, C.filt[si].first + (hi - lo), P2, g->groups,
                                                g->gpn, pa);
     C.prof->end();
@@ -2504,21 +2567,33 @@ gsi_status build_F(QueryCtx &C, const Loc *loc, unsigned long long nM, int E, un
 
 bool cahead_warp_enabled() { return GSI_CAHEAD_WARP && !env_flag("GSI_CAHEAD_TILE"); }
 
+// The warp count-ahead has the closed-form shape (k_cahead_lean): the last step links to a
+// parent column, the vertex this step adds is not one of its subtraction columns, one linking
+// edge here and at most one subtraction column.
+bool cahead_lean(const QueryCtx &C, const StepParams &P, const StepParams &P2) {
+    (void)C;
+    bool xinj = false;
+    for (int c = 0; c < P2.n_inj; c++) xinj |= P2.inj_col[c] >= P.t;
+    return GSI_CAHEAD_LEAN && !env_flag("GSI_CAHEAD_NOLEAN") && P2.col[0] < P.t && !xinj && P.E == 1 &&
+           P.n_inj <= 1;
+}
+
 // The last level of an enumerating count on shared runs is walked row-wise by the lean warp
 // kernel (no F, holes allowed).
 bool final_walks_rows(const QueryCtx &C, const StepParams &P, int mode) {
-    return mode == J_COUNT && GSI_COUNT_LEAN && !env_flag("GSI_COUNT_NOLEAN") && P.prefiltered && !P.fp && P.E == 1 &&
+    return mode == J_COUNT && GSI_COUNT_LEAN && !env_flag("GSI_COUNT_NOLEAN") && P.prefiltered && P.E == 1 &&
            P.n_inj <= 1 && cahead_warp_enabled();
 }
 
 // The level after step si will walk its rows without F (the warp count-ahead, or the lean last
 // level), so step si may skip F' and write its rows at their Prealloc slots.
 bool next_walks_rows(const QueryCtx &C, size_t si, bool pf_next) {
-    if (!pf_next || !C.sharded || C.opts.want_table || C.opts.fingerprint || C.opts.e0_mode != 0 ||
-        C.opts.no_shared_lists || !cahead_warp_enabled())
+    if (!pf_next || !C.sharded || C.opts.want_table || C.opts.e0_mode != 0 || C.opts.no_shared_lists ||
+        !cahead_warp_enabled())
         return false;
     const size_t nl = si + 1;
-    if (nl + 2 == C.steps.size()) return !C.opts.no_count_ahead && C.steps[nl + 1].col.size() == 1;
+    if (nl + 2 == C.steps.size())
+        return !C.opts.no_count_ahead && !C.opts.fingerprint && C.steps[nl + 1].col.size() == 1;
     if (nl + 1 == C.steps.size()) return GSI_COUNT_LEAN && !env_flag("GSI_COUNT_NOLEAN") && C.steps[nl].col.size() == 1;
     return false;
 }
@@ -2561,6 +2636,7 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
             GSI_CUDA(cudaMemsetAsync(rst, 0, 8ull * (rt + 1) + sizeof(Counters), st));
             Counters *rctr = reinterpret_cast<Counters *>(rst + rt + 1);
             prof.begin(GSI_K_OTHER);
+            S.variant_launches[GSI_V_REFILTER]++;
             k_refilter<<<rt, kThreads, 0, st>>>(loc, (long long)nM, C.filt[si].first, lo, hi, F, rst + 1,
                                                 (unsigned *)rst, rctr);
             prof.end();
@@ -2730,6 +2806,18 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         }
         Counters hc_local;
         prof.begin(GSI_K_JOIN);
+        {
+            int v;
+            if (lean_next) v = GSI_V_NEXT_LEAN;
+            else if (warp_ca) v = cahead_lean(C, P, P2) ? GSI_V_CAHEAD_LEAN : GSI_V_CAHEAD_WARP;
+            else if (final_lean) v = P.fp ? GSI_V_FINAL_FP : GSI_V_FINAL_LEAN;
+            else if (fast) v = GSI_V_COUNT_FAST;
+            else if (mode == J_COUNT) v = GSI_V_JOIN_COUNT;
+            else if (mode == J_CAHEAD) v = GSI_V_JOIN_CAHEAD;
+            else if (mode == J_TABLE) v = GSI_V_JOIN_TABLE;
+            else v = GSI_V_JOIN_NEXT;
+            S.variant_launches[v]++;
+        }
         if (lean_next) {
             int sms = 148;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
@@ -2747,9 +2835,7 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
             const unsigned long long units = ((unsigned long long)(r_hi - r_lo) + 31) / 32;
             const unsigned wg = (unsigned)std::max<unsigned long long>(
                 1, std::min<unsigned long long>((units + 7) / 8, (unsigned long long)sms * 8));
-            bool xinj = false;
-            for (int c = 0; c < P2.n_inj; c++) xinj |= P2.inj_col[c] >= P.t;
-            const bool lean = GSI_CAHEAD_LEAN && !env_flag("GSI_CAHEAD_NOLEAN") && P2.col[0] < P.t && !xinj && P.E == 1 && P.n_inj <= 1;
+            const bool lean = cahead_lean(C, P, P2);
             if (lean && P.n_inj == 0)
                 k_cahead_lean<0, false><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, P2, cip, g->groups, g->gpn, lctr);
             else if (lean)
@@ -2765,7 +2851,11 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
             const unsigned long long units = ((unsigned long long)(r_hi - r_lo) + 31) / 32;
             const unsigned wg = (unsigned)std::max<unsigned long long>(
                 1, std::min<unsigned long long>((units + 7) / 8, (unsigned long long)sms * 8));
-            if (P.n_inj == 0)
+            if (P.fp && P.n_inj == 0)
+                k_final_fp<0><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, s.u, cip, lctr);
+            else if (P.fp)
+                k_final_fp<1><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, s.u, cip, lctr);
+            else if (P.n_inj == 0)
                 k_cahead_lean<0, true><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, P2, cip, g->groups, g->gpn, lctr);
             else
                 k_cahead_lean<1, true><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, P2, cip, g->groups, g->gpn, lctr);
@@ -2788,7 +2878,7 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         prof.end();
         // the level's counters come back through pinned memory (a pageable copy stages
         // through a driver buffer: ~10 us more per level on the small-query critical path)
-        Counters *hp = pinned_counters();
+        Counters *hp = C.pinned;
         GSI_CUDA(d2h(S, hp ? (void *)hp : (void *)&hc_local, lctr, sizeof(Counters), st));
         GSI_CUDA(sync_timed(S, st));
         GSI_CUDA(cudaGetLastError());
@@ -2875,6 +2965,8 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     S.k = k;
     S.shard_level = -1;
     Arena A(st);
+    PinnedCounters pinned;
+    C.pinned = pinned.p;
     Prof prof;
     prof.on = opts.profile != 0;
     prof.st = st;

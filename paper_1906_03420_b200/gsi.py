@@ -24,6 +24,10 @@ HEADER = os.path.join(os.path.dirname(_PKG), "include", "gsi.h")
 GSI_MAX_K = 32
 GSI_N_KCLASS = 8
 KCLASS = ["filter", "compact", "probe", "join", "link", "other", "r6", "r7"]
+GSI_N_KVARIANT = 16
+KVARIANT = ["join_next", "join_count", "join_table", "join_cahead", "count_fast", "next_lean", "cahead_warp",
+            "cahead_lean", "final_lean", "final_fp", "filter_partition", "refilter", "probe_ahead", "small",
+            "two_step", "reserved"]
 STATUS = {0: "GSI_OK", -1: "GSI_ERR_INVALID_ARG", -2: "GSI_ERR_VERTEX_RANGE", -3: "GSI_ERR_LABEL_RANGE",
           -4: "GSI_ERR_SELF_LOOP", -5: "GSI_ERR_DUPLICATE_EDGE", -6: "GSI_ERR_QUERY_DISCONNECTED",
           -7: "GSI_ERR_QUERY_TOO_LARGE", -8: "GSI_ERR_OOM", -9: "GSI_ERR_TIMEOUT", -10: "GSI_ERR_CUDA",
@@ -66,7 +70,8 @@ class gsi_stats(ctypes.Structure):
                 ("launches", U32 * GSI_N_KCLASS), ("alg_bytes", ctypes.c_double * GSI_N_KCLASS),
                 ("total_launches", U32), ("n_chunks", U32), ("capped", I32), ("h2d_bytes", U64),
                 ("d2h_bytes", U64), ("n_shared_lists", U32), ("ms_host_alloc", ctypes.c_float),
-                ("ms_host_sync", ctypes.c_float), ("count_ahead", I32), ("n_probe_ahead", U32)]
+                ("ms_host_sync", ctypes.c_float), ("count_ahead", I32), ("n_probe_ahead", U32),
+                ("variant_launches", U32 * GSI_N_KVARIANT)]
 
 
 _SIGS = {
@@ -242,13 +247,16 @@ class Result:
         for f, _ in gsi_stats._fields_:
             v = getattr(s, f)
             d[f] = list(v) if hasattr(v, "__len__") else v
+        d["variants"] = {KVARIANT[i]: d["variant_launches"][i] for i in range(GSI_N_KVARIANT)
+                         if d["variant_launches"][i]}
         return d
 
 
 class Prepared:
-    def __init__(self, h: int, k: int):
+    def __init__(self, h: int, k: int, graph: "GraphHandle" = None):
         self.h = h
         self.k = k
+        self.graph = graph   # the C handle points at its graph: keep the graph alive
 
     def __del__(self):
         h = getattr(self, "h", None)
@@ -295,7 +303,7 @@ def gsi_query_prepare(g: GraphHandle, q_vlabels, q_src, q_dst, q_elabels) -> Pre
     out = P()
     _check(lib.gsi_query_prepare(g.h, len(qv), _ptr(qv), len(qs), _ptr(qs), _ptr(qd), _ptr(qe), ctypes.byref(out)),
            "gsi_query_prepare")
-    return Prepared(out.value, len(qv))
+    return Prepared(out.value, len(qv), g)
 
 
 def gsi_query_run(g: GraphHandle, p: Prepared, **opts) -> Result:
