@@ -208,9 +208,10 @@ def workload_config(args, g):
     return {"workload": f"{args.config}: {BENCH_CONFIGS[args.config]['desc']}", "n": int(g.n), "m": int(g.m),
             "queries_per_step": args.queries, "query_k": args.k, "query_seeds": f"1000..{999 + args.queries}",
             "graph_seed": 1,
-            "mode": "count-only (gsi_query count; a one-edge last step is counted by the level before it "
-                    "as |N(v,l0) ∩ C(u)| minus the row's own vertices, see DESIGN.md; 'enumerated' = every "
-                    "match of the last level visited and checked)",
+            "mode": "count (gsi_query count-only: the last two levels are counted in closed form per row of "
+                    "M_{k-2}, |L|-[inj in L] survivors x (|RR| - row hits) extensions, DESIGN.md §6 count-ahead; "
+                    "'enumerated' = fingerprint mode, every final match produced, read and hashed; 'table' = "
+                    "every final match written)",
             "l2": "inputs larger than L2 (PCSR+signatures >> 126 MB); no flush",
             "concurrency": args.concurrency}
 
@@ -264,24 +265,30 @@ def run_gsi(args):
             log(f"[bench] NCCL broadcast of the graph {time.time() - t:.2f}s")
     info = graph.info()
 
-    shard = dict(shard_rank=rank, shard_count=ws) if ws > 1 else {}
+    shard = dict(shard_rank=rank, shard_count=ws, shard_pieces=args.shard_pieces) if ws > 1 else {}
     prepared = [gsi.prepare(graph, q) for q in qs]
     counts = torch.zeros(len(qs), dtype=torch.int64, device="cuda")
+    MODES = {"count": dict(fingerprint=False),                    # the count path (closed-form last level)
+             "fp": dict(fingerprint=True),                        # every final match read and hashed
+             "table": dict(fingerprint=False, want_table=True)}   # every final match written (query-id order)
 
-    def step(profile=False, stats=None, enumerate_all=False):
-        # count-only (the product's count path: the last level may be counted ahead);
-        # enumerate_all=True visits and checks every match of the last level instead.  The
-        # batch runs its queries concurrently (--concurrency host workers / streams); the
-        # profiled pass runs them one at a time so per-kernel event times are not shared.
-        rs = gsi.gsi_query_run_batch(graph, prepared, concurrency=1 if profile else args.concurrency,
-                                     timeout_s=args.query_timeout, profile=profile, partial_on_timeout=True,
-                                     fingerprint=False, count_ahead=not enumerate_all, **shard)
-        counts.copy_(torch.tensor([r.count for r in rs], dtype=torch.int64))
+    def step(mode="count", profile=False, stats=None, which=None, timeout=None, sh=None):
+        """One pass of the hot path over the batch (or the queries `which`).  The batch runs its
+        queries concurrently (--concurrency host workers / streams); the profiled pass runs them
+        one at a time so per-kernel event times are not shared."""
+        ps = prepared if which is None else [prepared[i] for i in which]
+        rs = gsi.gsi_query_run_batch(graph, ps, concurrency=1 if profile else args.concurrency,
+                                     timeout_s=args.query_timeout if timeout is None else timeout, profile=profile,
+                                     partial_on_timeout=True, **MODES[mode], **(shard if sh is None else sh))
+        c = torch.tensor([r.count for r in rs], dtype=torch.int64, device="cuda")
         if stats is not None:
             stats.extend(r.stats() for r in rs)
-        if ws > 1:
-            dist.all_reduce(counts)
-        return counts
+        if which is None:
+            counts.copy_(c)
+            c = counts
+        if ws > 1 and sh is None:
+            dist.all_reduce(c)
+        return c
 
     def e2e_step():
         # the public API from host arrays: validate + encode + H2D of every query, the
@@ -294,10 +301,26 @@ def run_gsi(args):
             dist.all_reduce(counts)
         return int(counts.sum().item())
 
+    def timed(fn):
+        """Device time of fn() on the launching stream, max over ranks (ms)."""
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        out = fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+        if ws > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()), out
+
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    total_matches = int(step().sum().item())
+    per_query_counts = step().tolist()
+    total_matches = int(sum(per_query_counts))
 
     # ---- timed region: device-timed, prepared (resident) queries ------------------------
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -323,6 +346,7 @@ def run_gsi(args):
     launches = sum(s["total_launches"] for s in launch_stats)
     capped = sum(s["capped"] for s in launch_stats) / args.steps
     q_ms = np.array([s["ms_total"] for s in launch_stats])
+    q_ms_by_query = q_ms.reshape(args.steps, len(qs)).mean(axis=0)
 
     # ---- e2e: public API from host arrays, H2D of the query + D2H of the count -----------
     if ws > 1:
@@ -340,63 +364,101 @@ def run_gsi(args):
     h2d = sum(4 * q.n + 12 * len(q.src) + 64 * q.n for q in qs)        # query arrays + signatures
     d2h = sum(8 * q.n + 64 * (2 * q.n + 2) for q in qs)                # |C(u)|, per-level sizes, count
 
-    # ---- secondary: every match of the last level enumerated (and hashed), one step --------
+    # ---- enumerated: every match of the last level read and hashed (set fingerprint) -------
     enumerated = None
-    if ws > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    en_stats = []
-    if args.no_enumerated:
-        en_stats = None
-    ev0.record(stream)
-    en_counts = step(stats=en_stats, enumerate_all=True) if en_stats is not None else counts
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    en_ms = ev0.elapsed_time(ev1)
-    en_t = torch.tensor([en_ms], dtype=torch.float64, device="cuda")
-    if ws > 1:
-        dist.all_reduce(en_t, op=dist.ReduceOp.MAX)
-    en_ms = float(en_t.item())
-    en_matches = int(en_counts.sum().item())
-    if en_stats is not None:
+    if not args.no_enumerated:
+        en_stats = []
+        en_ms, en_counts = timed(lambda: step("fp", stats=en_stats, timeout=args.enum_timeout))
+        en_counts = en_counts.tolist()
+        en_capped = int(sum(s_["capped"] for s_ in en_stats))
+        en_matches = int(sum(en_counts))
+        fp_var = {}
+        for s_ in en_stats:
+            for k_, v_ in s_["variants"].items():
+                fp_var[k_] = fp_var.get(k_, 0) + v_
         enumerated = {"value": en_matches / (en_ms / 1000.0), "unit": "matches/s", "ms_per_step": en_ms,
-                      "matches_per_step": en_matches,
-                      "capped_queries": int(sum(s_["capped"] for s_ in en_stats)),
-                      "note": "count_ahead off: every match of the last level enumerated and checked on the device "
-                              "(the paper's join; capped queries report their completed prefix)"}
+                      "matches_per_step": en_matches, "capped_queries": en_capped,
+                      "counts_equal_count_mode": en_capped == 0 and en_counts == per_query_counts,
+                      "kernel_variants": fp_var,
+                      "note": "fingerprint mode: every match of the last level is produced on the device, its "
+                              "candidate read and checked, and the match hashed into the order-free set "
+                              "fingerprint (no closed-form counting); the enumerating join throughput"}
 
-    # ---- profiled pass: per-kernel CUDA-event times + algorithmic bytes -----------------
+    # ---- table: every match written to HBM as a k-int32 row in query-id order -------------
+    table = None
+    if not args.no_table:
+        row_b = 4 * args.k
+        which = [i for i, c in enumerate(per_query_counts) if 0 < c * row_b <= args.table_max_gb * 1e9]
+        if which:
+            t_stats = []
+            t_ms, t_counts = timed(lambda: step("table", stats=t_stats, which=which, timeout=args.enum_timeout))
+            t_m = int(t_counts.sum().item())
+            table = {"value": t_m / (t_ms / 1000.0), "unit": "matches/s", "ms": t_ms, "queries": which,
+                     "matches": t_m, "GB_written": t_m * row_b / 1e9,
+                     "write_GBps": t_m * row_b / 1e9 / (t_ms / 1000.0),
+                     "counts_equal_count_mode": t_counts.tolist() == [per_query_counts[i] for i in which],
+                     "note": f"want_table on the bench queries whose table fits {args.table_max_gb} GB "
+                             f"(4k B per match, device-resident)"}
+
+    # ---- profiled pass: per-kernel-variant CUDA-event times + algorithmic bytes ------------
     pstats = []
     step(profile=True, stats=pstats)
     torch.cuda.synchronize()
-    ms_k = np.zeros(8)
-    bytes_k = np.zeros(8)
-    launches_k = np.zeros(8)
+    ms_k, bytes_k, launches_k = np.zeros(8), np.zeros(8), np.zeros(8)
+    nv = gsi.GSI_N_KVARIANT
+    ms_v, bytes_v, launches_v = np.zeros(nv), np.zeros(nv), np.zeros(nv)
     for s in pstats:
         ms_k += np.array(s["ms_kernel"])
         bytes_k += np.array(s["alg_bytes"])
         launches_k += np.array(s["launches"])
-    dom = int(np.argmax(ms_k))
+        ms_v += np.array(s["ms_variant"])
+        bytes_v += np.array(s["alg_bytes_variant"])
+        launches_v += np.array(s["variant_launches"])
+    dom = int(np.argmax(ms_v))
+    dname = gsi.KVARIANT[dom]
     peak, peak_src = load_peaks()
-    achieved = (bytes_k[dom] / (ms_k[dom] / 1e3)) / 1e9 if ms_k[dom] > 0 else 0.0
-    # DRAM traffic of the dominant kernel from the committed `ncu --set full` capture of this
-    # workload (dram__bytes_read.sum + dram__bytes_write.sum per launch, averaged over the
-    # captured launches; profiles/ncu_traffic.json names the capture)
-    traffic, traffic_src = None, None
+    achieved = (bytes_v[dom] / (ms_v[dom] / 1e3)) / 1e9 if ms_v[dom] > 0 else 0.0
+    # DRAM traffic of the dominant kernel from the committed ncu capture of this workload
+    # (dram__bytes_read.sum + dram__bytes_write.sum per launch; profiles/ncu_traffic.json
+    # names the capture, tools/ncu_traffic.py writes it)
+    traffic, traffic_src, ncu_frac = None, None, None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
-        tt = json.load(open(tp)).get(args.config, {}).get(gsi.KCLASS[dom])
+        tt = json.load(open(tp)).get(args.config, {}).get(dname)
         if tt is not None:
             traffic, traffic_src = tt.get("dram_bytes_per_launch"), tt.get("source")
-    roofline = {"bound": "hbm", "kernel": f"k_{gsi.KCLASS[dom]}", "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-                "alg_bytes_per_launch": float(bytes_k[dom] / max(launches_k[dom], 1)),
-                "ms_per_launch": float(ms_k[dom] / max(launches_k[dom], 1)), "peak_source": peak_src,
-                "share_of_step": float(ms_k[dom] / max(ms_k.sum(), 1e-9)),
-                "per_kernel_ms": {gsi.KCLASS[i]: float(ms_k[i]) for i in range(6)},
-                "per_kernel_alg_GBps": {gsi.KCLASS[i]: float(bytes_k[i] / (ms_k[i] / 1e3) / 1e9) if ms_k[i] else 0.0
-                                        for i in range(6)},
-                "launches_per_step": {gsi.KCLASS[i]: int(launches_k[i]) for i in range(6)}}
+            ncu_frac = tt.get("dram_frac")
+    roofline = {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                "ncu_dram_frac": ncu_frac,
+                "alg_bytes_per_launch": float(bytes_v[dom] / max(launches_v[dom], 1)),
+                "ms_per_launch": float(ms_v[dom] / max(launches_v[dom], 1)), "peak_source": peak_src,
+                "share_of_step": float(ms_v[dom] / max(ms_k.sum(), 1e-9)),
+                "per_variant": {gsi.KVARIANT[i]: {"ms": float(ms_v[i]), "launches": int(launches_v[i]),
+                                                  "alg_GB": float(bytes_v[i] / 1e9),
+                                                  "frac": float(bytes_v[i] / (ms_v[i] / 1e3) / 1e9 / peak)}
+                                for i in range(nv) if launches_v[i]},
+                "per_class_ms": {gsi.KCLASS[i]: float(ms_k[i]) for i in range(6)},
+                "model": "algorithmic bytes = what the kernel must move at least once: rows it extends "
+                         "(row, loc, F), candidates streamed from ci (shared N(v,l0)∩C(u) runs are L2-"
+                         "resident, not charged per slot), one 32 B PCSR sector + fpos per lookup, every "
+                         "byte written (DESIGN.md §6)"}
+
+    # ---- multi-GPU balance, emulated on this GPU: each rank's shard run alone -------------
+    balance = None
+    if ws == 1 and not args.no_balance:
+        balance = {}
+        for W_ in (2, 4, 8):
+            per_rank = []
+            tot = 0
+            for r_ in range(W_):
+                t_ms, c_ = timed(lambda: step(sh=dict(shard_rank=r_, shard_count=W_,
+                                                      shard_pieces=args.shard_pieces)))
+                per_rank.append(t_ms)
+                tot += int(c_.sum().item())
+            balance[str(W_)] = {"rank_ms": per_rank, "max_ms": max(per_rank),
+                                "efficiency": sum(per_rank) / (W_ * max(per_rank)),
+                                "count_equal": tot == total_matches}
 
     if rank != 0:
         if ws > 1:
@@ -423,10 +485,12 @@ def run_gsi(args):
         "vs_baseline": None, "dtype": "int32", "data": "synthetic", "config": workload_config(args, g),
         "ms_per_query": ms_per_step / len(qs), "matches_per_step": total_matches,
         "query_ms_p50": float(np.percentile(q_ms, 50)), "query_ms_p95": float(np.percentile(q_ms, 95)),
+        "per_query": [{"count": int(c), "ms": round(float(t_), 3)} for c, t_ in zip(per_query_counts, q_ms_by_query)],
         "capped_queries_per_step": capped, "query_timeout_s": args.query_timeout,
         "e2e": {"value": m_e2e * args.steps / e2e_s, "unit": "matches/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_query": 1000.0 * e2e_s / args.steps / len(qs)},
-        "enumerated": enumerated, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": launches,
+        "enumerated": enumerated, "table": table, "roofline": roofline, "multi_gpu_balance_emulated": balance,
+        "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": launches,
         "graph": {"n_groups": info["n_groups"], "max_chain": info["max_chain"],
                   "bytes_total": info["bytes_total"], "build_ms": info["ms_build"]},
     }
@@ -434,6 +498,23 @@ def run_gsi(args):
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def spawn_ranks(args) -> int:
+    """`--gpus N` without a torchrun environment: launch N ranks of this script (one per GPU,
+    NCCL over 127.0.0.1) and return their exit status."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        log(f"[bench] --gpus {args.gpus} but only {have} CUDA device(s) visible")
+        return 1
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -454,7 +535,18 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-enumerated", action="store_true", help="skip the secondary enumerated pass")
     ap.add_argument("--concurrency", type=int, default=2, help="queries in flight (host workers / streams)")
+    ap.add_argument("--enum-timeout", type=float, default=30.0, help="per-query cap of the enumerated/table passes")
+    ap.add_argument("--no-table", action="store_true", help="skip the with-table pass")
+    ap.add_argument("--table-max-gb", type=float, default=40.0, help="table pass: queries whose table fits")
+    ap.add_argument("--no-balance", action="store_true", help="skip the emulated multi-GPU balance")
+    ap.add_argument("--shard-pieces", type=int, default=8, help="interleaved shard pieces per rank (N > 1)")
     args = ap.parse_args()
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args))
+    if args.impl == "gsi" and ws != args.gpus:
+        log(f"[bench] --gpus {args.gpus} but WORLD_SIZE={ws}")
+        sys.exit(1)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -173,6 +173,17 @@ typedef struct {
                                     each new row's extensions as |N(v,l0) ∩ C(u)| minus the row's
                                     own vertices in that run (Alg. 3 lines 9-10 applied to a
                                     count), so M_{k-1} is never stored and M_k never enumerated  */
+    int32_t shard_pieces;        /* with shard_count > 1: the shard level's slot range is cut into
+                                    shard_count x shard_pieces equal pieces (row granularity) and
+                                    rank r keeps pieces r, r + shard_count, ...; 0/1 = one
+                                    contiguous range per rank (concatenating the ranks' tables in
+                                    rank order then gives the 1-GPU row order)                  */
+    int32_t force_paths;         /* test hook, bit 0: take the shared-run paths (shared
+                                    N(v,l0) ∩ C(u) runs, prefiltered next levels, probe-ahead
+                                    tables, count-ahead, lean kernels) whenever the query's shape
+                                    allows them, ignoring the size thresholds that normally decide
+                                    — so small root-restricted runs exercise the kernels a large
+                                    query uses.  Results are identical either way.               */
 } gsi_query_opts;
 
 void gsi_query_opts_default(gsi_query_opts *opts);
@@ -237,6 +248,11 @@ typedef struct {
     uint32_t n_probe_ahead;           /* levels whose next-step locate came from a per-candidate
                                          probe-ahead table instead of a PCSR probe per new row   */
     uint32_t variant_launches[GSI_N_KVARIANT]; /* launches per kernel variant (GSI_V_*)         */
+    /* profile mode, per kernel variant: summed device ms and algorithmic bytes (the bytes the
+       variant must move at least once: rows, loc/F, output rows, candidates streamed from ci,
+       one 32 B sector + fpos per PCSR lookup)                                   */
+    float ms_variant[GSI_N_KVARIANT];
+    double alg_bytes_variant[GSI_N_KVARIANT];
 } gsi_stats;
 
 gsi_status gsi_result_count(const gsi_result *r, uint64_t *count);
@@ -270,6 +286,13 @@ gsi_status gsi_debug_filter(const gsi_graph *g, int32_t k, const int32_t *q_vlab
 gsi_status gsi_debug_query_signatures(int32_t k, const int32_t *q_vlabels, int32_t qm,
                                       const int32_t *q_src, const int32_t *q_dst,
                                       const int32_t *q_elabels, int32_t distinct, uint32_t *qsig);
+
+/* The hash functions of the written spec, evaluated by the library's own code
+ * (host side of the __host__ __device__ functions the kernels use), for known-answer tests:
+ * kind 0 = MurmurHash2 of the 4 LE bytes of (uint32)key with (uint32)seed (PCSR group f),
+ * kind 1 = MurmurHash64A of the 8 LE bytes of key (signature groups), kind 2 = the fingerprint
+ * finaliser mix(key) (seed ignored).  Pure host computation: needs no device.  Unknown kind -> 0. */
+uint64_t gsi_debug_hash(int32_t kind, uint64_t key, uint64_t seed);
 
 /* ------------------------------------------------------------------ memory ---------- */
 /* Queries keep one device workspace per device between calls (a double-ended stack the

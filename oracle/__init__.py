@@ -65,6 +65,14 @@ def lib():
         L.og_sig_group_of.restype = I32
         L.og_sig_group_of.argtypes = [I32, I32]
         L.og_max_threads.restype = I32
+        L.og_murmur2_bytes.restype = ctypes.c_uint32
+        L.og_murmur2_bytes.argtypes = [P, I64, ctypes.c_uint32]
+        L.og_murmur64a_bytes.restype = ctypes.c_uint64
+        L.og_murmur64a_bytes.argtypes = [P, I64, ctypes.c_uint64]
+        L.og_smhasher_verify.restype = ctypes.c_uint32
+        L.og_smhasher_verify.argtypes = [I32]
+        L.og_murmur64a_key.restype = ctypes.c_uint64
+        L.og_murmur64a_key.argtypes = [ctypes.c_uint64, ctypes.c_uint64]
         _lib = L
     return _lib
 
@@ -183,6 +191,28 @@ def filter(og: OracleGraph, planes: np.ndarray, qsig: np.ndarray) -> Tuple[np.nd
 
 def sig_group(elabel: int, nlabel: int) -> int:
     return int(lib().og_sig_group_of(elabel, nlabel))
+
+
+def murmur2(data: bytes, seed: int) -> int:
+    """MurmurHash2 (32-bit) of a byte string (the oracle's general restatement)."""
+    b = np.frombuffer(data, np.uint8).copy() if data else np.zeros(1, np.uint8)
+    return int(lib().og_murmur2_bytes(_p(b), len(data), seed & 0xFFFFFFFF))
+
+
+def murmur64a(data: bytes, seed: int) -> int:
+    """MurmurHash64A of a byte string (the oracle's general restatement)."""
+    b = np.frombuffer(data, np.uint8).copy() if data else np.zeros(1, np.uint8)
+    return int(lib().og_murmur64a_bytes(_p(b), len(data), seed & 0xFFFFFFFFFFFFFFFF))
+
+
+def murmur64a_key(key: int, seed: int) -> int:
+    """The oracle's signature hash (8-byte specialisation used by og_sig_group)."""
+    return int(lib().og_murmur64a_key(key, seed))
+
+
+def smhasher_verify(which: int) -> int:
+    """SMHasher's verification value of the general hash: 0 = MurmurHash2, 1 = MurmurHash64A."""
+    return int(lib().og_smhasher_verify(which))
 
 
 def max_threads() -> int:

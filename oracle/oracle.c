@@ -363,6 +363,65 @@ static uint64_t og_murmur64a_u64(uint64_t key, uint64_t seed) {
     return h;
 }
 
+/* Appleby's MurmurHash2 (32-bit) and MurmurHash64A over an arbitrary byte string, restated
+ * from the public-domain reference algorithm.  They pin the hash functions of the written
+ * signature/PCSR spec (reading A6/A7) against external known answers: SMHasher's
+ * verification value (hash the keys {}, {0}, {0,1}, ..., {0..254} with seed 256 - len, then
+ * hash the concatenated results with seed 0) is 0x27864C1E for MurmurHash2 and 0x1F0D3804 for
+ * MurmurHash64A.  og_murmur64a_u64 above must equal og_murmur64a_bytes on 8 LE bytes.        */
+uint32_t og_murmur2_bytes(const uint8_t *data, int64_t len, uint32_t seed) {
+    const uint32_t m = 0x5bd1e995u;
+    uint32_t h = seed ^ (uint32_t)len;
+    while (len >= 4) {
+        uint32_t k = (uint32_t)data[0] | (uint32_t)data[1] << 8 | (uint32_t)data[2] << 16 | (uint32_t)data[3] << 24;
+        k *= m; k ^= k >> 24; k *= m;
+        h *= m; h ^= k;
+        data += 4; len -= 4;
+    }
+    if (len == 3) h ^= (uint32_t)data[2] << 16;
+    if (len >= 2) h ^= (uint32_t)data[1] << 8;
+    if (len >= 1) { h ^= data[0]; h *= m; }
+    h ^= h >> 13; h *= m; h ^= h >> 15;
+    return h;
+}
+uint64_t og_murmur64a_bytes(const uint8_t *data, int64_t len, uint64_t seed) {
+    const uint64_t m = 0xc6a4a7935bd1e995ull;
+    uint64_t h = seed ^ ((uint64_t)len * m);
+    int64_t nblk = len / 8;
+    for (int64_t b = 0; b < nblk; b++) {
+        uint64_t k = 0;
+        for (int j = 7; j >= 0; j--) k = (k << 8) | data[8 * b + j];
+        k *= m; k ^= k >> 47; k *= m;
+        h ^= k; h *= m;
+    }
+    const uint8_t *t = data + 8 * nblk;
+    int rem = (int)(len & 7);
+    if (rem) {
+        for (int j = rem - 1; j >= 0; j--) h ^= (uint64_t)t[j] << (8 * j);
+        h *= m;
+    }
+    h ^= h >> 47; h *= m; h ^= h >> 47;
+    return h;
+}
+/* SMHasher's VerificationTest: which = 0 MurmurHash2, 1 MurmurHash64A. */
+uint32_t og_smhasher_verify(int32_t which) {
+    uint8_t key[256], hashes[256 * 8];
+    const int hb = which ? 8 : 4;
+    for (int i = 0; i < 256; i++) {
+        key[i] = (uint8_t)i;
+        if (which) {
+            uint64_t h = og_murmur64a_bytes(key, i, (uint64_t)(256 - i));
+            for (int j = 0; j < 8; j++) hashes[8 * i + j] = (uint8_t)(h >> (8 * j));
+        } else {
+            uint32_t h = og_murmur2_bytes(key, i, (uint32_t)(256 - i));
+            for (int j = 0; j < 4; j++) hashes[4 * i + j] = (uint8_t)(h >> (8 * j));
+        }
+    }
+    if (which) return (uint32_t)og_murmur64a_bytes(hashes, 256 * hb, 0);
+    return og_murmur2_bytes(hashes, 256 * hb, 0);
+}
+uint64_t og_murmur64a_key(uint64_t key, uint64_t seed) { return og_murmur64a_u64(key, seed); }
+
 #define OG_SIG_SEED 0x9747B28Cull
 #define OG_SIG_GROUPS 240          /* (N-K)/2 with N = 512, K = 32      */
 #define OG_SIG_PLANES 16           /* 512 bits = 16 x 32-bit words                      */

@@ -247,6 +247,15 @@ gsi_status gsi_query_run(const gsi_graph *g, const gsi_prepared *q, const gsi_qu
     return run_impl(g, q, opts, out);
 }
 
+uint64_t gsi_debug_hash(int32_t kind, uint64_t key, uint64_t seed) {
+    switch (kind) {
+    case 0: return gsi::murmur2_u32((uint32_t)key, (uint32_t)seed);
+    case 1: return gsi::murmur64a_u64(key, seed);
+    case 2: return gsi::fp_mix(key);
+    default: return 0;
+    }
+}
+
 void gsi_prepared_free(gsi_prepared *q) {
     if (!q) return;
     cudaSetDevice(q->device);   // its device copy of the signatures lives on the graph's device

@@ -1291,7 +1291,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_cahead_lean(const int32_t *__re
     const long long gw = (blockIdx.x * (long long)kThreads + threadIdx.x) >> 5;
     const long long nw = ((long long)gridDim.x * kThreads) >> 5;
     const int ninj2 = P2.n_inj;
-    unsigned long long cnt = 0, surv = 0, bound = 0;
+    unsigned long long cnt = 0, surv = 0, bound = 0, act = 0;
     for (long long base = r0 + gw * 32; base < r1; base += nw * 32) {
         const long long i = base + lane;
         const bool valid = i < r1;
@@ -1313,14 +1313,17 @@ __global__ void __launch_bounds__(kThreads, 4) k_cahead_lean(const int32_t *__re
         surv += sv;
         bound += (unsigned long long)sv * RR.len;
         cnt += (unsigned long long)sv * rbase;
+        act += need ? 1u : 0u;
     }
     cnt = warp_sum_u64(cnt);
     surv = warp_sum_u64(surv);
     bound = warp_sum_u64(bound);
+    act = warp_sum_u64(act);
     if (lane == 0) {
         if (cnt) atomicAdd(&ctr->count, cnt);
         if (surv) atomicAdd(&ctr->total, surv);
         if (bound) atomicAdd(&ctr->total2, bound);
+        if (act) atomicAdd(&ctr->active_rows, act);
     }
 }
 
@@ -1339,13 +1342,14 @@ __global__ void __launch_bounds__(kThreads, 4) k_final_fp(const int32_t *__restr
     const int lane = threadIdx.x & 31;
     const long long gw = (blockIdx.x * (long long)kThreads + threadIdx.x) >> 5;
     const long long nw = ((long long)gridDim.x * kThreads) >> 5;
-    unsigned long long cnt = 0, h1 = 0, h2 = 0;
+    unsigned long long cnt = 0, h1 = 0, h2 = 0, act = 0;
     for (long long base = r0 + gw * 32; base < r1; base += nw * 32) {
         const long long i = base + lane;
         const bool valid = i < r1;
         const Loc L = valid ? loc[(unsigned long long)i] : Loc{0u, 0u};
         const int32_t *row = M + (unsigned long long)(valid ? i : r0) * (unsigned)P.t;
         const int32_t inj = (NINJ > 0 && valid && L.len) ? __ldg(row + P.inj_col[0]) : -1;
+        act += (valid && L.len) ? 1u : 0u;
         unsigned long long s1 = 0, s2 = 0;   // the parent row's terms (every column but x)
         if (valid && L.len) {
             for (int q = 0; q < P.k; q++) {
@@ -1419,6 +1423,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_final_fp(const int32_t *__restr
         }
     }
     cnt = warp_sum_u64(cnt);
+    act = warp_sum_u64(act);
     h1 = warp_sum_u64(h1);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) h2 ^= __shfl_xor_sync(0xffffffffu, h2, o);
@@ -1427,6 +1432,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_final_fp(const int32_t *__restr
         atomicAdd(&ctr->fp1, h1);
         atomicXor(&ctr->fp2, h2);
     }
+    if (lane == 0 && act) atomicAdd(&ctr->active_rows, act);
 }
 
 // Lean J_NEXT (count-only mode, one linking edge on shared runs in this step and the next):
@@ -1758,26 +1764,30 @@ __global__ void k_fp_rows(const int32_t *__restrict__ T, long long nrows, StepPa
     }
 }
 
-// Shard boundaries: a_r = first row with F[i] >= ceil(r*T/W).
-__global__ void k_shard_bounds(const unsigned long long *F, long long nM, int rank, int W, long long *out) {
-    if (threadIdx.x >= 2) return;
-    const int r = rank + threadIdx.x;
+// Shard boundaries: the level's slot range [0, T = F[|M|]) is cut into NP
+// equal pieces at row granularity: a_j = first row with F[i] >= ceil(j T / NP) (a_0 = 0,
+// a_NP = |M|); out[j] = a_j and out[NP + 1 + j] = F[a_j] for j = 0..NP.
+__global__ void k_shard_bounds(const unsigned long long *F, long long nM, int NP, long long *out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j > NP) return;
     const unsigned long long T = F[nM];
     long long a;
-    if (r >= W) {
+    if (j == 0) {
+        a = 0;
+    } else if (j >= NP) {
         a = nM;
     } else {
-        unsigned __int128 num = (unsigned __int128)r * T + (W - 1);
-        unsigned long long target = (unsigned long long)(num / W);
+        unsigned __int128 num = (unsigned __int128)j * T + (NP - 1);
+        unsigned long long target = (unsigned long long)(num / NP);
         long long lo = 0, hi = nM;   // lower_bound over F[0..nM)
         while (lo < hi) {
             long long mid = (lo + hi) >> 1;
             if (F[mid] < target) lo = mid + 1; else hi = mid;
         }
-        a = r == 0 ? 0 : lo;
+        a = lo;
     }
-    out[threadIdx.x] = a;
-    out[2 + threadIdx.x] = (long long)F[a];
+    out[j] = a;
+    out[NP + 1 + j] = (long long)F[a];
 }
 
 }  // namespace
@@ -2002,17 +2012,17 @@ struct Prof {
     bool on = false;
     cudaStream_t st = nullptr;
     struct Rec {
-        int cls;
+        int cls, var;
         cudaEvent_t a, b;
     };
     std::vector<Rec> recs;
     uint32_t launches[GSI_N_KCLASS] = {0};
     uint32_t total = 0;
-    void begin(int cls) {
+    void begin(int cls, int var = -1) {
         total++;
         launches[cls]++;
         if (!on) return;
-        Rec r{cls, nullptr, nullptr};
+        Rec r{cls, var, nullptr, nullptr};
         host_t.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count() - host_base);
         cudaEventCreate(&r.a);
         cudaEventCreate(&r.b);
@@ -2052,7 +2062,10 @@ struct Prof {
         base = nullptr;
         for (auto &r : recs) {
             float ms = 0.f;
-            if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) s->ms_kernel[r.cls] += ms;
+            if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
+                s->ms_kernel[r.cls] += ms;
+                if (r.var >= 0) s->ms_variant[r.var] += ms;
+            }
             cudaEventDestroy(r.a);
             cudaEventDestroy(r.b);
         }
@@ -2399,6 +2412,7 @@ struct QueryCtx {
     std::vector<int> order, pos_of_q;
     int W = 1, rank = 0;
     bool sharded = true;
+    bool force_shared = false;   // test hook: the shared-run paths at any size (opts.force_paths & 1)
     unsigned long long shard_min = 65536;
     unsigned long long cap_slots = 0;
     double deadline = 0;
@@ -2517,11 +2531,12 @@ gsi_status ensure_filtered(QueryCtx &C, size_t si, uint32_t lab) {
     GSI_TRY(A.get_big(&fst, (unsigned long long)ft + 1));
     GSI_CUDA(cudaMemsetAsync(fst, 0, 8ull * (ft + 1), st));
     const uint32_t *cu0 = C.bm + (long long)C.steps[si].u * C.words;
-    C.prof->begin(GSI_K_OTHER);
+    C.prof->begin(GSI_K_OTHER, GSI_V_FILTER_PARTITION);
     C.S->variant_launches[GSI_V_FILTER_PARTITION]++;
     k_filter_partition<<<ft, kThreads, 0, st>>>(g->ci, lo, hi, cu0, fpos, fci, fst + 1, (unsigned *)fst);
     C.prof->end();
     C.S->alg_bytes[GSI_K_OTHER] += 12.0 * (hi - lo);
+    C.S->alg_bytes_variant[GSI_V_FILTER_PARTITION] += 12.0 * (hi - lo);
     C.filt[si] = {fpos, fci};
     return GSI_OK;
 }
@@ -2537,12 +2552,14 @@ gsi_status ensure_probe_ahead(QueryCtx &C, size_t si, const StepParams &P, const
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
     const unsigned grid = std::min<unsigned>(grid_for(hi - lo, 4 * kThreads), (unsigned)sms * 8);
-    C.prof->begin(GSI_K_OTHER);
+    C.prof->begin(GSI_K_OTHER, GSI_V_PROBE_AHEAD);
     C.S->variant_launches[GSI_V_PROBE_AHEAD]++;
     k_probe_ahead<<<grid, kThreads, 0, C.st>>>(C.filt[si].second, C.filt[si].first + (hi - lo), P2, g->groups,
                                                g->gpn, pa);
     C.prof->end();
-    C.S->alg_bytes[GSI_K_OTHER] += 20.0 * (hi - lo);   // read x, locate (8 B), re-point (8 B write)
+    // read x, one PCSR sector + two fpos words per candidate, 8 B entry write
+    C.S->alg_bytes[GSI_K_OTHER] += 52.0 * (hi - lo);
+    C.S->alg_bytes_variant[GSI_V_PROBE_AHEAD] += 52.0 * (hi - lo);
     C.pa[si] = pa;
     return GSI_OK;
 }
@@ -2628,18 +2645,20 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         cip = C.filt[si].second;
     } else if (shared_lists_allowed(C, P)) {
         const uint32_t lo = g->ci_lo[P.lab[0]], hi = g->ci_lo[P.lab[0] + 1];
-        if (hi > lo && gba >= (unsigned long long)GSI_PREFILTER_RATIO * (hi - lo)) {
+        if (hi > lo && (C.force_shared || gba >= (unsigned long long)GSI_PREFILTER_RATIO * (hi - lo))) {
             GSI_TRY(ensure_filtered(C, si, P.lab[0]));
             const unsigned rt = grid_for(nM, kThreads);
             unsigned long long *rst = nullptr;
             GSI_TRY(A.get(&rst, (unsigned long long)rt + 1 + sizeof(Counters) / 8));
             GSI_CUDA(cudaMemsetAsync(rst, 0, 8ull * (rt + 1) + sizeof(Counters), st));
             Counters *rctr = reinterpret_cast<Counters *>(rst + rt + 1);
-            prof.begin(GSI_K_OTHER);
+            prof.begin(GSI_K_OTHER, GSI_V_REFILTER);
             S.variant_launches[GSI_V_REFILTER]++;
             k_refilter<<<rt, kThreads, 0, st>>>(loc, (long long)nM, C.filt[si].first, lo, hi, F, rst + 1,
                                                 (unsigned *)rst, rctr);
             prof.end();
+            S.alg_bytes_variant[GSI_V_REFILTER] += 32.0 * nM;   // loc read + write, two fpos words, F
+            S.alg_bytes[GSI_K_OTHER] += 32.0 * nM;
             Counters hc0;
             GSI_CUDA(d2h(S, &gba, F + nM, 8, st));
             GSI_CUDA(d2h(S, &hc0, rctr, sizeof(Counters), st));
@@ -2660,7 +2679,7 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         !C.opts.no_count_ahead && shared_lists_allowed(C, P2)) {
         const uint32_t lo2 = g->ci_lo[P2.lab[0]], hi2 = g->ci_lo[P2.lab[0] + 1];
         cahead = hi2 > lo2 && ((C.filt.size() > si + 1 && C.filt[si + 1].first) ||
-                               gba * (unsigned long long)GSI_PREFILTER_AHEAD >= (unsigned long long)(hi2 - lo2));
+                               C.force_shared || gba * (unsigned long long)GSI_PREFILTER_AHEAD >= (unsigned long long)(hi2 - lo2));
     }
 
     // rows without F (see no_f2): build it unless the warp count-ahead consumes them as they are
@@ -2672,34 +2691,47 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
     }
 
     // ---- shard this level's slot range ----
-    unsigned long long s0 = 0, s1 = gba;
-    long long r_lo = 0, r_hi = (long long)nM;   // rows of this level that are ours
+    // W ranks x `pieces` equal slot pieces at row granularity; rank r keeps pieces r, r + W,
+    // r + 2W, ... (pieces = 1: one contiguous F-weighted range, the 1-GPU row order when the
+    // shards are concatenated in rank order; pieces > 1 interleave, so a query whose work is
+    // concentrated in part of the level still splits evenly).
+    struct Piece {
+        unsigned long long s0, s1;
+        long long r0, r1;
+    };
+    std::vector<Piece> pieces{{0ull, gba, 0ll, (long long)nM}};
     if (!C.sharded && (nM >= C.shard_min || gba > C.cap_slots || last || cahead)) {
+        const int per = std::max(1, (int)C.opts.shard_pieces);
+        const int NP = C.W * per;
         long long *bounds = nullptr;
-        GSI_TRY(A.get(&bounds, 4));
+        GSI_TRY(A.get(&bounds, 2ull * (NP + 1)));
         prof.begin(GSI_K_OTHER);
-        k_shard_bounds<<<1, 32, 0, st>>>(F, (long long)nM, C.rank, C.W, bounds);
+        k_shard_bounds<<<grid_for((unsigned long long)NP + 1, kThreads), kThreads, 0, st>>>(F, (long long)nM, NP,
+                                                                                            bounds);
         prof.end();
-        long long hb[4];
-        GSI_CUDA(d2h(S, hb, bounds, sizeof(hb), st));
+        std::vector<long long> hb(2 * (NP + 1));
+        GSI_CUDA(d2h(S, hb.data(), bounds, 8ull * hb.size(), st));
         GSI_CUDA(sync_timed(S, st));
         A.release(bounds);
-        s0 = (unsigned long long)hb[2];
-        s1 = (unsigned long long)hb[3];
-        r_lo = hb[0];
-        r_hi = hb[1];
+        pieces.clear();
+        for (int j = C.rank; j < NP; j += C.W)
+            pieces.push_back({(unsigned long long)hb[NP + 1 + j], (unsigned long long)hb[NP + 1 + j + 1], hb[j],
+                              hb[j + 1]});
         S.shard_level = t;
-        S.shard_row_begin = (uint64_t)hb[0];
-        S.shard_row_end = (uint64_t)hb[1];
+        S.shard_row_begin = (uint64_t)pieces.front().r0;
+        S.shard_row_end = (uint64_t)pieces.back().r1;
         C.sharded = true;
     }
 
     const int mode = cahead ? J_CAHEAD : (!last ? J_NEXT : (C.opts.want_table ? J_TABLE : J_COUNT));
+    const uint32_t *cu = C.bm + (long long)s.u * C.words;
+    gsi_status rc = GSI_OK;
+    for (const Piece &pc : pieces) {
+    const unsigned long long s0 = pc.s0, s1 = pc.s1;
+    const long long r_lo = pc.r0, r_hi = pc.r1;
     const unsigned long long chunk = (mode == J_COUNT || mode == J_CAHEAD)
                                          ? std::max<unsigned long long>(s1 - s0, 1)
                                          : std::max<unsigned long long>(C.cap_slots, kJoinTile);
-    const uint32_t *cu = C.bm + (long long)s.u * C.words;
-    gsi_status rc = GSI_OK;
     for (unsigned long long c0 = s0; c0 < s1 && rc == GSI_OK; c0 += chunk) {
         if (C.deadline > 0 && now_ms() > C.deadline) {
             C.capped = true;
@@ -2749,7 +2781,7 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         } else if (mode == J_NEXT && shared_lists_allowed(C, P2)) {
             const uint32_t lo2 = g->ci_lo[P2.lab[0]], hi2 = g->ci_lo[P2.lab[0] + 1];
             if (hi2 > lo2 && (C.filt.size() > si + 1 && C.filt[si + 1].first ||
-                              slots * (unsigned long long)GSI_PREFILTER_AHEAD >= (unsigned long long)(hi2 - lo2))) {
+                              C.force_shared || slots * (unsigned long long)GSI_PREFILTER_AHEAD >= (unsigned long long)(hi2 - lo2))) {
                 GSI_TRY(ensure_filtered(C, si + 1, P2.lab[0]));
                 P2.prefiltered = 1;
                 P2.fpos = C.filt[si + 1].first;
@@ -2767,7 +2799,7 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
             P2.col[0] == P.t && GSI_PROBE_AHEAD > 0) {
             const uint32_t plo = g->ci_lo[P.lab[0]], phi = g->ci_lo[P.lab[0] + 1];
             if ((C.pa.size() > si && C.pa[si]) ||
-                slots >= (unsigned long long)GSI_PROBE_AHEAD * (unsigned long long)(phi - plo)) {
+                C.force_shared || slots >= (unsigned long long)GSI_PROBE_AHEAD * (unsigned long long)(phi - plo)) {
                 GSI_TRY(ensure_probe_ahead(C, si, P, P2));
                 P.pa = C.pa[si];
                 S.n_probe_ahead++;
@@ -2805,7 +2837,7 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
             prof.end();
         }
         Counters hc_local;
-        prof.begin(GSI_K_JOIN);
+        int var;
         {
             int v;
             if (lean_next) v = GSI_V_NEXT_LEAN;
@@ -2817,7 +2849,9 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
             else if (mode == J_TABLE) v = GSI_V_JOIN_TABLE;
             else v = GSI_V_JOIN_NEXT;
             S.variant_launches[v]++;
+            var = v;
         }
+        prof.begin(GSI_K_JOIN, var);
         if (lean_next) {
             int sms = 148;
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
@@ -2890,14 +2924,52 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         const unsigned long long kept = lean_next ? hc.active_rows : nout;   // rows with a next buffer
         // holes cost the next level a row each: below 60 % kept, this level's later chunks
         // go back to the compacting tile kernel
-        if (lean_next && kept * 5 < slots * 3) C.lean_off[si] = 1;
+        if (lean_next && kept * 5 < slots * 3 && !C.force_shared) C.lean_off[si] = 1;
+        // Algorithmic bytes of this launch: what the variant must move at least
+        // once — the rows of M it extends (row, loc, F), candidates streamed from ci (shared
+        // N(v,l0) ∩ C(u) runs are re-read by many rows and stay in L2: not charged per slot),
+        // one 32 B PCSR sector + two fpos words per lookup, and every byte it writes.
         const double frac = gba ? (double)slots / (double)gba : 0.0;
-        double jb = frac * (4.0 * P.t * active + 4.0 * elems + (8.0 * E + 8.0) * active);
-        if (mode == J_TABLE) jb += 4.0 * C.q->k * nout;
-        if (mode == J_NEXT) jb += kept * (4.0 * P.out_w + 16.0 * P2.E + 8.0);
+        const double rows_in = frac * (double)active;     // rows of the chunk with a non-empty buffer
+        const double row_b = 4.0 * P.t + 8.0 * E + 8.0;    // row + loc + F
+        const double cand_b = P.prefiltered ? 0.0 : 4.0 * (double)slots;
+        constexpr double kLook = 40.0;                      // one PCSR sector + fpos pair
+        const double surv_next = (double)hc.count;          // J_NEXT survivors (stored or not)
+        double jb = 0.0;
+        switch (var) {
+        case GSI_V_NEXT_LEAN:   // rows at their Prealloc slots: loc2 for every slot, rows where kept
+            jb = rows_in * row_b + cand_b + 8.0 * (double)slots + 4.0 * P.out_w * (double)kept +
+                 kLook * ((P2.col[0] < P.t) ? rows_in : (P.pa ? 0.0 : surv_next)) + (P.pa ? 8.0 * surv_next : 0.0);
+            break;
+        case GSI_V_CAHEAD_LEAN:
+        case GSI_V_FINAL_LEAN:   // closed form per row: loc of every slot, the active rows' columns
+        case GSI_V_FINAL_FP:
+            jb = 8.0 * (double)(r_hi - r_lo) + 4.0 * P.t * (double)hc.active_rows +
+                 (var == GSI_V_CAHEAD_LEAN ? kLook * (double)hc.active_rows : 0.0);
+            break;
+        case GSI_V_CAHEAD_WARP:
+        case GSI_V_JOIN_CAHEAD:   // rows + candidates + the last step's run per row or survivor
+            jb = rows_in * row_b + cand_b + kLook * ((P2.col[0] < P.t) ? rows_in : (P.pa ? 0.0 : (double)hc.total)) +
+                 (P.pa ? 8.0 * (double)hc.total : 0.0);
+            break;
+        case GSI_V_JOIN_NEXT: {   // + next-step locates, compacted rows, loc', F'
+            double looks = 0.0;
+            if (P2.E == 1) looks = (P.stage_next && !P.pa) ? rows_in : (P.pa ? 0.0 : surv_next);
+            else looks = P2.E * (surv_next + (double)nout);
+            jb = rows_in * row_b + cand_b + kLook * looks + (P.pa ? 8.0 * surv_next : 0.0) +
+                 (double)nout * (4.0 * P.out_w + 8.0 * P2.E + (P.no_f2 ? 0.0 : 8.0));
+            break;
+        }
+        case GSI_V_JOIN_TABLE:
+            jb = rows_in * row_b + cand_b + 4.0 * C.q->k * (double)nout;
+            break;
+        default:   // GSI_V_JOIN_COUNT, GSI_V_COUNT_FAST
+            jb = rows_in * row_b + cand_b;
+        }
+        if (E > 1) jb += 8.0 * rows_in * (E - 1);   // the other linking lists' locate entries
+        S.alg_bytes_variant[var] += jb;
         if (mode == J_NEXT) S.rows[t] += hc.count;   // |M_{t+1}|: every survivor, stored or not
         if (mode == J_CAHEAD) {                        // survivors = |M_{t+1}|, counted = |M_{t+2}|
-            jb += 8.0 * hc.total;                      // locate of the last step's run per survivor
             S.rows[t] += hc.total;
             S.rows[t + 1] += hc.count;
             S.gba[t + 1] += hc.total2;
@@ -2928,6 +3000,8 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
             A.release(F2);
         }
         A.reset(mk);
+    }
+    if (rc != GSI_OK) break;
     }
     return rc;
 }
@@ -3054,6 +3128,7 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     }
     C.shard_min = opts.shard_min_rows ? opts.shard_min_rows : 65536;
     C.sharded = C.W == 1;
+    C.force_shared = (opts.force_paths & 1) != 0;
     C.deadline = opts.timeout_s > 0 ? t_start + 1000.0 * opts.timeout_s : 0;
 
     bool empty = q->absent_label;

@@ -47,7 +47,7 @@ class gsi_query_opts(ctypes.Structure):
                 ("shard_rank", I32), ("shard_count", I32), ("shard_min_rows", U64),
                 ("mem_budget_bytes", U64), ("timeout_s", ctypes.c_double), ("profile", I32), ("stream", P),
                 ("chunk_slots", U64), ("partial_on_timeout", I32), ("fingerprint", I32), ("no_shared_lists", I32),
-                ("no_count_ahead", I32)]
+                ("no_count_ahead", I32), ("shard_pieces", I32), ("force_paths", I32)]
 
 
 class gsi_graph_info(ctypes.Structure):
@@ -71,7 +71,8 @@ class gsi_stats(ctypes.Structure):
                 ("total_launches", U32), ("n_chunks", U32), ("capped", I32), ("h2d_bytes", U64),
                 ("d2h_bytes", U64), ("n_shared_lists", U32), ("ms_host_alloc", ctypes.c_float),
                 ("ms_host_sync", ctypes.c_float), ("count_ahead", I32), ("n_probe_ahead", U32),
-                ("variant_launches", U32 * GSI_N_KVARIANT)]
+                ("variant_launches", U32 * GSI_N_KVARIANT), ("ms_variant", ctypes.c_float * GSI_N_KVARIANT),
+                ("alg_bytes_variant", ctypes.c_double * GSI_N_KVARIANT)]
 
 
 _SIGS = {
@@ -98,6 +99,7 @@ _SIGS = {
     "gsi_debug_signatures": (I32, [P, P]),
     "gsi_debug_filter": (I32, [P, I32, P, I32, P, P, P, I32, P, P]),
     "gsi_debug_query_signatures": (I32, [I32, P, I32, P, P, P, I32, P]),
+    "gsi_debug_hash": (U64, [I32, U64, U64]),
     "gsi_last_error": (ctypes.c_char_p, []),
     "gsi_version": (ctypes.c_char_p, []),
     "gsi_device_count": (I32, []),
@@ -268,7 +270,8 @@ class Prepared:
 def _opts(want_table=False, homomorphism=False, filter_mode=0, e0_mode=0, force_order=None,
           force_first_edge=None, roots=None, shard_rank=0, shard_count=1, shard_min_rows=0,
           mem_budget_bytes=0, timeout_s=0.0, profile=False, stream=None, chunk_slots=0,
-          partial_on_timeout=False, fingerprint=True, shared_lists=True, count_ahead=True):
+          partial_on_timeout=False, fingerprint=True, shared_lists=True, count_ahead=True, shard_pieces=1,
+          force_paths=0):
     o = gsi_query_opts()
     lib.gsi_query_opts_default(ctypes.byref(o))
     keep = []
@@ -286,6 +289,8 @@ def _opts(want_table=False, homomorphism=False, filter_mode=0, e0_mode=0, force_
     o.fingerprint = int(fingerprint)   # binding default: on (the C default is off)
     o.no_shared_lists = 0 if shared_lists else 1
     o.no_count_ahead = 0 if count_ahead else 1
+    o.shard_pieces = shard_pieces
+    o.force_paths = force_paths
     return o, keep
 
 
@@ -362,6 +367,10 @@ def gsi_debug_query_signatures(q_vlabels, q_src, q_dst, q_elabels, distinct: boo
                                           _ptr(out)),
            "gsi_debug_query_signatures")
     return out
+
+
+def gsi_debug_hash(kind: int, key: int, seed: int = 0) -> int:
+    return int(lib.gsi_debug_hash(kind, key & 0xFFFFFFFFFFFFFFFF, seed & 0xFFFFFFFFFFFFFFFF))
 
 
 def gsi_trim_workspace(device: int = -1) -> None:

@@ -92,3 +92,21 @@ def test_query_signature_encoding_matches_oracle():
 def test_invalid_arguments_are_errors():
     with pytest.raises(gsi.GsiError):
         gsi.gsi_debug_query_signatures(np.zeros(33), [], [], [])
+
+
+def test_library_hashes_equal_known_answer_hashes():
+    """The library's own hash code (host side of the __host__ __device__ functions its kernels
+    call) against the oracle's general MurmurHash2 / MurmurHash64A, which are pinned to
+    SMHasher's verification values in tests/test_oracle.py::test_murmur_known_answers.  A
+    transcription slip shared by the device and the oracle specialisations would fail here."""
+    rng = np.random.default_rng(12)
+    for _ in range(300):
+        x = int(rng.integers(0, 1 << 32))
+        seed = int(rng.integers(0, 1 << 32))
+        assert gsi.gsi_debug_hash(0, x, seed) == oracle.murmur2(x.to_bytes(4, "little"), seed)
+        key = int(rng.integers(0, 1 << 62)) * 4 + int(rng.integers(0, 4))
+        assert gsi.gsi_debug_hash(1, key, seed) == oracle.murmur64a(key.to_bytes(8, "little"), seed)
+    # PCSR seeds are 0x9747B28C ^ label (reading A7)
+    for l in range(5):
+        assert gsi.gsi_debug_hash(0, 12345, 0x9747B28C ^ l) == oracle.murmur2((12345).to_bytes(4, "little"),
+                                                                             0x9747B28C ^ l)

@@ -1,0 +1,205 @@
+"""GPU parity at the BASELINE configs' full sizes in the
+launch configuration bench.py times, against the CPU oracle.
+
+Protocol (SURVEY.md §8(c) 'Scale'): where the oracle finishes, the whole query (count and set
+fingerprint); otherwise root-restricted parity — both sides restricted to f(pi_1) in S for a
+sample S of the oracle's own C(pi_1) (its independent signature filter), pi_1 being the only
+thing taken from the GPU side (its plan).  Each comparison runs the count path (closed-form
+count-ahead), count-ahead off, the fingerprinted enumeration, and the same with the shared-run
+paths forced (`force_paths`), and asserts through gsi_stats.variant_launches that the kernels
+the bench's heavy queries use (k_filter_partition, k_next_lean, k_cahead_lean, k_final_fp,
+k_probe_ahead) actually ran on the full-size graph.  Every expected value comes from oracle/.
+"""
+import gc
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as W
+from paper_1906_03420_b200 import gsi
+
+pytestmark = pytest.mark.gpu
+
+if gsi.gsi_device_count() == 0:
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+MODES = {"count": dict(fingerprint=False), "enum": dict(fingerprint=False, count_ahead=False),
+         "fp": dict(fingerprint=True)}
+
+
+class Env:
+    def __init__(self, cfg, nq=16, k=12):
+        import torch
+        self.cfg = cfg
+        self.g = W.make_config(cfg, device="cuda")
+        adj = W._Adj(self.g, device="cuda")
+        self.qs = [W.random_walk_query(self.g, k, 1000 + i, adj) for i in range(nq)]
+        del adj
+        torch.cuda.empty_cache()
+        self.graph = gsi.build(self.g)
+        self.og = oracle.OracleGraph(self.g)
+        self._planes = None
+
+    def planes(self):
+        if self._planes is None:
+            self._planes = oracle.signatures(self.og)
+        return self._planes
+
+    def oracle_cu(self, q, u):
+        """The oracle's own C(u) (independent signature filter) as a vertex array."""
+        bm, _ = oracle.filter(self.og, self.planes(), oracle.query_signatures(q))
+        words = bm[u]
+        bits = np.unpackbits(words.view(np.uint8), bitorder="little")
+        return np.nonzero(bits[: self.g.n])[0]
+
+    def close(self):
+        import torch
+        self.graph = None
+        self.og = None
+        self._planes = None
+        gc.collect()
+        gsi.gsi_trim_workspace()
+        torch.cuda.empty_cache()
+
+
+@pytest.fixture(scope="module")
+def env_cache():
+    cache = {}
+    yield cache
+    for e in cache.values():
+        e.close()
+
+
+def get_env(cache, cfg):
+    for k in list(cache):
+        if k != cfg:
+            cache.pop(k).close()
+    if cfg not in cache:
+        cache[cfg] = Env(cfg)
+    return cache[cfg]
+
+
+def check_query(e, q, roots=None, root=None, modes=("count", "enum", "fp"), force=(0, 1), timeout=60.0):
+    """GPU count (all modes) == oracle count; fingerprints equal where hashed.  Returns the
+    union of kernel variants launched and the oracle count (None if the oracle timed out)."""
+    kw = {} if roots is None else dict(roots=roots)
+    okw = {} if roots is None else dict(roots=roots, root=root)
+    try:
+        cnt, fp, _ = oracle.match(e.og, q, table=False, timeout=timeout, **okw)
+    except oracle.OracleError:
+        return None, {}
+    seen = {}
+    for fmode in force:
+        for m in modes:
+            r = gsi.query(e.graph, q, force_paths=fmode, **MODES[m], **kw)
+            assert r.count == cnt, (e.cfg, m, fmode, r.count, cnt)
+            if m == "fp":
+                assert r.fingerprint() == fp, (e.cfg, fmode)
+            for k_, v_ in r.stats()["variants"].items():
+                seen[k_] = seen.get(k_, 0) + v_
+    return cnt, seen
+
+
+def root_sample(e, q, rng, n, must=None):
+    """pi_1 from the GPU plan, then n roots of the oracle's C(pi_1) (plus the walk's own start
+    for pi_1, which has >= 1 match)."""
+    root = gsi.query(e.graph, q, fingerprint=False).stats()["order"][0]
+    cu = e.oracle_cu(q, root)
+    s = rng.choice(cu, min(n, len(cu)), replace=False) if len(cu) else np.zeros(0, np.int64)
+    s = np.unique(np.append(s, q.embedding[root]))
+    return root, s
+
+
+@pytest.mark.parametrize("cfg", ["C3", "C4"])
+def test_full_config_whole_queries(cfg, env_cache):
+    """C3 gowalla-shaped (196 591 V / 950 327 E) and C4 road-shaped (14.0 M V / 17 M E): the
+    bench's 16 twelve-vertex walk queries, whole-query parity (count + fingerprint) in every
+    mode, with and without the forced shared-run paths."""
+    e = get_env(env_cache, cfg)
+    done = 0
+    for q in e.qs:
+        cnt, _ = check_query(e, q, timeout=60.0)
+        if cnt is not None:
+            assert cnt >= 1   # the walk's own embedding is a match
+            done += 1
+    assert done >= 12
+
+
+def test_c5a_whole_and_root_restricted(env_cache):
+    """C5a (R-MAT scale 25, |L_V| = 1000, |L_E| = 86): whole-query parity where the oracle
+    finishes, root-restricted otherwise."""
+    e = get_env(env_cache, "C5a")
+    rng = np.random.default_rng(3)
+    done = 0
+    for q in e.qs[:12]:
+        cnt, _ = check_query(e, q, timeout=30.0, force=(0,))
+        if cnt is None:
+            root, s = root_sample(e, q, rng, 64)
+            cnt, _ = check_query(e, q, roots=s, root=root, timeout=60.0, force=(0,))
+        if cnt is not None:
+            done += 1
+    assert done >= 10
+
+
+@pytest.mark.parametrize("cfg", ["C5b", "C5m"])
+def test_c5_root_restricted_bench_kernels(cfg, env_cache):
+    """C5b (|L_V| = 10) and C5m (the bench default, |L_V| = 100), 264 M edges: root-restricted
+    parity in every mode, with the shared-run paths forced so that the bench's heavy-query
+    kernels run on the full-size graph (asserted through the variant counters)."""
+    e = get_env(env_cache, cfg)
+    rng = np.random.default_rng(7)
+    seen, checked = {}, 0
+    for q in e.qs:
+        for ns in (16, 4, 1):
+            root, s = root_sample(e, q, rng, ns)
+            cnt, sv = check_query(e, q, roots=s, root=root, timeout=30.0)
+            if cnt is None:
+                continue
+            checked += 1
+            for k_, v_ in sv.items():
+                seen[k_] = seen.get(k_, 0) + v_
+            break
+        if checked >= 8:
+            break
+    assert checked >= 6, checked
+    for v in ("filter_partition", "next_lean", "final_fp", "cahead_lean"):
+        assert seen.get(v, 0) > 0, (v, seen)
+
+
+def test_c5m_bench_queries_modes_agree(env_cache):
+    """The bench's 16 C5m queries at full size (1.7e12 matches per step): the closed-form count
+    path equals count-ahead off and the fingerprinted enumeration (every final match produced,
+    read and hashed by k_final_fp / k_join) query by query — three different kernel paths."""
+    e = get_env(env_cache, "C5m")
+    seen = {}
+    for q in e.qs:
+        cs = []
+        for m in ("count", "enum", "fp"):
+            r = gsi.query(e.graph, q, timeout_s=120.0, **MODES[m])
+            cs.append(r.count)
+            for k_, v_ in r.stats()["variants"].items():
+                seen[k_] = seen.get(k_, 0) + v_
+        assert cs[0] == cs[1] == cs[2], cs
+    assert seen.get("cahead_lean", 0) > 0 and seen.get("final_fp", 0) > 0 and seen.get("next_lean", 0) > 0, seen
+
+
+def test_c5m_unforced_root_restricted_many_roots(env_cache):
+    """Root-restricted parity with enough roots inside C(pi_1) that a heavy query takes its
+    shared-run paths unforced (the size thresholds decide, as in the bench)."""
+    e = get_env(env_cache, "C5m")
+    rng = np.random.default_rng(9)
+    seen, checked = {}, 0
+    for qi in (11, 13, 7):
+        q = e.qs[qi]
+        for ns in (400, 100, 25):
+            root, s = root_sample(e, q, rng, ns)
+            cnt, sv = check_query(e, q, roots=s, root=root, timeout=120.0, modes=("count", "fp"), force=(0,))
+            if cnt is None:
+                continue
+            checked += 1
+            for k_, v_ in sv.items():
+                seen[k_] = seen.get(k_, 0) + v_
+            break
+    assert checked >= 2
+    assert seen.get("filter_partition", 0) > 0, seen

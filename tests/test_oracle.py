@@ -344,3 +344,22 @@ def test_partial_count_on_timeout():
         oracle.match(og, q, table=False, timeout=1e-3)
     c, fp, _ = oracle.match(og, q, table=False, timeout=1e-3, partial=True)
     assert 0 <= c == fp[0]
+
+
+def test_murmur_known_answers():
+    """External known answers for the hash functions of the written spec (DESIGN.md §3,
+    readings A6/A7): SMHasher's published verification values of Appleby's MurmurHash2
+    (0x27864C1E) and MurmurHash64A (0x1F0D3804) pin the oracle's general byte-string
+    restatements; the oracle's 8-byte signature hash must equal the general one on the key's
+    8 little-endian bytes."""
+    assert oracle.smhasher_verify(0) == 0x27864C1E
+    assert oracle.smhasher_verify(1) == 0x1F0D3804
+    rng = np.random.default_rng(11)
+    for _ in range(200):
+        key = int(rng.integers(0, 1 << 63)) * 2 + int(rng.integers(0, 2))
+        seed = int(rng.integers(0, 1 << 32))
+        assert oracle.murmur64a_key(key, seed) == oracle.murmur64a(key.to_bytes(8, "little"), seed)
+    # and the signature groups the oracle derives from it (reading A6: key = L_E << 32 | L_V)
+    for le, lv in [(0, 0), (1, 2), (85, 99), (999, 7)]:
+        h = oracle.murmur64a(((le << 32) | lv).to_bytes(8, "little"), 0x9747B28C)
+        assert oracle.sig_group(le, lv) == h % 240
