@@ -460,6 +460,13 @@ def run_gsi(args):
                                 "efficiency": sum(per_rank) / (W_ * max(per_rank)),
                                 "count_equal": tot == total_matches}
 
+    # ---- small queries (C2 enron-shaped, C4 road-shaped): per-query latency ---------------
+    small = None
+    if ws == 1 and not args.no_small:
+        small = {}
+        for cfg in args.small_configs:
+            small[cfg] = small_query_latency(gsi, cfg, args.queries, args.k, local)
+
     if rank != 0:
         if ws > 1:
             dist.barrier()
@@ -490,6 +497,7 @@ def run_gsi(args):
         "e2e": {"value": m_e2e * args.steps / e2e_s, "unit": "matches/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_query": 1000.0 * e2e_s / args.steps / len(qs)},
         "enumerated": enumerated, "table": table, "roofline": roofline, "multi_gpu_balance_emulated": balance,
+        "small_queries": small,
         "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": launches,
         "graph": {"n_groups": info["n_groups"], "max_chain": info["max_chain"],
                   "bytes_total": info["bytes_total"], "build_ms": info["ms_build"]},
@@ -498,6 +506,41 @@ def run_gsi(args):
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def small_query_latency(gsi, cfg, nq, k, device):
+    """Latency of single queries on a small-query config: each of the nq walk queries runs
+    alone (prepared, count-only) 5 times after one warm-up; per query the median of the host
+    wall time around the synchronous gsi_query_run (filter, plan, every level, count on the
+    host), then p50 / mean / p95 over the queries, with the kernel path taken."""
+    import torch
+    g, qs = make_workload(cfg, nq, k, "cuda")
+    graph = gsi.build(g, device=device)
+    torch.cuda.synchronize()
+    prepared = [gsi.prepare(graph, q) for q in qs]
+    per_q, dev_ms, paths, counts = [], [], {}, []
+    for p in prepared:
+        gsi.gsi_query_run(graph, p, fingerprint=False)
+        ts = []
+        for _ in range(5):
+            t = time.perf_counter()
+            r = gsi.gsi_query_run(graph, p, fingerprint=False)
+            ts.append(1000.0 * (time.perf_counter() - t))
+        st = r.stats()
+        per_q.append(float(np.median(ts)))
+        dev_ms.append(st["ms_total"])
+        counts.append(r.count)
+        path = "small" if st["variants"].get("small", 0) and not st["small_aborted"] else "regular"
+        paths[path] = paths.get(path, 0) + 1
+    a = np.array(per_q)
+    out = {"workload": BENCH_CONFIGS[cfg]["desc"], "queries": len(per_q), "p50_ms": float(np.percentile(a, 50)),
+           "mean_ms": float(a.mean()), "p95_ms": float(np.percentile(a, 95)), "paths": paths,
+           "matches": int(sum(counts)), "timing": "host wall time around one synchronous gsi_query_run "
+                                                 "(prepared query, count-only), median of 5 per query"}
+    del prepared, graph
+    gsi.gsi_trim_workspace(device)
+    torch.cuda.empty_cache()
+    return out
 
 
 def spawn_ranks(args) -> int:
@@ -540,6 +583,8 @@ def main():
     ap.add_argument("--table-max-gb", type=float, default=40.0, help="table pass: queries whose table fits")
     ap.add_argument("--no-balance", action="store_true", help="skip the emulated multi-GPU balance")
     ap.add_argument("--shard-pieces", type=int, default=8, help="interleaved shard pieces per rank (N > 1)")
+    ap.add_argument("--no-small", action="store_true", help="skip the small-query latency section")
+    ap.add_argument("--small-configs", nargs="*", default=["C2", "C4"])
     args = ap.parse_args()
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:

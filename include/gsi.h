@@ -76,7 +76,17 @@ enum { GSI_V_JOIN_NEXT = 0,       /* k_join<J_NEXT>: slot tiles, compacting (Com
        GSI_V_PROBE_AHEAD = 12,    /* k_probe_ahead: per-candidate next-step locate table       */
        GSI_V_SMALL = 13,          /* k_small_query: whole query in one launch                  */
        GSI_V_TWO_STEP = 14,       /* ablation: count pass of the two-step output               */
-       GSI_V_RESERVED = 15 };
+       GSI_V_ABLATION = 15 };     /* ablation engine join launches (warp per row, paper design) */
+
+/* gsi_query_opts.ablation bits (NEXT-3: the paper's join-phase study, Tables VI-VIII):
+ * any bit set runs the query on the paper-style engine (one warp per row of M, Alg. 3/4) with
+ * the named technique switched off; 0 = the B200 default path.  Results are identical. */
+#define GSI_ABL_ENGINE   1   /* paper-style engine with PCSR, Prealloc-Combine, write cache, set ops */
+#define GSI_ABL_CR       2   /* locate N(v,l) in the Compressed Representation (binary search, L674-682) */
+#define GSI_ABL_TWO_STEP 4   /* two-step output (join twice: count, scan, join + write; L1635-1641) */
+#define GSI_ABL_NO_WCACHE 8  /* no write cache: each lane stores its own survivor row (L1155-1158)  */
+#define GSI_ABL_NAIVE_SO 16  /* naive set operation: C(u) by binary search in the candidate list,
+                                 other linking lists by linear scan (L1136-1158 off)                */
 
 typedef struct gsi_graph gsi_graph;       /* opaque: PCSR + signature table on one device   */
 typedef struct gsi_result gsi_result;     /* opaque: count, fingerprint, optional table     */
@@ -184,6 +194,11 @@ typedef struct {
                                     allows them, ignoring the size thresholds that normally decide
                                     — so small root-restricted runs exercise the kernels a large
                                     query uses.  Results are identical either way.               */
+    int32_t small_mode;          /* 0: a query with a small first level runs all its levels in one
+                                    launch (k_small_query) when it fits, else the regular path;
+                                    1: always the regular per-level path                       */
+    int32_t ablation;            /* GSI_ABL_* bits (0: off).  Count / fingerprint only: with
+                                    want_table the call returns GSI_ERR_INVALID_ARG             */
 } gsi_query_opts;
 
 void gsi_query_opts_default(gsi_query_opts *opts);
@@ -253,6 +268,7 @@ typedef struct {
        one 32 B sector + fpos per PCSR lookup)                                   */
     float ms_variant[GSI_N_KVARIANT];
     double alg_bytes_variant[GSI_N_KVARIANT];
+    int32_t small_aborted;            /* the small-query kernel stopped at this level (0: not)  */
 } gsi_stats;
 
 gsi_status gsi_result_count(const gsi_result *r, uint64_t *count);

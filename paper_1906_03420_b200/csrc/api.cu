@@ -52,6 +52,8 @@ static void free_graph(gsi_graph *g) {
     if (g->sig) cudaFree(g->sig);
     if (g->groups) cudaFree(g->groups);
     if (g->ci) cudaFree(g->ci);
+    if (g->cr_key) cudaFree(g->cr_key);
+    if (g->cr_loc) cudaFree(g->cr_loc);
     cudaSetDevice(cur);
     delete g;
 }

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -327,6 +328,7 @@ __device__ __forceinline__ unsigned long long block_exclusive_scan(unsigned long
 namespace gsi {
 
 void set_error(const std::string &msg);
+gsi_status ensure_cr(const gsi_graph *g, cudaStream_t st);   // graph.cu: build the CR layer once
 std::string gsi_last_error_str();   // this thread's last error message
 size_t workspace_idle_bytes(int dev);
 gsi_status cuda_fail(cudaError_t e, const char *what);
@@ -373,6 +375,12 @@ struct gsi_graph {
     std::vector<uint32_t> ngroups;  // |V(D_l)|
     std::vector<uint32_t> ci_lo;    // [nl+1]: P(G,l)'s runs are ci[ci_lo[l], ci_lo[l+1])
     int dense_label(int32_t raw) const;   // -1 if absent
+    // Compressed Representation, built on demand for the NEXT-3 ablation:
+    // per partition l the sorted "vertex ID" layer cr_key[gbase_l .. gbase_l + ngroups_l)
+    // (key = l << 32 | v) and each vertex's run cr_loc (offset into ci, length).
+    mutable std::mutex cr_mu;
+    mutable unsigned long long *cr_key = nullptr;
+    mutable uint2 *cr_loc = nullptr;
 };
 
 // A validated, encoded query (opaque to callers).

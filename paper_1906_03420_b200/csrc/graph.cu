@@ -294,6 +294,67 @@ static gsi_status exclusive_scan_u32(const uint32_t *in, uint32_t *out, int64_t 
     return GSI_OK;
 }
 
+// ---------------------------------------------------------------- CR (ablation) -----
+// The Compressed Representation of PAPER.md L674-682 ("a layer called vertex ID is added, and
+// binary search is performed over this layer"), derived from the PCSR groups: every occupied
+// slot (v, o_v) of partition l becomes (l << 32 | v, run), then the entries are sorted by key.
+// Partition l has exactly ngroups_l keys (one group per partition vertex), so its layer is
+// [gbase_l, gbase_l + ngroups_l) of the sorted arrays.
+namespace {
+__global__ void k_cr_emit(const uint2 *groups, int gpn, long long ngroups_total, const long long *gb, int nl,
+                          unsigned long long *key, uint2 *loc, unsigned long long *ctr) {
+    for (long long g = blockIdx.x * (long long)blockDim.x + threadIdx.x; g < ngroups_total;
+         g += (long long)gridDim.x * blockDim.x) {
+        int lo = 0, hi = nl;   // partition of group g: last l with gb[l] <= g
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (gb[mid] <= g) lo = mid; else hi = mid;
+        }
+        const uint2 *G = groups + g * (long long)gpn;
+        for (int sl = 0; sl < gpn - 1; sl++) {
+            const uint2 p = G[sl];
+            if (p.x == kEmpty) break;
+            const unsigned long long i = atomicAdd(ctr, 1ull);
+            key[i] = ((unsigned long long)(uint32_t)lo << 32) | p.x;
+            loc[i] = make_uint2(p.y, G[sl + 1].y - p.y);
+        }
+    }
+}
+}  // namespace
+
+gsi_status ensure_cr(const gsi_graph *g, cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(g->cr_mu);
+    if (g->cr_key || g->n_groups == 0) return GSI_OK;
+    const long long K = g->n_groups;
+    const int nl = g->n_labels;
+    DevBuf<unsigned long long> k1, ctr;
+    DevBuf<uint2> l1;
+    DevBuf<long long> gb;
+    GSI_CUDA(k1.alloc(K, st));
+    GSI_CUDA(l1.alloc(K, st));
+    GSI_CUDA(ctr.alloc(1, st));
+    GSI_CUDA(gb.alloc(nl + 1, st));
+    GSI_CUDA(cudaMemsetAsync(ctr.p, 0, 8, st));
+    std::vector<long long> hgb(nl + 1);
+    for (int l = 0; l < nl; l++) hgb[l] = g->gbase[l];
+    hgb[nl] = K;
+    GSI_CUDA(cudaMemcpyAsync(gb.p, hgb.data(), 8ull * (nl + 1), cudaMemcpyHostToDevice, st));
+    k_cr_emit<<<blocks_for(K), kB, 0, st>>>(g->groups, g->gpn, K, gb.p, nl, k1.p, l1.p, ctr.p);
+    unsigned long long *key = nullptr;
+    uint2 *loc = nullptr;
+    GSI_CUDA(cudaMalloc(&key, 8ull * K));
+    GSI_CUDA(cudaMalloc(&loc, 8ull * K));
+    size_t t = 0;
+    GSI_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t, k1.p, key, l1.p, loc, (int)K, 0, 64, st));
+    DevBuf<unsigned char> tmp;
+    GSI_CUDA(tmp.alloc(t, st));
+    GSI_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, t, k1.p, key, l1.p, loc, (int)K, 0, 64, st));
+    GSI_CUDA(cudaStreamSynchronize(st));
+    g->cr_key = key;
+    g->cr_loc = loc;
+    return GSI_OK;
+}
+
 gsi_status build_graph_impl(int64_t n, const int32_t *h_vl, int64_t m, const int32_t *h_src, const int32_t *h_dst,
                             const int32_t *h_el, const gsi_build_opts *opts, gsi_graph **out) {
     auto t0 = std::chrono::steady_clock::now();

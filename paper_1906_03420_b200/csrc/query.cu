@@ -66,7 +66,7 @@ constexpr int kThreads = 256;
 #define GSI_FILTER_MINB 4   // k_filter: resident blocks per SM the registers are sized for
 #endif
 #ifndef GSI_FILTER_FW
-#define GSI_FILTER_FW 4     // k_filter: bitmap words per warp per iteration
+#define GSI_FILTER_FW 8     // k_filter: bitmap words per warp per iteration
 #endif
 #ifndef GSI_NEXT_LEAN
 #define GSI_NEXT_LEAN 1     // lean warp-centric J_NEXT writing rows at their Prealloc slots (0: off)
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kThreads, GSI_FILTER_MINB) k_filter(const uint
                                                      uint32_t *__restrict__ bitmaps, long long words,
                                                      unsigned long long *__restrict__ counts,
                                                      Counters *__restrict__ ctr) {
-    static_assert(GSI_FILTER_FW == 4, "the bitmap store is one 16 B vector per query vertex");
+    static_assert(GSI_FILTER_FW % 4 == 0, "the bitmap store is 16 B vectors per query vertex");
     constexpr int kHT = 64;                          // label -> query-vertex mask, open addressing
     __shared__ uint32_t qs[GSI_MAX_K * kPlanes];
     __shared__ uint32_t qneed[GSI_MAX_K];            // planes 1..15 where S(u) has a set bit
@@ -251,7 +251,9 @@ __global__ void __launch_bounds__(kThreads, GSI_FILTER_MINB) k_filter(const uint
         if (lane < k) {
             uint32_t *dst = bitmaps + (long long)lane * words + w0;
             if (w0 + kFW <= words && ((words & 3) == 0)) {
-                *reinterpret_cast<uint4 *>(dst) = make_uint4(mine[0], mine[1], mine[2], mine[3]);
+#pragma unroll
+                for (int j = 0; j < kFW; j += 4)
+                    *reinterpret_cast<uint4 *>(dst + j) = make_uint4(mine[j], mine[j + 1], mine[j + 2], mine[j + 3]);
             } else {
 #pragma unroll
                 for (int j = 0; j < kFW; j++)
@@ -1742,6 +1744,410 @@ __global__ void __launch_bounds__(kThreads) k_lens_scan(const Loc *__restrict__ 
     if (tile == gridDim.x - 1 && threadIdx.x == kThreads - 1) F[nM] = base_s + agg;
 }
 
+// ------------------------------------------------------------ NEXT-3 ablations ------
+// The paper's own join design (one warp per row of M, Alg. 3 / Alg. 4), with the switches of
+// its join-phase study (§VII, Tables VI-VIII): the lookup structure
+// (PCSR, or the Compressed Representation's binary search over a sorted vertex-ID layer,
+// L674-682), the output scheme (Prealloc-Combine: survivors written once into the Prealloc'd
+// GBA buffers then linked, Alg. 3 lines 14-21; or the two-step scheme of GpSM that joins twice,
+// counting first, L1635-1641), the write cache (survivor rows staged in shared memory and
+// written as a coalesced block, L1155-1158, or written by each lane directly) and the set
+// operation (GPU-friendly: C(u) bitset + binary search, L1136-1158; or naive: C(u) by binary
+// search in the sorted candidate list, other lists by linear scan).  Same R in every
+// combination; used to reproduce the paper's trends on B200, never by default.
+enum AblMode { AB_PC = 0, AB_COUNT = 1, AB_WRITE = 2, AB_FINAL = 3 };
+
+__device__ __forceinline__ Loc abl_lookup(const StepParams &P, int e, uint32_t v, bool cr,
+                                          const unsigned long long *__restrict__ cr_key,
+                                          const uint2 *__restrict__ cr_loc, const uint2 *__restrict__ groups,
+                                          int gpn) {
+    if (!cr) return pcsr_lookup(groups, gpn, P.gbase[e], P.ngroups[e], P.lab[e], v, nullptr);
+    const unsigned long long key = ((unsigned long long)P.lab[e] << 32) | v;
+    unsigned long long lo = P.gbase[e], hi = lo + P.ngroups[e];   // lower bound in the vertex-ID layer
+    while (lo < hi) {
+        const unsigned long long mid = (lo + hi) >> 1;
+        if (__ldg(cr_key + mid) < key) lo = mid + 1; else hi = mid;
+    }
+    if (lo < P.gbase[e] + P.ngroups[e] && __ldg(cr_key + lo) == key) {
+        const uint2 r = __ldg(cr_loc + lo);
+        return Loc{r.x, r.y};
+    }
+    return Loc{0u, 0u};
+}
+
+// Alg. 4: thread per row; lens[i] = the row's buffer bound (paper or per-row e0).
+__global__ void k_abl_probe(const int32_t *__restrict__ M, long long nM, StepParams P, int cr,
+                            const unsigned long long *__restrict__ cr_key, const uint2 *__restrict__ cr_loc,
+                            const uint2 *__restrict__ groups, int gpn, Loc *__restrict__ loc, uint32_t *__restrict__ lens) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nM; i += (long long)gridDim.x * blockDim.x) {
+        Loc first{0u, 0u}, best{0u, 0u};
+        int bi = 0;
+        bool anyzero = false;
+        for (int e = 0; e < P.E; e++) {
+            const Loc r = abl_lookup(P, e, (uint32_t)M[i * P.t + P.col[e]], cr != 0, cr_key, cr_loc, groups, gpn);
+            loc[i * P.E + e] = r;
+            if (e == 0) first = best = r;
+            else if (r.len < best.len) {
+                best = r;
+                bi = e;
+            }
+            anyzero |= r.len == 0;
+        }
+        if (P.per_row_e0 && bi != 0) {
+            loc[i * P.E] = best;
+            loc[i * P.E + bi] = first;
+        }
+        lens[i] = P.per_row_e0 ? (anyzero ? 0u : best.len) : first.len;
+    }
+}
+
+// Exclusive scan of u32 counts into u64 offsets (decoupled look-back); out[n] = total.
+__global__ void __launch_bounds__(kThreads) k_scan_counts(const uint32_t *__restrict__ in, long long n,
+                                                          unsigned long long *__restrict__ out,
+                                                          unsigned long long *status, unsigned *tile_ctr) {
+    __shared__ unsigned long long sm[33];
+    __shared__ unsigned tile_s;
+    __shared__ unsigned long long base_s;
+    if (threadIdx.x == 0) tile_s = atomicAdd(tile_ctr, 1u);
+    __syncthreads();
+    const unsigned tile = tile_s;
+    const long long i = (long long)tile * kThreads + threadIdx.x;
+    const unsigned long long x = i < n ? in[i] : 0ull;
+    unsigned long long agg;
+    const unsigned long long ex = block_exclusive_scan(x, sm, &agg);
+    if (threadIdx.x < 32) {
+        const unsigned long long pre = lookback_exclusive(status, tile, agg);
+        if (threadIdx.x == 0) base_s = pre;
+    }
+    __syncthreads();
+    if (i < n) out[i] = base_s + ex;
+    if (tile == gridDim.x - 1 && threadIdx.x == kThreads - 1) out[n] = base_s + agg;
+}
+
+// Alg. 3 with one warp per row: lanes stride over the row's buffer N(m_i[c0], l0).
+//   AB_PC    : survivors into the row's Prealloc buffer gba[F_i ..], cnt[i] = survivors
+//   AB_COUNT : two-step pass 1, cnt[i] only
+//   AB_WRITE : two-step pass 2, rows m_i || x written at G_i (write cache: staged per warp)
+//   AB_FINAL : last level, count (+ fingerprint)
+template <int MODE, bool WCACHE, bool NAIVE>
+__global__ void __launch_bounds__(kThreads) k_abl_join(const int32_t *__restrict__ M, long long nM,
+                                                       const Loc *__restrict__ loc,
+                                                       const unsigned long long *__restrict__ off, StepParams P,
+                                                       const int32_t *__restrict__ ci,
+                                                       const uint32_t *__restrict__ cu_bm,
+                                                       const int32_t *__restrict__ cu_list, long long cu_n,
+                                                       int32_t *__restrict__ gba, uint32_t *__restrict__ cnt,
+                                                       int32_t *__restrict__ out, Counters *ctr) {
+    __shared__ int32_t stage[kThreads / 32][32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const int t = P.t, W = t + 1;
+    unsigned long long c_all = 0, h1 = 0, h2 = 0;
+    for (long long i = gw; i < nM; i += nw) {
+        const Loc L0 = loc[i * P.E];
+        const int32_t *row = M + i * t;
+        uint32_t c = 0;
+        const unsigned long long base = (MODE == AB_PC || MODE == AB_WRITE) ? off[i] : 0ull;
+        for (uint32_t j0 = 0; j0 < L0.len; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            bool keep = j < L0.len;
+            int32_t x = keep ? __ldg(ci + L0.off + j) : 0;
+            if (keep) keep = NAIVE ? in_sorted(cu_list, (uint32_t)cu_n, x)
+                                   : ((__ldg(cu_bm + ((uint32_t)x >> 5)) >> (x & 31)) & 1u);
+            for (int q = 0; q < P.n_inj && keep; q++) keep = row[P.inj_col[q]] != x;      // line 10
+            for (int e = 1; e < P.E && keep; e++) {                                      // line 13
+                const Loc Le = loc[i * P.E + e];
+                if (NAIVE) {
+                    bool f = false;
+                    for (uint32_t q = 0; q < Le.len && !f; q++) f = __ldg(ci + Le.off + q) == x;
+                    keep = f;
+                } else {
+                    keep = in_sorted(ci + Le.off, Le.len, x);
+                }
+            }
+            const unsigned b = __ballot_sync(0xffffffffu, keep);
+            const uint32_t pos = c + __popc(b & lt);
+            if (MODE == AB_PC && keep) gba[base + pos] = x;
+            if (MODE == AB_FINAL && keep) {
+                c_all++;
+                if (P.fp) row_hash(row, (uint32_t)x, P, h1, h2);
+            }
+            if (MODE == AB_WRITE) {
+                if (WCACHE) {   // stage the chunk's survivors, then one coalesced block of rows
+                    if (keep) stage[wib][__popc(b & lt)] = x;
+                    __syncwarp();
+                    const int ns = __popc(b);
+                    int32_t *o = out + (base + c) * (unsigned long long)W;
+                    for (int e = lane; e < ns * W; e += 32) {
+                        const int r = e / W, col = e - r * W;
+                        o[e] = col < t ? row[col] : stage[wib][r];
+                    }
+                    __syncwarp();
+                } else if (keep) {   // each lane writes its own row (strided stores)
+                    int32_t *o = out + (base + pos) * (unsigned long long)W;
+                    for (int col = 0; col < t; col++) o[col] = row[col];
+                    o[t] = x;
+                }
+            }
+            c += __popc(b);
+        }
+        if ((MODE == AB_PC || MODE == AB_COUNT) && lane == 0) cnt[i] = c;
+    }
+    if (MODE == AB_FINAL) {
+        c_all = warp_sum_u64(c_all);
+        h1 = warp_sum_u64(h1);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) h2 ^= __shfl_xor_sync(0xffffffffu, h2, o);
+        if (lane == 0 && c_all) {
+            atomicAdd(&ctr->count, c_all);
+            atomicAdd(&ctr->fp1, h1);
+            atomicXor(&ctr->fp2, h2);
+        }
+    }
+}
+
+// Combine (Alg. 3 lines 15-21): M'[G_i + j] = m_i || gba[F_i + j].  Write cache: one thread per
+// output int (coalesced); off: one thread per output row.
+template <bool WCACHE>
+__global__ void k_abl_link(const int32_t *__restrict__ M, long long nM, const unsigned long long *__restrict__ F,
+                           const unsigned long long *__restrict__ G, const int32_t *__restrict__ gba, int t,
+                           unsigned long long nout, int32_t *__restrict__ out) {
+    const int W = t + 1;
+    const unsigned long long total = WCACHE ? nout * (unsigned long long)W : nout;
+    for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < total;
+         e += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long r = WCACHE ? e / W : e;
+        long long lo = 0, hi = nM;   // last row i with G[i] <= r
+        while (hi - lo > 1) {
+            const long long mid = (lo + hi) >> 1;
+            if (G[mid] <= r) lo = mid; else hi = mid;
+        }
+        const int32_t x = gba[F[lo] + (r - G[lo])];
+        if (WCACHE) {
+            const int col = (int)(e - r * W);
+            out[e] = col < t ? M[lo * t + col] : x;
+        } else {
+            for (int col = 0; col < t; col++) out[r * W + col] = M[lo * t + col];
+            out[r * W + t] = x;
+        }
+    }
+}
+
+// ------------------------------------------------------------ small-query path -----
+// A query whose levels all stay small (C2-C4-shaped: |C(pi_1)| of a few to a few thousand,
+// ~11 levels of tens to thousands of rows) is latency-bound on the regular path: one join
+// launch and one counter read-back per level.  k_small_query runs every level of one query
+// inside one CTA of 1024 threads — Prealloc probe + block scan (Alg. 4), the join over the
+// slot range in rounds of 1024 slots (Alg. 3 lines 2-13: C(u) bit, subtraction, the other
+// linking lists), and an ordered block-scan compaction into the next level's rows (the Combine,
+// Alg. 3 lines 14-21) — with the level sizes kept on the device, so the whole query costs one
+// launch after the filter/plan and one read-back.  Rows are produced in the same
+// lexicographic pi order as the regular path.  If a level exceeds the row or slot capacity the
+// kernel stops and reports the level; the host then runs the regular path (identical results).
+constexpr int kSmallThreads = 1024;
+constexpr int kSmallMaxE = 8;
+constexpr int kSmallMaxInj = 8;
+struct SmallStep {
+    int E, n_inj;
+    int col[kSmallMaxE];
+    uint32_t lab[kSmallMaxE];
+    uint32_t ngroups[kSmallMaxE];
+    unsigned long long gbase[kSmallMaxE];
+    int inj_col[kSmallMaxInj];
+    const uint32_t *cu;
+};
+struct SmallPlan {
+    int k, want_table, fp, gpn;
+    unsigned long long row_cap, slot_cap;
+    int pos_of_q[GSI_MAX_K];
+    SmallStep st[GSI_MAX_K - 1];   // st[j]: the step joining column j + 1 (j + 1 columns before it)
+};
+struct SmallOut {
+    unsigned long long count, fp1, fp2, nout;
+    int aborted;                              // 0: done; t: level t exceeded a capacity
+    unsigned long long rows[GSI_MAX_K];       // |M_t| at t - 1
+    unsigned long long gba[GSI_MAX_K];        // |GBA| of level t at t
+    unsigned long long elems[GSI_MAX_K];
+};
+
+__global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const SmallPlan plan, const int32_t *__restrict__ M1,
+                                                                  const unsigned long long *__restrict__ nM1p,
+                                                                  const uint2 *__restrict__ groups,
+                                                                  const int32_t *__restrict__ ci,
+                                                                  int32_t *__restrict__ bufA, int32_t *__restrict__ bufB,
+                                                                  Loc *__restrict__ loc,
+                                                                  unsigned long long *__restrict__ F,
+                                                                  int32_t *__restrict__ table, SmallOut *out) {
+    __shared__ unsigned long long sm[34];
+    __shared__ unsigned long long cnt_s, h1_s, h2_s, el_s;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int k = plan.k;
+    unsigned long long nM = *nM1p;
+    if (tid == 0) {
+        out->rows[0] = nM;
+        cnt_s = h1_s = h2_s = 0;
+    }
+    if (nM > plan.row_cap) {
+        if (tid == 0) out->aborted = 1;
+        return;
+    }
+    const int32_t *cur = M1;
+    int32_t *nxt = bufA;
+    for (int t = 1; t < k; t++) {
+        const SmallStep &S = plan.st[t - 1];
+        const int E = S.E;
+        const bool last = t == k - 1;
+        // ---- Prealloc (Alg. 4): locate every linking list, per-row shortest list bounds the
+        //      buffer (any linking edge bounds it, L967-981), F = exclusive scan
+        unsigned long long run = 0;
+        if (tid == 0) el_s = 0;
+        for (unsigned long long b0 = 0; b0 < nM; b0 += kSmallThreads) {
+            const unsigned long long i = b0 + tid;
+            unsigned long long len0 = 0, el = 0;
+            if (i < nM) {
+                Loc best{0u, 0xFFFFFFFFu}, first{0u, 0u};
+                int bi = 0;
+                bool anyzero = false;
+                for (int e = 0; e < E; e++) {
+                    const uint32_t v = (uint32_t)cur[i * t + S.col[e]];
+                    const Loc r = pcsr_lookup(groups, plan.gpn, S.gbase[e], S.ngroups[e], S.lab[e], v, nullptr);
+                    loc[i * E + e] = r;
+                    if (e == 0) first = r;
+                    if (r.len < best.len) {
+                        best = r;
+                        bi = e;
+                    }
+                    anyzero |= r.len == 0;
+                    el += r.len;
+                }
+                if (bi != 0) {
+                    loc[i * E] = best;
+                    loc[i * E + bi] = first;
+                }
+                len0 = anyzero ? 0ull : best.len;
+                if (anyzero) el = 0;
+            }
+            unsigned long long agg;
+            const unsigned long long ex = block_exclusive_scan(len0, sm, &agg);
+            if (i < nM) F[i] = run + ex;
+            run += agg;
+            el = warp_sum_u64(el);
+            if (lane == 0 && el) atomicAdd(&el_s, el);
+        }
+        const unsigned long long T = run;
+        __syncthreads();
+        if (tid == 0) {
+            F[nM] = T;
+            out->gba[t] = T;
+            out->elems[t] = el_s;
+        }
+        if (T > plan.slot_cap) {
+            if (tid == 0) out->aborted = t;
+            return;
+        }
+        __syncthreads();   // F visible to the whole block
+        // ---- join: slots in rounds of 1024, ordered compaction into the next level -------
+        unsigned long long nout = 0;
+        for (unsigned long long s0 = 0; s0 < T; s0 += kSmallThreads) {
+            const unsigned long long sl = s0 + tid;
+            bool keep = false;
+            int32_t x = 0;
+            unsigned long long row = 0;
+            if (sl < T) {
+                unsigned long long lo = 0, hi = nM;   // last row with F[row] <= sl
+                while (hi - lo > 1) {
+                    const unsigned long long mid = (lo + hi) >> 1;
+                    if (F[mid] <= sl) lo = mid; else hi = mid;
+                }
+                row = lo;
+                const Loc L0 = loc[row * E];
+                x = __ldg(ci + L0.off + (uint32_t)(sl - F[row]));
+                keep = (__ldg(S.cu + ((uint32_t)x >> 5)) >> (x & 31)) & 1u;              // x in C(u)
+                for (int c = 0; c < S.n_inj && keep; c++) keep = cur[row * t + S.inj_col[c]] != x;   // line 10
+                for (int e = 1; e < E && keep; e++) {                                       // line 13
+                    const Loc Le = loc[row * E + e];
+                    keep = in_sorted(ci + Le.off, Le.len, x);
+                }
+            }
+            if (last && !plan.want_table) {
+                unsigned long long c = keep ? 1ull : 0ull, a1 = 0, a2 = 0;
+                if (keep && plan.fp) {
+                    for (int q = 0; q < k; q++) {
+                        const int col = plan.pos_of_q[q];
+                        const uint32_t val = col < t ? (uint32_t)cur[row * t + col] : (uint32_t)x;
+                        a1 += fp_term(kFpSeed1, q, val);
+                        a2 += fp_term(kFpSeed2, q, val);
+                    }
+                    a1 = fp_mix(a1);
+                    a2 = fp_mix(a2);
+                }
+                c = warp_sum_u64(c);
+                a1 = warp_sum_u64(a1);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) a2 ^= __shfl_xor_sync(0xffffffffu, a2, o);
+                if (lane == 0 && c) {
+                    atomicAdd(&cnt_s, c);
+                    atomicAdd(&h1_s, a1);
+                    atomicXor(&h2_s, a2);
+                }
+                continue;
+            }
+            unsigned long long agg;
+            const unsigned long long ex = block_exclusive_scan(keep ? 1ull : 0ull, sm, &agg);
+            if (nout + agg > plan.row_cap) {
+                if (tid == 0) out->aborted = t + 1;
+                return;
+            }
+            if (keep) {
+                const unsigned long long p = nout + ex;
+                if (last) {   // the table in query-id order (+ fingerprint)
+                    unsigned long long a1 = 0, a2 = 0;
+                    for (int q = 0; q < k; q++) {
+                        const int col = plan.pos_of_q[q];
+                        const int32_t val = col < t ? cur[row * t + col] : x;
+                        table[p * k + q] = val;
+                        a1 += fp_term(kFpSeed1, q, (uint32_t)val);
+                        a2 += fp_term(kFpSeed2, q, (uint32_t)val);
+                    }
+                    if (plan.fp) {
+                        atomicAdd(&h1_s, fp_mix(a1));
+                        atomicXor(&h2_s, fp_mix(a2));
+                    }
+                } else {
+                    for (int c = 0; c < t; c++) nxt[p * (t + 1) + c] = cur[row * t + c];
+                    nxt[p * (t + 1) + t] = x;
+                }
+            }
+            nout += agg;
+        }
+        __syncthreads();   // every row of the next level written before it is read
+        if (last) {
+            if (tid == 0) {
+                const unsigned long long c = plan.want_table ? nout : cnt_s;
+                out->count = c;
+                out->nout = nout;
+                out->rows[t] = c;
+                out->fp1 = h1_s;
+                out->fp2 = h2_s;
+                out->aborted = 0;
+            }
+            return;
+        }
+        if (tid == 0) out->rows[t] = nout;
+        nM = nout;
+        cur = nxt;
+        nxt = (nxt == bufA) ? bufB : bufA;
+        if (nM == 0) break;
+    }
+    if (tid == 0) {   // a level came out empty: no matches (later rows stay 0)
+        out->count = 0;
+        out->nout = 0;
+        out->aborted = 0;
+    }
+}
+
 // Count + fingerprint of a table whose columns are in pi order (k = 1 queries).
 __global__ void k_fp_rows(const int32_t *__restrict__ T, long long nrows, StepParams P, Counters *ctr) {
     unsigned long long h1 = 0, h2 = 0;
@@ -3008,6 +3414,248 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
 
 }  // namespace
 
+// ------------------------------------------------------------------ small path ---------
+// Eligible: one shard, per-row e0, every step with <= 8 linking edges and subtraction columns,
+// and a small first level (the kernel aborts to the regular path if a later level grows).
+constexpr unsigned long long kSmallRowCap = 1ull << 15;
+constexpr unsigned long long kSmallSlotCap = 1ull << 16;
+constexpr unsigned long long kSmallMaxRoots = 4096;
+
+bool small_eligible(const QueryCtx &C, unsigned long long nM1, bool known) {
+    if (C.opts.small_mode == 1 || env_flag("GSI_SMALL_OFF") || C.W != 1 || C.opts.e0_mode != 0) return false;
+    if (!known || nM1 == 0 || nM1 > kSmallMaxRoots) return false;
+    if (C.opts.chunk_slots || C.opts.force_paths) return false;
+    for (auto &s : C.steps) {
+        if ((int)s.col.size() > kSmallMaxE) return false;
+        int ninj = 0;
+        if (!C.opts.homomorphism)
+            for (int c = 0; c < s.t; c++) {
+                if (C.q->qvl[C.order[c]] != C.q->qvl[s.u]) continue;
+                bool linked = false;
+                for (int lc : s.col) linked |= lc == c;
+                ninj += linked ? 0 : 1;
+            }
+        if (ninj > kSmallMaxInj) return false;
+    }
+    return true;
+}
+
+// Run every level in k_small_query; done = false if it stopped at a capacity (the caller then
+// takes the regular path from M_1, which is left untouched).
+gsi_status run_small(QueryCtx &C, const int32_t *M1, bool &done) {
+    done = false;
+    const gsi_graph *g = C.g;
+    gsi_stats &S = *C.S;
+    Arena &A = *C.A;
+    const int k = C.q->k;
+    SmallPlan plan;
+    std::memset(&plan, 0, sizeof(plan));
+    plan.k = k;
+    plan.want_table = C.opts.want_table ? 1 : 0;
+    plan.fp = C.opts.fingerprint ? 1 : 0;
+    plan.gpn = g->gpn;
+    plan.row_cap = kSmallRowCap;
+    plan.slot_cap = kSmallSlotCap;
+    for (int q = 0; q < k; q++) plan.pos_of_q[q] = C.pos_of_q[q];
+    int maxE = 1;
+    for (size_t j = 0; j < C.steps.size(); j++) {
+        const Step &s = C.steps[j];
+        SmallStep &T = plan.st[j];
+        T.E = (int)s.col.size();
+        maxE = std::max(maxE, T.E);
+        for (int e = 0; e < T.E; e++) {
+            T.col[e] = s.col[e];
+            T.lab[e] = (uint32_t)s.lab[e];
+            T.gbase[e] = (unsigned long long)g->gbase[s.lab[e]];
+            T.ngroups[e] = g->ngroups[s.lab[e]];
+        }
+        T.n_inj = 0;
+        if (!C.opts.homomorphism)
+            for (int c = 0; c < s.t; c++) {
+                if (C.q->qvl[C.order[c]] != C.q->qvl[s.u]) continue;   // C(u) excludes other labels
+                bool linked = false;
+                for (int lc : s.col) linked |= lc == c;                // x in N(m[c],l) => x != m[c]
+                if (!linked) T.inj_col[T.n_inj++] = c;
+            }
+        T.cu = C.bm + (long long)s.u * C.words;
+    }
+    int32_t *bufA = nullptr, *bufB = nullptr, *table = nullptr;
+    Loc *loc = nullptr;
+    unsigned long long *F = nullptr;
+    SmallOut *dout = nullptr;
+    const size_t mk = A.mark();
+    GSI_TRY(A.get(&bufA, kSmallRowCap * (unsigned long long)k));
+    GSI_TRY(A.get(&bufB, kSmallRowCap * (unsigned long long)k));
+    GSI_TRY(A.get(&loc, kSmallRowCap * (unsigned long long)maxE));
+    GSI_TRY(A.get(&F, kSmallRowCap + 1));
+    if (plan.want_table) GSI_TRY(A.get(&table, kSmallRowCap * (unsigned long long)k));
+    GSI_TRY(A.get(&dout, 1));
+    GSI_CUDA(cudaMemsetAsync(dout, 0, sizeof(SmallOut), C.st));
+    C.prof->begin(GSI_K_JOIN, GSI_V_SMALL);
+    S.variant_launches[GSI_V_SMALL]++;
+    k_small_query<<<1, kSmallThreads, 0, C.st>>>(plan, M1, &C.ctr->total, g->groups, g->ci, bufA, bufB, loc, F, table,
+                                                  dout);
+    C.prof->end();
+    SmallOut h;
+    GSI_CUDA(d2h(S, &h, dout, sizeof(h), C.st));
+    GSI_CUDA(sync_timed(S, C.st));
+    GSI_CUDA(cudaGetLastError());
+    if (h.aborted) {
+        S.small_aborted = h.aborted;
+        A.reset(mk);
+        return GSI_OK;
+    }
+    S.levels = 1;
+    for (int t = 0; t < k; t++) {
+        S.rows[t] = h.rows[t];
+        S.gba[t] = h.gba[t];
+        S.list_elems[t] = h.elems[t];
+        if (t > 0 && h.rows[t - 1]) S.levels = t + 1;   // level t + 1 was produced
+    }
+    C.count = h.count;
+    C.fp1 = h.fp1;
+    C.fp2 = h.fp2;
+    if (plan.want_table && h.nout) {
+        int32_t *piece = nullptr;
+        GSI_CUDA(cudaMallocAsync(&piece, 4ull * h.nout * k, C.st));
+        GSI_CUDA(cudaMemcpyAsync(piece, table, 4ull * h.nout * k, cudaMemcpyDeviceToDevice, C.st));
+        C.pieces.push_back({piece, h.nout});
+    }
+    A.reset(mk);
+    done = true;
+    return GSI_OK;
+}
+
+// ------------------------------------------------------------------ ablation engine ----
+// Every level with the paper-style kernels (one warp per row); see k_abl_join.
+gsi_status run_ablation(QueryCtx &C, int32_t *M, unsigned long long nM) {
+    const gsi_graph *g = C.g;
+    gsi_stats &S = *C.S;
+    Arena &A = *C.A;
+    cudaStream_t st = C.st;
+    const int ab = C.opts.ablation;
+    const bool cr = ab & GSI_ABL_CR, two = ab & GSI_ABL_TWO_STEP, wc = !(ab & GSI_ABL_NO_WCACHE),
+               naive = ab & GSI_ABL_NAIVE_SO;
+    if (cr) GSI_TRY(ensure_cr(g, st));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
+    auto warp_grid = [&](unsigned long long rows) {
+        return (unsigned)std::max<unsigned long long>(1, std::min<unsigned long long>((rows * 32 + kThreads - 1) / kThreads,
+                                                                                   (unsigned long long)sms * 16));
+    };
+    auto scan = [&](const uint32_t *in, unsigned long long n, unsigned long long **outp) -> gsi_status {
+        const unsigned tiles = grid_for(n, kThreads);
+        unsigned long long *status = nullptr;
+        GSI_TRY(A.get(outp, n + 1));
+        GSI_TRY(A.get(&status, (unsigned long long)tiles + 1));
+        GSI_CUDA(cudaMemsetAsync(status, 0, 8ull * (tiles + 1), st));
+        GSI_CUDA(cudaMemsetAsync(*outp, 0, 8, st));
+        C.prof->begin(GSI_K_OTHER);
+        if (n) k_scan_counts<<<tiles, kThreads, 0, st>>>(in, (long long)n, *outp, status + 1, (unsigned *)status);
+        C.prof->end();
+        return GSI_OK;
+    };
+    Counters *ctr = nullptr;
+    GSI_TRY(A.get(&ctr, 1));
+    for (size_t si = 0; si < C.steps.size(); si++) {
+        const Step &s = C.steps[si];
+        const int t = s.t;
+        const bool last = si + 1 == C.steps.size();
+        StepParams P;
+        fill_params(C, s, P, t);
+        if (S.levels < t) S.levels = t;
+        const uint32_t *cu = C.bm + (long long)s.u * C.words;
+        int32_t *cul = nullptr;
+        long long cun = 0;
+        if (naive) {   // the sorted candidate list C(u) (bitmap compaction)
+            cun = S.cand[s.u];
+            const unsigned tiles = grid_for(C.words, kThreads);
+            unsigned long long *status = nullptr;
+            GSI_TRY(A.get(&cul, cun));
+            GSI_TRY(A.get(&status, (unsigned long long)tiles + 1));
+            GSI_CUDA(cudaMemsetAsync(status, 0, 8ull * (tiles + 1), st));
+            C.prof->begin(GSI_K_COMPACT);
+            k_compact_bitmap<<<tiles, kThreads, 0, st>>>(cu, C.words, cul, status + 1, (unsigned *)status, ctr);
+            C.prof->end();
+        }
+        Loc *loc = nullptr;
+        uint32_t *lens = nullptr, *cnt = nullptr;
+        unsigned long long *F = nullptr, *G = nullptr;
+        GSI_TRY(A.get(&loc, std::max<unsigned long long>(nM, 1) * (unsigned long long)P.E));
+        GSI_TRY(A.get(&lens, nM));
+        C.prof->begin(GSI_K_PROBE);
+        k_abl_probe<<<grid_for(nM, kThreads), kThreads, 0, st>>>(M, (long long)nM, P, cr ? 1 : 0, g->cr_key, g->cr_loc,
+                                                                  g->groups, g->gpn, loc, lens);
+        C.prof->end();
+        GSI_TRY(scan(lens, nM, &F));
+        unsigned long long gba = 0;
+        GSI_CUDA(d2h(S, &gba, F + nM, 8, st));
+        GSI_CUDA(sync_timed(S, st));
+        S.gba[t] += gba;
+        if (gba == 0) break;
+        const unsigned wg = warp_grid(nM);
+#define GSI_ABL_JOIN(MODE, WC, NV, OFF, GBA, CNT, OUT)                                                            \
+    k_abl_join<MODE, WC, NV><<<wg, kThreads, 0, st>>>(M, (long long)nM, loc, OFF, P, g->ci, cu, cul, cun, GBA, CNT, \
+                                                       OUT, ctr)
+        if (last) {
+            GSI_CUDA(cudaMemsetAsync(ctr, 0, sizeof(Counters), st));
+            C.prof->begin(GSI_K_JOIN, GSI_V_ABLATION);
+            S.variant_launches[GSI_V_ABLATION]++;
+            if (naive) GSI_ABL_JOIN(AB_FINAL, true, true, nullptr, nullptr, nullptr, nullptr);
+            else GSI_ABL_JOIN(AB_FINAL, true, false, nullptr, nullptr, nullptr, nullptr);
+            C.prof->end();
+            Counters hc;
+            GSI_CUDA(d2h(S, &hc, ctr, sizeof(hc), st));
+            GSI_CUDA(sync_timed(S, st));
+            C.count = hc.count;
+            C.fp1 = hc.fp1;
+            C.fp2 = hc.fp2;
+            S.rows[t] = hc.count;
+            S.levels = t + 1;
+            break;
+        }
+        GSI_TRY(A.get(&cnt, nM));
+        int32_t *gbuf = nullptr, *out = nullptr;
+        if (!two) GSI_TRY(A.get(&gbuf, gba));
+        C.prof->begin(GSI_K_JOIN, two ? GSI_V_TWO_STEP : GSI_V_ABLATION);
+        S.variant_launches[two ? GSI_V_TWO_STEP : GSI_V_ABLATION]++;
+        if (two) {   // pass 1: count only
+            if (naive) GSI_ABL_JOIN(AB_COUNT, true, true, nullptr, nullptr, cnt, nullptr);
+            else GSI_ABL_JOIN(AB_COUNT, true, false, nullptr, nullptr, cnt, nullptr);
+        } else {     // Prealloc: survivors into the row's buffer
+            if (naive) GSI_ABL_JOIN(AB_PC, true, true, F, gbuf, cnt, nullptr);
+            else GSI_ABL_JOIN(AB_PC, true, false, F, gbuf, cnt, nullptr);
+        }
+        C.prof->end();
+        GSI_TRY(scan(cnt, nM, &G));
+        unsigned long long nout = 0;
+        GSI_CUDA(d2h(S, &nout, G + nM, 8, st));
+        GSI_CUDA(sync_timed(S, st));
+        S.rows[t] += nout;
+        if (nout == 0) break;
+        GSI_TRY(A.get(&out, nout * (unsigned long long)(t + 1)));
+        C.prof->begin(GSI_K_JOIN, GSI_V_ABLATION);
+        S.variant_launches[GSI_V_ABLATION]++;
+        if (two) {   // pass 2: join again, write the rows
+            if (naive && wc) GSI_ABL_JOIN(AB_WRITE, true, true, G, nullptr, nullptr, out);
+            else if (naive) GSI_ABL_JOIN(AB_WRITE, false, true, G, nullptr, nullptr, out);
+            else if (wc) GSI_ABL_JOIN(AB_WRITE, true, false, G, nullptr, nullptr, out);
+            else GSI_ABL_JOIN(AB_WRITE, false, false, G, nullptr, nullptr, out);
+        } else {     // Combine: link the buffers into M'
+            const unsigned long long items = wc ? nout * (unsigned long long)(t + 1) : nout;
+            const unsigned lg = (unsigned)std::min<unsigned long long>(grid_for(items, kThreads), (unsigned long long)sms * 32);
+            if (wc) k_abl_link<true><<<lg, kThreads, 0, st>>>(M, (long long)nM, F, G, gbuf, t, nout, out);
+            else k_abl_link<false><<<lg, kThreads, 0, st>>>(M, (long long)nM, F, G, gbuf, t, nout, out);
+        }
+#undef GSI_ABL_JOIN
+        C.prof->end();
+        M = out;
+        nM = nout;
+    }
+    GSI_CUDA(cudaGetLastError());
+    return GSI_OK;
+}
+
 gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_opts *opts_in, gsi_result **out) {
     *out = nullptr;
     if (!g || !q || q->g != g) {
@@ -3025,6 +3673,10 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     const int k = q->k;
     const long long n = g->n;
     const long long words = (n + 31) / 32;
+    if (opts.ablation && (opts.want_table || opts.shard_count > 1)) {
+        set_error("ablation runs are count / fingerprint only and unsharded");
+        return GSI_ERR_INVALID_ARG;
+    }
     C.W = opts.shard_count > 1 ? opts.shard_count : 1;
     C.rank = C.W > 1 ? opts.shard_rank : 0;
     if (C.rank < 0 || C.rank >= C.W) {
@@ -3110,7 +3762,7 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     }
     C.pos_of_q.assign(k, 0);
     for (int j = 0; j < k; j++) C.pos_of_q[C.order[j]] = j;
-    plan_layout(C, !opts.want_table && !opts.fingerprint);
+    plan_layout(C, !opts.want_table && !opts.fingerprint && !opts.ablation);
     const double t_plan = now_ms();
     S.ms_plan = (float)(t_plan - t_filter);
 
@@ -3137,6 +3789,7 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     // ---------------- level 1 (a5) ----------------
     int32_t *M = nullptr;
     unsigned long long nM = 0;
+    const bool nM_known = true;   // |M_1|: |C(pi_1)| from the filter, or read back (roots hook)
     if (!empty) {
         unsigned long long *status = nullptr;
         const int u1 = C.order[0];
@@ -3177,7 +3830,15 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     }
 
     gsi_status rc = GSI_OK;
-    if (!empty && k == 1) {
+    bool small_done = false;
+    if (!empty && k > 1 && !opts.ablation && small_eligible(C, nM_known ? nM : 0, nM_known)) {
+        GSI_TRY(run_small(C, M, small_done));
+    }
+    if (small_done) {
+        // every level ran in k_small_query
+    } else if (!empty && k > 1 && opts.ablation) {
+        rc = run_ablation(C, M, nM);
+    } else if (!empty && k == 1) {
         S.rows[0] = nM;
         S.levels = 1;
         StepParams P;

@@ -25,6 +25,7 @@ GSI_MAX_K = 32
 GSI_N_KCLASS = 8
 KCLASS = ["filter", "compact", "probe", "join", "link", "other", "r6", "r7"]
 GSI_N_KVARIANT = 16
+ABL_ENGINE, ABL_CR, ABL_TWO_STEP, ABL_NO_WCACHE, ABL_NAIVE_SO = 1, 2, 4, 8, 16
 KVARIANT = ["join_next", "join_count", "join_table", "join_cahead", "count_fast", "next_lean", "cahead_warp",
             "cahead_lean", "final_lean", "final_fp", "filter_partition", "refilter", "probe_ahead", "small",
             "two_step", "reserved"]
@@ -47,7 +48,8 @@ class gsi_query_opts(ctypes.Structure):
                 ("shard_rank", I32), ("shard_count", I32), ("shard_min_rows", U64),
                 ("mem_budget_bytes", U64), ("timeout_s", ctypes.c_double), ("profile", I32), ("stream", P),
                 ("chunk_slots", U64), ("partial_on_timeout", I32), ("fingerprint", I32), ("no_shared_lists", I32),
-                ("no_count_ahead", I32), ("shard_pieces", I32), ("force_paths", I32)]
+                ("no_count_ahead", I32), ("shard_pieces", I32), ("force_paths", I32),
+                ("small_mode", I32), ("ablation", I32)]
 
 
 class gsi_graph_info(ctypes.Structure):
@@ -72,7 +74,7 @@ class gsi_stats(ctypes.Structure):
                 ("d2h_bytes", U64), ("n_shared_lists", U32), ("ms_host_alloc", ctypes.c_float),
                 ("ms_host_sync", ctypes.c_float), ("count_ahead", I32), ("n_probe_ahead", U32),
                 ("variant_launches", U32 * GSI_N_KVARIANT), ("ms_variant", ctypes.c_float * GSI_N_KVARIANT),
-                ("alg_bytes_variant", ctypes.c_double * GSI_N_KVARIANT)]
+                ("alg_bytes_variant", ctypes.c_double * GSI_N_KVARIANT), ("small_aborted", I32)]
 
 
 _SIGS = {
@@ -271,7 +273,7 @@ def _opts(want_table=False, homomorphism=False, filter_mode=0, e0_mode=0, force_
           force_first_edge=None, roots=None, shard_rank=0, shard_count=1, shard_min_rows=0,
           mem_budget_bytes=0, timeout_s=0.0, profile=False, stream=None, chunk_slots=0,
           partial_on_timeout=False, fingerprint=True, shared_lists=True, count_ahead=True, shard_pieces=1,
-          force_paths=0):
+          force_paths=0, small=True, ablation=0):
     o = gsi_query_opts()
     lib.gsi_query_opts_default(ctypes.byref(o))
     keep = []
@@ -291,6 +293,8 @@ def _opts(want_table=False, homomorphism=False, filter_mode=0, e0_mode=0, force_
     o.no_count_ahead = 0 if count_ahead else 1
     o.shard_pieces = shard_pieces
     o.force_paths = force_paths
+    o.small_mode = 0 if small else 1
+    o.ablation = ablation
     return o, keep
 
 

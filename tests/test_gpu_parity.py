@@ -162,10 +162,12 @@ def test_filter_bitmaps_bit_exact(mode):
 
 
 # ------------------------------------------------------------------ closed forms -----
+@pytest.mark.parametrize("small", [True, False])
 @pytest.mark.parametrize("n,k", [(6, 2), (7, 4), (8, 5), (9, 3)])
-def test_clique_counts_and_levels(n, k):
+def test_clique_counts_and_levels(n, k, small):
     graph = gsi.build(W.complete_graph(n))
-    r = gsi.query(graph, W.clique_query(k), want_table=True)
+    r = gsi.query(graph, W.clique_query(k), want_table=True, small=small)
+    assert r.stats()["variants"].get("small", 0) == (1 if small else 0)
     assert r.count == math.perm(n, k)
     s = r.stats()
     assert s["rows"][:k] == [math.perm(n, t) for t in range(1, k + 1)]
@@ -192,21 +194,24 @@ def test_square_in_grid_and_star():
 
 
 # ------------------------------------------------------------------ random parity ----
-def test_tiny_random_vs_oracle():
-    """Seeded tiny instances (n <= 9, k <= 5, parallel edges with distinct labels included)."""
+@pytest.mark.parametrize("small", [True, False])
+def test_tiny_random_vs_oracle(small):
+    """Seeded tiny instances (n <= 9, k <= 5, parallel edges with distinct labels included),
+    through the one-launch small-query path and the regular per-level path."""
     for s in range(300):
         g = W.random_tiny_graph(s, nlv=1 + s % 3, nle=1 + s % 2)
         if g.m == 0:
             continue
         q = W.random_connected_query(20_000 + s, 1 + s % 5, nlv=1 + s % 3, nle=1 + s % 2)
-        r, tab, cnt, fp, otab = run_both(g, q)
+        r, tab, cnt, fp, otab = run_both(g, q, small=small)
         assert r.count == cnt, s
         assert np.array_equal(canon(tab), otab), s
         assert r.fingerprint() == fp, s
 
 
+@pytest.mark.parametrize("small", [True, False])
 @pytest.mark.parametrize("seed", [1, 2, 3])
-def test_medium_random_walk_queries(seed):
+def test_medium_random_walk_queries(seed, small):
     """Power-law graphs with several tiles of rows and ragged tails; exact sorted tables."""
     g = W.chung_lu(20_000, 120_000, 2_000, nlv=16, nle=8, seed=seed)
     graph = gsi.build(g)
@@ -214,12 +219,12 @@ def test_medium_random_walk_queries(seed):
     qs = bounded_queries(g, og, lambda s: 4 + s % 6, range(5000 + 100 * seed, 5000 + 100 * seed + 40), want=10)
     assert len(qs) >= 5
     for q in qs:
-        r, tab, cnt, fp, otab = run_both(g, q, graph, og)
+        r, tab, cnt, fp, otab = run_both(g, q, graph, og, small=small)
         assert r.count == cnt and r.fingerprint() == fp
         assert np.array_equal(canon(tab), otab)
         assert strictly_increasing_in_order(tab, r.stats()["order"][:q.n])
         assert tuple(q.embedding.tolist()) in {tuple(x) for x in tab.tolist()}
-        assert gsi.query(graph, q, fingerprint=False).count == cnt
+        assert gsi.query(graph, q, fingerprint=False, small=small).count == cnt
 
 
 def test_large_counts_fingerprint():
@@ -228,18 +233,20 @@ def test_large_counts_fingerprint():
     g = W.chung_lu(4000, 30000, 500, nlv=3, nle=4, seed=31)
     graph = gsi.build(g)
     og = oracle.OracleGraph(g)
-    shared = 0
+    shared, fpk = 0, 0
     for s in (700, 703, 705):
         q = W.random_walk_query(g, 6, s)
         cnt, fp, _ = oracle.match(og, q, table=False)
         for sl in (True, False):   # with and without shared N(v,l0) ∩ C(u) lists
-            r = gsi.query(graph, q, shared_lists=sl)
+            r = gsi.query(graph, q, shared_lists=sl, small=False)
             assert r.count == cnt and r.fingerprint() == fp, (s, sl)
             shared += r.stats()["n_shared_lists"] if sl else 0
-            r = gsi.query(graph, q, shared_lists=sl, fingerprint=False)   # lean count-only kernel
+            if sl:
+                fpk += r.stats()["variants"].get("final_fp", 0)
+            r = gsi.query(graph, q, shared_lists=sl, fingerprint=False, small=False)   # count-only kernels
             assert r.count == cnt, (s, sl)
         assert cnt > 10_000_000 or s == 703
-    assert shared > 0
+    assert shared > 0 and fpk > 0   # the fingerprinted lean last level (k_final_fp) ran
 
 
 def test_enron_shaped_config():
@@ -432,19 +439,21 @@ def test_count_ahead_matches_oracle(kernel, monkeypatch):
                 cnt = oracle.match(og, q, table=False, timeout=20.0)[0]
             except oracle.OracleError:
                 continue
-            r = gsi.query(graph, q, fingerprint=False)
+            r = gsi.query(graph, q, fingerprint=False, small=False)
             assert r.count == cnt, (gs, s)
             seen += r.stats()["count_ahead"]
-            assert gsi.query(graph, q, fingerprint=False, count_ahead=False).count == cnt
+            assert gsi.query(graph, q, fingerprint=False, count_ahead=False, small=False).count == cnt
+            assert gsi.query(graph, q, fingerprint=False, force_paths=1).count == cnt
             for W_ in (2, 3):   # sharded at the count-ahead level at the latest
-                assert sum(gsi.query(graph, q, fingerprint=False, shard_rank=r_, shard_count=W_).count
-                           for r_ in range(W_)) == cnt
+                for pcs in (1, 3):
+                    assert sum(gsi.query(graph, q, fingerprint=False, shard_rank=r_, shard_count=W_,
+                                         shard_pieces=pcs).count for r_ in range(W_)) == cnt
             assert gsi.query(graph, q, fingerprint=False, chunk_slots=4096).count == cnt
             try:
                 hc = oracle.match(og, q, table=False, hom=True, timeout=20.0)[0]
             except oracle.OracleError:
                 continue
-            assert gsi.query(graph, q, fingerprint=False, homomorphism=True).count == hc
+            assert gsi.query(graph, q, fingerprint=False, homomorphism=True, small=False).count == hc
     assert seen >= 4
 
 
@@ -523,3 +532,61 @@ def test_workspace_trim_and_reuse():
         gsi.gsi_trim_workspace()
         gsi.gsi_trim_workspace(0)
     assert gsi.query(graph, qs[0], fingerprint=False, mem_budget_bytes=64 << 20).count == ref[0]
+
+
+def test_small_path_equals_regular_and_aborts_cleanly():
+    """The one-launch small-query path (k_small_query) gives the regular path's exact results
+    (count, fingerprint, table in the same pi order, per-level |M_t|) on C2-shaped queries; a
+    query whose levels outgrow its capacity stops the kernel and falls back to the regular path
+    with identical results."""
+    g = W.make_config("C2")
+    graph = gsi.build(g)
+    og = oracle.OracleGraph(g)
+    ran = 0
+    for j in range(16):
+        q = W.random_walk_query(g, 12, 1000 + j)
+        a = gsi.query(graph, q, want_table=True)
+        b = gsi.query(graph, q, want_table=True, small=False)
+        cnt, fp, otab = oracle.match(og, q)
+        assert a.count == b.count == cnt and a.fingerprint() == b.fingerprint() == fp
+        assert np.array_equal(a.table(), b.table()) and np.array_equal(canon(a.table()), otab)
+        sa, sb = a.stats(), b.stats()
+        ran += sa["variants"].get("small", 0) and not sa["small_aborted"]
+        if sa["variants"].get("small", 0) and not sa["small_aborted"]:
+            assert sa["rows"][:q.n] == sb["rows"][:q.n]
+        c = gsi.query(graph, q, fingerprint=False)
+        assert c.count == cnt
+    assert ran >= 12
+    # abort: a dense graph whose levels exceed the kernel's row capacity (2^15)
+    g2 = W.chung_lu(3000, 40000, 400, nlv=1, nle=1, seed=5)
+    graph2 = gsi.build(g2)
+    og2 = oracle.OracleGraph(g2)
+    q = W.path_query(4)
+    r = gsi.query(graph2, q, fingerprint=True)
+    assert r.stats()["small_aborted"] > 0
+    cnt, fp, _ = oracle.match(og2, q, table=False)
+    assert r.count == cnt and r.fingerprint() == fp
+
+
+@pytest.mark.parametrize("ab", [1, 1 | 2, 1 | 4, 1 | 8, 1 | 16, 31])
+def test_ablation_engine_same_result(ab):
+    """NEXT-3: the paper-style engine (warp per row, Alg. 3/4) with each join technique of
+    Tables VI-VIII switched off — CR lookup instead of PCSR, two-step output instead of
+    Prealloc-Combine, no write cache, naive set operation — gives the oracle's count and
+    fingerprint (same R)."""
+    g = W.chung_lu(20_000, 120_000, 2_000, nlv=8, nle=6, seed=97)
+    graph = gsi.build(g)
+    og = oracle.OracleGraph(g)
+    qs = bounded_queries(g, og, lambda s: 4 + s % 5, range(9700, 9760), lo=10, hi=3_000_000, want=6)
+    assert len(qs) >= 4
+    for q in qs:
+        cnt, fp, _ = oracle.match(og, q, table=False)
+        r = gsi.query(graph, q, ablation=ab)
+        assert r.count == cnt and r.fingerprint() == fp, (ab, r.count, cnt)
+        v = r.stats()["variants"]
+        assert v.get("ablation", 0) > 0 and v.get("small", 0) == 0
+        if ab & 4 and q.n > 2:
+            assert v.get("two_step", 0) > 0
+        assert gsi.query(graph, q, ablation=ab, fingerprint=False).count == cnt
+    with pytest.raises(gsi.GsiError):
+        gsi.query(graph, qs[0], ablation=ab, want_table=True)
