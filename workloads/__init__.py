@@ -27,7 +27,8 @@ __all__ = [
     "path_query", "clique_query", "cycle_query", "star_query", "edge_query",
     "random_tiny_graph", "random_connected_query", "labels_8020", "labels_zipf",
     "chung_lu", "rmat", "road_grid", "random_walk_query", "random_walk_queries", "CONFIGS",
-    "make_config",
+    "make_config", "MLGraph", "MLQuery", "ml_random_graph", "ml_walk_query", "ml_tiny_graph",
+    "ml_random_query",
 ]
 
 
@@ -464,3 +465,116 @@ def make_config(name: str, seed: int = 1, device="cpu", **override) -> Graph:
         return fig1()[0]
     fn = {"chung_lu": chung_lu, "rmat": rmat, "road_grid": road_grid}[kind]
     return fn(seed=seed, device=device, name=name, **kw)
+
+
+# ----------------------------------------------------------------------------------------
+# Multi-label graphs (§VII-B): vertex label SETS and edge label SETS
+# ----------------------------------------------------------------------------------------
+_PURPOSE.update({"mlv": 11, "mle": 12, "mlq": 13})
+
+
+@dataclasses.dataclass
+class MLGraph:
+    """Undirected graph whose vertices and edges carry label SETS: L_V(v) =
+    vls[vls_off[v]:vls_off[v+1]], L_E(e) = els[els_off[e]:els_off[e+1]] (each edge listed once,
+    no two edges on the same vertex pair, no self-loops; labels >= 0, no repeats in a set)."""
+    n: int
+    vls_off: np.ndarray
+    vls: np.ndarray
+    src: np.ndarray
+    dst: np.ndarray
+    els_off: np.ndarray
+    els: np.ndarray
+    name: str = ""
+    embedding: Optional[np.ndarray] = None   # queries: the data vertex of each query vertex
+
+    @property
+    def m(self) -> int:
+        return int(self.src.shape[0])
+
+    def __post_init__(self):
+        self.vls_off = np.ascontiguousarray(self.vls_off, dtype=np.int64)
+        self.vls = np.ascontiguousarray(self.vls, dtype=np.int32)
+        self.src = np.ascontiguousarray(self.src, dtype=np.int32)
+        self.dst = np.ascontiguousarray(self.dst, dtype=np.int32)
+        self.els_off = np.ascontiguousarray(self.els_off, dtype=np.int64)
+        self.els = np.ascontiguousarray(self.els, dtype=np.int32)
+
+    def vset(self, v: int) -> List[int]:
+        return self.vls[self.vls_off[v]:self.vls_off[v + 1]].tolist()
+
+    def eset(self, e: int) -> List[int]:
+        return self.els[self.els_off[e]:self.els_off[e + 1]].tolist()
+
+
+MLQuery = MLGraph
+
+
+def _label_sets(count: int, nlabels: int, max_per: int, seed: int, purpose: str) -> Tuple[np.ndarray, np.ndarray]:
+    """1..max_per distinct labels per item, each drawn by the 80/20 rule (reading A15)."""
+    g = np.random.default_rng([seed, _PURPOSE[purpose]])
+    sizes = g.integers(1, max_per + 1, count)
+    draws = labels_8020(int(sizes.sum()), nlabels, seed, purpose=purpose).numpy()
+    off = np.zeros(count + 1, np.int64)
+    out = []
+    pos = 0
+    for i in range(count):
+        st = sorted(set(draws[pos:pos + sizes[i]].tolist()))
+        pos += sizes[i]
+        out.extend(st)
+        off[i + 1] = len(out)
+    return off, np.array(out, np.int32)
+
+
+def ml_random_graph(n: int, m: int, dmax: float, nlv: int, nle: int, max_vl: int = 3, max_el: int = 2,
+                    seed: int = 1, name: str = "ml") -> MLGraph:
+    """Chung-Lu topology (as chung_lu) with 1..max_vl vertex labels and 1..max_el edge labels."""
+    base = chung_lu(n, m, dmax, 1, 1, seed=seed, name=name)
+    voff, vls = _label_sets(n, nlv, max_vl, seed, "mlv")
+    eoff, els = _label_sets(base.m, nle, max_el, seed, "mle")
+    return MLGraph(n, voff, vls, base.src, base.dst, eoff, els, name=name)
+
+
+def ml_tiny_graph(seed: int, nlv: int = 3, nle: int = 2) -> MLGraph:
+    """Tiny multi-label graph for brute force (n <= 8)."""
+    t = random_tiny_graph(seed, nlv=1, nle=1, p=0.5)
+    keys = sorted({(min(a, b), max(a, b)) for a, b in zip(t.src.tolist(), t.dst.tolist())})
+    src = np.array([a for a, _ in keys], np.int32)
+    dst = np.array([b for _, b in keys], np.int32)
+    voff, vls = _label_sets(t.n, nlv, 2, seed, "mlv")
+    eoff, els = _label_sets(len(keys), nle, 2, seed, "mle")
+    return MLGraph(t.n, voff, vls, src, dst, eoff, els, name=f"mltiny{seed}")
+
+
+def ml_walk_query(g: MLGraph, k: int, seed: int) -> MLGraph:
+    """Random-walk query (A14) on a multi-label graph: the walked vertices and edges, each
+    query label set a random non-empty subset of its data vertex's / edge's set, so the walk's
+    own embedding is a match."""
+    plain = Graph(g.n, np.zeros(g.n, np.int32), g.src, g.dst, np.arange(g.m, dtype=np.int32) % (1 << 30))
+    q = random_walk_query(plain, k, seed)   # elabels = data edge ids (placeholder labels)
+    rng = np.random.default_rng([seed, _PURPOSE["mlq"]])
+    emb = q.embedding.astype(np.int64)
+    qv_off = np.zeros(k + 1, np.int64)
+    qv = []
+    for u in range(k):
+        st = g.vset(int(emb[u]))
+        keep = [x for x in st if rng.random() < 0.6] or [st[int(rng.integers(len(st)))]]
+        qv.extend(keep)
+        qv_off[u + 1] = len(qv)
+    qe_off = np.zeros(len(q.src) + 1, np.int64)
+    qe = []
+    for i, eid in enumerate(q.elabels.tolist()):
+        st = g.eset(int(eid))
+        keep = [x for x in st if rng.random() < 0.6] or [st[int(rng.integers(len(st)))]]
+        qe.extend(keep)
+        qe_off[i + 1] = len(qe)
+    return MLGraph(k, qv_off, np.array(qv, np.int32), q.src, q.dst, qe_off, np.array(qe, np.int32),
+                   name=f"mlwalk{seed}", embedding=q.embedding)
+
+
+def ml_random_query(seed: int, k: int, nlv: int = 3, nle: int = 2) -> MLGraph:
+    """Random connected multi-label query (spanning tree + extra edges, 1-2 labels each)."""
+    q = random_connected_query(seed, k, nlv=1, nle=1, extra=0.3)
+    voff, vls = _label_sets(k, nlv, 2, seed + 7, "mlv")
+    eoff, els = _label_sets(len(q.src), nle, 2, seed + 7, "mle")
+    return MLGraph(k, voff, vls, q.src, q.dst, eoff, els, name=f"mlq{seed}")
