@@ -208,10 +208,11 @@ def workload_config(args, g):
     return {"workload": f"{args.config}: {BENCH_CONFIGS[args.config]['desc']}", "n": int(g.n), "m": int(g.m),
             "queries_per_step": args.queries, "query_k": args.k, "query_seeds": f"1000..{999 + args.queries}",
             "graph_seed": 1,
-            "mode": "count (gsi_query count-only: the last two levels are counted in closed form per row of "
-                    "M_{k-2}, |L|-[inj in L] survivors x (|RR| - row hits) extensions, DESIGN.md §6 count-ahead; "
-                    "'enumerated' = fingerprint mode, every final match produced, read and hashed; 'table' = "
-                    "every final match written)",
+            "mode": {"fp": "fingerprint (every match of the last level produced on the device, its candidate "
+                           "read and checked, the match hashed into the order-free set fingerprint; no "
+                           "closed-form counting)",
+                     "count": "count (closed-form last two levels, DESIGN.md §6 count-ahead)",
+                     "table": "table (every match written to HBM, query-id order)"}[args.mode],
             "l2": "inputs larger than L2 (PCSR+signatures >> 126 MB); no flush",
             "concurrency": args.concurrency}
 
@@ -272,12 +273,12 @@ def run_gsi(args):
              "fp": dict(fingerprint=True),                        # every final match read and hashed
              "table": dict(fingerprint=False, want_table=True)}   # every final match written (query-id order)
 
-    def step(mode="count", profile=False, stats=None, which=None, timeout=None, sh=None):
+    def step(mode="count", profile=False, stats=None, which=None, timeout=None, sh=None, conc=None):
         """One pass of the hot path over the batch (or the queries `which`).  The batch runs its
         queries concurrently (--concurrency host workers / streams); the profiled pass runs them
         one at a time so per-kernel event times are not shared."""
         ps = prepared if which is None else [prepared[i] for i in which]
-        rs = gsi.gsi_query_run_batch(graph, ps, concurrency=1 if profile else args.concurrency,
+        rs = gsi.gsi_query_run_batch(graph, ps, concurrency=1 if profile else (conc or args.concurrency),
                                      timeout_s=args.query_timeout if timeout is None else timeout, profile=profile,
                                      partial_on_timeout=True, **MODES[mode], **(shard if sh is None else sh))
         c = torch.tensor([r.count for r in rs], dtype=torch.int64, device="cuda")
@@ -294,8 +295,8 @@ def run_gsi(args):
         # the public API from host arrays: validate + encode + H2D of every query, the
         # concurrent batch run, and the counts back on the host
         ps = [gsi.prepare(graph, q) for q in qs]
-        rs = gsi.gsi_query_run_batch(graph, ps, concurrency=args.concurrency, timeout_s=args.query_timeout,
-                                     partial_on_timeout=True, fingerprint=False, **shard)
+        rs = gsi.gsi_query_run_batch(graph, ps, concurrency=args.concurrency, timeout_s=args.enum_timeout,
+                                     partial_on_timeout=True, **MODES[args.mode], **shard)
         counts.copy_(torch.tensor([r.count for r in rs], dtype=torch.int64))
         if ws > 1:
             dist.all_reduce(counts)
@@ -316,10 +317,11 @@ def run_gsi(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item()), out
 
+    HEAD = args.mode   # the headline pass: "fp" = every match produced, read and hashed
     for _ in range(args.warmup):
-        step()
+        step(HEAD, timeout=args.enum_timeout)
     torch.cuda.synchronize()
-    per_query_counts = step().tolist()
+    per_query_counts = step(HEAD, timeout=args.enum_timeout).tolist()
     total_matches = int(sum(per_query_counts))
 
     # ---- timed region: device-timed, prepared (resident) queries ------------------------
@@ -331,7 +333,7 @@ def run_gsi(args):
         torch.cuda.synchronize()
         ev0.record(stream)
         for _ in range(args.steps):
-            step(stats=launch_stats)
+            step(HEAD, stats=launch_stats, timeout=args.enum_timeout)
         ev1.record(stream)
         torch.cuda.synchronize()
         if ws > 1:
@@ -364,25 +366,22 @@ def run_gsi(args):
     h2d = sum(4 * q.n + 12 * len(q.src) + 64 * q.n for q in qs)        # query arrays + signatures
     d2h = sum(8 * q.n + 64 * (2 * q.n + 2) for q in qs)                # |C(u)|, per-level sizes, count
 
-    # ---- enumerated: every match of the last level read and hashed (set fingerprint) -------
-    enumerated = None
-    if not args.no_enumerated:
-        en_stats = []
-        en_ms, en_counts = timed(lambda: step("fp", stats=en_stats, timeout=args.enum_timeout))
-        en_counts = en_counts.tolist()
-        en_capped = int(sum(s_["capped"] for s_ in en_stats))
-        en_matches = int(sum(en_counts))
-        fp_var = {}
-        for s_ in en_stats:
-            for k_, v_ in s_["variants"].items():
-                fp_var[k_] = fp_var.get(k_, 0) + v_
-        enumerated = {"value": en_matches / (en_ms / 1000.0), "unit": "matches/s", "ms_per_step": en_ms,
-                      "matches_per_step": en_matches, "capped_queries": en_capped,
-                      "counts_equal_count_mode": en_capped == 0 and en_counts == per_query_counts,
-                      "kernel_variants": fp_var,
-                      "note": "fingerprint mode: every match of the last level is produced on the device, its "
-                              "candidate read and checked, and the match hashed into the order-free set "
-                              "fingerprint (no closed-form counting); the enumerating join throughput"}
+    # ---- count-only: the library's default count path (the last two levels in closed form
+    # per row of M_{k-2}, DESIGN.md §6 count-ahead) -- per-query latency, not join throughput
+    count_only = None
+    if not args.no_count_only:
+        c_stats = []
+        c_ms, c_counts = timed(lambda: step("count", stats=c_stats))
+        c_counts = c_counts.tolist()
+        c_q = np.array([s_["ms_total"] for s_ in c_stats])
+        count_only = {"value": sum(c_counts) / (c_ms / 1000.0), "unit": "matches/s", "ms_per_step": c_ms,
+                      "ms_per_query": c_ms / len(qs), "query_ms_p50": float(np.percentile(c_q, 50)),
+                      "query_ms_p95": float(np.percentile(c_q, 95)),
+                      "capped_queries": int(sum(s_["capped"] for s_ in c_stats)),
+                      "counts_equal_headline": c_counts == per_query_counts,
+                      "note": "count-only gsi_query (C ABI default): the last two levels are counted in closed "
+                              "form per row of M_{k-2} (|L|-[inj in L] survivors x (|RR| - row hits) extensions), "
+                              "so no per-match work; reported for ms/query, not as join throughput"}
 
     # ---- table: every match written to HBM as a k-int32 row in query-id order -------------
     table = None
@@ -391,18 +390,21 @@ def run_gsi(args):
         which = [i for i, c in enumerate(per_query_counts) if 0 < c * row_b <= args.table_max_gb * 1e9]
         if which:
             t_stats = []
-            t_ms, t_counts = timed(lambda: step("table", stats=t_stats, which=which, timeout=args.enum_timeout))
+            gsi.gsi_trim_workspace(local)   # the tables need the memory the count passes reserved
+            t_ms, t_counts = timed(lambda: step("table", stats=t_stats, which=which, timeout=args.enum_timeout,
+                                                conc=1))
             t_m = int(t_counts.sum().item())
             table = {"value": t_m / (t_ms / 1000.0), "unit": "matches/s", "ms": t_ms, "queries": which,
                      "matches": t_m, "GB_written": t_m * row_b / 1e9,
                      "write_GBps": t_m * row_b / 1e9 / (t_ms / 1000.0),
-                     "counts_equal_count_mode": t_counts.tolist() == [per_query_counts[i] for i in which],
+                     "counts_equal_headline": t_counts.tolist() == [per_query_counts[i] for i in which],
+                     "kernel_variants": _variants(t_stats),
                      "note": f"want_table on the bench queries whose table fits {args.table_max_gb} GB "
                              f"(4k B per match, device-resident)"}
 
     # ---- profiled pass: per-kernel-variant CUDA-event times + algorithmic bytes ------------
     pstats = []
-    step(profile=True, stats=pstats)
+    step(HEAD, profile=True, stats=pstats, timeout=args.enum_timeout)
     torch.cuda.synchronize()
     ms_k, bytes_k, launches_k = np.zeros(8), np.zeros(8), np.zeros(8)
     nv = gsi.GSI_N_KVARIANT
@@ -452,8 +454,8 @@ def run_gsi(args):
             per_rank = []
             tot = 0
             for r_ in range(W_):
-                t_ms, c_ = timed(lambda: step(sh=dict(shard_rank=r_, shard_count=W_,
-                                                      shard_pieces=args.shard_pieces)))
+                t_ms, c_ = timed(lambda: step(HEAD, timeout=args.enum_timeout,
+                                              sh=dict(shard_rank=r_, shard_count=W_, shard_pieces=args.shard_pieces)))
                 per_rank.append(t_ms)
                 tot += int(c_.sum().item())
             balance[str(W_)] = {"rank_ms": per_rank, "max_ms": max(per_rank),
@@ -493,10 +495,10 @@ def run_gsi(args):
         "ms_per_query": ms_per_step / len(qs), "matches_per_step": total_matches,
         "query_ms_p50": float(np.percentile(q_ms, 50)), "query_ms_p95": float(np.percentile(q_ms, 95)),
         "per_query": [{"count": int(c), "ms": round(float(t_), 3)} for c, t_ in zip(per_query_counts, q_ms_by_query)],
-        "capped_queries_per_step": capped, "query_timeout_s": args.query_timeout,
+        "capped_queries_per_step": capped, "query_timeout_s": args.enum_timeout,
         "e2e": {"value": m_e2e * args.steps / e2e_s, "unit": "matches/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_query": 1000.0 * e2e_s / args.steps / len(qs)},
-        "enumerated": enumerated, "table": table, "roofline": roofline, "multi_gpu_balance_emulated": balance,
+        "kernel_variants": _variants(launch_stats), "count_only": count_only, "table": table, "roofline": roofline, "multi_gpu_balance_emulated": balance,
         "small_queries": small,
         "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": launches,
         "graph": {"n_groups": info["n_groups"], "max_chain": info["max_chain"],
@@ -506,6 +508,14 @@ def run_gsi(args):
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _variants(stats):
+    out = {}
+    for s_ in stats:
+        for k_, v_ in s_["variants"].items():
+            out[k_] = out.get(k_, 0) + v_
+    return out
 
 
 def small_query_latency(gsi, cfg, nq, k, device):
@@ -576,11 +586,14 @@ def main():
     ap.add_argument("--ref-step-budget", type=float, default=8.0)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-enumerated", action="store_true", help="skip the secondary enumerated pass")
+    ap.add_argument("--mode", choices=["fp", "count", "table"], default="fp",
+                    help="headline pass: fp = every match produced, read and hashed (default); count = the "
+                         "closed-form count path")
+    ap.add_argument("--no-count-only", action="store_true", help="skip the secondary count-only pass")
     ap.add_argument("--concurrency", type=int, default=2, help="queries in flight (host workers / streams)")
-    ap.add_argument("--enum-timeout", type=float, default=30.0, help="per-query cap of the enumerated/table passes")
+    ap.add_argument("--enum-timeout", type=float, default=30.0, help="per-query cap of the headline and table passes")
     ap.add_argument("--no-table", action="store_true", help="skip the with-table pass")
-    ap.add_argument("--table-max-gb", type=float, default=40.0, help="table pass: queries whose table fits")
+    ap.add_argument("--table-max-gb", type=float, default=32.0, help="table pass: queries whose table fits")
     ap.add_argument("--no-balance", action="store_true", help="skip the emulated multi-GPU balance")
     ap.add_argument("--shard-pieces", type=int, default=8, help="interleaved shard pieces per rank (N > 1)")
     ap.add_argument("--no-small", action="store_true", help="skip the small-query latency section")

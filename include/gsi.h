@@ -60,7 +60,7 @@ enum { GSI_K_FILTER = 0, GSI_K_COMPACT = 1, GSI_K_PROBE = 2, GSI_K_JOIN = 3, GSI
 
 /* Kernel variants: gsi_stats.variant_launches[v] counts the launches of each (always, not only
  * in profile mode), so a test can prove which code path produced a result. */
-#define GSI_N_KVARIANT 16
+#define GSI_N_KVARIANT 20
 enum { GSI_V_JOIN_NEXT = 0,       /* k_join<J_NEXT>: slot tiles, compacting (Combine) write     */
        GSI_V_JOIN_COUNT = 1,      /* k_join<J_COUNT>: slot tiles, final level count (+ hash)    */
        GSI_V_JOIN_TABLE = 2,      /* k_join<J_TABLE>: slot tiles, final table                  */
@@ -76,7 +76,9 @@ enum { GSI_V_JOIN_NEXT = 0,       /* k_join<J_NEXT>: slot tiles, compacting (Com
        GSI_V_PROBE_AHEAD = 12,    /* k_probe_ahead: per-candidate next-step locate table       */
        GSI_V_SMALL = 13,          /* k_small_query: whole query in one launch                  */
        GSI_V_TWO_STEP = 14,       /* ablation: count pass of the two-step output               */
-       GSI_V_ABLATION = 15 };     /* ablation engine join launches (warp per row, paper design) */
+       GSI_V_ABLATION = 15,       /* ablation engine join launches (warp per row, paper design) */
+       GSI_V_FINAL_TABLE = 16,    /* k_final_table: every final match written (table mode)     */
+       GSI_V_SURV_SCAN = 17 };    /* k_surv_scan: table-mode Combine offsets per row           */
 
 /* gsi_query_opts.ablation bits (NEXT-3: the paper's join-phase study, Tables VI-VIII):
  * any bit set runs the query on the paper-style engine (one warp per row of M, Alg. 3/4) with
@@ -116,6 +118,35 @@ void gsi_build_opts_default(gsi_build_opts *opts);
 gsi_status gsi_build_graph(int64_t n, const int32_t *vlabels, int64_t m, const int32_t *src,
                            const int32_t *dst, const int32_t *elabels, const gsi_build_opts *opts,
                            gsi_graph **out);
+
+/*
+ * gsi_build_graph_ml — multi-label vertices and edges (§VII-B; NEXT-4).
+ * A match then needs L_V(u) ⊆ L_V(f(u)) and L_E(uv) ⊆ L_E(f(u)f(v)) (L1273-1275).
+ *   vls_off  n+1 int64 offsets, vls the labels: L_V(v) = vls[vls_off[v] .. vls_off[v+1]).
+ *   els_off  m+1 int64 offsets, els the labels of edge e = (src[e], dst[e]).
+ * Every edge label becomes one single-label parallel edge (L1283-1285); the signature
+ * table hashes the vertex label sets (reading A19) and the label sets stay on
+ * the device for the exact refine of C(u) (L1279-1281).  Repeated labels inside a set are
+ * ignored; a label in the sets of two edges on the same vertex pair -> DUPLICATE_EDGE.
+ * Query such a graph with gsi_query_prepare_ml (gsi_query_prepare refuses it).
+ * Errors as gsi_build_graph; offsets that do not start at 0 or decrease -> INVALID_ARG.
+ */
+gsi_status gsi_build_graph_ml(int64_t n, const int64_t *vls_off, const int32_t *vls, int64_t m,
+                              const int32_t *src, const int32_t *dst, const int64_t *els_off,
+                              const int32_t *els, const gsi_build_opts *opts, gsi_graph **out);
+
+/*
+ * gsi_build_line_graph — edge isomorphism (§VII-A, Fig. 9; NEXT-4):
+ * builds, on the device, the line graph G' of the input graph (arguments and errors as
+ * gsi_build_graph): vertex i of G' is input edge i, labelled elabels[i]; every two input
+ * edges sharing a vertex v give one G' edge labelled vlabels[v] (two parallel input edges
+ * whose shared ends carry the same label give it once).  Then PCSR + signatures of G' as
+ * gsi_build_graph.  sum_v deg(v)(deg(v)-1)/2 must stay below 2^30 -> else INVALID_ARG.
+ * Query it with gsi_query_prepare_line; result rows are input edge ids per query edge.
+ */
+gsi_status gsi_build_line_graph(int64_t n, const int32_t *vlabels, int64_t m, const int32_t *src,
+                                const int32_t *dst, const int32_t *elabels, const gsi_build_opts *opts,
+                                gsi_graph **out);
 
 typedef struct {
     int64_t n, m;                 /* |V|, |E| (undirected)                                  */
@@ -220,6 +251,20 @@ gsi_status gsi_query(const gsi_graph *g, int32_t k, const int32_t *q_vlabels, in
 gsi_status gsi_query_prepare(const gsi_graph *g, int32_t k, const int32_t *q_vlabels, int32_t qm,
                              const int32_t *q_src, const int32_t *q_dst, const int32_t *q_elabels,
                              gsi_prepared **out);
+/* Multi-label query for a gsi_build_graph_ml graph: q_vls_off (k+1
+ * int32 offsets) / q_vls the vertex label sets (at most 32 labels each), q_els_off (qm+1)
+ * / q_els the edge label sets.  Validation as gsi_query_prepare.  Rows of the result are
+ * data vertices in query-id order, as for single labels. */
+gsi_status gsi_query_prepare_ml(const gsi_graph *g, int32_t k, const int32_t *q_vls_off, const int32_t *q_vls,
+                                int32_t qm, const int32_t *q_src, const int32_t *q_dst,
+                                const int32_t *q_els_off, const int32_t *q_els, gsi_prepared **out);
+/* Edge-isomorphism query for a gsi_build_line_graph graph: Q (k
+ * vertices, 1 <= qm <= 32 edges, connected) is transformed into its line graph on the host
+ * and prepared against G'.  Result rows have qm columns: the data edge id (index into the
+ * build's edge list) matched by query edge 0..qm-1. */
+gsi_status gsi_query_prepare_line(const gsi_graph *g, int32_t k, const int32_t *q_vlabels, int32_t qm,
+                                  const int32_t *q_src, const int32_t *q_dst, const int32_t *q_elabels,
+                                  gsi_prepared **out);
 gsi_status gsi_query_run(const gsi_graph *g, const gsi_prepared *q, const gsi_query_opts *opts,
                          gsi_result **out);
 void gsi_prepared_free(gsi_prepared *q);
@@ -299,6 +344,9 @@ gsi_status gsi_debug_filter(const gsi_graph *g, int32_t k, const int32_t *q_vlab
                             int32_t filter_mode, uint32_t *bitmaps, int64_t *counts);
 /* Host query signatures (k x 16 uint32) as encoded by the library; distinct = 1 gives the
  * homomorphism encoding (each (edge label, neighbour label) key counted once). */
+/* Test hook: C(u) bitmaps / counts of a prepared query (any kind: single-label, multi-label
+ * with its refine step, line graph); mode 0 = isomorphism signatures, 2 = homomorphism. */
+gsi_status gsi_debug_filter_prepared(const gsi_prepared *q, int32_t mode, uint32_t *bitmaps, int64_t *counts);
 gsi_status gsi_debug_query_signatures(int32_t k, const int32_t *q_vlabels, int32_t qm,
                                       const int32_t *q_src, const int32_t *q_dst,
                                       const int32_t *q_elabels, int32_t distinct, uint32_t *qsig);

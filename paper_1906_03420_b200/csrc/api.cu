@@ -30,6 +30,17 @@ gsi_status prepare_impl(const gsi_graph *g, int32_t k, const int32_t *qvl, int32
 gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_opts *opts, gsi_result **out);
 gsi_status run_batch_impl(const gsi_graph *g, int32_t nq, const gsi_prepared *const *qs, const gsi_query_opts *opts,
                           int32_t conc, gsi_result **out);
+gsi_status build_graph_ml_impl(int64_t n, const int64_t *vls_off, const int32_t *vls, int64_t m, const int32_t *src,
+                               const int32_t *dst, const int64_t *els_off, const int32_t *els,
+                               const gsi_build_opts *opts, gsi_graph **out);
+gsi_status build_line_graph_impl(int64_t n, const int32_t *vl, int64_t m, const int32_t *src, const int32_t *dst,
+                                 const int32_t *el, const gsi_build_opts *opts, gsi_graph **out);
+gsi_status prepare_ml_impl(const gsi_graph *g, int32_t k, const int32_t *qvls_off, const int32_t *qvls, int32_t qm,
+                           const int32_t *qs, const int32_t *qd, const int32_t *qels_off, const int32_t *qels,
+                           gsi_prepared **out);
+gsi_status prepare_line_impl(const gsi_graph *g, int32_t k, const int32_t *qvl, int32_t qm, const int32_t *qs,
+                             const int32_t *qd, const int32_t *qe, gsi_prepared **out);
+gsi_status debug_filter_prepared_impl(const gsi_prepared *q, int32_t mode, uint32_t *bitmaps, int64_t *counts);
 gsi_status debug_filter_impl(const gsi_graph *g, int32_t k, const int32_t *qvl, int32_t qm, const int32_t *qs,
                              const int32_t *qd, const int32_t *qe, int32_t mode, uint32_t *bitmaps, int64_t *counts);
 
@@ -54,6 +65,8 @@ static void free_graph(gsi_graph *g) {
     if (g->ci) cudaFree(g->ci);
     if (g->cr_key) cudaFree(g->cr_key);
     if (g->cr_loc) cudaFree(g->cr_loc);
+    if (g->ml_off) cudaFree(g->ml_off);
+    if (g->ml_labs) cudaFree(g->ml_labs);
     cudaSetDevice(cur);
     delete g;
 }
@@ -62,6 +75,7 @@ struct MetaHeader {
     uint64_t magic;
     int64_t n, m, n_groups, overflow_groups;
     int32_t n_labels, gpn, max_chain, version;
+    int64_t line_n;      // line graph (edge isomorphism): |V| of the original graph, else -1
 };
 static const uint64_t kMetaMagic = 0x475349423230304dull;   // "GSIB200M"
 
@@ -136,6 +150,10 @@ gsi_status gsi_graph_buffers(const gsi_graph *g, gsi_buffer_desc *descs, int32_t
         set_error("null argument");
         return GSI_ERR_INVALID_ARG;
     }
+    if (g->ml) {
+        set_error("replicating a multi-label graph is not supported (build it on every device)");
+        return GSI_ERR_INVALID_ARG;
+    }
     const int nl = g->n_labels;
     const uint64_t need = sizeof(MetaHeader) + (uint64_t)nl * (4 + 8 + 8 + 4) + 4ull * (nl + 1);
     if (descs) {
@@ -149,7 +167,8 @@ gsi_status gsi_graph_buffers(const gsi_graph *g, gsi_buffer_desc *descs, int32_t
             set_error("meta buffer too small");
             return GSI_ERR_INVALID_ARG;
         }
-        MetaHeader h{kMetaMagic, g->n, g->m, g->n_groups, g->overflow_groups, nl, g->gpn, g->max_chain, 2};
+        MetaHeader h{kMetaMagic, g->n, g->m, g->n_groups, g->overflow_groups, nl, g->gpn, g->max_chain, 3,
+                     g->line ? g->line_n : -1};
         char *p = (char *)meta;
         std::memcpy(p, &h, sizeof(h));
         p += sizeof(h);
@@ -178,7 +197,7 @@ gsi_status gsi_graph_alloc_like(const void *meta, uint64_t meta_bytes, const gsi
     MetaHeader h;
     std::memcpy(&h, meta, sizeof(h));
     const int nl = h.n_labels;
-    if (h.magic != kMetaMagic || h.version != 2 || meta_bytes < sizeof(MetaHeader) + (uint64_t)nl * 24 + 4ull * (nl + 1)) {
+    if (h.magic != kMetaMagic || h.version != 3 || meta_bytes < sizeof(MetaHeader) + (uint64_t)nl * 24 + 4ull * (nl + 1)) {
         set_error("metadata blob is not a gsi graph description");
         return GSI_ERR_INVALID_ARG;
     }
@@ -193,6 +212,8 @@ gsi_status gsi_graph_alloc_like(const void *meta, uint64_t meta_bytes, const gsi
     g->n_labels = nl;
     g->gpn = h.gpn;
     g->max_chain = h.max_chain;
+    g->line = h.line_n >= 0;
+    g->line_n = g->line ? h.line_n : 0;
     const char *p = (const char *)meta + sizeof(h);
     g->lab_raw.resize(nl);
     g->freq.resize(nl);
@@ -236,7 +257,67 @@ gsi_status gsi_query_prepare(const gsi_graph *g, int32_t k, const int32_t *qvl, 
     }
     *out = nullptr;
     GSI_TRY(need_device());
+    if (g && g->ml) {
+        set_error("a multi-label graph takes gsi_query_prepare_ml");
+        return GSI_ERR_INVALID_ARG;
+    }
     return prepare_impl(g, k, qvl, qm, qs, qd, qe, out);
+}
+
+gsi_status gsi_query_prepare_ml(const gsi_graph *g, int32_t k, const int32_t *q_vls_off, const int32_t *q_vls,
+                                int32_t qm, const int32_t *q_src, const int32_t *q_dst, const int32_t *q_els_off,
+                                const int32_t *q_els, gsi_prepared **out) {
+    if (!out) {
+        set_error("out is NULL");
+        return GSI_ERR_INVALID_ARG;
+    }
+    *out = nullptr;
+    GSI_TRY(need_device());
+    return prepare_ml_impl(g, k, q_vls_off, q_vls, qm, q_src, q_dst, q_els_off, q_els, out);
+}
+
+gsi_status gsi_query_prepare_line(const gsi_graph *g, int32_t k, const int32_t *q_vlabels, int32_t qm,
+                                  const int32_t *q_src, const int32_t *q_dst, const int32_t *q_elabels,
+                                  gsi_prepared **out) {
+    if (!out) {
+        set_error("out is NULL");
+        return GSI_ERR_INVALID_ARG;
+    }
+    *out = nullptr;
+    GSI_TRY(need_device());
+    return prepare_line_impl(g, k, q_vlabels, qm, q_src, q_dst, q_elabels, out);
+}
+
+gsi_status gsi_build_graph_ml(int64_t n, const int64_t *vls_off, const int32_t *vls, int64_t m, const int32_t *src,
+                              const int32_t *dst, const int64_t *els_off, const int32_t *els,
+                              const gsi_build_opts *opts, gsi_graph **out) {
+    if (!out) {
+        set_error("out is NULL");
+        return GSI_ERR_INVALID_ARG;
+    }
+    *out = nullptr;
+    GSI_TRY(need_device());
+    return build_graph_ml_impl(n, vls_off, vls, m, src, dst, els_off, els, opts, out);
+}
+
+gsi_status gsi_build_line_graph(int64_t n, const int32_t *vlabels, int64_t m, const int32_t *src, const int32_t *dst,
+                                const int32_t *elabels, const gsi_build_opts *opts, gsi_graph **out) {
+    if (!out) {
+        set_error("out is NULL");
+        return GSI_ERR_INVALID_ARG;
+    }
+    *out = nullptr;
+    GSI_TRY(need_device());
+    return build_line_graph_impl(n, vlabels, m, src, dst, elabels, opts, out);
+}
+
+gsi_status gsi_debug_filter_prepared(const gsi_prepared *q, int32_t mode, uint32_t *bitmaps, int64_t *counts) {
+    GSI_TRY(need_device());
+    if (!q) {
+        set_error("q is NULL");
+        return GSI_ERR_INVALID_ARG;
+    }
+    return debug_filter_prepared_impl(q, mode, bitmaps, counts);
 }
 
 gsi_status gsi_query_run(const gsi_graph *g, const gsi_prepared *q, const gsi_query_opts *opts, gsi_result **out) {

@@ -352,6 +352,10 @@ void workspace_trim(int dev);
 void encode_query_signatures(int32_t k, const int32_t *qvl, int32_t qm, const int32_t *qs, const int32_t *qd,
                              const int32_t *qe, uint32_t *qsig /* k*16 */, int distinct);
 
+// ext.cu (NEXT-4): the multi-label filter (hashed-label signatures + exact label-set refine).
+cudaError_t launch_filter_ml(const gsi_graph *g, const gsi_prepared *q, int hom, uint32_t *bm, long long words,
+                             unsigned long long *counts, cudaStream_t st);
+
 }  // namespace gsi
 
 // The graph object (opaque to callers).
@@ -381,6 +385,16 @@ struct gsi_graph {
     mutable std::mutex cr_mu;
     mutable unsigned long long *cr_key = nullptr;
     mutable uint2 *cr_loc = nullptr;
+    // NEXT-4 (ext.cu).  Multi-label vertices (§VII-B): the label SETS on
+    // the device (refine step of the filter); the signatures hash them (reading A19).
+    bool ml = false;
+    int64_t ml_total = 0;
+    int64_t *ml_off = nullptr;       // [n+1]
+    int32_t *ml_labs = nullptr;      // ascending per vertex
+    // Edge isomorphism (§VII-A): this graph is the line graph of an input
+    // graph with line_n vertices; vertex i = input edge i.
+    bool line = false;
+    int64_t line_n = 0;
 };
 
 // A validated, encoded query (opaque to callers).
@@ -393,8 +407,15 @@ struct gsi_prepared {
     std::vector<uint32_t> qsig;      // 2 * k * 16: iso signatures, then homomorphism signatures
     uint32_t *d_qsig = nullptr;
     bool absent_label = false;
+    // multi-label query (ext.cu): vertex label sets, device copy [k+1 offsets | labels]
+    bool ml = false;
+    std::vector<int32_t> qls;        // [k+1 offsets | labels]
+    int32_t *d_qls = nullptr;
+    // edge-isomorphism query (ext.cu): this is Q' = L(Q); its vertex j = query edge j
+    bool line = false;
     ~gsi_prepared() {
         if (d_qsig) cudaFreeAsync(d_qsig, cudaStreamPerThread);
+        if (d_qls) cudaFreeAsync(d_qls, cudaStreamPerThread);
     }
 };
 

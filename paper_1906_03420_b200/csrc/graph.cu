@@ -384,11 +384,12 @@ gsi_status build_graph_impl(int64_t n, const int32_t *h_vl, int64_t m, const int
     GSI_CUDA(d_src.alloc(m, st));
     GSI_CUDA(d_dst.alloc(m, st));
     GSI_CUDA(d_el.alloc(m, st));
-    if (n) GSI_CUDA(cudaMemcpyAsync(d_vl.p, h_vl, 4 * n, cudaMemcpyHostToDevice, st));
+    // host arrays (the C ABI) or device arrays (the NEXT-4 builders in ext.cu): UVA copies
+    if (n) GSI_CUDA(cudaMemcpyAsync(d_vl.p, h_vl, 4 * n, cudaMemcpyDefault, st));
     if (m) {
-        GSI_CUDA(cudaMemcpyAsync(d_src.p, h_src, 4 * m, cudaMemcpyHostToDevice, st));
-        GSI_CUDA(cudaMemcpyAsync(d_dst.p, h_dst, 4 * m, cudaMemcpyHostToDevice, st));
-        GSI_CUDA(cudaMemcpyAsync(d_el.p, h_el, 4 * m, cudaMemcpyHostToDevice, st));
+        GSI_CUDA(cudaMemcpyAsync(d_src.p, h_src, 4 * m, cudaMemcpyDefault, st));
+        GSI_CUDA(cudaMemcpyAsync(d_dst.p, h_dst, 4 * m, cudaMemcpyDefault, st));
+        GSI_CUDA(cudaMemcpyAsync(d_el.p, h_el, 4 * m, cudaMemcpyDefault, st));
     }
     DevBuf<unsigned> d_flags;
     GSI_CUDA(d_flags.alloc(4, st));

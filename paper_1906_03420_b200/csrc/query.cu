@@ -19,10 +19,14 @@
 //                   pass instead of one launch per edge, Alg. 3 line 4).  Survivors are compacted
 //                   in slot order through shared memory (the write cache, L1155-1158) and their
 //                   global position comes from the same decoupled look-back — the Combine scan of
-//                   Alg. 3 line 14 fused into the join; nothing is joined twice.
-//   k_link          Combine (Alg. 3 lines 15-21): M'[r] = M[R[r]] || S[r], one thread per output
-//                   int (fully coalesced stores).  The last level is count-only unless the table
-//                   is wanted, and writes the final table in query-id order.
+//                   Alg. 3 line 14 fused into the join; nothing is joined twice.  The CTA then
+//                   writes its contiguous block of new rows m_i || x itself (the Combine of
+//                   Alg. 3 lines 15-21, coalesced), or, at the last level, counts / hashes /
+//                   writes the final table in query-id order.
+//   k_next_lean, k_cahead_lean, k_final_fp, k_final_table
+//                   warp-centric variants on shared N(v,l0) ∩ C(u) runs.
+//   k_abl_*         the paper-style ablation engine (one warp per row, NEXT-3).
+//   k_small_query   every level of a small query in one launch.
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -73,6 +77,9 @@ constexpr int kThreads = 256;
 #endif
 #ifndef GSI_COUNT_LEAN
 #define GSI_COUNT_LEAN 1    // enumerating last level on shared runs: lean warp walk (0: slot tiles)
+#endif
+#ifndef GSI_TABLE_LEAN
+#define GSI_TABLE_LEAN 1    // table-mode last level on shared runs: warp table kernel (0: slot tiles)
 #endif
 #ifndef GSI_CAHEAD_LONG
 #define GSI_CAHEAD_LONG 1   // k_cahead_lean: rows with >= 32 candidates walked warp-cooperatively
@@ -1284,6 +1291,30 @@ __global__ void __launch_bounds__(kThreads, GSI_CAHEAD_MINB) k_cahead_warp(const
 // last-step subtraction column in RR — no walk over the candidates.
 // FINAL: the same row formula as the last level of an enumerating count (count-ahead off):
 // the row's matches are the candidates of L minus the subtraction hit, s(m).
+// Up to N subtraction values of a row (Alg. 3 line 10: x must differ from the row's vertices
+// with u's label that are not linked to x), held in registers; -1 never equals a vertex.
+constexpr int kLeanInj = 4;
+template <int N>
+struct Inj {
+    int32_t v[N > 0 ? N : 1];
+    __device__ __forceinline__ void load(const int32_t *__restrict__ row, const StepParams &P, bool on) {
+#pragma unroll
+        for (int c = 0; c < N; c++) v[c] = (on && c < P.n_inj) ? __ldg(row + P.inj_col[c]) : -1;
+    }
+    __device__ __forceinline__ bool hit(int32_t x) const {
+        bool h = false;
+#pragma unroll
+        for (int c = 0; c < N; c++) h |= x == v[c];
+        return h;
+    }
+    __device__ __forceinline__ Inj shfl(int src) const {
+        Inj r;
+#pragma unroll
+        for (int c = 0; c < N; c++) r.v[c] = __shfl_sync(0xffffffffu, v[c], src);
+        return r;
+    }
+};
+
 template <int NINJ, bool FINAL>
 __global__ void __launch_bounds__(kThreads, 4) k_cahead_lean(const int32_t *__restrict__ M, long long r0, long long r1,
                                                              const Loc *__restrict__ loc, StepParams P, StepParams P2,
@@ -1308,9 +1339,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_cahead_lean(const int32_t *__re
             if (in_bitmap(P2.cu, y) && in_sorted(P2.fci + RR.off, RR.len, y)) rbase--;
         }
         uint32_t sv = need ? L.len : 0u;
-        if (NINJ > 0 && need) {
-            const int32_t inj = __ldg(row + P.inj_col[0]);
-            if (in_sorted(cip + L.off, L.len, inj)) sv--;
+        if (NINJ > 0 && need) {   // FINAL: up to kLeanInj columns, else one
+            const int ninj = FINAL ? P.n_inj : 1;
+            for (int c = 0; c < ninj; c++)
+                if (in_sorted(cip + L.off, L.len, __ldg(row + P.inj_col[c]))) sv--;
         }
         surv += sv;
         bound += (unsigned long long)sv * RR.len;
@@ -1350,7 +1382,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_final_fp(const int32_t *__restr
         const bool valid = i < r1;
         const Loc L = valid ? loc[(unsigned long long)i] : Loc{0u, 0u};
         const int32_t *row = M + (unsigned long long)(valid ? i : r0) * (unsigned)P.t;
-        const int32_t inj = (NINJ > 0 && valid && L.len) ? __ldg(row + P.inj_col[0]) : -1;
+        Inj<NINJ> inj;
+        inj.load(row, P, valid && L.len);
         act += (valid && L.len) ? 1u : 0u;
         unsigned long long s1 = 0, s2 = 0;   // the parent row's terms (every column but x)
         if (valid && L.len) {
@@ -1373,7 +1406,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_final_fp(const int32_t *__restr
         if (maxlen * 16 <= T) {   // even runs: every lane walks its own row
             for (uint32_t kk = 0; kk < L.len; kk++) {
                 const int32_t x = __ldg(cip + L.off + kk);
-                if (NINJ > 0 && x == inj) continue;
+                if (NINJ > 0 && inj.hit(x)) continue;
                 cnt++;
                 h1 += fp_mix(s1 + fp_term(kFpSeed1, qx, (uint32_t)x));
                 h2 ^= fp_mix(s2 + fp_term(kFpSeed2, qx, (uint32_t)x));
@@ -1386,10 +1419,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_final_fp(const int32_t *__restr
             longs &= longs - 1;
             const uint32_t off = __shfl_sync(0xffffffffu, L.off, r), len = __shfl_sync(0xffffffffu, L.len, r);
             const unsigned long long a1 = __shfl_sync(0xffffffffu, s1, r), a2 = __shfl_sync(0xffffffffu, s2, r);
-            const int32_t ri = NINJ > 0 ? __shfl_sync(0xffffffffu, inj, r) : -1;
+            const Inj<NINJ> ri = inj.shfl(r);
             for (uint32_t kk = lane; kk < len; kk += 32) {
                 const int32_t x = __ldg(cip + off + kk);
-                if (NINJ > 0 && x == ri) continue;
+                if (NINJ > 0 && ri.hit(x)) continue;
                 cnt++;
                 h1 += fp_mix(a1 + fp_term(kFpSeed1, qx, (uint32_t)x));
                 h2 ^= fp_mix(a2 + fp_term(kFpSeed2, qx, (uint32_t)x));
@@ -1415,10 +1448,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_final_fp(const int32_t *__restr
             o &= 31;
             const uint32_t pos = __shfl_sync(0xffffffffu, L.off, o) + (j - __shfl_sync(0xffffffffu, excl, o));
             const unsigned long long a1 = __shfl_sync(0xffffffffu, s1, o), a2 = __shfl_sync(0xffffffffu, s2, o);
-            const int32_t ri = NINJ > 0 ? __shfl_sync(0xffffffffu, inj, o) : -1;
+            const Inj<NINJ> ri = inj.shfl(o);
             if (j >= T2) continue;
             const int32_t x = __ldg(cip + pos);
-            if (NINJ > 0 && x == ri) continue;
+            if (NINJ > 0 && ri.hit(x)) continue;
             cnt++;
             h1 += fp_mix(a1 + fp_term(kFpSeed1, qx, (uint32_t)x));
             h2 ^= fp_mix(a2 + fp_term(kFpSeed2, qx, (uint32_t)x));
@@ -1435,6 +1468,135 @@ __global__ void __launch_bounds__(kThreads, 4) k_final_fp(const int32_t *__restr
         atomicXor(&ctr->fp2, h2);
     }
     if (lane == 0 && act) atomicAdd(&ctr->active_rows, act);
+}
+
+// Table-mode last level on shared runs (one linking edge, at most NINJ <= 1 subtraction
+// columns), pass 1: the Combine offsets of Alg. 3 line 14 in closed form per row.  Row i keeps
+// s_i = |L_i| - [inj_i in L_i] matches (lines 9-10; C(u) is already applied to the shared run),
+// O = exclusive scan of s over rows [r0, r0 + nrows) (decoupled look-back), O[nrows] = total.
+template <int NINJ>
+__global__ void __launch_bounds__(kThreads) k_surv_scan(const int32_t *__restrict__ M, long long r0, long long nrows,
+                                                        const Loc *__restrict__ loc, StepParams P,
+                                                        const int32_t *__restrict__ cip,
+                                                        unsigned long long *__restrict__ O,
+                                                        unsigned long long *status, unsigned *tile_ctr) {
+    __shared__ unsigned long long sm[33];
+    __shared__ unsigned tile_s;
+    __shared__ unsigned long long base_s;
+    if (threadIdx.x == 0) tile_s = atomicAdd(tile_ctr, 1u);
+    __syncthreads();
+    const unsigned tile = tile_s;
+    const long long i = (long long)tile * kThreads + threadIdx.x;
+    unsigned long long s = 0;
+    if (i < nrows) {
+        const Loc L = loc[(unsigned long long)(r0 + i)];
+        s = L.len;
+        if (NINJ > 0 && L.len) {
+            const int32_t *row = M + (unsigned long long)(r0 + i) * (unsigned)P.t;
+            for (int c = 0; c < P.n_inj; c++)
+                if (in_sorted(cip + L.off, L.len, __ldg(row + P.inj_col[c]))) s--;
+        }
+    }
+    unsigned long long agg;
+    const unsigned long long ex = block_exclusive_scan(s, sm, &agg);
+    if (threadIdx.x < 32) {
+        const unsigned long long pre = lookback_exclusive(status, tile, agg);
+        if (threadIdx.x == 0) base_s = pre;
+    }
+    __syncthreads();
+    if (i < nrows) O[i] = base_s + ex;
+    if (tile == gridDim.x - 1 && threadIdx.x == kThreads - 1) O[nrows] = base_s + agg;
+}
+
+// Table-mode last level on shared runs, pass 2: every match m_i || x written as a k-int32 row
+// in query-id order at out[O_i + j] (the final M of Alg. 3 lines 15-21; the paper's output,
+// 4k B per match).  A warp takes 32 consecutive rows and walks their concatenated candidates 32
+// at a time (owner by shuffle search); the survivors of a batch are contiguous in the output, so
+// they are compacted by ballot into a shared-memory staging tile (the write cache, L1155-1158)
+// and the warp stores the batch's 32·k ints as one coalesced stream.  HBM-write-bound.
+constexpr int kTabMaxK = 16;   // staging width; wider queries take the generic tile kernel
+template <int NINJ, bool FP>
+__global__ void __launch_bounds__(kThreads, 4) k_final_table(const int32_t *__restrict__ M, long long r0, long long r1,
+                                                             const Loc *__restrict__ loc,
+                                                             const unsigned long long *__restrict__ O, StepParams P,
+                                                             const int32_t *__restrict__ cip,
+                                                             int32_t *__restrict__ out, Counters *ctr) {
+    __shared__ int32_t stage[kThreads / 32][32 * kTabMaxK];
+    const int lane = threadIdx.x & 31;
+    int32_t *sw = stage[threadIdx.x >> 5];
+    const long long gw = (blockIdx.x * (long long)kThreads + threadIdx.x) >> 5;
+    const long long nw = ((long long)gridDim.x * kThreads) >> 5;
+    const int k = P.k;
+    const unsigned lt = (1u << lane) - 1u;
+    unsigned long long h1 = 0, h2 = 0;   // FP: the set fingerprint of the written rows
+    for (long long base = r0 + gw * 32; base < r1; base += nw * 32) {
+        const long long i = base + lane;
+        const bool valid = i < r1;
+        const Loc L = valid ? loc[(unsigned long long)i] : Loc{0u, 0u};
+        Inj<NINJ> inj;
+        inj.load(M + (unsigned long long)(valid ? i : r0) * (unsigned)P.t, P, valid && L.len);
+        unsigned long long ob = __shfl_sync(0xffffffffu, valid ? O[i - r0] : 0ull, 0);   // the unit's first output row
+        uint32_t inc = L.len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        const uint32_t excl = inc - L.len;
+        const uint32_t T = __shfl_sync(0xffffffffu, inc, 31);
+        for (uint32_t j0 = 0; j0 < T; j0 += 32) {
+            const uint32_t j = j0 + lane;
+            int o = 0;
+#pragma unroll
+            for (int st = 16; st > 0; st >>= 1) {
+                const uint32_t v = __shfl_sync(0xffffffffu, inc, o + st - 1);
+                if (v <= j) o += st;
+            }
+            o &= 31;
+            const uint32_t pos = __shfl_sync(0xffffffffu, L.off, o) + (j - __shfl_sync(0xffffffffu, excl, o));
+            const Inj<NINJ> ri = inj.shfl(o);
+            int32_t x = -1;
+            bool keep = j < T;
+            if (keep) {
+                x = __ldg(cip + pos);
+                if (NINJ > 0) keep = !ri.hit(x);
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+                const unsigned lp = __popc(bal & lt);
+                const int32_t *row = M + (unsigned long long)(base + o) * (unsigned)P.t;
+                unsigned long long a1 = 0, a2 = 0;
+                for (int q = 0; q < k; q++) {
+                    const int col = P.pos_of_q[q];
+                    const int32_t v = col < P.t ? __ldg(row + col) : x;
+                    sw[lp * k + q] = v;
+                    if (FP) {
+                        a1 += fp_term(kFpSeed1, q, (uint32_t)v);
+                        a2 += fp_term(kFpSeed2, q, (uint32_t)v);
+                    }
+                }
+                if (FP) {
+                    h1 += fp_mix(a1);
+                    h2 ^= fp_mix(a2);
+                }
+            }
+            __syncwarp();
+            const unsigned nk = (unsigned)__popc(bal) * (unsigned)k;
+            int32_t *dst = out + ob * (unsigned long long)k;
+            for (unsigned e = lane; e < nk; e += 32) __stcs(dst + e, sw[e]);
+            __syncwarp();
+            ob += __popc(bal);
+        }
+    }
+    if (FP) {
+        h1 = warp_sum_u64(h1);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) h2 ^= __shfl_xor_sync(0xffffffffu, h2, o);
+        if (lane == 0 && (h1 | h2)) {
+            atomicAdd(&ctr->fp1, h1);
+            atomicXor(&ctr->fp2, h2);
+        }
+    }
 }
 
 // Lean J_NEXT (count-only mode, one linking edge on shared runs in this step and the next):
@@ -3005,7 +3167,95 @@ bool cahead_lean(const QueryCtx &C, const StepParams &P, const StepParams &P2) {
 // kernel (no F, holes allowed).
 bool final_walks_rows(const QueryCtx &C, const StepParams &P, int mode) {
     return mode == J_COUNT && GSI_COUNT_LEAN && !env_flag("GSI_COUNT_NOLEAN") && P.prefiltered && P.E == 1 &&
-           P.n_inj <= 1 && cahead_warp_enabled();
+           P.n_inj <= kLeanInj && cahead_warp_enabled();
+}
+
+// The last level of a table query on shared runs is written by the warp table kernel: one
+// linking edge, at most one subtraction column, rows narrow enough for its staging tile.
+bool final_writes_rows(const QueryCtx &C, const StepParams &P) {
+    return GSI_TABLE_LEAN && !env_flag("GSI_TABLE_NOLEAN") && P.prefiltered && P.E == 1 && P.n_inj <= kLeanInj &&
+           C.q->k <= kTabMaxK;
+}
+
+// Rows [r0, r1) of the last level of a table query (final_writes_rows): survivors per row and
+// their offsets (k_surv_scan), then every match written straight into the result's table piece
+// (k_final_table) — no upper-bound buffer, no compaction copy.
+gsi_status final_table(QueryCtx &C, size_t si, const int32_t *M, long long r0, long long r1, const Loc *loc,
+                       const StepParams &P, const int32_t *cip) {
+    gsi_stats &S = *C.S;
+    Arena &A = *C.A;
+    cudaStream_t st = C.st;
+    const int k = C.q->k;
+    const unsigned long long nrows = (unsigned long long)(r1 - r0);
+    if (nrows == 0) return GSI_OK;
+    if (C.deadline > 0 && now_ms() > C.deadline) {
+        C.capped = true;
+        return GSI_OK;
+    }
+    const size_t mk = A.mark();
+    const unsigned rt = grid_for(nrows, kThreads);
+    unsigned long long *O = nullptr, *rst = nullptr;
+    GSI_TRY(A.get(&O, nrows + 1));
+    GSI_TRY(A.get(&rst, (unsigned long long)rt + 1));
+    GSI_CUDA(cudaMemsetAsync(rst, 0, 8ull * (rt + 1), st));
+    C.prof->begin(GSI_K_OTHER, GSI_V_SURV_SCAN);
+    S.variant_launches[GSI_V_SURV_SCAN]++;
+    if (P.n_inj == 0)
+        k_surv_scan<0><<<rt, kThreads, 0, st>>>(M, r0, (long long)nrows, loc, P, cip, O, rst + 1, (unsigned *)rst);
+    else
+        k_surv_scan<1><<<rt, kThreads, 0, st>>>(M, r0, (long long)nrows, loc, P, cip, O, rst + 1, (unsigned *)rst);
+    C.prof->end();
+    S.alg_bytes_variant[GSI_V_SURV_SCAN] += 16.0 * nrows;   // loc read + O write
+    S.alg_bytes[GSI_K_OTHER] += 16.0 * nrows;
+    unsigned long long total = 0;
+    GSI_CUDA(d2h(S, &total, O + nrows, 8, st));
+    GSI_CUDA(sync_timed(S, st));
+    if (total) {
+        int32_t *piece = nullptr;
+        if (cudaMallocAsync(&piece, 4ull * total * k, st) != cudaSuccess) {
+            cudaGetLastError();
+            A.reset(mk);
+            set_error("table of " + std::to_string(total) + " rows does not fit in device memory");
+            return GSI_ERR_OOM;
+        }
+        Counters *lctr = nullptr;
+        GSI_TRY(A.get(&lctr, 1));
+        GSI_CUDA(cudaMemsetAsync(lctr, 0, sizeof(Counters), st));
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, C.g->device);
+        const unsigned long long units = (nrows + 31) / 32;
+        const unsigned wg = (unsigned)std::max<unsigned long long>(
+            1, std::min<unsigned long long>((units + 7) / 8, (unsigned long long)sms * 8));
+        C.prof->begin(GSI_K_JOIN, GSI_V_FINAL_TABLE);
+        S.variant_launches[GSI_V_FINAL_TABLE]++;
+        if (P.fp) {
+            if (P.n_inj == 0) k_final_table<0, true><<<wg, kThreads, 0, st>>>(M, r0, r1, loc, O, P, cip, piece, lctr);
+            else k_final_table<kLeanInj, true><<<wg, kThreads, 0, st>>>(M, r0, r1, loc, O, P, cip, piece, lctr);
+        } else {
+            if (P.n_inj == 0) k_final_table<0, false><<<wg, kThreads, 0, st>>>(M, r0, r1, loc, O, P, cip, piece, lctr);
+            else k_final_table<kLeanInj, false><<<wg, kThreads, 0, st>>>(M, r0, r1, loc, O, P, cip, piece, lctr);
+        }
+        C.prof->end();
+        GSI_CUDA(cudaGetLastError());
+        // algorithmic bytes: the rows it extends (row + loc + O) and every byte it writes
+        const double jb = (4.0 * P.t + 16.0) * (double)nrows + 4.0 * k * (double)total;
+        S.alg_bytes_variant[GSI_V_FINAL_TABLE] += jb;
+        S.alg_bytes[GSI_K_JOIN] += jb;
+        if (P.fp) {
+            Counters hc;
+            GSI_CUDA(d2h(S, &hc, lctr, sizeof(Counters), st));
+            GSI_CUDA(sync_timed(S, st));
+            C.fp1 += hc.fp1;
+            C.fp2 ^= hc.fp2;
+        }
+        C.pieces.push_back({piece, total});
+    }
+    const int t = C.steps[si].t;
+    C.count += total;
+    S.rows[t] += total;
+    if (S.levels < t + 1) S.levels = t + 1;
+    A.reset(mk);
+    return GSI_OK;
 }
 
 // The level after step si will walk its rows without F (the warp count-ahead, or the lean last
@@ -3135,6 +3385,11 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
     for (const Piece &pc : pieces) {
     const unsigned long long s0 = pc.s0, s1 = pc.s1;
     const long long r_lo = pc.r0, r_hi = pc.r1;
+    if (mode == J_TABLE && final_writes_rows(C, P)) {
+        rc = final_table(C, si, M, r_lo, r_hi, loc, P, cip);
+        if (rc != GSI_OK) break;
+        continue;
+    }
     const unsigned long long chunk = (mode == J_COUNT || mode == J_CAHEAD)
                                          ? std::max<unsigned long long>(s1 - s0, 1)
                                          : std::max<unsigned long long>(C.cap_slots, kJoinTile);
@@ -3294,7 +3549,7 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
             if (P.fp && P.n_inj == 0)
                 k_final_fp<0><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, s.u, cip, lctr);
             else if (P.fp)
-                k_final_fp<1><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, s.u, cip, lctr);
+                k_final_fp<kLeanInj><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, s.u, cip, lctr);
             else if (P.n_inj == 0)
                 k_cahead_lean<0, true><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, P2, cip, g->groups, g->gpn, lctr);
             else
@@ -3737,8 +3992,11 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
         if (grid < 1) grid = 1;
         prof.begin(GSI_K_FILTER);
         const uint32_t *qsig = q->d_qsig + (opts.homomorphism ? (size_t)k * kPlanes : 0);
-        k_filter<<<grid, kThreads, 0, st>>>(g->sig, n, k, qsig, opts.filter_mode == 1, bm, words, d_counts,
-                                            C.ctr);
+        if (g->ml)   // multi-label: hashed label sets + exact refine (ext.cu)
+            GSI_CUDA(launch_filter_ml(g, q, opts.homomorphism, bm, words, d_counts, st));
+        else
+            k_filter<<<grid, kThreads, 0, st>>>(g->sig, n, k, qsig, opts.filter_mode == 1, bm, words, d_counts,
+                                                C.ctr);
         prof.end();
     }
     std::vector<long long> cand(k);
@@ -4006,11 +4264,20 @@ gsi_status run_batch_impl(const gsi_graph *g, int32_t nq, const gsi_prepared *co
 
 // ====================================================================== debug filter ===
 namespace gsi {
+gsi_status debug_filter_prepared_impl(const gsi_prepared *p, int32_t mode, uint32_t *bitmaps, int64_t *counts);
+
 gsi_status debug_filter_impl(const gsi_graph *g, int32_t k, const int32_t *qvl, int32_t qm, const int32_t *qs,
                              const int32_t *qd, const int32_t *qe, int32_t mode, uint32_t *bitmaps, int64_t *counts) {
     gsi_prepared *pp = nullptr;
     GSI_TRY(prepare_impl(g, k, qvl, qm, qs, qd, qe, &pp));
     std::unique_ptr<gsi_prepared> p(pp);
+    return debug_filter_prepared_impl(p.get(), mode, bitmaps, counts);
+}
+
+gsi_status debug_filter_prepared_impl(const gsi_prepared *p, int32_t mode, uint32_t *bitmaps, int64_t *counts) {
+    const gsi_graph *g = p->g;
+    const int k = p->k;
+    GSI_CUDA(cudaSetDevice(p->device));
     cudaStream_t st = cudaStreamPerThread;
     const long long n = g->n, words = (n + 31) / 32;
     Arena A(st);
@@ -4024,7 +4291,10 @@ gsi_status debug_filter_impl(const gsi_graph *g, int32_t k, const int32_t *qvl, 
     GSI_CUDA(cudaMemsetAsync(ctr, 0, sizeof(Counters), st));
     unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>((words + 7) / 8, 148 * 8));
     const uint32_t *qsig = p->d_qsig + (mode == 2 ? (size_t)k * kPlanes : 0);   // 2: homomorphism encoding
-    k_filter<<<grid, kThreads, 0, st>>>(g->sig, n, k, qsig, mode == 1, bm, words, cnt, ctr);
+    if (g->ml)
+        GSI_CUDA(launch_filter_ml(g, p, mode == 2, bm, words, cnt, st));
+    else
+        k_filter<<<grid, kThreads, 0, st>>>(g->sig, n, k, qsig, mode == 1, bm, words, cnt, ctr);
     if (bitmaps && words)
         GSI_CUDA(cudaMemcpyAsync(bitmaps, bm, 4ull * words * k, cudaMemcpyDeviceToHost, st));
     std::vector<unsigned long long> hc(k);

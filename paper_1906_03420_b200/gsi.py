@@ -24,11 +24,11 @@ HEADER = os.path.join(os.path.dirname(_PKG), "include", "gsi.h")
 GSI_MAX_K = 32
 GSI_N_KCLASS = 8
 KCLASS = ["filter", "compact", "probe", "join", "link", "other", "r6", "r7"]
-GSI_N_KVARIANT = 16
+GSI_N_KVARIANT = 20
 ABL_ENGINE, ABL_CR, ABL_TWO_STEP, ABL_NO_WCACHE, ABL_NAIVE_SO = 1, 2, 4, 8, 16
 KVARIANT = ["join_next", "join_count", "join_table", "join_cahead", "count_fast", "next_lean", "cahead_warp",
             "cahead_lean", "final_lean", "final_fp", "filter_partition", "refilter", "probe_ahead", "small",
-            "two_step", "reserved"]
+            "two_step", "ablation", "final_table", "surv_scan", "reserved18", "reserved19"]
 STATUS = {0: "GSI_OK", -1: "GSI_ERR_INVALID_ARG", -2: "GSI_ERR_VERTEX_RANGE", -3: "GSI_ERR_LABEL_RANGE",
           -4: "GSI_ERR_SELF_LOOP", -5: "GSI_ERR_DUPLICATE_EDGE", -6: "GSI_ERR_QUERY_DISCONNECTED",
           -7: "GSI_ERR_QUERY_TOO_LARGE", -8: "GSI_ERR_OOM", -9: "GSI_ERR_TIMEOUT", -10: "GSI_ERR_CUDA",
@@ -102,6 +102,11 @@ _SIGS = {
     "gsi_debug_filter": (I32, [P, I32, P, I32, P, P, P, I32, P, P]),
     "gsi_debug_query_signatures": (I32, [I32, P, I32, P, P, P, I32, P]),
     "gsi_debug_hash": (U64, [I32, U64, U64]),
+    "gsi_build_graph_ml": (I32, [I64, P, P, I64, P, P, P, P, P, P]),
+    "gsi_build_line_graph": (I32, [I64, P, I64, P, P, P, P, P]),
+    "gsi_query_prepare_ml": (I32, [P, I32, P, P, I32, P, P, P, P, P]),
+    "gsi_query_prepare_line": (I32, [P, I32, P, I32, P, P, P, P]),
+    "gsi_debug_filter_prepared": (I32, [P, I32, P, P]),
     "gsi_last_error": (ctypes.c_char_p, []),
     "gsi_version": (ctypes.c_char_p, []),
     "gsi_device_count": (I32, []),
@@ -177,6 +182,43 @@ def gsi_build_graph(n: int, vlabels, src, dst, elabels, gpn: int = 16, device: i
     out = P()
     _check(lib.gsi_build_graph(n, _ptr(vl), len(s), _ptr(s), _ptr(d), _ptr(e), ctypes.byref(o), ctypes.byref(out)),
            "gsi_build_graph")
+    return GraphHandle(out.value)
+
+
+def _opts_build(gpn, device, stream):
+    o = gsi_build_opts()
+    lib.gsi_build_opts_default(ctypes.byref(o))
+    o.gpn, o.device, o.stream = gpn, device, stream
+    return o
+
+
+def _i64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def gsi_build_graph_ml(n: int, vls_off, vls, src, dst, els_off, els, gpn: int = 16, device: int = -1,
+                       stream=None) -> GraphHandle:
+    """Multi-label graph (vertex and edge label SETS as offsets + labels), NEXT-4."""
+    vo, vl, s, d, eo, el = _i64(vls_off), _i32(vls), _i32(src), _i32(dst), _i64(els_off), _i32(els)
+    if len(vo) != n + 1 or len(eo) != len(s) + 1 or len(s) != len(d):
+        raise ValueError("label-set offsets / edge arrays have inconsistent lengths")
+    o = _opts_build(gpn, device, stream)
+    out = P()
+    _check(lib.gsi_build_graph_ml(n, _ptr(vo), _ptr(vl), len(s), _ptr(s), _ptr(d), _ptr(eo), _ptr(el),
+                                  ctypes.byref(o), ctypes.byref(out)), "gsi_build_graph_ml")
+    return GraphHandle(out.value)
+
+
+def gsi_build_line_graph(n: int, vlabels, src, dst, elabels, gpn: int = 16, device: int = -1,
+                         stream=None) -> GraphHandle:
+    """Line graph for edge isomorphism (NEXT-4): vertex i = input edge i."""
+    vl, s, d, e = _i32(vlabels), _i32(src), _i32(dst), _i32(elabels)
+    if not (len(s) == len(d) == len(e)):
+        raise ValueError("src/dst/elabels length mismatch")
+    o = _opts_build(gpn, device, stream)
+    out = P()
+    _check(lib.gsi_build_line_graph(n, _ptr(vl), len(s), _ptr(s), _ptr(d), _ptr(e), ctypes.byref(o),
+                                    ctypes.byref(out)), "gsi_build_line_graph")
     return GraphHandle(out.value)
 
 
@@ -315,6 +357,24 @@ def gsi_query_prepare(g: GraphHandle, q_vlabels, q_src, q_dst, q_elabels) -> Pre
     return Prepared(out.value, len(qv), g)
 
 
+def gsi_query_prepare_ml(g: GraphHandle, q_vls_off, q_vls, q_src, q_dst, q_els_off, q_els) -> Prepared:
+    vo, vl, qs, qd, eo, el = _i32(q_vls_off), _i32(q_vls), _i32(q_src), _i32(q_dst), _i32(q_els_off), _i32(q_els)
+    k = len(vo) - 1
+    out = P()
+    _check(lib.gsi_query_prepare_ml(g.h, k, _ptr(vo), _ptr(vl), len(qs), _ptr(qs), _ptr(qd), _ptr(eo), _ptr(el),
+                                    ctypes.byref(out)), "gsi_query_prepare_ml")
+    return Prepared(out.value, k, g)
+
+
+def gsi_query_prepare_line(g: GraphHandle, q_vlabels, q_src, q_dst, q_elabels) -> Prepared:
+    """Edge-isomorphism query: result rows hold one data edge id per query edge."""
+    qv, qs, qd, qe = _i32(q_vlabels), _i32(q_src), _i32(q_dst), _i32(q_elabels)
+    out = P()
+    _check(lib.gsi_query_prepare_line(g.h, len(qv), _ptr(qv), len(qs), _ptr(qs), _ptr(qd), _ptr(qe),
+                                      ctypes.byref(out)), "gsi_query_prepare_line")
+    return Prepared(out.value, len(qs), g)
+
+
 def gsi_query_run(g: GraphHandle, p: Prepared, **opts) -> Result:
     o, keep = _opts(**opts)
     out = P()
@@ -361,6 +421,14 @@ def gsi_debug_filter(g: GraphHandle, q_vlabels, q_src, q_dst, q_elabels, filter_
     cnt = np.zeros(len(qv), np.int64)
     _check(lib.gsi_debug_filter(g.h, len(qv), _ptr(qv), len(qs), _ptr(qs), _ptr(qd), _ptr(qe), filter_mode,
                                 _ptr(bm), _ptr(cnt)), "gsi_debug_filter")
+    return bm[:, :words], cnt
+
+
+def gsi_debug_filter_prepared(p: Prepared, n: int, mode: int = 0):
+    words = (n + 31) // 32
+    bm = np.zeros((p.k, max(words, 1)), np.uint32)
+    cnt = np.zeros(p.k, np.int64)
+    _check(lib.gsi_debug_filter_prepared(p.h, mode, _ptr(bm), _ptr(cnt)), "gsi_debug_filter_prepared")
     return bm[:, :words], cnt
 
 
@@ -417,3 +485,28 @@ def query(graph: GraphHandle, q, **opts) -> Result:
 
 def prepare(graph: GraphHandle, q) -> Prepared:
     return gsi_query_prepare(graph, q.vlabels, q.src, q.dst, q.elabels)
+
+
+def build_ml(g, gpn: int = 16, device: int = -1, stream=None) -> GraphHandle:
+    return gsi_build_graph_ml(g.n, g.vls_off, g.vls, g.src, g.dst, g.els_off, g.els, gpn=gpn, device=device,
+                              stream=stream)
+
+
+def prepare_ml(graph: GraphHandle, q) -> Prepared:
+    return gsi_query_prepare_ml(graph, q.vls_off, q.vls, q.src, q.dst, q.els_off, q.els)
+
+
+def query_ml(graph: GraphHandle, q, **opts) -> Result:
+    return gsi_query_run(graph, prepare_ml(graph, q), **opts)
+
+
+def build_line(g, gpn: int = 16, device: int = -1, stream=None) -> GraphHandle:
+    return gsi_build_line_graph(g.n, g.vlabels, g.src, g.dst, g.elabels, gpn=gpn, device=device, stream=stream)
+
+
+def prepare_line(graph: GraphHandle, q) -> Prepared:
+    return gsi_query_prepare_line(graph, q.vlabels, q.src, q.dst, q.elabels)
+
+
+def query_line(graph: GraphHandle, q, **opts) -> Result:
+    return gsi_query_run(graph, prepare_line(graph, q), **opts)

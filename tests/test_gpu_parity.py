@@ -590,3 +590,48 @@ def test_ablation_engine_same_result(ab):
         assert gsi.query(graph, q, ablation=ab, fingerprint=False).count == cnt
     with pytest.raises(gsi.GsiError):
         gsi.query(graph, qs[0], ablation=ab, want_table=True)
+
+
+def test_table_writer_on_shared_runs():
+    """Table mode on shared N(v,l0) ∩ C(u) runs (k_surv_scan + k_final_table: the Combine
+    offsets in closed form per row, every match written straight into the result) gives the
+    oracle's sorted table, in the order-preserving pi order, with and without the fingerprint
+    and sharded; the slot-tiled J_TABLE kernel gives the same table."""
+    g = W.chung_lu(6000, 40000, 600, nlv=2, nle=3, seed=131)
+    graph = gsi.build(g)
+    og = oracle.OracleGraph(g)
+    qs = bounded_queries(g, og, lambda s: 4 + s % 5, range(13100, 13160), lo=50, hi=2_000_000, want=6)
+    assert len(qs) >= 4
+    used = 0
+    for q in qs:
+        cnt, fp, otab = oracle.match(og, q)
+        for fpo in (True, False):
+            r = gsi.query(graph, q, want_table=True, fingerprint=fpo, force_paths=1, small=False)
+            tab = r.table()
+            assert r.count == cnt and np.array_equal(canon(tab), otab)
+            if fpo:
+                assert r.fingerprint() == fp
+            st = r.stats()
+            assert strictly_increasing_in_order(tab, st["order"][:q.n])
+            used += st["variants"].get("final_table", 0) > 0
+        parts = [gsi.query(graph, q, want_table=True, force_paths=1, small=False, shard_rank=r_, shard_count=3,
+                           shard_pieces=2).table() for r_ in range(3)]
+        assert np.array_equal(canon(np.concatenate(parts)), otab)
+    assert used >= 4
+
+
+def test_table_writer_env_off_same_table(monkeypatch):
+    """GSI_TABLE_NOLEAN=1 sends the table level back to the slot-tiled k_join<J_TABLE>: the
+    same rows in the same order."""
+    g = W.chung_lu(6000, 40000, 600, nlv=2, nle=3, seed=132)
+    graph = gsi.build(g)
+    og = oracle.OracleGraph(g)
+    qs = bounded_queries(g, og, 6, range(13200, 13240), lo=50, hi=2_000_000, want=3)
+    assert qs
+    for q in qs:
+        a = gsi.query(graph, q, want_table=True, force_paths=1, small=False)
+        monkeypatch.setenv("GSI_TABLE_NOLEAN", "1")
+        b = gsi.query(graph, q, want_table=True, force_paths=1, small=False)
+        monkeypatch.delenv("GSI_TABLE_NOLEAN")
+        assert b.stats()["variants"].get("final_table", 0) == 0
+        assert np.array_equal(a.table(), b.table()) and a.fingerprint() == b.fingerprint()
