@@ -89,6 +89,9 @@ enum { GSI_V_JOIN_NEXT = 0,       /* k_join<J_NEXT>: slot tiles, compacting (Com
 #define GSI_ABL_NO_WCACHE 8  /* no write cache: each lane stores its own survivor row (L1155-1158)  */
 #define GSI_ABL_NAIVE_SO 16  /* naive set operation: C(u) by binary search in the candidate list,
                                  other linking lists by linear scan (L1136-1158 off)                */
+#define GSI_ABL_NO_LB    32  /* no 4-layer balance (L1169-1176): every row by one warp; on, rows   */
+                             /* above W2 take a block and rows above W1 an 8-CTA cluster (DSMEM)   */
+#define GSI_ABL_NO_DR    64  /* no duplicate removal within the block (Alg. 5)         */
 
 typedef struct gsi_graph gsi_graph;       /* opaque: PCSR + signature table on one device   */
 typedef struct gsi_result gsi_result;     /* opaque: count, fingerprint, optional table     */
@@ -314,6 +317,8 @@ typedef struct {
     float ms_variant[GSI_N_KVARIANT];
     double alg_bytes_variant[GSI_N_KVARIANT];
     int32_t small_aborted;            /* the small-query kernel stopped at this level (0: not)  */
+    uint64_t abl_layer_rows[3];       /* ablation engine: rows per balance layer (warp / block /
+                                         8-CTA cluster), summed over levels                      */
 } gsi_stats;
 
 gsi_status gsi_result_count(const gsi_result *r, uint64_t *count);

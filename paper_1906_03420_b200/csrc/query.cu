@@ -27,6 +27,8 @@
 //                   warp-centric variants on shared N(v,l0) ∩ C(u) runs.
 //   k_abl_*         the paper-style ablation engine (one warp per row, NEXT-3).
 //   k_small_query   every level of a small query in one launch.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -1991,8 +1993,41 @@ __global__ void __launch_bounds__(kThreads) k_scan_counts(const uint32_t *__rest
 //   AB_COUNT : two-step pass 1, cnt[i] only
 //   AB_WRITE : two-step pass 2, rows m_i || x written at G_i (write cache: staged per warp)
 //   AB_FINAL : last level, count (+ fingerprint)
-template <int MODE, bool WCACHE, bool NAIVE>
+// The per-candidate test of Alg. 3 (lines 9-13) in the paper-style engine.
+template <bool NAIVE>
+__device__ __forceinline__ bool abl_keep(int32_t x, const int32_t *__restrict__ row, long long i, const Loc *__restrict__ loc,
+                                         const StepParams &P, const int32_t *__restrict__ ci,
+                                         const uint32_t *__restrict__ cu_bm, const int32_t *__restrict__ cu_list,
+                                         long long cu_n) {
+    bool keep = NAIVE ? in_sorted(cu_list, (uint32_t)cu_n, x) : ((__ldg(cu_bm + ((uint32_t)x >> 5)) >> (x & 31)) & 1u);
+    for (int q = 0; q < P.n_inj && keep; q++) keep = row[P.inj_col[q]] != x;      // line 10
+    for (int e = 1; e < P.E && keep; e++) {                                      // line 13
+        const Loc Le = loc[i * P.E + e];
+        if (NAIVE) {
+            bool f = false;
+            for (uint32_t q = 0; q < Le.len && !f; q++) f = __ldg(ci + Le.off + q) == x;
+            keep = f;
+        } else {
+            keep = in_sorted(ci + Le.off, Le.len, x);
+        }
+    }
+    return keep;
+}
+
+// Alg. 3 with one warp per row (layer 4 of the 4-layer balance): lanes stride over the
+// row's buffer N(m_i[c0], l0).  rows = the light rows of the level (null: every row).
+//   AB_PC    : survivors into the row's Prealloc buffer gba[F_i ..], cnt[i] = survivors
+//   AB_COUNT : two-step pass 1, cnt[i] only
+//   AB_WRITE : two-step pass 2, rows m_i || x written at G_i (write cache: staged per warp)
+//   AB_FINAL : last level, count (+ fingerprint)
+// DR: duplicate removal within the block (Alg. 5): the 8 warps take 8 rows at a
+// time; warps whose rows read the same run N(v,l0) share one input buffer in shared memory,
+// filled batch by batch by the first of them, every warp then processing the batch from that
+// buffer (block-synchronous, as in Alg. 5).
+constexpr int kDrBatch = 128;
+template <int MODE, bool WCACHE, bool NAIVE, bool DR>
 __global__ void __launch_bounds__(kThreads) k_abl_join(const int32_t *__restrict__ M, long long nM,
+                                                       const uint32_t *__restrict__ rows,
                                                        const Loc *__restrict__ loc,
                                                        const unsigned long long *__restrict__ off, StepParams P,
                                                        const int32_t *__restrict__ ci,
@@ -2000,62 +2035,97 @@ __global__ void __launch_bounds__(kThreads) k_abl_join(const int32_t *__restrict
                                                        const int32_t *__restrict__ cu_list, long long cu_n,
                                                        int32_t *__restrict__ gba, uint32_t *__restrict__ cnt,
                                                        int32_t *__restrict__ out, Counters *ctr) {
-    __shared__ int32_t stage[kThreads / 32][32];
+    constexpr int NW = kThreads / 32;
+    __shared__ int32_t stage[NW][32];
+    __shared__ int32_t dbuf[DR ? NW : 1][DR ? kDrBatch : 1];
+    __shared__ Loc dkey[NW];
+    __shared__ int daddr[NW];
+    __shared__ uint32_t dmax;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
     const unsigned lt = (1u << lane) - 1u;
     const int t = P.t, W = t + 1;
     unsigned long long c_all = 0, h1 = 0, h2 = 0;
-    for (long long i = gw; i < nM; i += nw) {
-        const Loc L0 = loc[i * P.E];
-        const int32_t *row = M + i * t;
-        uint32_t c = 0;
-        const unsigned long long base = (MODE == AB_PC || MODE == AB_WRITE) ? off[i] : 0ull;
-        for (uint32_t j0 = 0; j0 < L0.len; j0 += 32) {
-            const uint32_t j = j0 + lane;
-            bool keep = j < L0.len;
-            int32_t x = keep ? __ldg(ci + L0.off + j) : 0;
-            if (keep) keep = NAIVE ? in_sorted(cu_list, (uint32_t)cu_n, x)
-                                   : ((__ldg(cu_bm + ((uint32_t)x >> 5)) >> (x & 31)) & 1u);
-            for (int q = 0; q < P.n_inj && keep; q++) keep = row[P.inj_col[q]] != x;      // line 10
-            for (int e = 1; e < P.E && keep; e++) {                                      // line 13
-                const Loc Le = loc[i * P.E + e];
-                if (NAIVE) {
-                    bool f = false;
-                    for (uint32_t q = 0; q < Le.len && !f; q++) f = __ldg(ci + Le.off + q) == x;
-                    keep = f;
-                } else {
-                    keep = in_sorted(ci + Le.off, Le.len, x);
-                }
-            }
-            const unsigned b = __ballot_sync(0xffffffffu, keep);
-            const uint32_t pos = c + __popc(b & lt);
-            if (MODE == AB_PC && keep) gba[base + pos] = x;
-            if (MODE == AB_FINAL && keep) {
-                c_all++;
-                if (P.fp) row_hash(row, (uint32_t)x, P, h1, h2);
-            }
-            if (MODE == AB_WRITE) {
-                if (WCACHE) {   // stage the chunk's survivors, then one coalesced block of rows
-                    if (keep) stage[wib][__popc(b & lt)] = x;
-                    __syncwarp();
-                    const int ns = __popc(b);
-                    int32_t *o = out + (base + c) * (unsigned long long)W;
-                    for (int e = lane; e < ns * W; e += 32) {
-                        const int r = e / W, col = e - r * W;
-                        o[e] = col < t ? row[col] : stage[wib][r];
-                    }
-                    __syncwarp();
-                } else if (keep) {   // each lane writes its own row (strided stores)
-                    int32_t *o = out + (base + pos) * (unsigned long long)W;
-                    for (int col = 0; col < t; col++) o[col] = row[col];
-                    o[t] = x;
-                }
-            }
-            c += __popc(b);
+    // one row: survivors of candidates [j0, j0 + 32) read from src (global run or shared buffer)
+    // candidate j of the row is src[j - sbase] (the global run, or the shared DR buffer)
+    auto step32 = [&](long long i, const int32_t *row, const Loc &L0, uint32_t j0, const int32_t *src,
+                      uint32_t sbase, unsigned long long base, uint32_t &c) {
+        const uint32_t j = j0 + lane;
+        bool keep = j < L0.len;
+        const int32_t x = keep ? src[j - sbase] : 0;
+        if (keep) keep = abl_keep<NAIVE>(x, row, i, loc, P, ci, cu_bm, cu_list, cu_n);
+        const unsigned b = __ballot_sync(0xffffffffu, keep);
+        const uint32_t pos = c + __popc(b & lt);
+        if (MODE == AB_PC && keep) gba[base + pos] = x;
+        if (MODE == AB_FINAL && keep) {
+            c_all++;
+            if (P.fp) row_hash(row, (uint32_t)x, P, h1, h2);
         }
-        if ((MODE == AB_PC || MODE == AB_COUNT) && lane == 0) cnt[i] = c;
+        if (MODE == AB_WRITE) {
+            if (WCACHE) {   // stage the chunk's survivors, then one coalesced block of rows
+                if (keep) stage[wib][__popc(b & lt)] = x;
+                __syncwarp();
+                const int ns = __popc(b);
+                int32_t *o = out + (base + c) * (unsigned long long)W;
+                for (int e = lane; e < ns * W; e += 32) {
+                    const int r = e / W, col = e - r * W;
+                    o[e] = col < t ? row[col] : stage[wib][r];
+                }
+                __syncwarp();
+            } else if (keep) {   // each lane writes its own row (strided stores)
+                int32_t *o = out + (base + pos) * (unsigned long long)W;
+                for (int col = 0; col < t; col++) o[col] = row[col];
+                o[t] = x;
+            }
+        }
+        c += __popc(b);
+    };
+    if (!DR) {
+        const long long gw = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+        const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+        for (long long r = gw; r < nM; r += nw) {
+            const long long i = rows ? (long long)rows[r] : r;
+            const Loc L0 = loc[i * P.E];
+            const int32_t *row = M + i * t;
+            uint32_t c = 0;
+            const unsigned long long base = (MODE == AB_PC || MODE == AB_WRITE) ? off[i] : 0ull;
+            for (uint32_t j0 = 0; j0 < L0.len; j0 += 32) step32(i, row, L0, j0, ci + L0.off, 0u, base, c);
+            if ((MODE == AB_PC || MODE == AB_COUNT) && lane == 0) cnt[i] = c;
+        }
+    } else {
+        for (long long g0 = (long long)blockIdx.x * NW; g0 < nM; g0 += (long long)gridDim.x * NW) {
+            const long long r = g0 + wib;
+            const bool valid = r < nM;
+            const long long i = valid ? (rows ? (long long)rows[r] : r) : 0;
+            const Loc L0 = valid ? loc[i * P.E] : Loc{0u, 0u};
+            const int32_t *row = M + i * t;
+            if (threadIdx.x == 0) dmax = 0;
+            if (lane == 0) dkey[wib] = L0;
+            __syncthreads();
+            if (lane == 0) {   // Alg. 5 lines 2-5: the first warp of the block with the same run
+                int a = wib;
+                for (int w = 0; w < wib; w++)
+                    if (dkey[w].off == L0.off && dkey[w].len == L0.len) {
+                        a = w;
+                        break;
+                    }
+                daddr[wib] = L0.len ? a : wib;
+                atomicMax(&dmax, L0.len);
+            }
+            __syncthreads();
+            const int a = daddr[wib];
+            const uint32_t lmax = dmax;
+            uint32_t c = 0;
+            const unsigned long long base = (valid && (MODE == AB_PC || MODE == AB_WRITE)) ? off[i] : 0ull;
+            for (uint32_t b0 = 0; b0 < lmax; b0 += kDrBatch) {   // Alg. 5 lines 6-10
+                if (a == wib)
+                    for (uint32_t q = lane; q < kDrBatch && b0 + q < L0.len; q += 32) dbuf[wib][q] = __ldg(ci + L0.off + b0 + q);
+                __syncthreads();
+                for (uint32_t q0 = 0; q0 < kDrBatch && b0 + q0 < L0.len; q0 += 32)
+                    step32(i, row, L0, b0 + q0, dbuf[a], b0, base, c);
+                __syncthreads();
+            }
+            if (valid && (MODE == AB_PC || MODE == AB_COUNT) && lane == 0) cnt[i] = c;
+        }
     }
     if (MODE == AB_FINAL) {
         c_all = warp_sum_u64(c_all);
@@ -2068,6 +2138,153 @@ __global__ void __launch_bounds__(kThreads) k_abl_join(const int32_t *__restrict
             atomicXor(&ctr->fp2, h2);
         }
     }
+}
+
+// Layers 1-2 of the 4-layer balance for the paper-style engine.  A row whose
+// buffer exceeds W2 is processed by a whole block (layer 2); one above W1 by a thread-block
+// CLUSTER of up to 8 CTAs (layer 1 — the B200 form of the paper's dynamically launched child
+// kernel, L1172: no device-side launch, the cluster is part of the same grid).  The cluster's
+// rank-0 CTA stages the row (its columns and linking-list locations) in shared memory and the
+// other CTAs read it through distributed shared memory; each round, CTA r takes a contiguous
+// 1024-candidate slice, compacts its survivors in order into shared memory, publishes its
+// count, and reads the counts of ranks < r through DSMEM to place its survivors in the row's
+// buffer (Prealloc: gba[F_i + ...]; two-step pass 2: rows at G_i + ...) — an exact in-order
+// compaction with no global atomics.  rows = the level's rows of this layer.
+constexpr int kSegItems = 4;
+constexpr int kSegSlice = kThreads * kSegItems;
+template <int MODE, bool WCACHE, bool NAIVE>
+__global__ void __launch_bounds__(kThreads) k_abl_heavy(const int32_t *__restrict__ M, const uint32_t *__restrict__ rows,
+                                                        long long nrows, const Loc *__restrict__ loc,
+                                                        const unsigned long long *__restrict__ off, StepParams P,
+                                                        const int32_t *__restrict__ ci,
+                                                        const uint32_t *__restrict__ cu_bm,
+                                                        const int32_t *__restrict__ cu_list, long long cu_n,
+                                                        int32_t *__restrict__ gba, uint32_t *__restrict__ cnt,
+                                                        int32_t *__restrict__ out, Counters *ctr) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int CL = (int)cluster.num_blocks(), rank = (int)cluster.block_rank();
+    __shared__ int32_t s_row[GSI_MAX_K];
+    __shared__ Loc s_loc[GSI_MAX_K];
+    __shared__ int32_t s_x[kSegSlice];
+    __shared__ unsigned long long s_scan[33];
+    __shared__ unsigned long long s_cnt;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int t = P.t, W = t + 1;
+    unsigned long long c_all = 0, h1 = 0, h2 = 0;
+    const long long nclusters = gridDim.x / CL, cid = blockIdx.x / CL;
+    for (long long r = cid; r < nrows; r += nclusters) {
+        const long long i = rows[r];
+        if (rank == 0) {   // stage the row once per cluster
+            if (tid < t) s_row[tid] = M[i * t + tid];
+            if (tid < P.E) s_loc[tid] = loc[i * P.E + tid];
+        }
+        cluster.sync();
+        int32_t row[GSI_MAX_K];
+        const int32_t *rrow = cluster.map_shared_rank(s_row, 0);   // DSMEM reads of rank 0's copy
+        const Loc *rloc = cluster.map_shared_rank(s_loc, 0);
+        for (int c = 0; c < t; c++) row[c] = rrow[c];
+        const Loc L0 = rloc[0];
+        Loc Ls[GSI_MAX_K];
+        for (int e = 1; e < P.E; e++) Ls[e] = rloc[e];
+        const unsigned long long base = (MODE == AB_PC || MODE == AB_WRITE) ? off[i] : 0ull;
+        unsigned long long run = 0;
+        for (unsigned long long r0 = 0; r0 < L0.len; r0 += (unsigned long long)CL * kSegSlice) {
+            const unsigned long long s0 = r0 + (unsigned long long)rank * kSegSlice;
+            int32_t xs[kSegItems];
+            bool kp[kSegItems];
+            uint32_t mine = 0;
+#pragma unroll
+            for (int it = 0; it < kSegItems; it++) {   // blocked: thread tid owns slots [4 tid, 4 tid + 4)
+                const unsigned long long j = s0 + (unsigned long long)tid * kSegItems + it;
+                kp[it] = j < L0.len;
+                xs[it] = kp[it] ? __ldg(ci + L0.off + j) : 0;
+                if (kp[it]) {
+                    bool keep = NAIVE ? in_sorted(cu_list, (uint32_t)cu_n, xs[it])
+                                      : ((__ldg(cu_bm + ((uint32_t)xs[it] >> 5)) >> (xs[it] & 31)) & 1u);
+                    for (int q = 0; q < P.n_inj && keep; q++) keep = row[P.inj_col[q]] != xs[it];
+                    for (int e = 1; e < P.E && keep; e++) {
+                        if (NAIVE) {
+                            bool f = false;
+                            for (uint32_t q = 0; q < Ls[e].len && !f; q++) f = __ldg(ci + Ls[e].off + q) == xs[it];
+                            keep = f;
+                        } else {
+                            keep = in_sorted(ci + Ls[e].off, Ls[e].len, xs[it]);
+                        }
+                    }
+                    kp[it] = keep;
+                }
+                mine += kp[it] ? 1u : 0u;
+            }
+            unsigned long long tot;
+            const unsigned long long ex = block_exclusive_scan(mine, s_scan, &tot);
+            uint32_t p = (uint32_t)ex;
+#pragma unroll
+            for (int it = 0; it < kSegItems; it++)
+                if (kp[it]) s_x[p++] = xs[it];
+            if (tid == 0) s_cnt = tot;
+            cluster.sync();   // every rank's count is published
+            unsigned long long before = 0, all = 0;
+            for (int q = 0; q < CL; q++) {
+                const unsigned long long cq = *cluster.map_shared_rank(&s_cnt, q);
+                all += cq;
+                if (q < rank) before += cq;
+            }
+            const unsigned long long o0 = run + before;
+            const unsigned n = (unsigned)tot;
+            if (MODE == AB_PC)
+                for (unsigned q = tid; q < n; q += kThreads) gba[base + o0 + q] = s_x[q];
+            if (MODE == AB_FINAL)
+                for (unsigned q = tid; q < n; q += kThreads) {
+                    c_all++;
+                    if (P.fp) row_hash(M + i * t, (uint32_t)s_x[q], P, h1, h2);
+                }
+            if (MODE == AB_WRITE) {
+                int32_t *o = out + (base + o0) * (unsigned long long)W;
+                if (WCACHE) {
+                    for (unsigned e = tid; e < n * (unsigned)W; e += kThreads) {
+                        const unsigned q = e / W, col = e - q * W;
+                        o[e] = col < (unsigned)t ? row[col] : s_x[q];
+                    }
+                } else {
+                    for (unsigned q = tid; q < n; q += kThreads) {
+                        for (int col = 0; col < t; col++) o[q * W + col] = row[col];
+                        o[q * W + t] = s_x[q];
+                    }
+                }
+            }
+            run += all;
+            cluster.sync();   // s_x / s_cnt are reused next round
+        }
+        if ((MODE == AB_PC || MODE == AB_COUNT) && rank == 0 && tid == 0) cnt[i] = (uint32_t)run;
+    }
+    if (MODE == AB_FINAL) {
+        c_all = warp_sum_u64(c_all);
+        h1 = warp_sum_u64(h1);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) h2 ^= __shfl_xor_sync(0xffffffffu, h2, o);
+        if (lane == 0 && c_all) {
+            atomicAdd(&ctr->count, c_all);
+            atomicAdd(&ctr->fp1, h1);
+            atomicXor(&ctr->fp2, h2);
+        }
+    }
+}
+
+// Stable split of a level's rows into the balance layers by buffer length: flag[i] = 1 if
+// the row belongs to layer `which` (0: len <= W2, 1: W2 < len <= W1, 2: len > W1).
+__global__ void k_abl_flags(const uint32_t *__restrict__ lens, long long n, uint32_t w1, uint32_t w2, int which,
+                            uint32_t *__restrict__ flag) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const uint32_t l = lens[i];
+        const int b = l > w1 ? 2 : (l > w2 ? 1 : 0);
+        flag[i] = b == which ? 1u : 0u;
+    }
+}
+__global__ void k_abl_gather(const uint32_t *__restrict__ flag, const unsigned long long *__restrict__ pos, long long n,
+                             uint32_t *__restrict__ rows) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        if (flag[i]) rows[pos[i]] = (uint32_t)i;
 }
 
 // Combine (Alg. 3 lines 15-21): M'[G_i + j] = m_i || gba[F_i + j].  Write cache: one thread per
@@ -3782,6 +3999,73 @@ gsi_status run_small(QueryCtx &C, const int32_t *M1, bool &done) {
 }
 
 // ------------------------------------------------------------------ ablation engine ----
+// Balance thresholds (reading A16: W1 = 4 W2 = 16 W3 = 4096; tunable, perf only).
+uint32_t abl_w1() {
+    const char *e = getenv("GSI_ABL_W1");
+    return e ? (uint32_t)atol(e) : 4096u;
+}
+uint32_t abl_w2() {
+    const char *e = getenv("GSI_ABL_W2");
+    return e ? (uint32_t)atol(e) : 1024u;
+}
+constexpr int kAblCluster = 8;   // CTAs per heavy row (layer 1)
+
+struct AblLayers {   // rows of each balance layer (null: every row, no balance)
+    uint32_t *rows[3] = {nullptr, nullptr, nullptr};
+    unsigned long long n[3] = {0, 0, 0};
+};
+struct AblArgs {
+    const int32_t *M;
+    unsigned long long nM;
+    const Loc *loc;
+    StepParams P;
+    const int32_t *ci;
+    const uint32_t *cu;
+    const int32_t *cul;
+    long long cun;
+    Counters *ctr;
+    int sms;
+    bool dr;
+};
+
+// Layer 4 (warp per row, + block duplicate removal) over the light rows, layer 2 (a block per
+// row) and layer 1 (an 8-CTA cluster per row) over the others.
+template <int MODE, bool WC, bool NV>
+gsi_status abl_layers(const AblArgs &X, const AblLayers &Ly, const unsigned long long *off, int32_t *gba,
+                      uint32_t *cnt, int32_t *out, cudaStream_t st) {
+    const unsigned long long nl = Ly.n[0];
+    if (nl) {
+        const unsigned wg = (unsigned)std::max<unsigned long long>(
+            1, std::min<unsigned long long>((nl * 32 + kThreads - 1) / kThreads, (unsigned long long)X.sms * 16));
+        if (X.dr)
+            k_abl_join<MODE, WC, NV, true><<<wg, kThreads, 0, st>>>(X.M, (long long)nl, Ly.rows[0], X.loc, off, X.P, X.ci,
+                                                                   X.cu, X.cul, X.cun, gba, cnt, out, X.ctr);
+        else
+            k_abl_join<MODE, WC, NV, false><<<wg, kThreads, 0, st>>>(X.M, (long long)nl, Ly.rows[0], X.loc, off, X.P, X.ci,
+                                                                    X.cu, X.cul, X.cun, gba, cnt, out, X.ctr);
+    }
+    for (int b = 1; b <= 2; b++) {
+        if (!Ly.n[b]) continue;
+        const int CL = b == 2 ? kAblCluster : 1;
+        const unsigned long long ncl = std::min<unsigned long long>(Ly.n[b], (unsigned long long)X.sms * 4 / CL);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(ncl * CL));
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = CL;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        GSI_CUDA(cudaLaunchKernelEx(&cfg, k_abl_heavy<MODE, WC, NV>, X.M, (const uint32_t *)Ly.rows[b], (long long)Ly.n[b],
+                                    X.loc, off, X.P, X.ci, X.cu, X.cul, X.cun, gba, cnt, out, X.ctr));
+    }
+    return GSI_OK;
+}
+
 // Every level with the paper-style kernels (one warp per row); see k_abl_join.
 gsi_status run_ablation(QueryCtx &C, int32_t *M, unsigned long long nM) {
     const gsi_graph *g = C.g;
@@ -3790,14 +4074,10 @@ gsi_status run_ablation(QueryCtx &C, int32_t *M, unsigned long long nM) {
     cudaStream_t st = C.st;
     const int ab = C.opts.ablation;
     const bool cr = ab & GSI_ABL_CR, two = ab & GSI_ABL_TWO_STEP, wc = !(ab & GSI_ABL_NO_WCACHE),
-               naive = ab & GSI_ABL_NAIVE_SO;
+               naive = ab & GSI_ABL_NAIVE_SO, lb = !(ab & GSI_ABL_NO_LB), dr = !(ab & GSI_ABL_NO_DR);
     if (cr) GSI_TRY(ensure_cr(g, st));
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
-    auto warp_grid = [&](unsigned long long rows) {
-        return (unsigned)std::max<unsigned long long>(1, std::min<unsigned long long>((rows * 32 + kThreads - 1) / kThreads,
-                                                                                   (unsigned long long)sms * 16));
-    };
     auto scan = [&](const uint32_t *in, unsigned long long n, unsigned long long **outp) -> gsi_status {
         const unsigned tiles = grid_for(n, kThreads);
         unsigned long long *status = nullptr;
@@ -3848,16 +4128,36 @@ gsi_status run_ablation(QueryCtx &C, int32_t *M, unsigned long long nM) {
         GSI_CUDA(sync_timed(S, st));
         S.gba[t] += gba;
         if (gba == 0) break;
-        const unsigned wg = warp_grid(nM);
-#define GSI_ABL_JOIN(MODE, WC, NV, OFF, GBA, CNT, OUT)                                                            \
-    k_abl_join<MODE, WC, NV><<<wg, kThreads, 0, st>>>(M, (long long)nM, loc, OFF, P, g->ci, cu, cul, cun, GBA, CNT, \
-                                                       OUT, ctr)
+        // the 4-layer balance (layers 1, 2, 4): stable split of the rows by buffer length
+        AblLayers Ly;
+        Ly.n[0] = nM;
+        if (lb) {
+            uint32_t *flag = nullptr;
+            GSI_TRY(A.get(&flag, nM));
+            for (int b = 0; b < 3; b++) {
+                unsigned long long *pos = nullptr;
+                C.prof->begin(GSI_K_OTHER);
+                k_abl_flags<<<grid_for(nM, kThreads), kThreads, 0, st>>>(lens, (long long)nM, abl_w1(), abl_w2(), b, flag);
+                C.prof->end();
+                GSI_TRY(scan(flag, nM, &pos));
+                GSI_TRY(A.get(&Ly.rows[b], nM));
+                C.prof->begin(GSI_K_OTHER);
+                k_abl_gather<<<grid_for(nM, kThreads), kThreads, 0, st>>>(flag, pos, (long long)nM, Ly.rows[b]);
+                C.prof->end();
+                GSI_CUDA(d2h(S, &Ly.n[b], pos + nM, 8, st));
+            }
+            GSI_CUDA(sync_timed(S, st));
+            S.abl_layer_rows[0] += Ly.n[0];
+            S.abl_layer_rows[1] += Ly.n[1];
+            S.abl_layer_rows[2] += Ly.n[2];
+        }
+        AblArgs X{M, nM, loc, P, g->ci, cu, cul, cun, ctr, sms, dr};
         if (last) {
             GSI_CUDA(cudaMemsetAsync(ctr, 0, sizeof(Counters), st));
             C.prof->begin(GSI_K_JOIN, GSI_V_ABLATION);
             S.variant_launches[GSI_V_ABLATION]++;
-            if (naive) GSI_ABL_JOIN(AB_FINAL, true, true, nullptr, nullptr, nullptr, nullptr);
-            else GSI_ABL_JOIN(AB_FINAL, true, false, nullptr, nullptr, nullptr, nullptr);
+            if (naive) GSI_TRY((abl_layers<AB_FINAL, true, true>(X, Ly, nullptr, nullptr, nullptr, nullptr, st)));
+            else GSI_TRY((abl_layers<AB_FINAL, true, false>(X, Ly, nullptr, nullptr, nullptr, nullptr, st)));
             C.prof->end();
             Counters hc;
             GSI_CUDA(d2h(S, &hc, ctr, sizeof(hc), st));
@@ -3875,11 +4175,11 @@ gsi_status run_ablation(QueryCtx &C, int32_t *M, unsigned long long nM) {
         C.prof->begin(GSI_K_JOIN, two ? GSI_V_TWO_STEP : GSI_V_ABLATION);
         S.variant_launches[two ? GSI_V_TWO_STEP : GSI_V_ABLATION]++;
         if (two) {   // pass 1: count only
-            if (naive) GSI_ABL_JOIN(AB_COUNT, true, true, nullptr, nullptr, cnt, nullptr);
-            else GSI_ABL_JOIN(AB_COUNT, true, false, nullptr, nullptr, cnt, nullptr);
+            if (naive) GSI_TRY((abl_layers<AB_COUNT, true, true>(X, Ly, nullptr, nullptr, cnt, nullptr, st)));
+            else GSI_TRY((abl_layers<AB_COUNT, true, false>(X, Ly, nullptr, nullptr, cnt, nullptr, st)));
         } else {     // Prealloc: survivors into the row's buffer
-            if (naive) GSI_ABL_JOIN(AB_PC, true, true, F, gbuf, cnt, nullptr);
-            else GSI_ABL_JOIN(AB_PC, true, false, F, gbuf, cnt, nullptr);
+            if (naive) GSI_TRY((abl_layers<AB_PC, true, true>(X, Ly, F, gbuf, cnt, nullptr, st)));
+            else GSI_TRY((abl_layers<AB_PC, true, false>(X, Ly, F, gbuf, cnt, nullptr, st)));
         }
         C.prof->end();
         GSI_TRY(scan(cnt, nM, &G));
@@ -3892,17 +4192,16 @@ gsi_status run_ablation(QueryCtx &C, int32_t *M, unsigned long long nM) {
         C.prof->begin(GSI_K_JOIN, GSI_V_ABLATION);
         S.variant_launches[GSI_V_ABLATION]++;
         if (two) {   // pass 2: join again, write the rows
-            if (naive && wc) GSI_ABL_JOIN(AB_WRITE, true, true, G, nullptr, nullptr, out);
-            else if (naive) GSI_ABL_JOIN(AB_WRITE, false, true, G, nullptr, nullptr, out);
-            else if (wc) GSI_ABL_JOIN(AB_WRITE, true, false, G, nullptr, nullptr, out);
-            else GSI_ABL_JOIN(AB_WRITE, false, false, G, nullptr, nullptr, out);
+            if (naive && wc) GSI_TRY((abl_layers<AB_WRITE, true, true>(X, Ly, G, nullptr, nullptr, out, st)));
+            else if (naive) GSI_TRY((abl_layers<AB_WRITE, false, true>(X, Ly, G, nullptr, nullptr, out, st)));
+            else if (wc) GSI_TRY((abl_layers<AB_WRITE, true, false>(X, Ly, G, nullptr, nullptr, out, st)));
+            else GSI_TRY((abl_layers<AB_WRITE, false, false>(X, Ly, G, nullptr, nullptr, out, st)));
         } else {     // Combine: link the buffers into M'
             const unsigned long long items = wc ? nout * (unsigned long long)(t + 1) : nout;
             const unsigned lg = (unsigned)std::min<unsigned long long>(grid_for(items, kThreads), (unsigned long long)sms * 32);
             if (wc) k_abl_link<true><<<lg, kThreads, 0, st>>>(M, (long long)nM, F, G, gbuf, t, nout, out);
             else k_abl_link<false><<<lg, kThreads, 0, st>>>(M, (long long)nM, F, G, gbuf, t, nout, out);
         }
-#undef GSI_ABL_JOIN
         C.prof->end();
         M = out;
         nM = nout;

@@ -25,7 +25,7 @@ GSI_MAX_K = 32
 GSI_N_KCLASS = 8
 KCLASS = ["filter", "compact", "probe", "join", "link", "other", "r6", "r7"]
 GSI_N_KVARIANT = 20
-ABL_ENGINE, ABL_CR, ABL_TWO_STEP, ABL_NO_WCACHE, ABL_NAIVE_SO = 1, 2, 4, 8, 16
+ABL_ENGINE, ABL_CR, ABL_TWO_STEP, ABL_NO_WCACHE, ABL_NAIVE_SO, ABL_NO_LB, ABL_NO_DR = 1, 2, 4, 8, 16, 32, 64
 KVARIANT = ["join_next", "join_count", "join_table", "join_cahead", "count_fast", "next_lean", "cahead_warp",
             "cahead_lean", "final_lean", "final_fp", "filter_partition", "refilter", "probe_ahead", "small",
             "two_step", "ablation", "final_table", "surv_scan", "reserved18", "reserved19"]
@@ -74,7 +74,8 @@ class gsi_stats(ctypes.Structure):
                 ("d2h_bytes", U64), ("n_shared_lists", U32), ("ms_host_alloc", ctypes.c_float),
                 ("ms_host_sync", ctypes.c_float), ("count_ahead", I32), ("n_probe_ahead", U32),
                 ("variant_launches", U32 * GSI_N_KVARIANT), ("ms_variant", ctypes.c_float * GSI_N_KVARIANT),
-                ("alg_bytes_variant", ctypes.c_double * GSI_N_KVARIANT), ("small_aborted", I32)]
+                ("alg_bytes_variant", ctypes.c_double * GSI_N_KVARIANT), ("small_aborted", I32),
+                ("abl_layer_rows", U64 * 3)]
 
 
 _SIGS = {

@@ -568,12 +568,13 @@ def test_small_path_equals_regular_and_aborts_cleanly():
     assert r.count == cnt and r.fingerprint() == fp
 
 
-@pytest.mark.parametrize("ab", [1, 1 | 2, 1 | 4, 1 | 8, 1 | 16, 31])
+@pytest.mark.parametrize("ab", [1, 1 | 2, 1 | 4, 1 | 8, 1 | 16, 31, 1 | 32, 1 | 64, 1 | 32 | 64, 127])
 def test_ablation_engine_same_result(ab):
     """NEXT-3: the paper-style engine (warp per row, Alg. 3/4) with each join technique of
     Tables VI-VIII switched off — CR lookup instead of PCSR, two-step output instead of
     Prealloc-Combine, no write cache, naive set operation — gives the oracle's count and
-    fingerprint (same R)."""
+    fingerprint (same R); likewise without the 4-layer balance (32) or
+    the block duplicate removal (64) of NEXT-2."""
     g = W.chung_lu(20_000, 120_000, 2_000, nlv=8, nle=6, seed=97)
     graph = gsi.build(g)
     og = oracle.OracleGraph(g)
@@ -635,3 +636,28 @@ def test_table_writer_env_off_same_table(monkeypatch):
         monkeypatch.delenv("GSI_TABLE_NOLEAN")
         assert b.stats()["variants"].get("final_table", 0) == 0
         assert np.array_equal(a.table(), b.table()) and a.fingerprint() == b.fingerprint()
+
+
+@pytest.mark.parametrize("ab", [1, 1 | 4, 1 | 8, 1 | 16, 1 | 64])
+def test_ablation_balance_layers_on_hubs(ab, monkeypatch):
+    """NEXT-2, the 4-layer balance of the paper-style engine: with small
+    thresholds W1 / W2 the hub rows of a power-law graph go to the 8-CTA cluster kernel (row
+    staged once, read by the other CTAs through distributed shared memory, in-order compaction
+    placed by DSMEM count exchange) and the medium rows to the block kernel; count, fingerprint
+    and (two-step) the written rows give the oracle's result, and every layer ran."""
+    monkeypatch.setenv("GSI_ABL_W1", "96")
+    monkeypatch.setenv("GSI_ABL_W2", "24")
+    g = W.chung_lu(20_000, 160_000, 4_000, nlv=4, nle=3, seed=141)
+    graph = gsi.build(g)
+    og = oracle.OracleGraph(g)
+    qs = bounded_queries(g, og, lambda s: 3 + s % 4, range(14100, 14160), lo=100, hi=3_000_000, want=6)
+    assert len(qs) >= 4
+    layers = np.zeros(3, np.int64)
+    for q in qs:
+        cnt, fp, _ = oracle.match(og, q, table=False)
+        r = gsi.query(graph, q, ablation=ab)
+        assert r.count == cnt and r.fingerprint() == fp, (ab, r.count, cnt)
+        layers += np.array(r.stats()["abl_layer_rows"], np.int64)
+        r2 = gsi.query(graph, q, ablation=ab | 32)   # balance off: the same result
+        assert r2.count == cnt and r2.fingerprint() == fp
+    assert (layers > 0).all(), layers
