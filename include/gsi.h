@@ -78,7 +78,8 @@ enum { GSI_V_JOIN_NEXT = 0,       /* k_join<J_NEXT>: slot tiles, compacting (Com
        GSI_V_TWO_STEP = 14,       /* ablation: count pass of the two-step output               */
        GSI_V_ABLATION = 15,       /* ablation engine join launches (warp per row, paper design) */
        GSI_V_FINAL_TABLE = 16,    /* k_final_table: every final match written (table mode)     */
-       GSI_V_SURV_SCAN = 17 };    /* k_surv_scan: table-mode Combine offsets per row           */
+       GSI_V_SURV_SCAN = 17,      /* k_surv_scan: table-mode Combine offsets per row           */
+       GSI_V_FP_TERMS = 18 };     /* k_fp_terms: per-candidate fingerprint terms of a shared run */
 
 /* gsi_query_opts.ablation bits (NEXT-3: the paper's join-phase study, Tables VI-VIII):
  * any bit set runs the query on the paper-style engine (one warp per row of M, Alg. 3/4) with

@@ -419,6 +419,20 @@ struct gsi_prepared {
     }
 };
 
+namespace gsi {
+// vm.cu: a device table that grows in place on a reserved virtual address range.
+struct TableVM {
+    int device = 0, k = 1;
+    unsigned long long base = 0;
+    size_t reserved = 0, mapped = 0, gran = 0;
+    unsigned long long used = 0;                                      // rows appended so far
+    std::vector<std::pair<unsigned long long, size_t>> chunks;        // (handle, bytes)
+    static TableVM *create(int device, int k);   // nullptr: VMM unavailable
+    int32_t *append(unsigned long long rows);     // the next `rows` rows, mapped
+    ~TableVM();
+};
+}  // namespace gsi
+
 struct gsi_result {
     int device = 0;
     int k = 0;
@@ -427,8 +441,10 @@ struct gsi_result {
     int32_t *table = nullptr;        // device, count x k, query-id order
     uint64_t nrows = 0;
     bool has_table = false;
+    gsi::TableVM *vm = nullptr;      // owner of `table` when it grew in place
     gsi_stats stats;
     ~gsi_result() {
-        if (table) cudaFreeAsync(table, cudaStreamPerThread);
+        if (vm) delete vm;
+        else if (table) cudaFreeAsync(table, cudaStreamPerThread);
     }
 };

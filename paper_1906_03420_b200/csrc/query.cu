@@ -80,6 +80,9 @@ constexpr int kThreads = 256;
 #ifndef GSI_COUNT_LEAN
 #define GSI_COUNT_LEAN 1    // enumerating last level on shared runs: lean warp walk (0: slot tiles)
 #endif
+#ifndef GSI_FP_TERMS
+#define GSI_FP_TERMS 1      // enumerating last level: per-candidate fingerprint term table (0: compute)
+#endif
 #ifndef GSI_TABLE_LEAN
 #define GSI_TABLE_LEAN 1    // table-mode last level on shared runs: warp table kernel (0: slot tiles)
 #endif
@@ -1374,11 +1377,31 @@ __global__ void __launch_bounds__(kThreads, 4) k_cahead_lean(const int32_t *__re
 template <int NINJ>
 __global__ void __launch_bounds__(kThreads, 4) k_final_fp(const int32_t *__restrict__ M, long long r0, long long r1,
                                                           const Loc *__restrict__ loc, StepParams P, int qx,
-                                                          const int32_t *__restrict__ cip, Counters *ctr) {
+                                                          const int32_t *__restrict__ cip,
+                                                          const ulonglong2 *__restrict__ T, Counters *ctr) {
     const int lane = threadIdx.x & 31;
     const long long gw = (blockIdx.x * (long long)kThreads + threadIdx.x) >> 5;
     const long long nw = ((long long)gridDim.x * kThreads) >> 5;
     unsigned long long cnt = 0, h1 = 0, h2 = 0, act = 0;
+    // one match m || x, x = cip[p]: the subtraction test, then the two row hashes from the
+    // parent's summed terms (a1, a2) and x's terms (from T, or computed)
+    auto fp_match = [&](uint32_t p, const Inj<NINJ> &in, unsigned long long a1, unsigned long long a2) {
+        unsigned long long t1, t2;
+        if (T) {
+            if (NINJ > 0 && in.hit(__ldg(cip + p))) return;
+            const ulonglong2 tt = __ldg(T + p);
+            t1 = tt.x;
+            t2 = tt.y;
+        } else {
+            const int32_t x = __ldg(cip + p);
+            if (NINJ > 0 && in.hit(x)) return;
+            t1 = fp_term(kFpSeed1, qx, (uint32_t)x);
+            t2 = fp_term(kFpSeed2, qx, (uint32_t)x);
+        }
+        cnt++;
+        h1 += fp_mix(a1 + t1);
+        h2 ^= fp_mix(a2 + t2);
+    };
     for (long long base = r0 + gw * 32; base < r1; base += nw * 32) {
         const long long i = base + lane;
         const bool valid = i < r1;
@@ -1406,13 +1429,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_final_fp(const int32_t *__restr
         const uint32_t T = __shfl_sync(0xffffffffu, inc, 31);
         const uint32_t maxlen = __reduce_max_sync(0xffffffffu, L.len);
         if (maxlen * 16 <= T) {   // even runs: every lane walks its own row
-            for (uint32_t kk = 0; kk < L.len; kk++) {
-                const int32_t x = __ldg(cip + L.off + kk);
-                if (NINJ > 0 && inj.hit(x)) continue;
-                cnt++;
-                h1 += fp_mix(s1 + fp_term(kFpSeed1, qx, (uint32_t)x));
-                h2 ^= fp_mix(s2 + fp_term(kFpSeed2, qx, (uint32_t)x));
-            }
+            for (uint32_t kk = 0; kk < L.len; kk++) fp_match(L.off + kk, inj, s1, s2);
             continue;
         }
         uint32_t longs = __ballot_sync(0xffffffffu, L.len >= 32);
@@ -1422,13 +1439,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_final_fp(const int32_t *__restr
             const uint32_t off = __shfl_sync(0xffffffffu, L.off, r), len = __shfl_sync(0xffffffffu, L.len, r);
             const unsigned long long a1 = __shfl_sync(0xffffffffu, s1, r), a2 = __shfl_sync(0xffffffffu, s2, r);
             const Inj<NINJ> ri = inj.shfl(r);
-            for (uint32_t kk = lane; kk < len; kk += 32) {
-                const int32_t x = __ldg(cip + off + kk);
-                if (NINJ > 0 && ri.hit(x)) continue;
-                cnt++;
-                h1 += fp_mix(a1 + fp_term(kFpSeed1, qx, (uint32_t)x));
-                h2 ^= fp_mix(a2 + fp_term(kFpSeed2, qx, (uint32_t)x));
-            }
+            for (uint32_t kk = lane; kk < len; kk += 32) fp_match(off + kk, ri, a1, a2);
         }
         const uint32_t sl = L.len >= 32 ? 0u : L.len;   // the short rows: balanced walk
         inc = sl;
@@ -1452,11 +1463,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_final_fp(const int32_t *__restr
             const unsigned long long a1 = __shfl_sync(0xffffffffu, s1, o), a2 = __shfl_sync(0xffffffffu, s2, o);
             const Inj<NINJ> ri = inj.shfl(o);
             if (j >= T2) continue;
-            const int32_t x = __ldg(cip + pos);
-            if (NINJ > 0 && ri.hit(x)) continue;
-            cnt++;
-            h1 += fp_mix(a1 + fp_term(kFpSeed1, qx, (uint32_t)x));
-            h2 ^= fp_mix(a2 + fp_term(kFpSeed2, qx, (uint32_t)x));
+            fp_match(pos, ri, a1, a2);
         }
     }
     cnt = warp_sum_u64(cnt);
@@ -1842,6 +1849,20 @@ __global__ void __launch_bounds__(kThreads) k_probe_ahead(const int32_t *__restr
             }
             pa[p0 + q * stride] = r;
         }
+    }
+}
+
+// Fingerprint terms of every candidate of a shared run array (the last step's x = fci[p]):
+// T[p] = (fp_term(seed1, q, x), fp_term(seed2, q, x)), q = the query vertex the step adds.
+// The enumerating last level then reads 16 B per match (L2-resident: the shared runs are
+// re-read by many rows) instead of computing two splitmix finalisers per match (DESIGN.md §3
+// 'Fingerprint': a keyed term per column).
+__global__ void __launch_bounds__(kThreads) k_fp_terms(const int32_t *__restrict__ fci, const uint32_t *__restrict__ ntotal,
+                                                       int q, ulonglong2 *__restrict__ T) {
+    const uint32_t total = *ntotal;
+    for (uint32_t p = blockIdx.x * kThreads + threadIdx.x; p < total; p += gridDim.x * kThreads) {
+        const uint32_t x = (uint32_t)__ldg(fci + p);
+        T[p] = make_ulonglong2(fp_term(kFpSeed1, q, x), fp_term(kFpSeed2, q, x));
     }
 }
 
@@ -3204,8 +3225,10 @@ struct QueryCtx {
     bool capped = false;
     unsigned long long count = 0, fp1 = 0, fp2 = 0;
     std::vector<std::pair<int32_t *, unsigned long long>> pieces;   // final table pieces (device)
+    TableVM *tv = nullptr;                                           // the table, grown in place (vm.cu)
     std::vector<std::pair<uint32_t *, int32_t *>> filt;             // per step: (fpos, fci) or null
     std::vector<Loc *> pa;                                           // per step: probe-ahead table or null
+    std::vector<ulonglong2 *> fpt;                                   // per step: fingerprint term table or null
     std::vector<char> lean_off;                                      // per step: lean J_NEXT left too many holes
     // Zeroed once per query; every level launch takes a never-used slice for its counters and
     // look-back status words (saves a memset per level on the small-query critical path).
@@ -3217,6 +3240,29 @@ struct QueryCtx {
     std::vector<std::vector<int>> phys;
     std::vector<int> width;
 };
+
+// The next `rows` rows of the final table: in place at the end of the growing table (VMM), or
+// a separate piece concatenated at the end when VMM is unavailable.
+gsi_status table_rows(QueryCtx &C, unsigned long long rows, int32_t **dst) {
+    if (C.tv) {
+        *dst = C.tv->append(rows);
+        return *dst ? GSI_OK : GSI_ERR_OOM;
+    }
+    if (cudaMallocAsync(dst, 4ull * rows * C.q->k, C.st) != cudaSuccess) {
+        cudaGetLastError();
+        set_error("table of " + std::to_string(rows) + " rows does not fit in device memory");
+        return GSI_ERR_OOM;
+    }
+    C.pieces.push_back({*dst, rows});
+    return GSI_OK;
+}
+
+gsi_status table_put(QueryCtx &C, const int32_t *src, unsigned long long rows) {
+    int32_t *dst = nullptr;
+    GSI_TRY(table_rows(C, rows, &dst));
+    GSI_CUDA(cudaMemcpyAsync(dst, src, 4ull * rows * C.q->k, cudaMemcpyDeviceToDevice, C.st));
+    return GSI_OK;
+}
 
 // Columns of M a step reads: linking columns and (isomorphism) the subtraction columns, i.e.
 // the earlier columns with u's vertex label that are not linked (x in N(m[c],l) => x != m[c]).
@@ -3349,6 +3395,29 @@ gsi_status ensure_probe_ahead(QueryCtx &C, size_t si, const StepParams &P, const
     return GSI_OK;
 }
 
+// Fingerprint terms of step si's shared run array (k_fp_terms), once per query.
+gsi_status ensure_fp_terms(QueryCtx &C, size_t si) {
+    if (C.fpt.size() < C.steps.size()) C.fpt.assign(C.steps.size(), nullptr);
+    if (C.fpt[si]) return GSI_OK;
+    const gsi_graph *g = C.g;
+    const Step &s = C.steps[si];
+    const uint32_t lab = (uint32_t)s.lab[0];
+    const uint32_t lo = g->ci_lo[lab], hi = g->ci_lo[lab + 1];
+    ulonglong2 *T = nullptr;
+    GSI_TRY(C.A->get_big(&T, (unsigned long long)(hi - lo)));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
+    const unsigned grid = std::min<unsigned>(grid_for(hi - lo, kThreads), (unsigned)sms * 8);
+    C.prof->begin(GSI_K_OTHER, GSI_V_FP_TERMS);
+    C.S->variant_launches[GSI_V_FP_TERMS]++;
+    k_fp_terms<<<grid, kThreads, 0, C.st>>>(C.filt[si].second, C.filt[si].first + (hi - lo), s.u, T);
+    C.prof->end();
+    C.S->alg_bytes[GSI_K_OTHER] += 20.0 * (hi - lo);
+    C.S->alg_bytes_variant[GSI_V_FP_TERMS] += 20.0 * (hi - lo);
+    C.fpt[si] = T;
+    return GSI_OK;
+}
+
 bool shared_lists_allowed(const QueryCtx &C, const StepParams &P) {
     return GSI_PREFILTER_RATIO > 0 && !C.opts.no_shared_lists && C.opts.e0_mode == 0 && P.E == 1;
 }
@@ -3429,11 +3498,12 @@ gsi_status final_table(QueryCtx &C, size_t si, const int32_t *M, long long r0, l
     GSI_CUDA(sync_timed(S, st));
     if (total) {
         int32_t *piece = nullptr;
-        if (cudaMallocAsync(&piece, 4ull * total * k, st) != cudaSuccess) {
-            cudaGetLastError();
-            A.reset(mk);
-            set_error("table of " + std::to_string(total) + " rows does not fit in device memory");
-            return GSI_ERR_OOM;
+        {
+            const gsi_status rs = table_rows(C, total, &piece);
+            if (rs != GSI_OK) {
+                A.reset(mk);
+                return rs;
+            }
         }
         Counters *lctr = nullptr;
         GSI_TRY(A.get(&lctr, 1));
@@ -3465,7 +3535,6 @@ gsi_status final_table(QueryCtx &C, size_t si, const int32_t *M, long long r0, l
             C.fp1 += hc.fp1;
             C.fp2 ^= hc.fp2;
         }
-        C.pieces.push_back({piece, total});
     }
     const int t = C.steps[si].t;
     C.count += total;
@@ -3763,10 +3832,15 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
             const unsigned long long units = ((unsigned long long)(r_hi - r_lo) + 31) / 32;
             const unsigned wg = (unsigned)std::max<unsigned long long>(
                 1, std::min<unsigned long long>((units + 7) / 8, (unsigned long long)sms * 8));
+            const ulonglong2 *T = nullptr;
+            if (P.fp && GSI_FP_TERMS && !env_flag("GSI_FP_NOTERMS") && C.filt.size() > si && cip == C.filt[si].second) {
+                GSI_TRY(ensure_fp_terms(C, si));
+                T = C.fpt[si];
+            }
             if (P.fp && P.n_inj == 0)
-                k_final_fp<0><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, s.u, cip, lctr);
+                k_final_fp<0><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, s.u, cip, T, lctr);
             else if (P.fp)
-                k_final_fp<kLeanInj><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, s.u, cip, lctr);
+                k_final_fp<kLeanInj><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, s.u, cip, T, lctr);
             else if (P.n_inj == 0)
                 k_cahead_lean<0, true><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, P2, cip, g->groups, g->gpn, lctr);
             else
@@ -3865,10 +3939,7 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         }
         if (mode == J_TABLE) {
             if (nout) {
-                int32_t *piece = nullptr;
-                GSI_CUDA(cudaMallocAsync(&piece, 4ull * nout * C.q->k, st));
-                GSI_CUDA(cudaMemcpyAsync(piece, out, 4ull * nout * C.q->k, cudaMemcpyDeviceToDevice, st));
-                C.pieces.push_back({piece, nout});
+                rc = table_put(C, out, nout);
             }
             A.release(out);
         } else if (mode == J_NEXT) {
@@ -3988,10 +4059,11 @@ gsi_status run_small(QueryCtx &C, const int32_t *M1, bool &done) {
     C.fp1 = h.fp1;
     C.fp2 = h.fp2;
     if (plan.want_table && h.nout) {
-        int32_t *piece = nullptr;
-        GSI_CUDA(cudaMallocAsync(&piece, 4ull * h.nout * k, C.st));
-        GSI_CUDA(cudaMemcpyAsync(piece, table, 4ull * h.nout * k, cudaMemcpyDeviceToDevice, C.st));
-        C.pieces.push_back({piece, h.nout});
+        const gsi_status rs = table_put(C, table, h.nout);
+        if (rs != GSI_OK) {
+            A.reset(mk);
+            return rs;
+        }
     }
     A.reset(mk);
     done = true;
@@ -4256,6 +4328,9 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     C.st = st;
     C.A = &A;
     C.prof = &prof;
+    // the table grows in place (vm.cu); owned here until the result takes it
+    std::unique_ptr<TableVM> tv_guard(opts.want_table ? TableVM::create(g->device, k) : nullptr);
+    C.tv = tv_guard.get();
     C.S = &S;
     C.words = words;
 
@@ -4414,10 +4489,7 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
         C.fp1 = hc.fp1;
         C.fp2 = hc.fp2;
         if (opts.want_table && nM) {
-            int32_t *T = nullptr;
-            GSI_CUDA(cudaMallocAsync(&T, 4ull * nM, st));
-            GSI_CUDA(cudaMemcpyAsync(T, M, 4ull * nM, cudaMemcpyDeviceToDevice, st));
-            C.pieces.push_back({T, nM});
+            GSI_TRY(table_put(C, M, nM));
         }
     } else if (!empty) {
         // level-1 Prealloc (Alg. 4) on M_1 = C(pi_1)
@@ -4470,7 +4542,11 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     if (opts.want_table) {
         res->has_table = true;
         res->nrows = C.count;
-        if (C.pieces.size() == 1) {
+        if (C.tv) {   // grown in place: the result owns the mapping
+            res->table = C.tv->used ? (int32_t *)C.tv->base : nullptr;
+            res->vm = tv_guard.release();
+            C.tv = nullptr;
+        } else if (C.pieces.size() == 1) {
             res->table = C.pieces[0].first;
         } else if (!C.pieces.empty()) {
             GSI_CUDA(cudaMallocAsync(&res->table, 4ull * C.count * k, st));

@@ -28,7 +28,7 @@ GSI_N_KVARIANT = 20
 ABL_ENGINE, ABL_CR, ABL_TWO_STEP, ABL_NO_WCACHE, ABL_NAIVE_SO, ABL_NO_LB, ABL_NO_DR = 1, 2, 4, 8, 16, 32, 64
 KVARIANT = ["join_next", "join_count", "join_table", "join_cahead", "count_fast", "next_lean", "cahead_warp",
             "cahead_lean", "final_lean", "final_fp", "filter_partition", "refilter", "probe_ahead", "small",
-            "two_step", "ablation", "final_table", "surv_scan", "reserved18", "reserved19"]
+            "two_step", "ablation", "final_table", "surv_scan", "fp_terms", "reserved19"]
 STATUS = {0: "GSI_OK", -1: "GSI_ERR_INVALID_ARG", -2: "GSI_ERR_VERTEX_RANGE", -3: "GSI_ERR_LABEL_RANGE",
           -4: "GSI_ERR_SELF_LOOP", -5: "GSI_ERR_DUPLICATE_EDGE", -6: "GSI_ERR_QUERY_DISCONNECTED",
           -7: "GSI_ERR_QUERY_TOO_LARGE", -8: "GSI_ERR_OOM", -9: "GSI_ERR_TIMEOUT", -10: "GSI_ERR_CUDA",
