@@ -601,7 +601,7 @@ def test_table_writer_on_shared_runs():
     g = W.chung_lu(6000, 40000, 600, nlv=2, nle=3, seed=131)
     graph = gsi.build(g)
     og = oracle.OracleGraph(g)
-    qs = bounded_queries(g, og, lambda s: 4 + s % 5, range(13100, 13160), lo=50, hi=2_000_000, want=6)
+    qs = bounded_queries(g, og, lambda s: 4 + s % 5, range(13100, 13160), lo=50, hi=300_000, want=5)
     assert len(qs) >= 4
     used = 0
     for q in qs:
@@ -627,7 +627,7 @@ def test_table_writer_env_off_same_table(monkeypatch):
     g = W.chung_lu(6000, 40000, 600, nlv=2, nle=3, seed=132)
     graph = gsi.build(g)
     og = oracle.OracleGraph(g)
-    qs = bounded_queries(g, og, 6, range(13200, 13240), lo=50, hi=2_000_000, want=3)
+    qs = bounded_queries(g, og, 6, range(13200, 13240), lo=50, hi=300_000, want=3)
     assert qs
     for q in qs:
         a = gsi.query(graph, q, want_table=True, force_paths=1, small=False)

@@ -24,7 +24,9 @@ VARIANTS = [("k_join<2>", "join_next"), ("k_join<0>", "join_count"), ("k_join<1>
             ("k_cahead_lean<1, 1>", "final_lean"), ("k_final_fp", "final_fp"),
             ("k_filter_partition", "filter_partition"), ("k_refilter", "refilter"),
             ("k_probe_ahead", "probe_ahead"), ("k_small", "small"), ("k_filter(", "filter"),
-            ("k_fused_cahead", "fused_cahead")]
+            ("k_fused_cahead", "fused_cahead"), ("k_final_table", "final_table"), ("k_surv_scan", "surv_scan"),
+            ("k_fp_terms", "fp_terms"), ("k_abl_heavy", "abl_heavy"), ("k_abl_join", "ablation"),
+            ("k_filter_ml", "filter_ml")]
 
 
 def variant_of(name: str) -> str:
