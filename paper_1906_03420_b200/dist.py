@@ -51,17 +51,25 @@ def allreduce_counts(counts: torch.Tensor) -> torch.Tensor:
     return counts
 
 
-def gather_tables(local: np.ndarray, k: int, dst: int = 0, device: str = "cpu") -> Optional[np.ndarray]:
-    """Concatenate the rank-local tables on `dst` in rank order (None elsewhere)."""
+def gather_tables(local, k: int, dst: int = 0, device: Optional[str] = None) -> Optional[np.ndarray]:
+    """Concatenate the rank-local tables on `dst` in rank order (None elsewhere).  `local` is a
+    numpy array or a torch tensor (a device-resident result table stays on the device: the
+    gather then runs over NCCL with no host staging).  device=None: CUDA under NCCL, else CPU."""
+    if device is None:
+        device = f"cuda:{torch.cuda.current_device()}" if dist.get_backend() == "nccl" else "cpu"
     ws, rank = dist.get_world_size(), dist.get_rank()
-    n = torch.tensor([len(local)], dtype=torch.int64, device=device)
+    if isinstance(local, torch.Tensor):
+        loc_t = local.to(device=device, dtype=torch.int32).reshape(-1, k)
+    else:
+        loc_t = torch.as_tensor(np.ascontiguousarray(local, dtype=np.int32).reshape(-1, k)).to(device)
+    n = torch.tensor([loc_t.shape[0]], dtype=torch.int64, device=device)
     sizes = [torch.zeros(1, dtype=torch.int64, device=device) for _ in range(ws)]
     dist.all_gather(sizes, n)
     sizes = [int(s.item()) for s in sizes]
     mx = max(sizes) if sizes else 0
     buf = torch.zeros((max(mx, 1), k), dtype=torch.int32, device=device)
-    if len(local):
-        buf[: len(local)] = torch.as_tensor(np.ascontiguousarray(local, dtype=np.int32)).to(device)
+    if loc_t.shape[0]:
+        buf[: loc_t.shape[0]] = loc_t
     outs = [torch.zeros_like(buf) for _ in range(ws)] if rank == dst else None
     if ws == 1:
         outs = [buf]
