@@ -416,35 +416,67 @@ def run_gsi(args):
         ms_v += np.array(s["ms_variant"])
         bytes_v += np.array(s["alg_bytes_variant"])
         launches_v += np.array(s["variant_launches"])
+    items_v = np.zeros(nv)
+    for s in pstats:
+        items_v += np.array(s["items_variant"], dtype=np.float64)
     dom = int(np.argmax(ms_v))
     dname = gsi.KVARIANT[dom]
     peak, peak_src = load_peaks()
-    achieved = (bytes_v[dom] / (ms_v[dom] / 1e3)) / 1e9 if ms_v[dom] > 0 else 0.0
-    # DRAM traffic of the dominant kernel from the committed ncu capture of this workload
-    # (dram__bytes_read.sum + dram__bytes_write.sum per launch; profiles/ncu_traffic.json
-    # names the capture, tools/ncu_traffic.py writes it)
-    traffic, traffic_src, ncu_frac = None, None, None
+    clk_mhz = clk.summary().get("sm_mhz") or 1965.0
+    # ncu evidence of this workload (profiles/ncu_traffic.json, tools/ncu_traffic.py): DRAM bytes
+    # per launch, and the ALU-pipe activity of the k_final_fp capture
+    tt_all = {}
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
-        tt = json.load(open(tp)).get(args.config, {}).get(dname)
-        if tt is not None:
-            traffic, traffic_src = tt.get("dram_bytes_per_launch"), tt.get("source")
-            ncu_frac = tt.get("dram_frac")
-    roofline = {"bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-                "ncu_dram_frac": ncu_frac,
-                "alg_bytes_per_launch": float(bytes_v[dom] / max(launches_v[dom], 1)),
-                "ms_per_launch": float(ms_v[dom] / max(launches_v[dom], 1)), "peak_source": peak_src,
-                "share_of_step": float(ms_v[dom] / max(ms_k.sum(), 1e-9)),
-                "per_variant": {gsi.KVARIANT[i]: {"ms": float(ms_v[i]), "launches": int(launches_v[i]),
-                                                  "alg_GB": float(bytes_v[i] / 1e9),
-                                                  "frac": float(bytes_v[i] / (ms_v[i] / 1e3) / 1e9 / peak)}
-                                for i in range(nv) if launches_v[i]},
-                "per_class_ms": {gsi.KCLASS[i]: float(ms_k[i]) for i in range(6)},
-                "model": "algorithmic bytes = what the kernel must move at least once: rows it extends "
-                         "(row, loc, F), candidates streamed from ci (shared N(v,l0)∩C(u) runs are L2-"
-                         "resident, not charged per slot), one 32 B PCSR sector + fpos per lookup, every "
-                         "byte written (DESIGN.md §6)"}
+        tt_all = json.load(open(tp)).get(args.config, {})
+
+    def hbm_entry(i):
+        nm = gsi.KVARIANT[i]
+        ach = (bytes_v[i] / (ms_v[i] / 1e3)) / 1e9 if ms_v[i] > 0 else 0.0
+        tt = tt_all.get(nm, {})
+        return {"bound": "hbm", "kernel": nm, "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "traffic": tt.get("dram_bytes_per_launch"), "traffic_source": tt.get("source"),
+                "ncu_dram_frac": tt.get("dram_frac"),
+                "alg_bytes_per_launch": float(bytes_v[i] / max(launches_v[i], 1)),
+                "ms_per_launch": float(ms_v[i] / max(launches_v[i], 1)), "peak_source": peak_src,
+                "share_of_step": float(ms_v[i] / max(ms_k.sum(), 1e-9))}
+
+    if dname == "final_fp":
+        # integer-ALU bound: per match the fingerprint spec needs two splitmix
+        # finalisers and four 64-bit add/xor combines; on the 32-bit ALU pipe (IADD3 / LOP3 /
+        # SHF; the multiplies run on the FMA pipe) that is FP_ALU_OPS lane-ops per match.
+        # Peak = 148 SMs x 4 SMSPs x 16 lanes/clk (ALU pipe, rt = 2) x the SM clock under load.
+        FP_ALU_OPS = 36
+        ops = items_v[dom] * FP_ALU_OPS
+        ach = ops / (ms_v[dom] / 1e3) / 1e9
+        pk = 148 * 4 * 16 * clk_mhz * 1e6 / 1e9
+        tt = tt_all.get(dname, {})
+        roofline = {"bound": "alu", "kernel": dname, "achieved": ach, "peak": pk, "unit": "Gop/s",
+                    "frac": ach / pk, "traffic": tt.get("dram_bytes_per_launch"),
+                    "traffic_source": tt.get("source"), "ncu_alu_pipe_active": tt.get("alu_pipe_active"),
+                    "ncu_issue_active": tt.get("issue_active"),
+                    "matches_per_launch": float(items_v[dom] / max(launches_v[dom], 1)),
+                    "ms_per_launch": float(ms_v[dom] / max(launches_v[dom], 1)),
+                    "peak_source": f"derived: 148 SMs x 4 SMSPs x 16 ALU lanes/clk x {clk_mhz:.0f} MHz "
+                                   "(B300_MICROARCH.md pipe rates; B200_PROFILING.md SM count/clock)",
+                    "ops_per_match": FP_ALU_OPS,
+                    "share_of_step": float(ms_v[dom] / max(ms_k.sum(), 1e-9))}
+    else:
+        roofline = hbm_entry(dom)
+    # the join-class kernels that move HBM data in this step (M_{t+1} producers, table writer)
+    hbm_kernels = {gsi.KVARIANT[i]: hbm_entry(i) for i in range(nv)
+                   if launches_v[i] and gsi.KVARIANT[i] in ("next_lean", "join_next", "final_table", "join_table")}
+    roofline.update({
+        "per_variant": {gsi.KVARIANT[i]: {"ms": float(ms_v[i]), "launches": int(launches_v[i]),
+                                          "alg_GB": float(bytes_v[i] / 1e9), "items": int(items_v[i]),
+                                          "frac": float(bytes_v[i] / (ms_v[i] / 1e3) / 1e9 / peak) if ms_v[i] else 0.0}
+                        for i in range(nv) if launches_v[i]},
+        "hbm_kernels": hbm_kernels,
+        "per_class_ms": {gsi.KCLASS[i]: float(ms_k[i]) for i in range(6)},
+        "model": "hbm kernels: algorithmic bytes = what the kernel must move at least once: rows it extends "
+                 "(row, loc, F), candidates streamed from ci (shared N(v,l0)∩C(u) runs are L2-resident, not "
+                 "charged per slot), one 32 B PCSR sector + fpos per lookup, every byte written; alu: ALU-pipe "
+                 "lane-ops of the fingerprint spec per match (DESIGN.md §6)"})
 
     # ---- multi-GPU balance, emulated on this GPU: each rank's shard run alone -------------
     balance = None

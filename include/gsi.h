@@ -320,6 +320,8 @@ typedef struct {
     int32_t small_aborted;            /* the small-query kernel stopped at this level (0: not)  */
     uint64_t abl_layer_rows[3];       /* ablation engine: rows per balance layer (warp / block /
                                          8-CTA cluster), summed over levels                      */
+    uint64_t items_variant[GSI_N_KVARIANT]; /* per kernel variant: matches it produced (last
+                                         level / count-ahead) or rows it stored (J_NEXT)          */
 } gsi_stats;
 
 gsi_status gsi_result_count(const gsi_result *r, uint64_t *count);

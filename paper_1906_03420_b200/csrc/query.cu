@@ -2833,11 +2833,15 @@ struct Prof {
         cudaEventCreate(&r.a);
         cudaEventCreate(&r.b);
         cudaEventRecord(r.a, st);
+        open_.push_back(recs.size());
         recs.push_back(r);
     }
-    void end() {
-        if (on && !recs.empty()) cudaEventRecord(recs.back().b, st);
+    void end() {   // closes the innermost open begin() (launches may nest a helper launch)
+        if (!on || open_.empty()) return;
+        cudaEventRecord(recs[open_.back()].b, st);
+        open_.pop_back();
     }
+    std::vector<size_t> open_;
     cudaEvent_t base = nullptr;
     double host_base = 0;
     std::vector<double> host_t;   // host time (ms since base) of every begin(), GSI_TRACE
@@ -2871,11 +2875,14 @@ struct Prof {
             if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
                 s->ms_kernel[r.cls] += ms;
                 if (r.var >= 0) s->ms_variant[r.var] += ms;
+            } else {
+                cudaGetLastError();   // an unrecorded end event must not poison later calls
             }
             cudaEventDestroy(r.a);
             cudaEventDestroy(r.b);
         }
         recs.clear();
+        open_.clear();
     }
     ~Prof() {
         for (auto &r : recs) {
@@ -3527,6 +3534,7 @@ gsi_status final_table(QueryCtx &C, size_t si, const int32_t *M, long long r0, l
         // algorithmic bytes: the rows it extends (row + loc + O) and every byte it writes
         const double jb = (4.0 * P.t + 16.0) * (double)nrows + 4.0 * k * (double)total;
         S.alg_bytes_variant[GSI_V_FINAL_TABLE] += jb;
+        S.items_variant[GSI_V_FINAL_TABLE] += total;
         S.alg_bytes[GSI_K_JOIN] += jb;
         if (P.fp) {
             Counters hc;
@@ -3798,6 +3806,13 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
             S.variant_launches[v]++;
             var = v;
         }
+        // the enumerating last level's fingerprint terms (built once per query, before the launch)
+        const ulonglong2 *fpT = nullptr;
+        if (final_lean && P.fp && GSI_FP_TERMS && !env_flag("GSI_FP_NOTERMS") && C.filt.size() > si &&
+            cip == C.filt[si].second) {
+            GSI_TRY(ensure_fp_terms(C, si));
+            fpT = C.fpt[si];
+        }
         prof.begin(GSI_K_JOIN, var);
         if (lean_next) {
             int sms = 148;
@@ -3832,15 +3847,10 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
             const unsigned long long units = ((unsigned long long)(r_hi - r_lo) + 31) / 32;
             const unsigned wg = (unsigned)std::max<unsigned long long>(
                 1, std::min<unsigned long long>((units + 7) / 8, (unsigned long long)sms * 8));
-            const ulonglong2 *T = nullptr;
-            if (P.fp && GSI_FP_TERMS && !env_flag("GSI_FP_NOTERMS") && C.filt.size() > si && cip == C.filt[si].second) {
-                GSI_TRY(ensure_fp_terms(C, si));
-                T = C.fpt[si];
-            }
             if (P.fp && P.n_inj == 0)
-                k_final_fp<0><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, s.u, cip, T, lctr);
+                k_final_fp<0><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, s.u, cip, fpT, lctr);
             else if (P.fp)
-                k_final_fp<kLeanInj><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, s.u, cip, T, lctr);
+                k_final_fp<kLeanInj><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, s.u, cip, fpT, lctr);
             else if (P.n_inj == 0)
                 k_cahead_lean<0, true><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, P2, cip, g->groups, g->gpn, lctr);
             else
@@ -3920,6 +3930,9 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
         }
         if (E > 1) jb += 8.0 * rows_in * (E - 1);   // the other linking lists' locate entries
         S.alg_bytes_variant[var] += jb;
+        // items: matches produced at the last level (or counted by the count-ahead), rows
+        // stored by a J_NEXT level
+        S.items_variant[var] += (mode == J_COUNT || mode == J_CAHEAD || mode == J_TABLE) ? (last ? nout : hc.count) : nout;
         if (mode == J_NEXT) S.rows[t] += hc.count;   // |M_{t+1}|: every survivor, stored or not
         if (mode == J_CAHEAD) {                        // survivors = |M_{t+1}|, counted = |M_{t+2}|
             S.rows[t] += hc.total;

@@ -75,7 +75,7 @@ class gsi_stats(ctypes.Structure):
                 ("ms_host_sync", ctypes.c_float), ("count_ahead", I32), ("n_probe_ahead", U32),
                 ("variant_launches", U32 * GSI_N_KVARIANT), ("ms_variant", ctypes.c_float * GSI_N_KVARIANT),
                 ("alg_bytes_variant", ctypes.c_double * GSI_N_KVARIANT), ("small_aborted", I32),
-                ("abl_layer_rows", U64 * 3)]
+                ("abl_layer_rows", U64 * 3), ("items_variant", U64 * GSI_N_KVARIANT)]
 
 
 _SIGS = {

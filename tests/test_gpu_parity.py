@@ -598,7 +598,7 @@ def test_table_writer_on_shared_runs():
     offsets in closed form per row, every match written straight into the result) gives the
     oracle's sorted table, in the order-preserving pi order, with and without the fingerprint
     and sharded; the slot-tiled J_TABLE kernel gives the same table."""
-    g = W.chung_lu(6000, 40000, 600, nlv=2, nle=3, seed=131)
+    g = W.chung_lu(6000, 40000, 600, nlv=3, nle=6, seed=131)
     graph = gsi.build(g)
     og = oracle.OracleGraph(g)
     qs = bounded_queries(g, og, lambda s: 4 + s % 5, range(13100, 13160), lo=50, hi=300_000, want=5)
@@ -624,7 +624,7 @@ def test_table_writer_on_shared_runs():
 def test_table_writer_env_off_same_table(monkeypatch):
     """GSI_TABLE_NOLEAN=1 sends the table level back to the slot-tiled k_join<J_TABLE>: the
     same rows in the same order."""
-    g = W.chung_lu(6000, 40000, 600, nlv=2, nle=3, seed=132)
+    g = W.chung_lu(6000, 40000, 600, nlv=3, nle=6, seed=132)
     graph = gsi.build(g)
     og = oracle.OracleGraph(g)
     qs = bounded_queries(g, og, 6, range(13200, 13240), lo=50, hi=300_000, want=3)
