@@ -1399,8 +1399,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_final_fp(const int32_t *__restr
             t2 = fp_term(kFpSeed2, qx, (uint32_t)x);
         }
         cnt++;
-        h1 += fp_mix(a1 + t1);
-        h2 ^= fp_mix(a2 + t2);
+        h1 += fp_mix_pre(a1 + t1);   // a1, a2 carry fp_mix's leading constant (added per row)
+        h2 ^= fp_mix_pre(a2 + t2);
     };
     for (long long base = r0 + gw * 32; base < r1; base += nw * 32) {
         const long long i = base + lane;
@@ -1410,7 +1410,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_final_fp(const int32_t *__restr
         Inj<NINJ> inj;
         inj.load(row, P, valid && L.len);
         act += (valid && L.len) ? 1u : 0u;
-        unsigned long long s1 = 0, s2 = 0;   // the parent row's terms (every column but x)
+        unsigned long long s1 = kFpMixAdd, s2 = kFpMixAdd;   // the parent row's terms (every column but x)
         if (valid && L.len) {
             for (int q = 0; q < P.k; q++) {
                 const int col = P.pos_of_q[q];
