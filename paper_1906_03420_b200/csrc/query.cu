@@ -80,6 +80,9 @@ constexpr int kThreads = 256;
 #ifndef GSI_COUNT_LEAN
 #define GSI_COUNT_LEAN 1    // enumerating last level on shared runs: lean warp walk (0: slot tiles)
 #endif
+#ifndef GSI_NEXT_STAGE
+#define GSI_NEXT_STAGE 1    // k_next_lean: stage a batch's rows in shared memory, one coalesced store run
+#endif
 #ifndef GSI_FP_TERMS
 #define GSI_FP_TERMS 1      // enumerating last level: per-candidate fingerprint term table (0: compute)
 #endif
@@ -1632,6 +1635,12 @@ __global__ void __launch_bounds__(kThreads, 4) k_next_lean(const int32_t *__rest
     const long long r0 = rowmap[0], r1 = (long long)rowmap[1] + 1;
     const int W = P.out_w;
     const bool rowN = P2.col[0] < P.t;   // the next step's run is per row
+#if GSI_NEXT_STAGE
+    // the 32 slots of a batch are 32 consecutive Prealloc slots: their rows are staged here
+    // and stored as one coalesced run (write cache); hole rows are masked out
+    __shared__ int32_t nstage[kThreads / 32][32 * GSI_MAX_K];
+    int32_t *sw = nstage[threadIdx.x >> 5];
+#endif
     unsigned long long surv = 0, kept = 0, nlen = 0;
     for (long long base = r0 + gw * 32; base < r1; base += nw * 32) {
         const long long i = base + lane;
@@ -1676,10 +1685,15 @@ __global__ void __launch_bounds__(kThreads, 4) k_next_lean(const int32_t *__rest
             Loc N0;
             N0.off = rowN ? __shfl_sync(0xffffffffu, RN.off, o) : 0u;
             N0.len = rowN ? __shfl_sync(0xffffffffu, RN.len, o) : 0u;
+#if GSI_NEXT_STAGE
+            const bool act = j < T;
+#else
             if (j >= T) continue;
+            const bool act = true;
+#endif
             const unsigned long long ro = (unsigned long long)(base + o);
-            const int32_t x = __ldg(cip + pos);
-            bool keep = P.prefiltered || in_bitmap(cu_bitmap, x);
+            const int32_t x = act ? __ldg(cip + pos) : -1;
+            bool keep = act && (P.prefiltered || in_bitmap(cu_bitmap, x));
             if (NINJ > 0) keep &= x != ri;
             if (keep) {
                 surv++;
@@ -1698,7 +1712,27 @@ __global__ void __launch_bounds__(kThreads, 4) k_next_lean(const int32_t *__rest
                 keep = N0.len > 0;   // a row with an empty next buffer is counted, never stored
             }
             const unsigned long long lo = slot - c0;
-            loc2[lo] = keep ? N0 : Loc{0u, 0u};
+            if (act) loc2[lo] = keep ? N0 : Loc{0u, 0u};
+#if GSI_NEXT_STAGE
+            if (keep) {
+                kept++;
+                nlen += N0.len;
+                for (int c = 0; c < W; c++) {
+                    const int src = P.out_src[c];
+                    sw[lane * W + c] = src >= 0 ? __ldg(M + ro * (unsigned)P.t + src) : x;
+                }
+            }
+            const unsigned km = __ballot_sync(0xffffffffu, keep);
+            __syncwarp();
+            if (km) {
+                const unsigned long long lo0 = __shfl_sync(0xffffffffu, lo, 0);   // lane 0 is always active
+                int32_t *dst = out + lo0 * (unsigned)W;
+                const unsigned nr = min(32u, T - j0) * (unsigned)W;
+                for (unsigned e = lane; e < nr; e += 32)
+                    if ((km >> (e / W)) & 1u) dst[e] = sw[e];
+            }
+            __syncwarp();
+#else
             if (keep) {
                 kept++;
                 nlen += N0.len;
@@ -1708,6 +1742,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_next_lean(const int32_t *__rest
                     orow[c] = src >= 0 ? __ldg(M + ro * (unsigned)P.t + src) : x;
                 }
             }
+#endif
         }
     }
     surv = warp_sum_u64(surv);
