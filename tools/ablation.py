@@ -1,9 +1,11 @@
-"""NEXT-3: the paper's join-phase ablations on B200 (Tables VI-VIII).
+"""NEXT-3 / NEXT-2: the paper's join-phase ablations on B200 (Tables VI-VIII,
+L1467-1641; load balance and duplicate removal, §VI).
 
 Runs the bench-style random-walk queries of a workload through the paper-style engine
 (`gsi_query_opts.ablation`, one warp per row of M) with the techniques added one by one —
 GSI- (CR lookup, two-step output, naive set operation, no write cache), +DS (PCSR), +PC
-(Prealloc-Combine), +SO (GPU-friendly set operation), +WC (write cache) — and then the B200
+(Prealloc-Combine), +SO (GPU-friendly set operation), +WC (write cache), +LB (4-layer balance,
+heavy rows by 8-CTA clusters), +DR (block duplicate removal, Alg. 5) — and then the B200
 default path (fused per-level kernels) and its one-launch small-query path.  Every variant
 must give the same count and fingerprint (asserted).  Device time per query = the library's
 own ms_total with the host waiting on the result.
@@ -25,11 +27,14 @@ import workloads as W  # noqa: E402
 from paper_1906_03420_b200 import gsi  # noqa: E402
 
 E, CR, TWO, NOWC, NAIVE = gsi.ABL_ENGINE, gsi.ABL_CR, gsi.ABL_TWO_STEP, gsi.ABL_NO_WCACHE, gsi.ABL_NAIVE_SO
-LADDER = [("GSI- (CR, two-step, naive SO, no WC)", dict(ablation=E | CR | TWO | NAIVE | NOWC)),
-          ("+DS (PCSR)", dict(ablation=E | TWO | NAIVE | NOWC)),
-          ("+PC (Prealloc-Combine)", dict(ablation=E | NAIVE | NOWC)),
-          ("+SO (GPU-friendly set op)", dict(ablation=E | NOWC)),
-          ("+WC (write cache) = paper GSI", dict(ablation=E)),
+NOLB, NODR = gsi.ABL_NO_LB, gsi.ABL_NO_DR
+LADDER = [("GSI- (CR, two-step, naive SO, no WC, no LB, no DR)", dict(ablation=E | CR | TWO | NAIVE | NOWC | NOLB | NODR)),
+          ("+DS (PCSR)", dict(ablation=E | TWO | NAIVE | NOWC | NOLB | NODR)),
+          ("+PC (Prealloc-Combine)", dict(ablation=E | NAIVE | NOWC | NOLB | NODR)),
+          ("+SO (GPU-friendly set op)", dict(ablation=E | NOWC | NOLB | NODR)),
+          ("+WC (write cache)", dict(ablation=E | NOLB | NODR)),
+          ("+LB (4-layer balance: block / 8-CTA cluster rows)", dict(ablation=E | NODR)),
+          ("+DR (block duplicate removal) = paper GSI", dict(ablation=E)),
           ("B200 fused per-level path", dict(small=False)),
           ("B200 default (small-query path when it fits)", dict())]
 
