@@ -1533,20 +1533,41 @@ __global__ void __launch_bounds__(kThreads, 4) k_final_table(const int32_t *__re
                                                              const unsigned long long *__restrict__ O, StepParams P,
                                                              const int32_t *__restrict__ cip,
                                                              int32_t *__restrict__ out, Counters *ctr) {
-    __shared__ int32_t stage[kThreads / 32][32 * kTabMaxK];
-    const int lane = threadIdx.x & 31;
-    int32_t *sw = stage[threadIdx.x >> 5];
+    // per warp: the unit's 32 parent rows in query-id column order (x's column unused), and
+    // the batch's survivors (x, owner lane) after ballot compaction
+    __shared__ int32_t prow_s[kThreads / 32][32 * kTabMaxK];
+    __shared__ int32_t sx_s[kThreads / 32][32];
+    __shared__ int32_t so_s[kThreads / 32][32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    int32_t *prow = prow_s[wib], *sx = sx_s[wib], *so = so_s[wib];
     const long long gw = (blockIdx.x * (long long)kThreads + threadIdx.x) >> 5;
     const long long nw = ((long long)gridDim.x * kThreads) >> 5;
     const int k = P.k;
+    int qx = 0;   // the query vertex this level adds (its column is x)
+    for (int q = 0; q < k; q++)
+        if (P.pos_of_q[q] >= P.t) qx = q;
+    const unsigned inv_k = (65536u + (unsigned)k - 1u) / (unsigned)k;   // e / k = (e * inv_k) >> 16, e < 32k
     const unsigned lt = (1u << lane) - 1u;
     unsigned long long h1 = 0, h2 = 0;   // FP: the set fingerprint of the written rows
     for (long long base = r0 + gw * 32; base < r1; base += nw * 32) {
         const long long i = base + lane;
         const bool valid = i < r1;
         const Loc L = valid ? loc[(unsigned long long)i] : Loc{0u, 0u};
+        const int32_t *row = M + (unsigned long long)(valid ? i : r0) * (unsigned)P.t;
         Inj<NINJ> inj;
-        inj.load(M + (unsigned long long)(valid ? i : r0) * (unsigned)P.t, P, valid && L.len);
+        inj.load(row, P, valid && L.len);
+        unsigned long long s1 = kFpMixAdd, s2 = kFpMixAdd;
+        if (valid && L.len)
+            for (int q = 0; q < k; q++) {
+                const int col = P.pos_of_q[q];
+                if (col >= P.t) continue;
+                const int32_t v = __ldg(row + col);
+                prow[lane * k + q] = v;
+                if (FP) {
+                    s1 += fp_term(kFpSeed1, q, (uint32_t)v);
+                    s2 += fp_term(kFpSeed2, q, (uint32_t)v);
+                }
+            }
         unsigned long long ob = __shfl_sync(0xffffffffu, valid ? O[i - r0] : 0ull, 0);   // the unit's first output row
         uint32_t inc = L.len;
 #pragma unroll
@@ -1556,6 +1577,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_final_table(const int32_t *__re
         }
         const uint32_t excl = inc - L.len;
         const uint32_t T = __shfl_sync(0xffffffffu, inc, 31);
+        __syncwarp();
         for (uint32_t j0 = 0; j0 < T; j0 += 32) {
             const uint32_t j = j0 + lane;
             int o = 0;
@@ -1567,6 +1589,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_final_table(const int32_t *__re
             o &= 31;
             const uint32_t pos = __shfl_sync(0xffffffffu, L.off, o) + (j - __shfl_sync(0xffffffffu, excl, o));
             const Inj<NINJ> ri = inj.shfl(o);
+            unsigned long long a1 = 0, a2 = 0;
+            if (FP) {
+                a1 = __shfl_sync(0xffffffffu, s1, o);
+                a2 = __shfl_sync(0xffffffffu, s2, o);
+            }
             int32_t x = -1;
             bool keep = j < T;
             if (keep) {
@@ -1576,29 +1603,24 @@ __global__ void __launch_bounds__(kThreads, 4) k_final_table(const int32_t *__re
             const unsigned bal = __ballot_sync(0xffffffffu, keep);
             if (keep) {
                 const unsigned lp = __popc(bal & lt);
-                const int32_t *row = M + (unsigned long long)(base + o) * (unsigned)P.t;
-                unsigned long long a1 = 0, a2 = 0;
-                for (int q = 0; q < k; q++) {
-                    const int col = P.pos_of_q[q];
-                    const int32_t v = col < P.t ? __ldg(row + col) : x;
-                    sw[lp * k + q] = v;
-                    if (FP) {
-                        a1 += fp_term(kFpSeed1, q, (uint32_t)v);
-                        a2 += fp_term(kFpSeed2, q, (uint32_t)v);
-                    }
-                }
+                sx[lp] = x;
+                so[lp] = o;
                 if (FP) {
-                    h1 += fp_mix(a1);
-                    h2 ^= fp_mix(a2);
+                    h1 += fp_mix_pre(a1 + fp_term(kFpSeed1, qx, (uint32_t)x));
+                    h2 ^= fp_mix_pre(a2 + fp_term(kFpSeed2, qx, (uint32_t)x));
                 }
             }
             __syncwarp();
             const unsigned nk = (unsigned)__popc(bal) * (unsigned)k;
             int32_t *dst = out + ob * (unsigned long long)k;
-            for (unsigned e = lane; e < nk; e += 32) __stcs(dst + e, sw[e]);
+            for (unsigned e = lane; e < nk; e += 32) {
+                const unsigned r = (e * inv_k) >> 16, q = e - r * (unsigned)k;
+                __stcs(dst + e, (int)q == qx ? sx[r] : prow[so[r] * k + q]);
+            }
             __syncwarp();
             ob += __popc(bal);
         }
+        __syncwarp();   // prow is rewritten by the next unit
     }
     if (FP) {
         h1 = warp_sum_u64(h1);

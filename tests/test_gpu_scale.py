@@ -117,7 +117,8 @@ def check_query(e, q, roots=None, root=None, modes=("count", "enum", "fp", "tabl
 def root_sample(e, q, rng, n, must=None):
     """pi_1 from the GPU plan, then n roots of the oracle's C(pi_1) (plus the walk's own start
     for pi_1, which has >= 1 match)."""
-    root = gsi.query(e.graph, q, fingerprint=False).stats()["order"][0]
+    # the plan (pi_1) depends only on Q and the filter; one root keeps the probe query tiny
+    root = gsi.query(e.graph, q, fingerprint=False, roots=[int(q.embedding[0])]).stats()["order"][0]
     cu = e.oracle_cu(q, root)
     s = rng.choice(cu, min(n, len(cu)), replace=False) if len(cu) else np.zeros(0, np.int64)
     s = np.unique(np.append(s, q.embedding[root]))
