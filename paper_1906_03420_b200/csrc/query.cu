@@ -2439,6 +2439,10 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const SmallPla
                                                                   int32_t *__restrict__ table, SmallOut *out) {
     __shared__ unsigned long long sm[34];
     __shared__ unsigned long long cnt_s, h1_s, h2_s, el_s;
+    // F of a level with fewer than kSmallFsh rows stays in shared memory: the join's per-slot
+    // row search then costs shared-memory latency instead of a chain of L2 round trips
+    constexpr int kSmallFsh = 4097;
+    __shared__ unsigned long long Fs[kSmallFsh];
     const int tid = threadIdx.x, lane = tid & 31;
     const int k = plan.k;
     unsigned long long nM = *nM1p;
@@ -2488,7 +2492,10 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const SmallPla
             }
             unsigned long long agg;
             const unsigned long long ex = block_exclusive_scan(len0, sm, &agg);
-            if (i < nM) F[i] = run + ex;
+            if (i < nM) {
+                if (nM < kSmallFsh) Fs[i] = run + ex;
+                else F[i] = run + ex;
+            }
             run += agg;
             el = warp_sum_u64(el);
             if (lane == 0 && el) atomicAdd(&el_s, el);
@@ -2496,10 +2503,12 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const SmallPla
         const unsigned long long T = run;
         __syncthreads();
         if (tid == 0) {
-            F[nM] = T;
+            if (nM < kSmallFsh) Fs[nM] = T;
+            else F[nM] = T;
             out->gba[t] = T;
             out->elems[t] = el_s;
         }
+        const unsigned long long *FF = nM < kSmallFsh ? Fs : F;
         if (T > plan.slot_cap) {
             if (tid == 0) out->aborted = t;
             return;
@@ -2516,11 +2525,11 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const SmallPla
                 unsigned long long lo = 0, hi = nM;   // last row with F[row] <= sl
                 while (hi - lo > 1) {
                     const unsigned long long mid = (lo + hi) >> 1;
-                    if (F[mid] <= sl) lo = mid; else hi = mid;
+                    if (FF[mid] <= sl) lo = mid; else hi = mid;
                 }
                 row = lo;
                 const Loc L0 = loc[row * E];
-                x = __ldg(ci + L0.off + (uint32_t)(sl - F[row]));
+                x = __ldg(ci + L0.off + (uint32_t)(sl - FF[row]));
                 keep = (__ldg(S.cu + ((uint32_t)x >> 5)) >> (x & 31)) & 1u;              // x in C(u)
                 for (int c = 0; c < S.n_inj && keep; c++) keep = cur[row * t + S.inj_col[c]] != x;   // line 10
                 for (int e = 1; e < E && keep; e++) {                                       // line 13
