@@ -73,19 +73,14 @@ __host__ __device__ __forceinline__ uint64_t fp_mix(uint64_t z) {
 // Set fingerprint: the hash of a final row (query-id order) is
 #ifdef __CUDACC__
 // The same finaliser for the per-match hot loop (bit-identical: fp_mix(z) == fp_mix_pre(z +
-// kFpMixAdd)): the leading constant add is folded into the caller's per-row partial sum, and
-// the high word's right shift of each 64-bit xor-shift runs on the FMA pipe as IMAD.HI
-// (hi >> s == umulhi(hi, 2^(32-s))), which balances the integer ALU and FMA pipes.
+// kFpMixAdd)): the leading constant add is folded into the caller's per-row partial sum.
+// (Moving the high words' right shifts onto the FMA pipe as IMAD.HI was measured slower:
+// IMAD.HI issues at a lower rate and raised the instruction count — profiles/r2/r2e.)
 constexpr uint64_t kFpMixAdd = 0x9E3779B97F4A7C15ull;
-template <int S>
-__device__ __forceinline__ uint64_t fp_xsr(uint64_t z) {
-    const uint32_t lo = (uint32_t)z, hi = (uint32_t)(z >> 32);
-    return ((uint64_t)(hi ^ __umulhi(hi, 1u << (32 - S))) << 32) | (lo ^ __funnelshift_r(lo, hi, S));
-}
 __device__ __forceinline__ uint64_t fp_mix_pre(uint64_t z) {
-    z = fp_xsr<30>(z) * 0xBF58476D1CE4E5B9ull;
-    z = fp_xsr<27>(z) * 0x94D049BB133111EBull;
-    return fp_xsr<31>(z);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
 }
 #endif
 

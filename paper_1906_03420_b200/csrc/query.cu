@@ -1535,7 +1535,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_final_table(const int32_t *__re
                                                              int32_t *__restrict__ out, Counters *ctr) {
     // per warp: the unit's 32 parent rows in query-id column order (x's column unused), and
     // the batch's survivors (x, owner lane) after ballot compaction
-    __shared__ int32_t prow_s[kThreads / 32][32 * kTabMaxK];
+    __shared__ __align__(16) int32_t prow_s[kThreads / 32][32 * kTabMaxK];
     __shared__ int32_t sx_s[kThreads / 32][32];
     __shared__ int32_t so_s[kThreads / 32][32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -1611,11 +1611,27 @@ __global__ void __launch_bounds__(kThreads, 4) k_final_table(const int32_t *__re
                 }
             }
             __syncwarp();
-            const unsigned nk = (unsigned)__popc(bal) * (unsigned)k;
             int32_t *dst = out + ob * (unsigned long long)k;
-            for (unsigned e = lane; e < nk; e += 32) {
-                const unsigned r = (e * inv_k) >> 16, q = e - r * (unsigned)k;
-                __stcs(dst + e, (int)q == qx ? sx[r] : prow[so[r] * k + q]);
+            if ((k & 3) == 0) {   // rows of 16 B multiples: one 16 B store per 4 columns
+                const unsigned k4 = (unsigned)k >> 2, inv_k4 = (65536u + k4 - 1u) / k4;
+                const unsigned nf = (unsigned)__popc(bal) * k4;
+                int4 *dst4 = reinterpret_cast<int4 *>(dst);
+                for (unsigned f = lane; f < nf; f += 32) {
+                    const unsigned r = (f * inv_k4) >> 16, q0 = (f - r * k4) * 4u;
+                    int4 v = *reinterpret_cast<const int4 *>(prow + so[r] * k + q0);
+                    const int d = qx - (int)q0;
+                    if (d == 0) v.x = sx[r];
+                    else if (d == 1) v.y = sx[r];
+                    else if (d == 2) v.z = sx[r];
+                    else if (d == 3) v.w = sx[r];
+                    __stcs(dst4 + f, v);
+                }
+            } else {
+                const unsigned nk = (unsigned)__popc(bal) * (unsigned)k;
+                for (unsigned e = lane; e < nk; e += 32) {
+                    const unsigned r = (e * inv_k) >> 16, q = e - r * (unsigned)k;
+                    __stcs(dst + e, (int)q == qx ? sx[r] : prow[so[r] * k + q]);
+                }
             }
             __syncwarp();
             ob += __popc(bal);
@@ -1662,6 +1678,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_next_lean(const int32_t *__rest
     // and stored as one coalesced run (write cache); hole rows are masked out
     __shared__ int32_t nstage[kThreads / 32][32 * GSI_MAX_K];
     int32_t *sw = nstage[threadIdx.x >> 5];
+    const unsigned invW = (65536u + (unsigned)max(W, 1) - 1u) / (unsigned)max(W, 1);   // e / W, e < 32 W
 #endif
     unsigned long long surv = 0, kept = 0, nlen = 0;
     for (long long base = r0 + gw * 32; base < r1; base += nw * 32) {
@@ -1751,7 +1768,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_next_lean(const int32_t *__rest
                 int32_t *dst = out + lo0 * (unsigned)W;
                 const unsigned nr = min(32u, T - j0) * (unsigned)W;
                 for (unsigned e = lane; e < nr; e += 32)
-                    if ((km >> (e / W)) & 1u) dst[e] = sw[e];
+                    if ((km >> ((e * invW) >> 16)) & 1u) dst[e] = sw[e];
             }
             __syncwarp();
 #else
