@@ -220,33 +220,47 @@ __global__ void __launch_bounds__(kThreads, GSI_FILTER_MINB) k_filter(const uint
             // whose query word is 0 is contained in anything), and the planes are read one at a
             // time: the first one tested rejects most of a label class, so the later planes
             // are read only for the few survivors (sector traffic ~1/3 of reading every needed
-            // plane up front).
+            // plane up front).  Rounds run over the kFW words together: each round issues the
+            // next needed plane load of every word before testing any of them, so kFW
+            // independent loads are in flight per lane instead of one dependent chain per word.
+            uint32_t tested[kFW];
 #pragma unroll
-            for (int j = 0; j < kFW; j++) {
-                const long long v = (w0 + j) * 32 + lane;
-                uint32_t mm = mask[j], tested = 0;
-                while (mm) {
-                    uint32_t need = 0, t = mm;
+            for (int j = 0; j < kFW; j++) tested[j] = 0u;
+            for (int round = 0; round < kPlanes; round++) {
+                uint32_t pv[kFW];
+                int pls[kFW];
+                bool any = false;
+#pragma unroll
+                for (int j = 0; j < kFW; j++) {
+                    uint32_t need = 0, t = mask[j];
                     while (t) {
                         const int u = __ffs(t) - 1;
                         t &= t - 1;
                         need |= qneed[u];
                     }
-                    need &= ~tested;
-                    if (!need) break;
-                    const int pl = __ffs(need) - 1;
-                    tested |= 1u << pl;
+                    need &= ~tested[j];
+                    pls[j] = need ? __ffs(need) - 1 : -1;
+                    pv[j] = 0u;
+                    if (pls[j] >= 0) {
+                        const long long v = (w0 + j) * 32 + lane;
+                        pv[j] = __ldcs(sig + (long long)pls[j] * n + v);
+                        any = true;
+                    }
+                }
+                if (!__any_sync(0xffffffffu, any)) break;
+#pragma unroll
+                for (int j = 0; j < kFW; j++) {
+                    if (pls[j] < 0) continue;
+                    tested[j] |= 1u << pls[j];
                     plane_words++;
-                    const uint32_t pv = __ldcs(sig + (long long)pl * n + v);
-                    t = mm;
+                    uint32_t t = mask[j];
                     while (t) {
                         const int u = __ffs(t) - 1;
                         t &= t - 1;
-                        const uint32_t sq = qs[u * kPlanes + pl];
-                        if ((pv & sq) != sq) mm &= ~(1u << u);   // S(v)&S(u)=S(u) fails on this plane
+                        const uint32_t sq = qs[u * kPlanes + pls[j]];
+                        if ((pv[j] & sq) != sq) mask[j] &= ~(1u << u);   // S(v)&S(u)=S(u) fails on this plane
                     }
                 }
-                mask[j] = mm;
             }
         }
         // lane u collects the kFW bitmap words of query vertex u (ballots only for the query
@@ -4391,6 +4405,7 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     const double t_start = now_ms();
     GSI_CUDA(cudaSetDevice(g->device));
     ensure_pool(g->device);
+    if (getenv("GSI_TRACE")) fprintf(stderr, "[host] pool %.3f ms\n", now_ms() - t_start);
     cudaStream_t st = opts.stream ? (cudaStream_t)opts.stream : cudaStreamPerThread;
     const int k = q->k;
     const long long n = g->n;
@@ -4435,7 +4450,10 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     if (!budget) {
         budget = (unsigned long long)(0.85 * (double)(available_bytes(g->device) + workspace_idle_bytes(g->device)));
     }
+    const bool htrace = getenv("GSI_TRACE") != nullptr;
+    if (htrace) fprintf(stderr, "[host] budget %.3f ms\n", now_ms() - t_start);
     A.init_workspace(g->device, budget);
+    if (htrace) fprintf(stderr, "[host] workspace %.3f ms\n", now_ms() - t_start);
     GSI_TRY(A.get(&C.ctr, 1));
     {
         constexpr unsigned long long kZWords = 1ull << 17;   // 1 MB
@@ -4447,6 +4465,7 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
         }
     }
     GSI_CUDA(cudaMemsetAsync(C.ctr, 0, sizeof(Counters), st));
+    if (htrace) fprintf(stderr, "[host] zeroed %.3f ms\n", now_ms() - t_start);
 
     // ---------------- filter (a3) ----------------
     uint32_t *bm = nullptr;
