@@ -94,7 +94,8 @@ def main():
     if a.record:
         p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         d = json.load(open(p)) if os.path.exists(p) else {}
-        d[a.config] = out
+        for v, e in out.items():   # merge: keep what other captures recorded for other variants
+            d.setdefault(a.config, {}).setdefault(v, {}).update(e)
         json.dump(d, open(p, "w"), indent=1)
 
 
