@@ -71,9 +71,6 @@ constexpr int kThreads = 256;
 #ifndef GSI_FILTER_MINB
 #define GSI_FILTER_MINB 4   // k_filter: resident blocks per SM the registers are sized for
 #endif
-#ifndef GSI_FILTER_FW
-#define GSI_FILTER_FW 8     // k_filter: bitmap words per warp per iteration
-#endif
 #ifndef GSI_NEXT_LEAN
 #define GSI_NEXT_LEAN 1     // lean warp-centric J_NEXT writing rows at their Prealloc slots (0: off)
 #endif
@@ -161,18 +158,39 @@ struct Counters {
 };
 
 // ---------------------------------------------------------------------- filter ------
+// One pass over the signature table (§III-A): per data vertex v, plane 0 (its label)
+// picks the query vertices u with L_V(u) = L_V(v) (A4: one hash probe, not k compares), then
+// S(v) & S(u) = S(u) is tested only on the planes where S(u) has a set bit (a plane whose
+// query word is 0 is contained in anything).  A warp takes FW bitmap words (32·FW vertices) per
+// iteration: the plane-0 loads of all FW words are issued together, then the vertices with a
+// label match — often a few percent of them — are compacted through a per-warp shared-memory
+// queue into ceil(matches / 32) dense columns, so the plane tests run on full lanes instead of
+// on the mostly idle lanes of FW sparse words.  The planes are tested in rounds: each round
+// issues the next needed plane load of every queued vertex before testing any of them (the
+// first plane tested rejects most of a label class; later planes are read for the survivors
+// only).  FW = 8 with streaming loads for large graphs; FW = 1 with cached loads for small
+// ones, whose signature table stays L2-resident and which need the extra warps.
+template <int FW>
 __global__ void __launch_bounds__(kThreads, GSI_FILTER_MINB) k_filter(const uint32_t *__restrict__ sig, long long n, int k,
                                                      const uint32_t *__restrict__ qsig, int label_only,
                                                      uint32_t *__restrict__ bitmaps, long long words,
                                                      unsigned long long *__restrict__ counts,
-                                                     Counters *__restrict__ ctr) {
-    static_assert(GSI_FILTER_FW % 4 == 0, "the bitmap store is 16 B vectors per query vertex");
+                                                     Counters *__restrict__ ctr,
+                                                     uint16_t *__restrict__ grp, long long grp_stride) {
+    // grp (optional): grp[u * grp_stride + g] = |C(u)| in bitmap words [g·FW, (g+1)·FW) — a
+    // summary the device-planned small path extracts M_1 = C(pi_1) from without a scan of
+    // the whole bitmap (a warp's FW words are always one whole group)
+    static_assert(FW == 1 || FW % 4 == 0, "the bitmap store is 16 B vectors per query vertex");
+    constexpr bool kStream = FW > 1;                 // large graphs: evict-first signature reads
     constexpr int kHT = 64;                          // label -> query-vertex mask, open addressing
+    constexpr int kWarps = kThreads / 32;
     __shared__ uint32_t qs[GSI_MAX_K * kPlanes];
     __shared__ uint32_t qneed[GSI_MAX_K];            // planes 1..15 where S(u) has a set bit
     __shared__ uint32_t ht_lab[kHT], ht_mask[kHT];
     __shared__ unsigned long long cnt_s[GSI_MAX_K];
     __shared__ unsigned long long loads_s;
+    __shared__ uint32_t q_slot[kWarps][32 * FW];     // queued vertex: j * 32 + lane of its word
+    __shared__ uint32_t q_mask[kWarps][32 * FW];     // its candidate mask, then its final mask
     for (int i = threadIdx.x; i < k * kPlanes; i += blockDim.x) qs[i] = qsig[i];
     if (threadIdx.x < GSI_MAX_K) cnt_s[threadIdx.x] = 0;
     if (threadIdx.x < kHT) {
@@ -196,78 +214,117 @@ __global__ void __launch_bounds__(kThreads, GSI_FILTER_MINB) k_filter(const uint
             ht_mask[h] |= 1u << u;
         }
     __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
-    constexpr int kFW = GSI_FILTER_FW;   // bitmap words per warp per iteration (coalesced plane-0 loads in flight)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    uint32_t *const qslot = q_slot[wid];
+    uint32_t *const qmask = q_mask[wid];
+    const long long warps = (long long)gridDim.x * kWarps;
     unsigned long long plane_words = 0;   // plane words this thread read (algorithmic bytes / 4)
     unsigned long long my_count = 0;      // |C(u)| partial for u = lane
-    for (long long w0 = (blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5)) * kFW; w0 < words;
-         w0 += warps * kFW) {
-        uint32_t lab[kFW], mask[kFW];
+    for (long long w0 = (blockIdx.x * (long long)kWarps + wid) * FW; w0 < words; w0 += warps * FW) {
+        uint32_t lab[FW], mask[FW];
 #pragma unroll
-        for (int j = 0; j < kFW; j++) {
+        for (int j = 0; j < FW; j++) {
             const long long v = (w0 + j) * 32 + lane;
-            lab[j] = (w0 + j < words && v < n) ? __ldcs(sig + v) : 0xFFFFFFFEu;   // matches no query label
+            const bool in = w0 + j < words && v < n;
+            lab[j] = in ? (kStream ? __ldcs(sig + v) : __ldg(sig + v)) : 0xFFFFFFFEu;   // matches no query label
         }
 #pragma unroll
-        for (int j = 0; j < kFW; j++) {   // label field by equality (A4): one hash probe, not k compares
+        for (int j = 0; j < FW; j++) {   // label field by equality (A4): one hash probe, not k compares
             uint32_t h = (lab[j] * 0x9E3779B1u) >> 26, e;
             while ((e = ht_lab[h]) != lab[j] && e != 0xFFFFFFFFu) h = (h + 1) & (kHT - 1);
             mask[j] = e == lab[j] ? ht_mask[h] : 0u;
         }
         if (!label_only) {
-            // Only the planes where some label-matching u has a set bit can reject v (a plane
-            // whose query word is 0 is contained in anything), and the planes are read one at a
-            // time: the first one tested rejects most of a label class, so the later planes
-            // are read only for the few survivors (sector traffic ~1/3 of reading every needed
-            // plane up front).  Rounds run over the kFW words together: each round issues the
-            // next needed plane load of every word before testing any of them, so kFW
-            // independent loads are in flight per lane instead of one dependent chain per word.
-            uint32_t tested[kFW];
+            // compact the label-matching vertices of the FW words into the warp's queue
+            int nq = 0;
+            uint32_t has = 0u;   // bit j: this lane's vertex of word j is queued (mask[j] lives in the queue)
 #pragma unroll
-            for (int j = 0; j < kFW; j++) tested[j] = 0u;
-            for (int round = 0; round < kPlanes; round++) {
-                uint32_t pv[kFW];
-                int pls[kFW];
-                bool any = false;
+            for (int j = 0; j < FW; j++) {
+                const unsigned bal = __ballot_sync(0xffffffffu, mask[j] != 0u);
+                if (mask[j]) {
+                    const int p = nq + __popc(bal & lt_mask);
+                    qslot[p] = (uint32_t)(j * 32 + lane);
+                    qmask[p] = mask[j];
+                    has |= 1u << j;
+                }
+                nq += __popc(bal);
+            }
+            __syncwarp();
+            if (nq) {
+                const int nc = (nq + 31) >> 5;   // dense columns of the queue
+                uint32_t m[FW], rem[FW], vv[FW];   // rem: needed planes not yet tested; vertex ids < 2^31
 #pragma unroll
-                for (int j = 0; j < kFW; j++) {
-                    uint32_t need = 0, t = mask[j];
-                    while (t) {
-                        const int u = __ffs(t) - 1;
-                        t &= t - 1;
-                        need |= qneed[u];
-                    }
-                    need &= ~tested[j];
-                    pls[j] = need ? __ffs(need) - 1 : -1;
-                    pv[j] = 0u;
-                    if (pls[j] >= 0) {
-                        const long long v = (w0 + j) * 32 + lane;
-                        pv[j] = __ldcs(sig + (long long)pls[j] * n + v);
-                        any = true;
+                for (int c = 0; c < FW; c++) {
+                    const int i = c * 32 + lane;
+                    m[c] = 0u;
+                    rem[c] = 0u;
+                    vv[c] = 0u;
+                    if (c < nc && i < nq) {
+                        const uint32_t sl = qslot[i];
+                        m[c] = qmask[i];
+                        vv[c] = (uint32_t)((w0 + (sl >> 5)) * 32 + (sl & 31));
+                        uint32_t t = m[c];
+                        while (t) {
+                            rem[c] |= qneed[__ffs(t) - 1];
+                            t &= t - 1;
+                        }
                     }
                 }
-                if (!__any_sync(0xffffffffu, any)) break;
+                for (int round = 0; round < kPlanes; round++) {
+                    uint32_t pv[FW];
+                    int pls[FW];
+                    bool any = false;
 #pragma unroll
-                for (int j = 0; j < kFW; j++) {
-                    if (pls[j] < 0) continue;
-                    tested[j] |= 1u << pls[j];
-                    plane_words++;
-                    uint32_t t = mask[j];
-                    while (t) {
-                        const int u = __ffs(t) - 1;
-                        t &= t - 1;
-                        const uint32_t sq = qs[u * kPlanes + pls[j]];
-                        if ((pv[j] & sq) != sq) mask[j] &= ~(1u << u);   // S(v)&S(u)=S(u) fails on this plane
+                    for (int c = 0; c < FW; c++) {
+                        pls[c] = -1;
+                        pv[c] = 0u;
+                        if (c < nc) {
+                            if (m[c] && rem[c]) {
+                                pls[c] = __ffs(rem[c]) - 1;
+                                const uint32_t *src = sig + (long long)pls[c] * n + vv[c];
+                                pv[c] = kStream ? __ldcs(src) : __ldg(src);
+                                any = true;
+                            }
+                        }
                     }
+                    if (!__any_sync(0xffffffffu, any)) break;
+#pragma unroll
+                    for (int c = 0; c < FW; c++) {
+                        if (pls[c] < 0) continue;
+                        rem[c] &= ~(1u << pls[c]);
+                        plane_words++;
+                        uint32_t t = m[c];
+                        while (t) {
+                            const int u = __ffs(t) - 1;
+                            t &= t - 1;
+                            const uint32_t sq = qs[u * kPlanes + pls[c]];
+                            if ((pv[c] & sq) != sq) m[c] &= ~(1u << u);   // S(v)&S(u)=S(u) fails on this plane
+                        }
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < FW; c++)
+                    if (c < nc && c * 32 + lane < nq) qmask[c * 32 + lane] = m[c];
+                __syncwarp();
+                // scatter the final masks back to the words (a queued vertex's slot is known
+                // to its own lane: the p-th match of word j is the lane's own vertex)
+                int base = 0;
+#pragma unroll
+                for (int j = 0; j < FW; j++) {
+                    const bool h = (has >> j) & 1u;
+                    const unsigned bal = __ballot_sync(0xffffffffu, h);
+                    mask[j] = h ? qmask[base + __popc(bal & lt_mask)] : 0u;
+                    base += __popc(bal);
                 }
             }
+            __syncwarp();   // the queue is reused by the next iteration
         }
-        // lane u collects the kFW bitmap words of query vertex u (ballots only for the query
-        // vertices some lane matched) and stores them as one 16 B vector
-        uint32_t mine[kFW];
+        // lane u collects the FW bitmap words of query vertex u (ballots only for the query
+        // vertices some lane matched)
+        uint32_t mine[FW];
 #pragma unroll
-        for (int j = 0; j < kFW; j++) {
+        for (int j = 0; j < FW; j++) {
             mine[j] = 0u;
             uint32_t present = __reduce_or_sync(0xffffffffu, mask[j]);
             while (present) {
@@ -279,17 +336,20 @@ __global__ void __launch_bounds__(kThreads, GSI_FILTER_MINB) k_filter(const uint
         }
         if (lane < k) {
             uint32_t *dst = bitmaps + (long long)lane * words + w0;
-            if (w0 + kFW <= words && ((words & 3) == 0)) {
+            if (FW % 4 == 0 && w0 + FW <= words && ((words & 3) == 0)) {
 #pragma unroll
-                for (int j = 0; j < kFW; j += 4)
+                for (int j = 0; j < FW; j += 4)
                     *reinterpret_cast<uint4 *>(dst + j) = make_uint4(mine[j], mine[j + 1], mine[j + 2], mine[j + 3]);
             } else {
 #pragma unroll
-                for (int j = 0; j < kFW; j++)
+                for (int j = 0; j < FW; j++)
                     if (w0 + j < words) dst[j] = mine[j];
             }
+            unsigned gc = 0;
 #pragma unroll
-            for (int j = 0; j < kFW; j++) my_count += __popc(mine[j]);
+            for (int j = 0; j < FW; j++) gc += __popc(mine[j]);
+            my_count += gc;
+            if (grp) grp[(long long)lane * grp_stride + w0 / FW] = (uint16_t)gc;
         }
     }
     if (lane < k && my_count) atomicAdd(&cnt_s[lane], my_count);
@@ -298,6 +358,24 @@ __global__ void __launch_bounds__(kThreads, GSI_FILTER_MINB) k_filter(const uint
     __syncthreads();
     if (threadIdx.x < k && cnt_s[threadIdx.x]) atomicAdd(&counts[threadIdx.x], cnt_s[threadIdx.x]);
     if (threadIdx.x == 0 && loads_s) atomicAdd(&ctr->plane_loads, loads_s);
+}
+
+// Words-per-warp variant of k_filter for a graph: FW = 1 while one wave of the device still
+// takes at most ~4 iterations per warp (small graphs: parallelism and L2 reuse), else 8.
+inline int filter_fw(long long words, int sms) { return words <= (long long)sms * 8 * 8 * 4 ? 1 : 8; }
+
+cudaError_t launch_filter(const uint32_t *sig, long long n, int k, const uint32_t *qsig, int label_only,
+                          uint32_t *bm, long long words, unsigned long long *counts, Counters *ctr, uint16_t *grp,
+                          long long grp_stride, int sms, cudaStream_t st) {
+    const int fw = filter_fw(words, sms);
+    const long long per_cta = (long long)fw * (kThreads / 32);
+    const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>((words + per_cta - 1) / per_cta,
+                                                                                (long long)sms * 8));
+    if (fw == 1)
+        k_filter<1><<<grid, kThreads, 0, st>>>(sig, n, k, qsig, label_only, bm, words, counts, ctr, grp, grp_stride);
+    else
+        k_filter<8><<<grid, kThreads, 0, st>>>(sig, n, k, qsig, label_only, bm, words, counts, ctr, grp, grp_stride);
+    return cudaGetLastError();
 }
 
 // ------------------------------------------------------------ level-1 compaction ----
@@ -2426,17 +2504,73 @@ __global__ void k_abl_link(const int32_t *__restrict__ M, long long nM, const un
 // ------------------------------------------------------------ small-query path -----
 // A query whose levels all stay small (C2-C4-shaped: |C(pi_1)| of a few to a few thousand,
 // ~11 levels of tens to thousands of rows) is latency-bound on the regular path: one join
-// launch and one counter read-back per level.  k_small_query runs every level of one query
-// inside one CTA of 1024 threads — Prealloc probe + block scan (Alg. 4), the join over the
+// launch and one counter read-back per level.  k_small_query runs the whole query after the
+// filter inside one CTA of 1024 threads, with nothing on the host between the filter and the
+// result: the join order (Alg. 2, the same greedy function the host planner calls), the steps
+// and their subtraction columns are planned by one thread from |C(u)| on the device; M_1 =
+// C(pi_1) is extracted in ascending order from the filter's bitmap through its per-group
+// counts; then every level runs — Prealloc probe + block scan (Alg. 4), the join over the
 // slot range in rounds of 1024 slots (Alg. 3 lines 2-13: C(u) bit, subtraction, the other
 // linking lists), and an ordered block-scan compaction into the next level's rows (the Combine,
-// Alg. 3 lines 14-21) — with the level sizes kept on the device, so the whole query costs one
-// launch after the filter/plan and one read-back.  Rows are produced in the same
-// lexicographic pi order as the regular path.  If a level exceeds the row or slot capacity the
-// kernel stops and reports the level; the host then runs the regular path (identical results).
+// Alg. 3 lines 14-21).  The host launches filter + this kernel back to back and reads one
+// block back.  Rows are produced in the same lexicographic pi order as the regular path.  If
+// the query does not fit (|C(pi_1)| > 4096 roots, more than 8 linking edges or subtraction
+// columns in a step, a level beyond the row or slot capacity) the kernel stops and reports
+// the level; the host then runs the regular path from the filter's output (identical results).
 constexpr int kSmallThreads = 1024;
 constexpr int kSmallMaxE = 8;
 constexpr int kSmallMaxInj = 8;
+constexpr int kSmallMaxQE = 64;        // query edges the device planner takes
+constexpr unsigned long long kSmallRowCap = 1ull << 15;
+constexpr unsigned long long kSmallSlotCap = 1ull << 16;
+constexpr unsigned long long kSmallMaxRoots = 4096;
+// Dynamic shared memory of k_small_query: two row buffers (a level's rows stay on chip when
+// they fit, so the next level's row reads and the Combine writes cost shared-memory latency
+// instead of L2 round trips) and the level's located lists.
+constexpr int kSmallSmRows = 16384;    // int32 per row buffer (64 KB each)
+constexpr int kSmallSmLoc = 2048;      // Loc entries (16 KB)
+constexpr size_t kSmallDynSmem = 2 * kSmallSmRows * sizeof(int32_t) + kSmallSmLoc * sizeof(Loc);
+
+// Alg. 2's greedy join order (reading A8 in DESIGN.md): start at the
+// vertex with the smallest score |C(u)|/deg(u), then repeatedly take the connected vertex of
+// smallest score, multiplying the scores of the taken vertex's neighbours by freq(l(e)).  One
+// function for the host planner and the device-planned small path, so both take the same order
+// (same double arithmetic, same tie rule: the smallest query id wins).
+__host__ __device__ inline int plan_greedy(int k, int qm, const int *qs, const int *qd, const long long *freq_e,
+                                           const long long *cand, int *order) {
+    double score[GSI_MAX_K];
+    uint32_t adj[GSI_MAX_K];
+    int deg[GSI_MAX_K];
+    for (int u = 0; u < k; u++) {
+        adj[u] = 0u;
+        deg[u] = 0;
+    }
+    for (int e = 0; e < qm; e++) {
+        deg[qs[e]]++;
+        deg[qd[e]]++;
+        adj[qs[e]] |= 1u << qd[e];
+        adj[qd[e]] |= 1u << qs[e];
+    }
+    for (int u = 0; u < k; u++) score[u] = deg[u] ? (double)cand[u] / deg[u] : (double)cand[u];
+    uint32_t in = 0u;
+    for (int i = 0; i < k; i++) {
+        int best = -1;
+        for (int u = 0; u < k; u++) {
+            if ((in >> u) & 1u) continue;
+            if (i > 0 && !(adj[u] & in)) continue;   // connected to the prefix
+            if (best < 0 || score[u] < score[best]) best = u;
+        }
+        if (best < 0) return -1;                      // disconnected query
+        order[i] = best;
+        in |= 1u << best;
+        for (int e = 0; e < qm; e++) {
+            const int o = qs[e] == best ? qd[e] : (qd[e] == best ? qs[e] : -1);
+            if (o >= 0) score[o] *= (double)freq_e[e];
+        }
+    }
+    return 0;
+}
+
 struct SmallStep {
     int E, n_inj;
     int col[kSmallMaxE];
@@ -2447,50 +2581,244 @@ struct SmallStep {
     const uint32_t *cu;
 };
 struct SmallPlan {
-    int k, want_table, fp, gpn;
-    unsigned long long row_cap, slot_cap;
+    int k;
     int pos_of_q[GSI_MAX_K];
     SmallStep st[GSI_MAX_K - 1];   // st[j]: the step joining column j + 1 (j + 1 columns before it)
+};
+// The query as the device planner reads it (passed by value, ~2.5 KB).
+struct SmallQuery {
+    int k, qm, homo, want_table, fp, gpn;
+    int qvl[GSI_MAX_K];
+    int qs[kSmallMaxQE], qd[kSmallMaxQE];
+    int lab[kSmallMaxQE], rawlab[kSmallMaxQE];   // dense / raw edge label
+    long long freq[kSmallMaxQE];                 // |E(P(G, lab))|
+    unsigned long long gbase[kSmallMaxQE];
+    uint32_t ngroups[kSmallMaxQE];
+    const uint32_t *bm;                          // the filter's bitmaps [k][words]
+    long long words;
+    const uint16_t *grp;                         // the filter's per-group counts [k][ngrp_pad]
+    long long ngrp, ngrp_pad;                    // groups of gw bitmap words; row stride (multiple of 8)
+    int gw;
+    const unsigned long long *cand;              // |C(u)|
+    const Counters *ctr;                         // the filter's plane-load counter
 };
 struct SmallOut {
     unsigned long long count, fp1, fp2, nout;
     int aborted;                              // 0: done; t: level t exceeded a capacity
+    int planned;                              // the device plan below is valid
     unsigned long long rows[GSI_MAX_K];       // |M_t| at t - 1
     unsigned long long gba[GSI_MAX_K];        // |GBA| of level t at t
     unsigned long long elems[GSI_MAX_K];
+    unsigned long long cand[GSI_MAX_K];       // |C(u)| (copied for the host: one read-back)
+    unsigned long long plane_loads;
+    int order[GSI_MAX_K];                     // pi
+    int n_edges[GSI_MAX_K], first_edge[GSI_MAX_K];
 };
 
-__global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const SmallPlan plan, const int32_t *__restrict__ M1,
-                                                                  const unsigned long long *__restrict__ nM1p,
+// Warp 0 plans (lane u = query vertex u, lane j = step j): Alg. 2's order with the same
+// arithmetic and tie rule as plan_greedy (lane o multiplies its own score by freq(l(e)) for the
+// edges e of the taken vertex in query-edge order, exactly the sequence plan_greedy applies to
+// score[o]; the argmin is lexicographic in (score, id), i.e. the first smallest id), then the
+// steps — linking columns, labels, subtraction columns — one lane per step.  Returns (on every
+// lane) 0, or 1 if the query is disconnected or a step does not fit the kernel's limits.
+__device__ int small_plan_warp(const SmallQuery &Q, SmallPlan &sp, SmallOut *out, int *order_s, int *pos_s) {
+    const int lane = threadIdx.x & 31, k = Q.k, qm = Q.qm;
+    int deg = 0;
+    uint32_t adj = 0u;
+    for (int e = 0; e < qm; e++) {   // uniform e: broadcast reads of the parameter block
+        if (Q.qs[e] == lane) {
+            deg++;
+            adj |= 1u << Q.qd[e];
+        }
+        if (Q.qd[e] == lane) {
+            deg++;
+            adj |= 1u << Q.qs[e];
+        }
+    }
+    double score = 0.0;
+    if (lane < k) score = deg ? (double)Q.cand[lane] / deg : (double)Q.cand[lane];
+    uint32_t in = 0u;
+    for (int i = 0; i < k; i++) {
+        const bool ok = lane < k && !((in >> lane) & 1u) && (i == 0 || (adj & in));
+        double bs = score;
+        int bu = ok ? lane : 32;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double s2 = __shfl_xor_sync(0xffffffffu, bs, o);
+            const int u2 = __shfl_xor_sync(0xffffffffu, bu, o);
+            if (u2 < 32 && (bu == 32 || s2 < bs || (s2 == bs && u2 < bu))) {
+                bs = s2;
+                bu = u2;
+            }
+        }
+        if (bu == 32) return 1;   // disconnected query
+        if (lane == 0) order_s[i] = bu;
+        in |= 1u << bu;
+        for (int e = 0; e < qm; e++) {
+            const int o = Q.qs[e] == bu ? Q.qd[e] : (Q.qd[e] == bu ? Q.qs[e] : -1);
+            if (o == lane) score *= (double)Q.freq[e];
+        }
+    }
+    __syncwarp();
+    if (lane < k) {
+        pos_s[order_s[lane]] = lane;
+        out->order[lane] = order_s[lane];
+    }
+    __syncwarp();
+    if (lane < k) sp.pos_of_q[lane] = pos_s[lane];
+    if (lane == 0) sp.k = k;
+    int fail = 0;
+    const int j = lane;
+    if (j >= 1 && j < k) {
+        SmallStep &T = sp.st[j - 1];
+        const int u = order_s[j];
+        int E = 0, other[kSmallMaxE], raw[kSmallMaxE];
+        long long fr[kSmallMaxE];
+        for (int e = 0; e < qm && !fail; e++) {   // linking edges in query-edge order (as build_steps)
+            const int o = Q.qs[e] == u ? Q.qd[e] : (Q.qd[e] == u ? Q.qs[e] : -1);
+            if (o < 0 || pos_s[o] >= j) continue;
+            if (E == kSmallMaxE) {
+                fail = 1;
+                break;
+            }
+            T.col[E] = pos_s[o];
+            T.lab[E] = (uint32_t)Q.lab[e];
+            T.gbase[E] = Q.gbase[e];
+            T.ngroups[E] = Q.ngroups[e];
+            other[E] = o;
+            raw[E] = Q.rawlab[e];
+            fr[E] = Q.freq[e];
+            E++;
+        }
+        if (!fail) {
+            T.E = E;
+            int best = 0;   // the paper's e0 (stats only: each row is bounded by its shortest list)
+            for (int e = 1; e < E; e++)
+                if (fr[e] < fr[best] ||
+                    (fr[e] == fr[best] && (raw[e] < raw[best] || (raw[e] == raw[best] && T.col[e] < T.col[best]))))
+                    best = e;
+            out->n_edges[j] = E;
+            out->first_edge[j] = other[best];
+            T.n_inj = 0;
+            if (!Q.homo)
+                for (int c = 0; c < j && !fail; c++) {
+                    if (Q.qvl[order_s[c]] != Q.qvl[u]) continue;   // C(u) excludes other labels
+                    bool linked = false;
+                    for (int e = 0; e < E; e++) linked |= T.col[e] == c;   // x in N(m[c],l) => x != m[c]
+                    if (linked) continue;
+                    if (T.n_inj == kSmallMaxInj) fail = 1;
+                    else T.inj_col[T.n_inj++] = c;
+                }
+            T.cu = Q.bm + (long long)u * Q.words;
+        }
+    }
+    return __any_sync(0xffffffffu, fail) ? 1 : 0;
+}
+
+__global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const __grid_constant__ SmallQuery Q,
                                                                   const uint2 *__restrict__ groups,
                                                                   const int32_t *__restrict__ ci,
                                                                   int32_t *__restrict__ bufA, int32_t *__restrict__ bufB,
-                                                                  Loc *__restrict__ loc,
+                                                                  Loc *__restrict__ locG,
                                                                   unsigned long long *__restrict__ F,
                                                                   int32_t *__restrict__ table, SmallOut *out) {
     __shared__ unsigned long long sm[34];
     __shared__ unsigned long long cnt_s, h1_s, h2_s, el_s;
+    __shared__ int fail_s;
+    __shared__ SmallPlan sp;
     // F of a level with fewer than kSmallFsh rows stays in shared memory: the join's per-slot
     // row search then costs shared-memory latency instead of a chain of L2 round trips
     constexpr int kSmallFsh = 4097;
     __shared__ unsigned long long Fs[kSmallFsh];
-    const int tid = threadIdx.x, lane = tid & 31;
-    const int k = plan.k;
-    unsigned long long nM = *nM1p;
-    if (tid == 0) {
-        out->rows[0] = nM;
-        cnt_s = h1_s = h2_s = 0;
+    extern __shared__ __align__(16) unsigned char small_dyn[];
+    int32_t *const sA = reinterpret_cast<int32_t *>(small_dyn);
+    int32_t *const sB = sA + kSmallSmRows;
+    Loc *const locS = reinterpret_cast<Loc *>(sB + kSmallSmRows);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int k = Q.k;
+    // ---- plan (Alg. 2) from |C(u)| (warp 0) ---------------------------------------------
+    __shared__ int order_s[GSI_MAX_K], pos_s[GSI_MAX_K];
+    if (tid < k) out->cand[tid] = Q.cand[tid];
+    if (warp == 0) {
+        bool any0 = lane < k && Q.cand[lane] == 0;
+        any0 = __any_sync(0xffffffffu, any0);
+        // an empty C(u) (no match) or a plan beyond the limits: the host's regular path
+        int f = any0 ? 1 : small_plan_warp(Q, sp, out, order_s, pos_s);
+        if (!f && Q.cand[order_s[0]] > kSmallMaxRoots) f = 1;
+        if (lane == 0) {
+            out->plane_loads = Q.ctr->plane_loads;
+            cnt_s = h1_s = h2_s = 0;
+            fail_s = f;
+            out->planned = f ? 0 : 1;
+            if (f) out->aborted = 1;
+        }
     }
-    if (nM > plan.row_cap) {
-        if (tid == 0) out->aborted = 1;
-        return;
+    __syncthreads();
+    if (fail_s) return;
+    // ---- level 1 (Alg. 2 line 7): M_1 = C(pi_1) ascending, from the per-group counts ------
+    // Each thread sums a contiguous, 16 B aligned range of groups (vector loads, all in flight
+    // at once); one block scan gives every thread its output offset and its first
+    // non-empty-group index; the non-empty groups (<= |M_1|) are listed in shared memory (Fs,
+    // free until level 1's Prealloc) and a warp per group writes its vertices in order.
+    const int u1 = order_s[0];
+    unsigned long long nM = Q.cand[u1];
+    {
+        const uint32_t *bm1 = Q.bm + (long long)u1 * Q.words;
+        const uint16_t *g1 = Q.grp + (long long)u1 * Q.ngrp_pad;
+        const long long ng = Q.ngrp;
+        const long long per = ((ng + kSmallThreads - 1) / kSmallThreads + 7) & ~7ll;
+        const long long a = tid * per, b = min(ng, a + per);
+        unsigned long long sum = 0, ne = 0;
+        for (long long x0 = a; x0 < b; x0 += 8) {
+            const uint4 v = *reinterpret_cast<const uint4 *>(g1 + x0);
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int i = 0; i < 8; i++) {
+                const unsigned c = x0 + i < b ? (w[i >> 1] >> (16 * (i & 1))) & 0xFFFFu : 0u;
+                sum += c;
+                ne += c ? 1 : 0;
+            }
+        }
+        unsigned long long tot;
+        const unsigned long long ex = block_exclusive_scan((sum << 32) | ne, sm, &tot);
+        unsigned long long obase = ex >> 32, li = ex & 0xFFFFFFFFull;
+        for (long long x = a; x < b && obase < (ex >> 32) + sum; x++) {
+            const unsigned c = g1[x];
+            if (!c) continue;
+            Fs[li++] = ((unsigned long long)x << 32) | obase;
+            obase += c;
+        }
+        __syncthreads();
+        const unsigned long long nne = tot & 0xFFFFFFFFull;
+        const int GW = Q.gw;
+        for (unsigned long long i = warp; i < nne; i += kSmallThreads / 32) {
+            const unsigned long long e = Fs[i];
+            const long long w = (long long)(e >> 32) * GW + lane;
+            const uint32_t word = (lane < GW && w < Q.words) ? bm1[w] : 0u;
+            const unsigned c = __popc(word);
+            unsigned inc = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            unsigned long long p = (e & 0xFFFFFFFFull) + inc - c;
+            uint32_t bits = word;
+            while (bits) {
+                sA[p++] = (int32_t)(w * 32 + __ffs(bits) - 1);   // M_1 (<= 4096 rows) on chip
+                bits &= bits - 1;
+            }
+        }
+        __syncthreads();   // M_1 written before level 1 reads it; Fs free again
     }
-    const int32_t *cur = M1;
-    int32_t *nxt = bufA;
+    if (tid == 0) out->rows[0] = nM;
+    // rows of the current level: a shared-memory buffer when they fit, else bufA / bufB
+    const int32_t *cur = sA;
     for (int t = 1; t < k; t++) {
-        const SmallStep &S = plan.st[t - 1];
+        const SmallStep &S = sp.st[t - 1];
         const int E = S.E;
         const bool last = t == k - 1;
+        Loc *const loc = nM * (unsigned long long)E <= (unsigned long long)kSmallSmLoc ? locS : locG;
         // ---- Prealloc (Alg. 4): locate every linking list, per-row shortest list bounds the
         //      buffer (any linking edge bounds it, L967-981), F = exclusive scan
         unsigned long long run = 0;
@@ -2504,7 +2832,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const SmallPla
                 bool anyzero = false;
                 for (int e = 0; e < E; e++) {
                     const uint32_t v = (uint32_t)cur[i * t + S.col[e]];
-                    const Loc r = pcsr_lookup(groups, plan.gpn, S.gbase[e], S.ngroups[e], S.lab[e], v, nullptr);
+                    const Loc r = pcsr_lookup(groups, Q.gpn, S.gbase[e], S.ngroups[e], S.lab[e], v, nullptr);
                     loc[i * E + e] = r;
                     if (e == 0) first = r;
                     if (r.len < best.len) {
@@ -2540,11 +2868,15 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const SmallPla
             out->elems[t] = el_s;
         }
         const unsigned long long *FF = nM < kSmallFsh ? Fs : F;
-        if (T > plan.slot_cap) {
+        if (T > kSmallSlotCap) {
             if (tid == 0) out->aborted = t;
             return;
         }
         __syncthreads();   // F visible to the whole block
+        // the next level's rows (at most T of t + 1 columns): on chip if they fit
+        int32_t *nxt;
+        if (T * (unsigned long long)(t + 1) <= (unsigned long long)kSmallSmRows) nxt = cur == sA ? sB : sA;
+        else nxt = cur == bufA ? bufB : bufA;
         // ---- join: slots in rounds of 1024, ordered compaction into the next level -------
         unsigned long long nout = 0;
         for (unsigned long long s0 = 0; s0 < T; s0 += kSmallThreads) {
@@ -2568,11 +2900,11 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const SmallPla
                     keep = in_sorted(ci + Le.off, Le.len, x);
                 }
             }
-            if (last && !plan.want_table) {
+            if (last && !Q.want_table) {
                 unsigned long long c = keep ? 1ull : 0ull, a1 = 0, a2 = 0;
-                if (keep && plan.fp) {
+                if (keep && Q.fp) {
                     for (int q = 0; q < k; q++) {
-                        const int col = plan.pos_of_q[q];
+                        const int col = sp.pos_of_q[q];
                         const uint32_t val = col < t ? (uint32_t)cur[row * t + col] : (uint32_t)x;
                         a1 += fp_term(kFpSeed1, q, val);
                         a2 += fp_term(kFpSeed2, q, val);
@@ -2593,7 +2925,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const SmallPla
             }
             unsigned long long agg;
             const unsigned long long ex = block_exclusive_scan(keep ? 1ull : 0ull, sm, &agg);
-            if (nout + agg > plan.row_cap) {
+            if (nout + agg > kSmallRowCap) {
                 if (tid == 0) out->aborted = t + 1;
                 return;
             }
@@ -2602,13 +2934,13 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const SmallPla
                 if (last) {   // the table in query-id order (+ fingerprint)
                     unsigned long long a1 = 0, a2 = 0;
                     for (int q = 0; q < k; q++) {
-                        const int col = plan.pos_of_q[q];
+                        const int col = sp.pos_of_q[q];
                         const int32_t val = col < t ? cur[row * t + col] : x;
                         table[p * k + q] = val;
                         a1 += fp_term(kFpSeed1, q, (uint32_t)val);
                         a2 += fp_term(kFpSeed2, q, (uint32_t)val);
                     }
-                    if (plan.fp) {
+                    if (Q.fp) {
                         atomicAdd(&h1_s, fp_mix(a1));
                         atomicXor(&h2_s, fp_mix(a2));
                     }
@@ -2622,7 +2954,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const SmallPla
         __syncthreads();   // every row of the next level written before it is read
         if (last) {
             if (tid == 0) {
-                const unsigned long long c = plan.want_table ? nout : cnt_s;
+                const unsigned long long c = Q.want_table ? nout : cnt_s;
                 out->count = c;
                 out->nout = nout;
                 out->rows[t] = c;
@@ -2635,7 +2967,6 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const SmallPla
         if (tid == 0) out->rows[t] = nout;
         nM = nout;
         cur = nxt;
-        nxt = (nxt == bufA) ? bufB : bufA;
         if (nM == 0) break;
     }
     if (tid == 0) {   // a level came out empty: no matches (later rows stay 0)
@@ -3025,6 +3356,7 @@ void ensure_pool(int dev) {
     cudaFuncSetAttribute(k_join<J_NEXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxJoinSmem);
     cudaFuncSetAttribute(k_join<J_CAHEAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxJoinSmem);
     cudaFuncSetAttribute(k_count_fast<kFastItems>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxJoinSmem);
+    cudaFuncSetAttribute(k_small_query, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallDynSmem);
     cudaGetLastError();
     g_pool_ready[dev] = true;
 }
@@ -3041,31 +3373,58 @@ unsigned long long available_bytes(int dev) {
     return (unsigned long long)fr + (reserved > used ? reserved - used : 0);
 }
 
+// True if an idle workspace slot of the device already has the size its next query takes
+// (taking it then allocates nothing, so it needs no budget).
+bool workspace_fits(int dev) {
+    if (dev < 0 || dev >= 64) return false;
+    for (int k = 0; k < kWsSlots; k++) {
+        Workspace &W = g_ws[dev][k];
+        std::lock_guard<std::mutex> lk(W.mu);
+        if (!W.busy) return W.cap >= std::max(std::max(W.want, g_ws_want[dev].load()), (size_t)64 << 20);
+    }
+    return false;
+}
+
+// A query's default memory budget: 85 % of free device memory, idle workspaces and the
+// workspace the query itself holds (own_ws bytes).
+unsigned long long device_budget(int dev, size_t own_ws) {
+    return (unsigned long long)(0.85 * (double)(available_bytes(dev) + workspace_idle_bytes(dev) + own_ws));
+}
+
+
 // Pinned Counters blocks (the per-level counter read-back of a query): a process-wide
 // free list, so host threads that come and go (batch workers) reuse a bounded set instead of
 // leaking one page-locked allocation each.  A query holds one block for its lifetime.
 std::mutex g_pinned_mu;
-std::vector<Counters *> g_pinned_free;
+struct PinnedBlock {
+    Counters c;                              // per-level counters
+    SmallOut so;                             // the small path's result block
+    unsigned long long cand[GSI_MAX_K];      // |C(u)|
+};
+std::vector<PinnedBlock *> g_pinned_free;
 struct PinnedCounters {
-    Counters *p = nullptr;   // nullptr if pinned memory is unavailable
+    PinnedBlock *blk = nullptr;   // nullptr if pinned memory is unavailable
+    Counters *p = nullptr;        // &blk->c
     PinnedCounters() {
         {
             std::lock_guard<std::mutex> lk(g_pinned_mu);
             if (!g_pinned_free.empty()) {
-                p = g_pinned_free.back();
+                blk = g_pinned_free.back();
                 g_pinned_free.pop_back();
+                p = &blk->c;
                 return;
             }
         }
-        if (cudaMallocHost((void **)&p, sizeof(Counters)) != cudaSuccess) {
+        if (cudaMallocHost((void **)&blk, sizeof(PinnedBlock)) != cudaSuccess) {
             cudaGetLastError();
-            p = nullptr;
+            blk = nullptr;
         }
+        p = blk ? &blk->c : nullptr;
     }
     ~PinnedCounters() {
-        if (!p) return;
+        if (!blk) return;
         std::lock_guard<std::mutex> lk(g_pinned_mu);
-        g_pinned_free.push_back(p);
+        g_pinned_free.push_back(blk);
     }
     PinnedCounters(const PinnedCounters &) = delete;
     PinnedCounters &operator=(const PinnedCounters &) = delete;
@@ -3209,34 +3568,12 @@ static gsi_status plan_order(const gsi_prepared *q, const std::vector<long long>
         }
         return GSI_OK;
     }
-    std::vector<double> score(k);
-    std::vector<int> deg(k, 0), in(k, 0);
-    for (int e = 0; e < qm; e++) {
-        deg[q->qs[e]]++;
-        deg[q->qd[e]]++;
-    }
-    for (int u = 0; u < k; u++) score[u] = deg[u] ? (double)cand[u] / deg[u] : (double)cand[u];
-    auto freq_of = [&](int e) -> double {
-        int d = q->qe_dense[e];
-        return d < 0 ? 0.0 : (double)g->freq[d];
-    };
-    for (int i = 0; i < k; i++) {
-        int best = -1;
-        for (int u = 0; u < k; u++) {
-            if (in[u]) continue;
-            if (i > 0) {
-                bool conn = false;
-                for (int c = 0; c < i && !conn; c++) conn = adjacent(u, order[c]);
-                if (!conn) continue;
-            }
-            if (best < 0 || score[u] < score[best]) best = u;
-        }
-        order.push_back(best);
-        in[best] = 1;
-        for (int e = 0; e < qm; e++) {
-            int o = q->qs[e] == best ? q->qd[e] : (q->qd[e] == best ? q->qs[e] : -1);
-            if (o >= 0) score[o] *= freq_of(e);
-        }
+    std::vector<long long> freq_e(qm);
+    for (int e = 0; e < qm; e++) freq_e[e] = q->qe_dense[e] < 0 ? 0ll : g->freq[q->qe_dense[e]];
+    order.assign(k, -1);
+    if (plan_greedy(k, qm, q->qs.data(), q->qd.data(), freq_e.data(), cand.data(), order.data()) != 0) {
+        set_error("query graph is not connected");
+        return GSI_ERR_INVALID_ARG;
     }
     return GSI_OK;
 }
@@ -4068,95 +4405,85 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
 }  // namespace
 
 // ------------------------------------------------------------------ small path ---------
-// Eligible: one shard, per-row e0, every step with <= 8 linking edges and subtraction columns,
-// and a small first level (the kernel aborts to the regular path if a later level grows).
-constexpr unsigned long long kSmallRowCap = 1ull << 15;
-constexpr unsigned long long kSmallSlotCap = 1ull << 16;
-constexpr unsigned long long kSmallMaxRoots = 4096;
-
-bool small_eligible(const QueryCtx &C, unsigned long long nM1, bool known) {
-    if (C.opts.small_mode == 1 || env_flag("GSI_SMALL_OFF") || C.W != 1 || C.opts.e0_mode != 0) return false;
-    if (!known || nM1 == 0 || nM1 > kSmallMaxRoots) return false;
-    if (C.opts.chunk_slots || C.opts.force_paths) return false;
-    for (auto &s : C.steps) {
-        if ((int)s.col.size() > kSmallMaxE) return false;
-        int ninj = 0;
-        if (!C.opts.homomorphism)
-            for (int c = 0; c < s.t; c++) {
-                if (C.q->qvl[C.order[c]] != C.q->qvl[s.u]) continue;
-                bool linked = false;
-                for (int lc : s.col) linked |= lc == c;
-                ninj += linked ? 0 : 1;
-            }
-        if (ninj > kSmallMaxInj) return false;
-    }
-    return true;
+// Eligible before the filter runs: one shard, per-row e0, no test hooks, <= 64 query edges.
+// Whether the query really is small (|C(pi_1)| <= 4096, every step within the kernel's limits,
+// every level within its capacity) is found out on the device; otherwise the kernel stops and
+// the host takes the regular path.
+bool small_apriori(const QueryCtx &C) {
+    const gsi_query_opts &o = C.opts;
+    if (o.small_mode == 1 || env_flag("GSI_SMALL_OFF") || C.W != 1 || o.e0_mode != 0) return false;
+    if (o.chunk_slots || o.force_paths || o.ablation || (o.roots && o.n_roots > 0)) return false;
+    if (o.force_order || o.force_first_edge) return false;
+    return C.q->k > 1 && (int)C.q->qs.size() <= kSmallMaxQE && !C.q->absent_label;
 }
 
-// Run every level in k_small_query; done = false if it stopped at a capacity (the caller then
-// takes the regular path from M_1, which is left untouched).
-gsi_status run_small(QueryCtx &C, const int32_t *M1, bool &done) {
+// Launch k_small_query right behind the filter (no host round trip) and read its block back.
+// done = true: every level ran on the device and the stats/results are filled in; else the
+// caller takes the regular path (out->cand / plane_loads are valid either way).
+gsi_status run_small(QueryCtx &C, const uint16_t *grp, long long ngrp, long long ngrp_pad, int gw,
+                     const unsigned long long *d_counts,
+                     SmallOut *dout, SmallOut *hout, bool &done) {
     done = false;
     const gsi_graph *g = C.g;
+    const gsi_prepared *q = C.q;
     gsi_stats &S = *C.S;
     Arena &A = *C.A;
-    const int k = C.q->k;
-    SmallPlan plan;
-    std::memset(&plan, 0, sizeof(plan));
-    plan.k = k;
-    plan.want_table = C.opts.want_table ? 1 : 0;
-    plan.fp = C.opts.fingerprint ? 1 : 0;
-    plan.gpn = g->gpn;
-    plan.row_cap = kSmallRowCap;
-    plan.slot_cap = kSmallSlotCap;
-    for (int q = 0; q < k; q++) plan.pos_of_q[q] = C.pos_of_q[q];
-    int maxE = 1;
-    for (size_t j = 0; j < C.steps.size(); j++) {
-        const Step &s = C.steps[j];
-        SmallStep &T = plan.st[j];
-        T.E = (int)s.col.size();
-        maxE = std::max(maxE, T.E);
-        for (int e = 0; e < T.E; e++) {
-            T.col[e] = s.col[e];
-            T.lab[e] = (uint32_t)s.lab[e];
-            T.gbase[e] = (unsigned long long)g->gbase[s.lab[e]];
-            T.ngroups[e] = g->ngroups[s.lab[e]];
-        }
-        T.n_inj = 0;
-        if (!C.opts.homomorphism)
-            for (int c = 0; c < s.t; c++) {
-                if (C.q->qvl[C.order[c]] != C.q->qvl[s.u]) continue;   // C(u) excludes other labels
-                bool linked = false;
-                for (int lc : s.col) linked |= lc == c;                // x in N(m[c],l) => x != m[c]
-                if (!linked) T.inj_col[T.n_inj++] = c;
-            }
-        T.cu = C.bm + (long long)s.u * C.words;
+    const int k = q->k, qm = (int)q->qs.size();
+    SmallQuery Q;
+    std::memset(&Q, 0, sizeof(Q));
+    Q.k = k;
+    Q.qm = qm;
+    Q.homo = C.opts.homomorphism ? 1 : 0;
+    Q.want_table = C.opts.want_table ? 1 : 0;
+    Q.fp = C.opts.fingerprint ? 1 : 0;
+    Q.gpn = g->gpn;
+    for (int u = 0; u < k; u++) Q.qvl[u] = q->qvl[u];
+    for (int e = 0; e < qm; e++) {
+        const int d = q->qe_dense[e];   // >= 0: absent labels are not eligible
+        Q.qs[e] = q->qs[e];
+        Q.qd[e] = q->qd[e];
+        Q.lab[e] = d;
+        Q.rawlab[e] = q->qe[e];
+        Q.freq[e] = g->freq[d];
+        Q.gbase[e] = (unsigned long long)g->gbase[d];
+        Q.ngroups[e] = g->ngroups[d];
     }
+    Q.bm = C.bm;
+    Q.words = C.words;
+    Q.grp = grp;
+    Q.ngrp = ngrp;
+    Q.ngrp_pad = ngrp_pad;
+    Q.gw = gw;
+    Q.cand = d_counts;
+    Q.ctr = C.ctr;
     int32_t *bufA = nullptr, *bufB = nullptr, *table = nullptr;
     Loc *loc = nullptr;
     unsigned long long *F = nullptr;
-    SmallOut *dout = nullptr;
     const size_t mk = A.mark();
     GSI_TRY(A.get(&bufA, kSmallRowCap * (unsigned long long)k));
     GSI_TRY(A.get(&bufB, kSmallRowCap * (unsigned long long)k));
-    GSI_TRY(A.get(&loc, kSmallRowCap * (unsigned long long)maxE));
+    GSI_TRY(A.get(&loc, kSmallRowCap * (unsigned long long)kSmallMaxE));
     GSI_TRY(A.get(&F, kSmallRowCap + 1));
-    if (plan.want_table) GSI_TRY(A.get(&table, kSmallRowCap * (unsigned long long)k));
-    GSI_TRY(A.get(&dout, 1));
-    GSI_CUDA(cudaMemsetAsync(dout, 0, sizeof(SmallOut), C.st));
-    C.prof->begin(GSI_K_JOIN, GSI_V_SMALL);
+    if (Q.want_table) GSI_TRY(A.get(&table, kSmallRowCap * (unsigned long long)k));
+    C.prof->begin(GSI_K_JOIN, GSI_V_SMALL);   // dout: zeroed with the query's counter pool
     S.variant_launches[GSI_V_SMALL]++;
-    k_small_query<<<1, kSmallThreads, 0, C.st>>>(plan, M1, &C.ctr->total, g->groups, g->ci, bufA, bufB, loc, F, table,
-                                                  dout);
+    k_small_query<<<1, kSmallThreads, kSmallDynSmem, C.st>>>(Q, g->groups, g->ci, bufA, bufB, loc, F, table, dout);
     C.prof->end();
-    SmallOut h;
-    GSI_CUDA(d2h(S, &h, dout, sizeof(h), C.st));
+    GSI_CUDA(d2h(S, hout, dout, sizeof(SmallOut), C.st));
     GSI_CUDA(sync_timed(S, C.st));
     GSI_CUDA(cudaGetLastError());
-    if (h.aborted) {
-        S.small_aborted = h.aborted;
+    if (hout->aborted) {
+        // the regular path takes over from the filter's output (level 1: not planned — too
+        // many roots, an empty C(u) or a step beyond the limits; t > 1: level t outgrew it)
+        S.small_aborted = hout->aborted;
         A.reset(mk);
         return GSI_OK;
+    }
+    const SmallOut &h = *hout;
+    for (int j = 0; j < k; j++) S.order[j] = h.order[j];
+    for (int t = 1; t < k; t++) {
+        S.n_edges[t] = h.n_edges[t];
+        S.first_edge[t] = h.first_edge[t];
     }
     S.levels = 1;
     for (int t = 0; t < k; t++) {
@@ -4165,10 +4492,11 @@ gsi_status run_small(QueryCtx &C, const int32_t *M1, bool &done) {
         S.list_elems[t] = h.elems[t];
         if (t > 0 && h.rows[t - 1]) S.levels = t + 1;   // level t + 1 was produced
     }
+    S.alg_bytes[GSI_K_COMPACT] += 4.0 * C.words + 4.0 * h.rows[0];
     C.count = h.count;
     C.fp1 = h.fp1;
     C.fp2 = h.fp2;
-    if (plan.want_table && h.nout) {
+    if (Q.want_table && h.nout) {
         const gsi_status rs = table_put(C, table, h.nout);
         if (rs != GSI_OK) {
             A.reset(mk);
@@ -4392,6 +4720,156 @@ gsi_status run_ablation(QueryCtx &C, int32_t *M, unsigned long long nM) {
     return GSI_OK;
 }
 
+// Plan (a4), level 1 (a5) and the levels (a6-a8) on the host-driven path: every query the
+// small path did not take.  Leaves the count / fingerprint / table pieces in C.
+gsi_status run_regular(QueryCtx &C, const std::vector<long long> &cand, unsigned long long budget, double t_start,
+                       double t_filter, double &t_plan) {
+    const gsi_graph *g = C.g;
+    const gsi_prepared *q = C.q;
+    const gsi_query_opts &opts = C.opts;
+    gsi_stats &S = *C.S;
+    Arena &A = *C.A;
+    Prof &prof = *C.prof;
+    cudaStream_t st = C.st;
+    const int k = q->k;
+    const long long n = g->n;
+    const long long words = C.words;
+    const uint32_t *bm = C.bm;
+    Counters hc;
+    // ---------------- plan (a4) ----------------
+    GSI_TRY(plan_order(q, cand, opts.force_order, C.order));
+    GSI_TRY(build_steps(q, C.order, opts.force_first_edge, C.steps));
+    for (int j = 0; j < k; j++) S.order[j] = C.order[j];
+    for (auto &s : C.steps) {
+        S.n_edges[s.t] = (int)s.col.size();
+        S.first_edge[s.t] = s.other[s.paper_e0];
+    }
+    C.pos_of_q.assign(k, 0);
+    for (int j = 0; j < k; j++) C.pos_of_q[C.order[j]] = j;
+    plan_layout(C, !opts.want_table && !opts.fingerprint && !opts.ablation);
+    t_plan = now_ms();
+    S.ms_plan = (float)(t_plan - t_filter);
+
+    // memory budget -> chunk capacity in GBA slots (bytes per slot per level: S,R 8 B,
+    // M' 4(t+1) B, the child level's loc/F 8E+8 B), over the k-1 levels that may nest.
+    {
+        // (the chunk capacity depends on the budget only, never on the workspace size, so the
+        // chunking of a query is reproducible)
+        int maxE = 1;
+        for (auto &s : C.steps) maxE = std::max(maxE, (int)s.col.size());
+        const double per_slot = 8.0 + 4.0 * (k + 1) + 8.0 * maxE + 8.0;
+        const double levels = std::max(1, k - 1);
+        C.cap_slots = (unsigned long long)std::max(1.0, budget / (per_slot * levels));
+        if (opts.chunk_slots) C.cap_slots = opts.chunk_slots;
+    }
+    C.shard_min = opts.shard_min_rows ? opts.shard_min_rows : 65536;
+    C.sharded = C.W == 1;
+    C.force_shared = (opts.force_paths & 1) != 0;
+    C.deadline = opts.timeout_s > 0 ? t_start + 1000.0 * opts.timeout_s : 0;
+
+    bool empty = q->absent_label;
+    for (int u = 0; u < k; u++) empty |= cand[u] == 0;
+
+    // ---------------- level 1 (a5) ----------------
+    int32_t *M = nullptr;
+    unsigned long long nM = 0;
+    if (!empty) {
+        unsigned long long *status = nullptr;
+        const int u1 = C.order[0];
+        const uint32_t *bm1 = bm + (long long)u1 * words;
+        if (opts.roots && opts.n_roots > 0) {
+            std::vector<int32_t> roots(opts.roots, opts.roots + opts.n_roots);
+            std::sort(roots.begin(), roots.end());
+            roots.erase(std::unique(roots.begin(), roots.end()), roots.end());
+            roots.erase(std::remove_if(roots.begin(), roots.end(), [&](int32_t v) { return v < 0 || v >= n; }),
+                        roots.end());
+            long long nr = (long long)roots.size();
+            int32_t *d_roots = nullptr;
+            GSI_TRY(A.get(&d_roots, nr));
+            if (nr) GSI_CUDA(h2d(S, d_roots, roots.data(), 4ull * nr, st));
+            GSI_TRY(A.get(&M, nr));
+            unsigned tiles = grid_for(nr, kThreads);
+            GSI_TRY(A.get(&status, tiles + 1));
+            GSI_CUDA(cudaMemsetAsync(status, 0, 8ull * (tiles + 1), st));
+            prof.begin(GSI_K_COMPACT);
+            k_compact_roots<<<tiles, kThreads, 0, st>>>(d_roots, nr, bm1, M, status + 1, (unsigned *)status, C.ctr);
+            prof.end();
+            GSI_CUDA(d2h(S, &hc, C.ctr, sizeof(Counters), st));
+            GSI_CUDA(sync_timed(S, st));
+            nM = hc.total;
+            S.alg_bytes[GSI_K_COMPACT] += 8.0 * nr + 4.0 * nM;
+        } else {
+            nM = (unsigned long long)cand[u1];
+            GSI_TRY(A.get(&M, nM));
+            unsigned tiles = grid_for(words, kThreads);
+            GSI_TRY(A.get(&status, tiles + 1));
+            GSI_CUDA(cudaMemsetAsync(status, 0, 8ull * (tiles + 1), st));
+            prof.begin(GSI_K_COMPACT);
+            k_compact_bitmap<<<tiles, kThreads, 0, st>>>(bm1, words, M, status + 1, (unsigned *)status, C.ctr);
+            prof.end();
+            S.alg_bytes[GSI_K_COMPACT] += 4.0 * words + 4.0 * nM;
+        }
+        A.release(status);
+    }
+
+    gsi_status rc = GSI_OK;
+    if (!empty && k > 1 && opts.ablation) {
+        rc = run_ablation(C, M, nM);
+    } else if (!empty && k == 1) {
+        S.rows[0] = nM;
+        S.levels = 1;
+        StepParams P;
+        std::memset(&P, 0, sizeof(P));
+        P.k = 1;
+        P.t = 1;
+        GSI_CUDA(cudaMemsetAsync(C.ctr, 0, sizeof(Counters), st));
+        if (nM && opts.fingerprint) {
+            prof.begin(GSI_K_OTHER);
+            k_fp_rows<<<grid_for(nM, kThreads), kThreads, 0, st>>>(M, (long long)nM, P, C.ctr);
+            prof.end();
+        }
+        GSI_CUDA(d2h(S, &hc, C.ctr, sizeof(Counters), st));
+        GSI_CUDA(sync_timed(S, st));
+        C.count = nM;
+        C.fp1 = hc.fp1;
+        C.fp2 = hc.fp2;
+        if (opts.want_table && nM) {
+            GSI_TRY(table_put(C, M, nM));
+        }
+    } else if (!empty) {
+        // level-1 Prealloc (Alg. 4) on M_1 = C(pi_1)
+        StepParams P;
+        fill_params(C, C.steps[0], P, 1);
+        Loc *loc = nullptr;
+        unsigned long long *F = nullptr, *status = nullptr;
+        GSI_TRY(A.get(&loc, std::max<unsigned long long>(nM, 1) * (unsigned long long)P.E));
+        GSI_TRY(A.get(&F, nM + 1));
+        const unsigned ptiles = grid_for(nM, kThreads);
+        GSI_TRY(A.get(&status, ptiles + 1));
+        GSI_CUDA(cudaMemsetAsync(status, 0, 8ull * (ptiles + 1), st));
+        GSI_CUDA(cudaMemsetAsync(C.ctr, 0, sizeof(Counters), st));
+        GSI_CUDA(cudaMemsetAsync(F, 0, 8, st));
+        if (nM) {
+            prof.begin(GSI_K_PROBE);
+            k_probe<<<ptiles, kThreads, 0, st>>>(M, (long long)nM, P, g->groups, g->gpn, loc, F, status + 1,
+                                                 (unsigned *)status, C.ctr);
+            prof.end();
+        }
+        unsigned long long gba = 0;
+        GSI_CUDA(d2h(S, &gba, F + nM, 8, st));
+        GSI_CUDA(d2h(S, &hc, C.ctr, sizeof(Counters), st));
+        GSI_CUDA(sync_timed(S, st));
+        A.release(status);
+        S.alg_bytes[GSI_K_PROBE] += (double)nM * (20.0 * P.E + 8.0);
+        S.rows[0] += nM;
+        rc = level(C, 0, M, nM, loc, F, gba, hc.active_rows, hc.list_elems, false);
+        A.release(loc);
+        A.release(F);
+    }
+    if (M) A.release(M);
+    return rc;
+}
+
 gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_opts *opts_in, gsi_result **out) {
     *out = nullptr;
     if (!g || !q || q->g != g) {
@@ -4446,197 +4924,108 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     C.words = words;
 
     // device memory the query may use; the workspace grows to the demand seen so far
+    // (cudaMemGetInfo costs tens of microseconds: a query that fits the workspace it takes
+    // computes the budget only if it leaves the small path, in run_regular)
     unsigned long long budget = opts.mem_budget_bytes;
-    if (!budget) {
-        budget = (unsigned long long)(0.85 * (double)(available_bytes(g->device) + workspace_idle_bytes(g->device)));
-    }
+    if (!budget && !workspace_fits(g->device)) budget = device_budget(g->device, 0);
     const bool htrace = getenv("GSI_TRACE") != nullptr;
     if (htrace) fprintf(stderr, "[host] budget %.3f ms\n", now_ms() - t_start);
-    A.init_workspace(g->device, budget);
+    A.init_workspace(g->device, budget ? budget : ~(size_t)0);
     if (htrace) fprintf(stderr, "[host] workspace %.3f ms\n", now_ms() - t_start);
-    GSI_TRY(A.get(&C.ctr, 1));
+    // One zeroed pool per query (a single memset): the query counters, |C(u)|, the small
+    // path's output block, then the per-level counter / look-back slices (C.zoff).
+    uint32_t *bm = nullptr;
+    unsigned long long *d_counts = nullptr;
+    SmallOut *d_small = nullptr;
     {
         constexpr unsigned long long kZWords = 1ull << 17;   // 1 MB
+        constexpr unsigned long long kCtrW = (sizeof(Counters) + 31) / 32 * 4;
+        constexpr unsigned long long kSmallW = (sizeof(SmallOut) + 31) / 32 * 4;
         if (A.get_big(&C.zpool, kZWords) == GSI_OK && cudaMemsetAsync(C.zpool, 0, 8ull * kZWords, st) == cudaSuccess) {
             C.zcap = kZWords;
+            C.ctr = reinterpret_cast<Counters *>(C.zpool);
+            d_counts = C.zpool + kCtrW;
+            d_small = reinterpret_cast<SmallOut *>(C.zpool + kCtrW + 4 * ((GSI_MAX_K + 3) / 4));
+            C.zoff = kCtrW + 4 * ((GSI_MAX_K + 3) / 4) + kSmallW;
         } else {
             cudaGetLastError();
             C.zpool = nullptr;
+            GSI_TRY(A.get(&C.ctr, 1));
+            GSI_TRY(A.get(&d_counts, k));
+            GSI_TRY(A.get(&d_small, 1));
+            GSI_CUDA(cudaMemsetAsync(C.ctr, 0, sizeof(Counters), st));
+            GSI_CUDA(cudaMemsetAsync(d_counts, 0, 8ull * k, st));
+            GSI_CUDA(cudaMemsetAsync(d_small, 0, sizeof(SmallOut), st));
         }
     }
-    GSI_CUDA(cudaMemsetAsync(C.ctr, 0, sizeof(Counters), st));
     if (htrace) fprintf(stderr, "[host] zeroed %.3f ms\n", now_ms() - t_start);
 
     // ---------------- filter (a3) ----------------
-    uint32_t *bm = nullptr;
-    unsigned long long *d_counts = nullptr;
+    const bool small_try = small_apriori(C) && !g->ml;
+    uint16_t *grp = nullptr;
+    static int sms_cached[64] = {0};
+    int sms = g->device >= 0 && g->device < 64 ? sms_cached[g->device] : 0;
+    if (!sms) {
+        sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
+        if (g->device >= 0 && g->device < 64) sms_cached[g->device] = sms;
+    }
+    const int gw = filter_fw(words, sms);   // bitmap words per group count (= the filter's words per warp)
+    const long long ngrp = (words + gw - 1) / gw;
+    const long long ngrp_pad = (ngrp + 7) & ~7ll;
     GSI_TRY(A.get(&bm, (unsigned long long)words * k));
-    GSI_TRY(A.get(&d_counts, k));
-    GSI_CUDA(cudaMemsetAsync(d_counts, 0, 8ull * k, st));
+    if (small_try) GSI_TRY(A.get(&grp, (unsigned long long)ngrp_pad * k));
     C.bm = bm;
     {
-        int sms = 148;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
-        unsigned grid = (unsigned)std::min<long long>((words + 31) / 32, (long long)sms * 8);
-        if (grid < 1) grid = 1;
         prof.begin(GSI_K_FILTER);
         const uint32_t *qsig = q->d_qsig + (opts.homomorphism ? (size_t)k * kPlanes : 0);
         if (g->ml)   // multi-label: hashed label sets + exact refine (ext.cu)
             GSI_CUDA(launch_filter_ml(g, q, opts.homomorphism, bm, words, d_counts, st));
         else
-            k_filter<<<grid, kThreads, 0, st>>>(g->sig, n, k, qsig, opts.filter_mode == 1, bm, words, d_counts,
-                                                C.ctr);
+            GSI_CUDA(launch_filter(g->sig, n, k, qsig, opts.filter_mode == 1, bm, words, d_counts, C.ctr, grp, ngrp_pad,
+                                   sms, st));
         prof.end();
     }
+    if (htrace) fprintf(stderr, "[host] filter launched %.3f ms\n", now_ms() - t_start);
+    // the read-back block (pinned when available)
+    SmallOut hsmall_pageable;
+    SmallOut *hsmall = C.pinned ? &pinned.blk->so : &hsmall_pageable;
     std::vector<long long> cand(k);
-    Counters hc;
-    GSI_CUDA(d2h(S, cand.data(), d_counts, 8ull * k, st));
-    GSI_CUDA(d2h(S, &hc, C.ctr, sizeof(Counters), st));
-    GSI_CUDA(sync_timed(S, st));
-    GSI_CUDA(cudaGetLastError());
+    unsigned long long plane_loads = 0;
+    bool small_done = false;
+    if (small_try) {
+        // the whole query on the device if it is small; |C(u)| comes back in the same block
+        GSI_TRY(run_small(C, grp, ngrp, ngrp_pad, gw, d_counts, d_small, hsmall, small_done));
+        for (int u = 0; u < k; u++) cand[u] = (long long)hsmall->cand[u];
+        plane_loads = hsmall->plane_loads;
+    } else {
+        unsigned long long *hc_cand = C.pinned ? pinned.blk->cand : nullptr;
+        std::vector<unsigned long long> cand_pageable;
+        if (!hc_cand) {
+            cand_pageable.resize(k);
+            hc_cand = cand_pageable.data();
+        }
+        Counters hc_pageable;
+        Counters *hcp = C.pinned ? C.pinned : &hc_pageable;
+        GSI_CUDA(d2h(S, hc_cand, d_counts, 8ull * k, st));
+        GSI_CUDA(d2h(S, hcp, C.ctr, sizeof(Counters), st));
+        GSI_CUDA(sync_timed(S, st));
+        GSI_CUDA(cudaGetLastError());
+        for (int u = 0; u < k; u++) cand[u] = (long long)hc_cand[u];
+        plane_loads = hcp->plane_loads;
+    }
+    if (htrace) fprintf(stderr, "[host] read back %.3f ms\n", now_ms() - t_start);
     const double t_filter = now_ms();
     S.ms_filter = (float)(t_filter - t_start);
     for (int u = 0; u < k; u++) S.cand[u] = cand[u];
-    S.alg_bytes[GSI_K_FILTER] = 4.0 * n + 4.0 * hc.plane_loads + 4.0 * words * k;
-
-    // ---------------- plan (a4) ----------------
-    GSI_TRY(plan_order(q, cand, opts.force_order, C.order));
-    GSI_TRY(build_steps(q, C.order, opts.force_first_edge, C.steps));
-    for (int j = 0; j < k; j++) S.order[j] = C.order[j];
-    for (auto &s : C.steps) {
-        S.n_edges[s.t] = (int)s.col.size();
-        S.first_edge[s.t] = s.other[s.paper_e0];
-    }
-    C.pos_of_q.assign(k, 0);
-    for (int j = 0; j < k; j++) C.pos_of_q[C.order[j]] = j;
-    plan_layout(C, !opts.want_table && !opts.fingerprint && !opts.ablation);
-    const double t_plan = now_ms();
-    S.ms_plan = (float)(t_plan - t_filter);
-
-    // memory budget -> chunk capacity in GBA slots (bytes per slot per level: S,R 8 B,
-    // M' 4(t+1) B, the child level's loc/F 8E+8 B), over the k-1 levels that may nest.
-    {
-        // (the chunk capacity depends on the budget only, never on the workspace size, so the
-        // chunking of a query is reproducible)
-        int maxE = 1;
-        for (auto &s : C.steps) maxE = std::max(maxE, (int)s.col.size());
-        const double per_slot = 8.0 + 4.0 * (k + 1) + 8.0 * maxE + 8.0;
-        const double levels = std::max(1, k - 1);
-        C.cap_slots = (unsigned long long)std::max(1.0, budget / (per_slot * levels));
-        if (opts.chunk_slots) C.cap_slots = opts.chunk_slots;
-    }
-    C.shard_min = opts.shard_min_rows ? opts.shard_min_rows : 65536;
-    C.sharded = C.W == 1;
-    C.force_shared = (opts.force_paths & 1) != 0;
-    C.deadline = opts.timeout_s > 0 ? t_start + 1000.0 * opts.timeout_s : 0;
-
-    bool empty = q->absent_label;
-    for (int u = 0; u < k; u++) empty |= cand[u] == 0;
-
-    // ---------------- level 1 (a5) ----------------
-    int32_t *M = nullptr;
-    unsigned long long nM = 0;
-    const bool nM_known = true;   // |M_1|: |C(pi_1)| from the filter, or read back (roots hook)
-    if (!empty) {
-        unsigned long long *status = nullptr;
-        const int u1 = C.order[0];
-        const uint32_t *bm1 = bm + (long long)u1 * words;
-        if (opts.roots && opts.n_roots > 0) {
-            std::vector<int32_t> roots(opts.roots, opts.roots + opts.n_roots);
-            std::sort(roots.begin(), roots.end());
-            roots.erase(std::unique(roots.begin(), roots.end()), roots.end());
-            roots.erase(std::remove_if(roots.begin(), roots.end(), [&](int32_t v) { return v < 0 || v >= n; }),
-                        roots.end());
-            long long nr = (long long)roots.size();
-            int32_t *d_roots = nullptr;
-            GSI_TRY(A.get(&d_roots, nr));
-            if (nr) GSI_CUDA(h2d(S, d_roots, roots.data(), 4ull * nr, st));
-            GSI_TRY(A.get(&M, nr));
-            unsigned tiles = grid_for(nr, kThreads);
-            GSI_TRY(A.get(&status, tiles + 1));
-            GSI_CUDA(cudaMemsetAsync(status, 0, 8ull * (tiles + 1), st));
-            prof.begin(GSI_K_COMPACT);
-            k_compact_roots<<<tiles, kThreads, 0, st>>>(d_roots, nr, bm1, M, status + 1, (unsigned *)status, C.ctr);
-            prof.end();
-            GSI_CUDA(d2h(S, &hc, C.ctr, sizeof(Counters), st));
-            GSI_CUDA(sync_timed(S, st));
-            nM = hc.total;
-            S.alg_bytes[GSI_K_COMPACT] += 8.0 * nr + 4.0 * nM;
-        } else {
-            nM = (unsigned long long)cand[u1];
-            GSI_TRY(A.get(&M, nM));
-            unsigned tiles = grid_for(words, kThreads);
-            GSI_TRY(A.get(&status, tiles + 1));
-            GSI_CUDA(cudaMemsetAsync(status, 0, 8ull * (tiles + 1), st));
-            prof.begin(GSI_K_COMPACT);
-            k_compact_bitmap<<<tiles, kThreads, 0, st>>>(bm1, words, M, status + 1, (unsigned *)status, C.ctr);
-            prof.end();
-            S.alg_bytes[GSI_K_COMPACT] += 4.0 * words + 4.0 * nM;
-        }
-        A.release(status);
-    }
+    S.alg_bytes[GSI_K_FILTER] = 4.0 * n + 4.0 * plane_loads + 4.0 * words * k;
 
     gsi_status rc = GSI_OK;
-    bool small_done = false;
-    if (!empty && k > 1 && !opts.ablation && small_eligible(C, nM_known ? nM : 0, nM_known)) {
-        GSI_TRY(run_small(C, M, small_done));
+    double t_plan = t_filter;
+    if (!small_done) {
+        if (!budget) budget = device_budget(g->device, A.ws_dev >= 0 ? A.cap : 0);
+        rc = run_regular(C, cand, budget, t_start, t_filter, t_plan);
     }
-    if (small_done) {
-        // every level ran in k_small_query
-    } else if (!empty && k > 1 && opts.ablation) {
-        rc = run_ablation(C, M, nM);
-    } else if (!empty && k == 1) {
-        S.rows[0] = nM;
-        S.levels = 1;
-        StepParams P;
-        std::memset(&P, 0, sizeof(P));
-        P.k = 1;
-        P.t = 1;
-        GSI_CUDA(cudaMemsetAsync(C.ctr, 0, sizeof(Counters), st));
-        if (nM && opts.fingerprint) {
-            prof.begin(GSI_K_OTHER);
-            k_fp_rows<<<grid_for(nM, kThreads), kThreads, 0, st>>>(M, (long long)nM, P, C.ctr);
-            prof.end();
-        }
-        GSI_CUDA(d2h(S, &hc, C.ctr, sizeof(Counters), st));
-        GSI_CUDA(sync_timed(S, st));
-        C.count = nM;
-        C.fp1 = hc.fp1;
-        C.fp2 = hc.fp2;
-        if (opts.want_table && nM) {
-            GSI_TRY(table_put(C, M, nM));
-        }
-    } else if (!empty) {
-        // level-1 Prealloc (Alg. 4) on M_1 = C(pi_1)
-        StepParams P;
-        fill_params(C, C.steps[0], P, 1);
-        Loc *loc = nullptr;
-        unsigned long long *F = nullptr, *status = nullptr;
-        GSI_TRY(A.get(&loc, std::max<unsigned long long>(nM, 1) * (unsigned long long)P.E));
-        GSI_TRY(A.get(&F, nM + 1));
-        const unsigned ptiles = grid_for(nM, kThreads);
-        GSI_TRY(A.get(&status, ptiles + 1));
-        GSI_CUDA(cudaMemsetAsync(status, 0, 8ull * (ptiles + 1), st));
-        GSI_CUDA(cudaMemsetAsync(C.ctr, 0, sizeof(Counters), st));
-        GSI_CUDA(cudaMemsetAsync(F, 0, 8, st));
-        if (nM) {
-            prof.begin(GSI_K_PROBE);
-            k_probe<<<ptiles, kThreads, 0, st>>>(M, (long long)nM, P, g->groups, g->gpn, loc, F, status + 1,
-                                                 (unsigned *)status, C.ctr);
-            prof.end();
-        }
-        unsigned long long gba = 0;
-        GSI_CUDA(d2h(S, &gba, F + nM, 8, st));
-        GSI_CUDA(d2h(S, &hc, C.ctr, sizeof(Counters), st));
-        GSI_CUDA(sync_timed(S, st));
-        A.release(status);
-        S.alg_bytes[GSI_K_PROBE] += (double)nM * (20.0 * P.E + 8.0);
-        S.rows[0] += nM;
-        rc = level(C, 0, M, nM, loc, F, gba, hc.active_rows, hc.list_elems, false);
-        A.release(loc);
-        A.release(F);
-    }
-    if (M) A.release(M);
     if (rc != GSI_OK) {
         for (auto &p : C.pieces) cudaFreeAsync(p.first, st);
         cudaStreamSynchronize(st);
@@ -4779,12 +5168,11 @@ gsi_status debug_filter_prepared_impl(const gsi_prepared *p, int32_t mode, uint3
     GSI_TRY(A.get(&ctr, 1));
     GSI_CUDA(cudaMemsetAsync(cnt, 0, 8ull * k, st));
     GSI_CUDA(cudaMemsetAsync(ctr, 0, sizeof(Counters), st));
-    unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>((words + 7) / 8, 148 * 8));
     const uint32_t *qsig = p->d_qsig + (mode == 2 ? (size_t)k * kPlanes : 0);   // 2: homomorphism encoding
     if (g->ml)
         GSI_CUDA(launch_filter_ml(g, p, mode == 2, bm, words, cnt, st));
     else
-        k_filter<<<grid, kThreads, 0, st>>>(g->sig, n, k, qsig, mode == 1, bm, words, cnt, ctr);
+        GSI_CUDA(launch_filter(g->sig, n, k, qsig, mode == 1, bm, words, cnt, ctr, nullptr, 0, 148, st));
     if (bitmaps && words)
         GSI_CUDA(cudaMemcpyAsync(bitmaps, bm, 4ull * words * k, cudaMemcpyDeviceToHost, st));
     std::vector<unsigned long long> hc(k);
