@@ -360,21 +360,238 @@ __global__ void __launch_bounds__(kThreads, GSI_FILTER_MINB) k_filter(const uint
     if (threadIdx.x == 0 && loads_s) atomicAdd(&ctr->plane_loads, loads_s);
 }
 
-// Words-per-warp variant of k_filter for a graph: FW = 1 while one wave of the device still
-// takes at most ~4 iterations per warp (small graphs: parallelism and L2 reuse), else 8.
-inline int filter_fw(long long words, int sms) { return words <= (long long)sms * 8 * 8 * 4 ? 1 : 8; }
+// Large graphs: one thread per bitmap word (32 consecutive vertices), so the k output words of
+// a word are assembled with bit operations instead of one warp ballot per (word, query vertex).
+// Phase A: the thread reads its 32 plane-0 labels (eight 16 B loads) and marks the vertices
+// whose label some query vertex has (a register copy of the hash table's occupancy rejects most
+// labels without a shared-memory probe).  Phase B: the warp queues the marked vertices
+// (vertex id, candidate mask) in shared memory and tests the needed planes on the queue in
+// rounds, 32 lanes × up to kTwCols dense columns, exactly as k_filter; a survivor sets its
+// bit of every remaining u in the warp's shared output tile.  Phase C: thread w stores word w
+// of every C(u) — coalesced 128 B per u across the warp — and the warp sums |C(u)| per group
+// of 32 words (grp, gw = 32).
+constexpr int kTwCols = 8;                       // queue columns per round (256 entries per warp)
+constexpr int kTwWarps = kThreads / 32;
+inline size_t filter_tw_smem(int k) { return (size_t)kTwWarps * (32 * kTwCols * 8 + (size_t)k * 32 * 4); }
+
+__device__ __forceinline__ uint32_t ht_lookup(const uint32_t *ht_lab, const uint32_t *ht_mask, uint32_t L) {
+    constexpr int kHT = 64;
+    uint32_t h = (L * 0x9E3779B1u) >> 26, e;
+    while ((e = ht_lab[h]) != L && e != 0xFFFFFFFFu) h = (h + 1) & (kHT - 1);
+    return e == L ? ht_mask[h] : 0u;
+}
+
+__global__ void __launch_bounds__(kThreads, 4) k_filter_tw(const uint32_t *__restrict__ sig, long long n, int k,
+                                                           const uint32_t *__restrict__ qsig, int label_only,
+                                                           uint32_t *__restrict__ bitmaps, long long words,
+                                                           unsigned long long *__restrict__ counts,
+                                                           Counters *__restrict__ ctr,
+                                                           uint16_t *__restrict__ grp, long long grp_stride) {
+    constexpr int kHT = 64;
+    constexpr int kCap = 32 * kTwCols;
+    __shared__ uint32_t qs[GSI_MAX_K * kPlanes];
+    __shared__ uint32_t qneed[GSI_MAX_K];
+    __shared__ uint32_t ht_lab[kHT], ht_mask[kHT];
+    __shared__ unsigned long long occ_s;
+    __shared__ unsigned long long cnt_s[GSI_MAX_K];
+    __shared__ unsigned long long loads_s;
+    extern __shared__ __align__(16) uint32_t tw_dyn[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t *const q_v = tw_dyn + wid * (kCap * 2);             // queued vertex ids
+    uint32_t *const q_m = q_v + kCap;                             // their candidate masks
+    uint32_t *const outw = tw_dyn + kTwWarps * kCap * 2 + wid * k * 32;   // [u][word in the warp]
+    for (int i = threadIdx.x; i < k * kPlanes; i += blockDim.x) qs[i] = qsig[i];
+    if (threadIdx.x < GSI_MAX_K) cnt_s[threadIdx.x] = 0;
+    if (threadIdx.x < kHT) {
+        ht_lab[threadIdx.x] = 0xFFFFFFFFu;
+        ht_mask[threadIdx.x] = 0u;
+    }
+    if (threadIdx.x == 0) loads_s = 0;
+    for (int i = lane; i < k * 32; i += 32) outw[i] = 0u;
+    __syncthreads();
+    if (threadIdx.x < k) {
+        uint32_t m = 0;
+        for (int pl = 1; pl < kPlanes; pl++)
+            if (qs[threadIdx.x * kPlanes + pl]) m |= 1u << pl;
+        qneed[threadIdx.x] = m;
+    }
+    if (threadIdx.x == 0) {
+        unsigned long long occ = 0;
+        for (int u = 0; u < k; u++) {
+            const uint32_t L = qs[u * kPlanes];
+            uint32_t h = (L * 0x9E3779B1u) >> 26;
+            while (ht_lab[h] != 0xFFFFFFFFu && ht_lab[h] != L) h = (h + 1) & (kHT - 1);
+            ht_lab[h] = L;
+            ht_mask[h] |= 1u << u;
+            occ |= 1ull << h;
+        }
+        occ_s = occ;
+    }
+    __syncthreads();
+    const unsigned long long occ = occ_s;   // slot h empty => no query vertex has a label hashing to h
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const long long nwarps = (long long)gridDim.x * kTwWarps;
+    unsigned long long plane_words = 0, my_count = 0;
+    for (long long wb = (blockIdx.x * (long long)kTwWarps + wid) * 32; wb < words; wb += nwarps * 32) {
+        const long long w = wb + lane;
+        const long long v0 = w * 32;
+        // ---- phase A: this word's label matches
+        uint32_t mb = 0u;
+        if (w < words) {
+            const uint4 *src = reinterpret_cast<const uint4 *>(sig + v0);
+            const int nv = (int)min(32ll, n - v0);
+#pragma unroll
+            for (int c = 0; c < 8; c++) {
+                const uint4 l4 = __ldg(src + c);
+                const uint32_t l[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    const int b = c * 4 + i;
+                    const uint32_t h = (l[i] * 0x9E3779B1u) >> 26;
+                    if (b < nv && ((occ >> h) & 1ull) && ht_lookup(ht_lab, ht_mask, l[i])) mb |= 1u << b;
+                }
+            }
+        }
+        if (label_only) {
+            // C(u) by label alone: every marked vertex joins all its label's query vertices
+            uint32_t rem = mb;
+            while (rem) {
+                const int b = __ffs(rem) - 1;
+                rem &= rem - 1;
+                uint32_t m = ht_lookup(ht_lab, ht_mask, __ldg(sig + v0 + b));
+                while (m) {
+                    const int u = __ffs(m) - 1;
+                    m &= m - 1;
+                    atomicOr(&outw[u * 32 + lane], 1u << b);
+                }
+            }
+        } else {
+            // ---- phase B: queue the marked vertices, test their planes in rounds
+            uint32_t rem = mb;
+            int qn = 0;
+            for (;;) {
+                const bool more = __any_sync(0xffffffffu, rem != 0u);
+                if (more) {
+                    const bool act = rem != 0u;
+                    const unsigned bal = __ballot_sync(0xffffffffu, act);
+                    if (act) {
+                        const int b = __ffs(rem) - 1;
+                        rem &= rem - 1;
+                        const int p = qn + __popc(bal & lt_mask);
+                        q_v[p] = (uint32_t)(v0 + b);
+                        q_m[p] = ht_lookup(ht_lab, ht_mask, __ldg(sig + v0 + b));
+                    }
+                    qn += __popc(bal);
+                }
+                if (qn == 0 && !more) break;
+                if (qn > kCap - 32 || !more) {
+                    __syncwarp();
+                    const int nc = (qn + 31) >> 5;
+                    uint32_t m[kTwCols], need[kTwCols], vv[kTwCols];
+#pragma unroll
+                    for (int c = 0; c < kTwCols; c++) {
+                        const int i = c * 32 + lane;
+                        m[c] = 0u;
+                        need[c] = 0u;
+                        vv[c] = 0u;
+                        if (c < nc && i < qn) {
+                            vv[c] = q_v[i];
+                            m[c] = q_m[i];
+                            uint32_t t = m[c];
+                            while (t) {
+                                need[c] |= qneed[__ffs(t) - 1];
+                                t &= t - 1;
+                            }
+                        }
+                    }
+                    for (int round = 0; round < kPlanes; round++) {
+                        uint32_t pv[kTwCols];
+                        int pls[kTwCols];
+                        bool any = false;
+#pragma unroll
+                        for (int c = 0; c < kTwCols; c++) {
+                            pls[c] = -1;
+                            pv[c] = 0u;
+                            if (c < nc && m[c] && need[c]) {
+                                pls[c] = __ffs(need[c]) - 1;
+                                pv[c] = __ldcs(sig + (long long)pls[c] * n + vv[c]);
+                                any = true;
+                            }
+                        }
+                        if (!__any_sync(0xffffffffu, any)) break;
+#pragma unroll
+                        for (int c = 0; c < kTwCols; c++) {
+                            if (pls[c] < 0) continue;
+                            need[c] &= ~(1u << pls[c]);
+                            plane_words++;
+                            uint32_t t = m[c];
+                            while (t) {
+                                const int u = __ffs(t) - 1;
+                                t &= t - 1;
+                                const uint32_t sq = qs[u * kPlanes + pls[c]];
+                                if ((pv[c] & sq) != sq) m[c] &= ~(1u << u);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int c = 0; c < kTwCols; c++) {
+                        uint32_t t = m[c];
+                        if (!t) continue;
+                        const uint32_t wl = (uint32_t)((long long)(vv[c] >> 5) - wb), bit = 1u << (vv[c] & 31);
+                        while (t) {
+                            const int u = __ffs(t) - 1;
+                            t &= t - 1;
+                            atomicOr(&outw[u * 32 + wl], bit);
+                        }
+                    }
+                    __syncwarp();
+                    qn = 0;
+                    if (!more) break;
+                }
+            }
+        }
+        __syncwarp();
+        // ---- phase C: word w of every C(u), coalesced per u; |C(u)| per 32-word group
+        for (int u = 0; u < k; u++) {
+            const uint32_t word = outw[u * 32 + lane];
+            outw[u * 32 + lane] = 0u;
+            if (w < words) bitmaps[(long long)u * words + w] = word;
+            const unsigned c = __reduce_add_sync(0xffffffffu, (unsigned)__popc(word));
+            if (lane == u) {
+                my_count += c;
+                if (grp) grp[(long long)u * grp_stride + wb / 32] = (uint16_t)c;
+            }
+        }
+        __syncwarp();
+    }
+    if (lane < k && my_count) atomicAdd(&cnt_s[lane], my_count);
+    plane_words = warp_sum_u64(plane_words);
+    if (lane == 0 && plane_words) atomicAdd(&loads_s, plane_words);
+    __syncthreads();
+    if (threadIdx.x < k && cnt_s[threadIdx.x]) atomicAdd(&counts[threadIdx.x], cnt_s[threadIdx.x]);
+    if (threadIdx.x == 0 && loads_s) atomicAdd(&ctr->plane_loads, loads_s);
+}
+
+// Filter variant for a graph: the warp-per-word kernel (FW = 1) while one wave of the device
+// still takes at most ~4 iterations per warp (small graphs: parallelism and L2 reuse), else the
+// thread-per-word kernel.  Returns the group width of the per-group counts (grp).
+inline int filter_fw(long long words, int sms) { return words <= (long long)sms * 8 * 8 * 4 ? 1 : 32; }
 
 cudaError_t launch_filter(const uint32_t *sig, long long n, int k, const uint32_t *qsig, int label_only,
                           uint32_t *bm, long long words, unsigned long long *counts, Counters *ctr, uint16_t *grp,
                           long long grp_stride, int sms, cudaStream_t st) {
-    const int fw = filter_fw(words, sms);
-    const long long per_cta = (long long)fw * (kThreads / 32);
-    const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>((words + per_cta - 1) / per_cta,
-                                                                                (long long)sms * 8));
-    if (fw == 1)
+    if (filter_fw(words, sms) == 1) {
+        const long long per_cta = kThreads / 32;
+        const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>((words + per_cta - 1) / per_cta,
+                                                                                    (long long)sms * 8));
         k_filter<1><<<grid, kThreads, 0, st>>>(sig, n, k, qsig, label_only, bm, words, counts, ctr, grp, grp_stride);
-    else
-        k_filter<8><<<grid, kThreads, 0, st>>>(sig, n, k, qsig, label_only, bm, words, counts, ctr, grp, grp_stride);
+    } else {
+        const long long per_cta = 32ll * kTwWarps;
+        const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>((words + per_cta - 1) / per_cta,
+                                                                                    (long long)sms * 4));
+        k_filter_tw<<<grid, kThreads, filter_tw_smem(k), st>>>(sig, n, k, qsig, label_only, bm, words, counts, ctr,
+                                                                grp, grp_stride);
+    }
     return cudaGetLastError();
 }
 
@@ -2613,6 +2830,7 @@ struct SmallOut {
     unsigned long long plane_loads;
     int order[GSI_MAX_K];                     // pi
     int n_edges[GSI_MAX_K], first_edge[GSI_MAX_K];
+    long long clk[GSI_MAX_K + 2];             // SM clock at: start, plan done, M_1 done, level t done (GSI_TRACE)
 };
 
 // Warp 0 plans (lane u = query vertex u, lane j = step j): Alg. 2's order with the same
@@ -2738,6 +2956,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const __grid_c
     const int k = Q.k;
     // ---- plan (Alg. 2) from |C(u)| (warp 0) ---------------------------------------------
     __shared__ int order_s[GSI_MAX_K], pos_s[GSI_MAX_K];
+    if (tid == 0) out->clk[0] = clock64();
     if (tid < k) out->cand[tid] = Q.cand[tid];
     if (warp == 0) {
         bool any0 = lane < k && Q.cand[lane] == 0;
@@ -2755,6 +2974,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const __grid_c
     }
     __syncthreads();
     if (fail_s) return;
+    if (tid == 0) out->clk[1] = clock64();
     // ---- level 1 (Alg. 2 line 7): M_1 = C(pi_1) ascending, from the per-group counts ------
     // Each thread sums a contiguous, 16 B aligned range of groups (vector loads, all in flight
     // at once); one block scan gives every thread its output offset and its first
@@ -2811,6 +3031,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const __grid_c
         }
         __syncthreads();   // M_1 written before level 1 reads it; Fs free again
     }
+    if (tid == 0) out->clk[2] = clock64();
     if (tid == 0) out->rows[0] = nM;
     // rows of the current level: a shared-memory buffer when they fit, else bufA / bufB
     const int32_t *cur = sA;
@@ -2954,6 +3175,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const __grid_c
         __syncthreads();   // every row of the next level written before it is read
         if (last) {
             if (tid == 0) {
+                out->clk[2 + t] = clock64();
                 const unsigned long long c = Q.want_table ? nout : cnt_s;
                 out->count = c;
                 out->nout = nout;
@@ -2964,7 +3186,10 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const __grid_c
             }
             return;
         }
-        if (tid == 0) out->rows[t] = nout;
+        if (tid == 0) {
+            out->rows[t] = nout;
+            out->clk[2 + t] = clock64();
+        }
         nM = nout;
         cur = nxt;
         if (nM == 0) break;
@@ -3357,6 +3582,7 @@ void ensure_pool(int dev) {
     cudaFuncSetAttribute(k_join<J_CAHEAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxJoinSmem);
     cudaFuncSetAttribute(k_count_fast<kFastItems>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxJoinSmem);
     cudaFuncSetAttribute(k_small_query, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmallDynSmem);
+    cudaFuncSetAttribute(k_filter_tw, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)filter_tw_smem(GSI_MAX_K));
     cudaGetLastError();
     g_pool_ready[dev] = true;
 }
@@ -4480,6 +4706,16 @@ gsi_status run_small(QueryCtx &C, const uint16_t *grp, long long ngrp, long long
         return GSI_OK;
     }
     const SmallOut &h = *hout;
+    if (getenv("GSI_TRACE")) {   // device phase times (SM clock cycles -> us at the current SM clock)
+        int khz = 0;
+        cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, g->device);
+        const double us = khz > 0 ? 1000.0 / khz : 0.0;
+        fprintf(stderr, "[small] plan %.2f us, M1 %.2f us, levels", (h.clk[1] - h.clk[0]) * us, (h.clk[2] - h.clk[1]) * us);
+        for (int t = 1; t < k && h.clk[2 + t]; t++) fprintf(stderr, " %.2f", (h.clk[2 + t] - h.clk[1 + t]) * us);
+        fprintf(stderr, " (rows");
+        for (int t = 0; t < k; t++) fprintf(stderr, " %llu", h.rows[t]);
+        fprintf(stderr, ")\n");
+    }
     for (int j = 0; j < k; j++) S.order[j] = h.order[j];
     for (int t = 1; t < k; t++) {
         S.n_edges[t] = h.n_edges[t];
@@ -5159,6 +5395,7 @@ gsi_status debug_filter_prepared_impl(const gsi_prepared *p, int32_t mode, uint3
     GSI_CUDA(cudaSetDevice(p->device));
     cudaStream_t st = cudaStreamPerThread;
     const long long n = g->n, words = (n + 31) / 32;
+    ensure_pool(p->device);
     Arena A(st);
     uint32_t *bm = nullptr;
     unsigned long long *cnt = nullptr;

@@ -145,13 +145,21 @@ def test_signature_table_bit_exact():
 
 
 @pytest.mark.parametrize("mode", [0, 1, 2])
-def test_filter_bitmaps_bit_exact(mode):
-    g = W.chung_lu(5000, 30000, 600, nlv=5, nle=7, seed=23)
+@pytest.mark.parametrize("size", ["small", "large"])
+def test_filter_bitmaps_bit_exact(mode, size):
+    """Both filter kernels: warp per word (small graphs) and thread per word (n > ~1.2 M; a
+    ragged last word, 8- and 24-vertex queries)."""
+    if size == "small":
+        g = W.chung_lu(5000, 30000, 600, nlv=5, nle=7, seed=23)
+        ks = [8] * 6
+    else:
+        g = W.chung_lu(1_500_007, 6_000_000, 3000, nlv=40, nle=7, seed=23)
+        ks = [8, 24, 12]
     graph = gsi.build(g)
     og = oracle.OracleGraph(g)
     planes = oracle.signatures(og)
-    for s in range(6):
-        q = W.random_walk_query(g, 8, 300 + s)
+    for s, kq in enumerate(ks):
+        q = W.random_walk_query(g, kq, 300 + s)
         bm, cnt = gsi.gsi_debug_filter(graph, q.vlabels, q.src, q.dst, q.elabels, filter_mode=mode)
         if mode in (0, 2):
             obm, ocnt = oracle.filter(og, planes, oracle.query_signatures(q, distinct=mode == 2))
