@@ -371,6 +371,7 @@ __global__ void __launch_bounds__(kThreads, GSI_FILTER_MINB) k_filter(const uint
 // of every C(u) — coalesced 128 B per u across the warp — and the warp sums |C(u)| per group
 // of 32 words (grp, gw = 32).
 constexpr int kTwCols = 8;                       // queue columns per round (256 entries per warp)
+constexpr int kTwLabelBits = 4096;               // labels below this are matched exactly by a bit test
 constexpr int kTwWarps = kThreads / 32;
 inline size_t filter_tw_smem(int k) { return (size_t)kTwWarps * (32 * kTwCols * 8 + (size_t)k * 32 * 4); }
 
@@ -379,6 +380,73 @@ __device__ __forceinline__ uint32_t ht_lookup(const uint32_t *ht_lab, const uint
     uint32_t h = (L * 0x9E3779B1u) >> 26, e;
     while ((e = ht_lab[h]) != L && e != 0xFFFFFFFFu) h = (h + 1) & (kHT - 1);
     return e == L ? ht_mask[h] : 0u;
+}
+
+// Plane rounds on a warp's queue of qn <= 32·NC label-matched vertices (k_filter_tw phase B):
+// lane takes entries lane + 32c; each round issues the next needed plane load of every entry
+// before testing any; a survivor sets its bit of each remaining u in the output tile.
+template <int NC>
+__device__ __forceinline__ void tw_rounds(const uint32_t *q_v, const uint32_t *q_m, int qn, const uint32_t *qneed,
+                                          const uint32_t *qs, const uint32_t *__restrict__ sig, long long n,
+                                          uint32_t *outw, long long wb, unsigned long long &plane_words) {
+    const int lane = threadIdx.x & 31;
+    uint32_t m[NC], need[NC], vv[NC];
+#pragma unroll
+    for (int c = 0; c < NC; c++) {
+        const int i = c * 32 + lane;
+        m[c] = 0u;
+        need[c] = 0u;
+        vv[c] = 0u;
+        if (i < qn) {
+            vv[c] = q_v[i];
+            m[c] = q_m[i];
+            uint32_t t = m[c];
+            while (t) {
+                need[c] |= qneed[__ffs(t) - 1];
+                t &= t - 1;
+            }
+        }
+    }
+    for (int round = 0; round < kPlanes; round++) {
+        uint32_t pv[NC];
+        int pls[NC];
+        bool any = false;
+#pragma unroll
+        for (int c = 0; c < NC; c++) {
+            pls[c] = -1;
+            pv[c] = 0u;
+            if (m[c] && need[c]) {
+                pls[c] = __ffs(need[c]) - 1;
+                pv[c] = __ldcs(sig + (long long)pls[c] * n + vv[c]);
+                any = true;
+            }
+        }
+        if (!__any_sync(0xffffffffu, any)) break;
+#pragma unroll
+        for (int c = 0; c < NC; c++) {
+            if (pls[c] < 0) continue;
+            need[c] &= ~(1u << pls[c]);
+            plane_words++;
+            uint32_t t = m[c];
+            while (t) {
+                const int u = __ffs(t) - 1;
+                t &= t - 1;
+                const uint32_t sq = qs[u * kPlanes + pls[c]];
+                if ((pv[c] & sq) != sq) m[c] &= ~(1u << u);   // S(v)&S(u)=S(u) fails on this plane
+            }
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < NC; c++) {
+        uint32_t t = m[c];
+        if (!t) continue;
+        const uint32_t wl = (uint32_t)((long long)(vv[c] >> 5) - wb), bit = 1u << (vv[c] & 31);
+        while (t) {
+            const int u = __ffs(t) - 1;
+            t &= t - 1;
+            atomicOr(&outw[u * 32 + wl], bit);
+        }
+    }
 }
 
 __global__ void __launch_bounds__(kThreads, 4) k_filter_tw(const uint32_t *__restrict__ sig, long long n, int k,
@@ -393,6 +461,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_filter_tw(const uint32_t *__res
     __shared__ uint32_t qneed[GSI_MAX_K];
     __shared__ uint32_t ht_lab[kHT], ht_mask[kHT];
     __shared__ unsigned long long occ_s;
+    __shared__ uint32_t lbits[kTwLabelBits / 32];   // bit L: some query vertex has label L (L < 4096)
     __shared__ unsigned long long cnt_s[GSI_MAX_K];
     __shared__ unsigned long long loads_s;
     extern __shared__ __align__(16) uint32_t tw_dyn[];
@@ -408,7 +477,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_filter_tw(const uint32_t *__res
     }
     if (threadIdx.x == 0) loads_s = 0;
     for (int i = lane; i < k * 32; i += 32) outw[i] = 0u;
+    for (int i = threadIdx.x; i < kTwLabelBits / 32; i += blockDim.x) lbits[i] = 0u;
     __syncthreads();
+    if (threadIdx.x < k && qs[threadIdx.x * kPlanes] < (uint32_t)kTwLabelBits)
+        atomicOr(&lbits[qs[threadIdx.x * kPlanes] >> 5], 1u << (qs[threadIdx.x * kPlanes] & 31));
     if (threadIdx.x < k) {
         uint32_t m = 0;
         for (int pl = 1; pl < kPlanes; pl++)
@@ -446,9 +518,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_filter_tw(const uint32_t *__res
                 const uint32_t l[4] = {l4.x, l4.y, l4.z, l4.w};
 #pragma unroll
                 for (int i = 0; i < 4; i++) {
+                    // exact for labels < 4096 (one shared-memory bit), else the hash table's
+                    // occupancy (a candidate only; the probe below decides)
                     const int b = c * 4 + i;
-                    const uint32_t h = (l[i] * 0x9E3779B1u) >> 26;
-                    if (b < nv && ((occ >> h) & 1ull) && ht_lookup(ht_lab, ht_mask, l[i])) mb |= 1u << b;
+                    const uint32_t L = l[i];
+                    const bool hit = L < (uint32_t)kTwLabelBits ? (lbits[L >> 5] >> (L & 31)) & 1u
+                                                                : (occ >> ((L * 0x9E3779B1u) >> 26)) & 1ull;
+                    if (b < nv && hit) mb |= 1u << b;
                 }
             }
         }
@@ -486,64 +562,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_filter_tw(const uint32_t *__res
                 if (qn == 0 && !more) break;
                 if (qn > kCap - 32 || !more) {
                     __syncwarp();
-                    const int nc = (qn + 31) >> 5;
-                    uint32_t m[kTwCols], need[kTwCols], vv[kTwCols];
-#pragma unroll
-                    for (int c = 0; c < kTwCols; c++) {
-                        const int i = c * 32 + lane;
-                        m[c] = 0u;
-                        need[c] = 0u;
-                        vv[c] = 0u;
-                        if (c < nc && i < qn) {
-                            vv[c] = q_v[i];
-                            m[c] = q_m[i];
-                            uint32_t t = m[c];
-                            while (t) {
-                                need[c] |= qneed[__ffs(t) - 1];
-                                t &= t - 1;
-                            }
-                        }
-                    }
-                    for (int round = 0; round < kPlanes; round++) {
-                        uint32_t pv[kTwCols];
-                        int pls[kTwCols];
-                        bool any = false;
-#pragma unroll
-                        for (int c = 0; c < kTwCols; c++) {
-                            pls[c] = -1;
-                            pv[c] = 0u;
-                            if (c < nc && m[c] && need[c]) {
-                                pls[c] = __ffs(need[c]) - 1;
-                                pv[c] = __ldcs(sig + (long long)pls[c] * n + vv[c]);
-                                any = true;
-                            }
-                        }
-                        if (!__any_sync(0xffffffffu, any)) break;
-#pragma unroll
-                        for (int c = 0; c < kTwCols; c++) {
-                            if (pls[c] < 0) continue;
-                            need[c] &= ~(1u << pls[c]);
-                            plane_words++;
-                            uint32_t t = m[c];
-                            while (t) {
-                                const int u = __ffs(t) - 1;
-                                t &= t - 1;
-                                const uint32_t sq = qs[u * kPlanes + pls[c]];
-                                if ((pv[c] & sq) != sq) m[c] &= ~(1u << u);
-                            }
-                        }
-                    }
-#pragma unroll
-                    for (int c = 0; c < kTwCols; c++) {
-                        uint32_t t = m[c];
-                        if (!t) continue;
-                        const uint32_t wl = (uint32_t)((long long)(vv[c] >> 5) - wb), bit = 1u << (vv[c] & 31);
-                        while (t) {
-                            const int u = __ffs(t) - 1;
-                            t &= t - 1;
-                            atomicOr(&outw[u * 32 + wl], bit);
-                        }
-                    }
+                    const int nc = (qn + 31) >> 5;   // dense columns: the rounds run on NC >= nc
+                    if (nc <= 1) tw_rounds<1>(q_v, q_m, qn, qneed, qs, sig, n, outw, wb, plane_words);
+                    else if (nc <= 2) tw_rounds<2>(q_v, q_m, qn, qneed, qs, sig, n, outw, wb, plane_words);
+                    else if (nc <= 4) tw_rounds<4>(q_v, q_m, qn, qneed, qs, sig, n, outw, wb, plane_words);
+                    else tw_rounds<kTwCols>(q_v, q_m, qn, qneed, qs, sig, n, outw, wb, plane_words);
                     __syncwarp();
                     qn = 0;
                     if (!more) break;
@@ -2803,12 +2826,13 @@ struct SmallPlan {
     SmallStep st[GSI_MAX_K - 1];   // st[j]: the step joining column j + 1 (j + 1 columns before it)
 };
 // The query as the device planner reads it (passed by value, ~2.5 KB).
-struct SmallQuery {
+struct __align__(16) SmallQuery {
     int k, qm, homo, want_table, fp, gpn;
     int qvl[GSI_MAX_K];
     int qs[kSmallMaxQE], qd[kSmallMaxQE];
     int lab[kSmallMaxQE], rawlab[kSmallMaxQE];   // dense / raw edge label
     long long freq[kSmallMaxQE];                 // |E(P(G, lab))|
+    uint64_t freqd[kSmallMaxQE];                 // the same as a double's bit pattern
     unsigned long long gbase[kSmallMaxQE];
     uint32_t ngroups[kSmallMaxQE];
     const uint32_t *bm;                          // the filter's bitmaps [k][words]
@@ -2829,42 +2853,48 @@ struct SmallOut {
     unsigned long long cand[GSI_MAX_K];       // |C(u)| (copied for the host: one read-back)
     unsigned long long plane_loads;
     int order[GSI_MAX_K];                     // pi
-    int n_edges[GSI_MAX_K], first_edge[GSI_MAX_K];
     long long clk[GSI_MAX_K + 2];             // SM clock at: start, plan done, M_1 done, level t done (GSI_TRACE)
+    long long clkp[4];                        // plan phases: query copied, -, planned, flags
 };
 
 // Warp 0 plans (lane u = query vertex u, lane j = step j): Alg. 2's order with the same
-// arithmetic and tie rule as plan_greedy (lane o multiplies its own score by freq(l(e)) for the
-// edges e of the taken vertex in query-edge order, exactly the sequence plan_greedy applies to
-// score[o]; the argmin is lexicographic in (score, id), i.e. the first smallest id), then the
-// steps — linking columns, labels, subtraction columns — one lane per step.  Returns (on every
-// lane) 0, or 1 if the query is disconnected or a step does not fit the kernel's limits.
-__device__ int small_plan_warp(const SmallQuery &Q, SmallPlan &sp, SmallOut *out, int *order_s, int *pos_s) {
+// arithmetic and tie rule as plan_greedy — scores kept as bit patterns of non-negative doubles
+// (ordered like unsigned integers), one correctly rounded division per lane, the products by
+// freq(l(e)) in query-edge order through dmul_pos (lane o applies the edges between o and the
+// taken vertex, in edge order, exactly the sequence plan_greedy applies to score[o]), the argmin
+// lexicographic in (score, id) — then the steps (linking columns, labels, subtraction columns),
+// one lane per step.  The paper's e0 (a statistic here) is derived on the host afterwards.
+// Returns (on every lane) 0, or 1 if the query is disconnected or a step does not fit.
+__device__ int small_plan_warp(const SmallQuery &Q, SmallPlan &sp, SmallOut *out, int *order_s, int *pos_s,
+                               int *inc_e) {
     const int lane = threadIdx.x & 31, k = Q.k, qm = Q.qm;
-    int deg = 0;
+    int deg = 0, nmy = 0;
     uint32_t adj = 0u;
-    for (int e = 0; e < qm; e++) {   // uniform e: broadcast reads of the parameter block
-        if (Q.qs[e] == lane) {
+    int *my = inc_e + lane * kSmallMaxQE;   // this lane's incident edges, in edge order
+    for (int e = 0; e < qm; e++) {           // uniform e: broadcast shared-memory reads
+        const int a = Q.qs[e], b = Q.qd[e];
+        if (a == lane) {
             deg++;
-            adj |= 1u << Q.qd[e];
+            adj |= 1u << b;
         }
-        if (Q.qd[e] == lane) {
+        if (b == lane) {
             deg++;
-            adj |= 1u << Q.qs[e];
+            adj |= 1u << a;
         }
+        if (a == lane || b == lane) my[nmy++] = e;
     }
-    double score = 0.0;
-    if (lane < k) score = deg ? (double)Q.cand[lane] / deg : (double)Q.cand[lane];
+    uint64_t score = 0;
+    if (lane < k) score = dbl_bits(deg ? (double)Q.cand[lane] / deg : (double)Q.cand[lane]);
     uint32_t in = 0u;
     for (int i = 0; i < k; i++) {
         const bool ok = lane < k && !((in >> lane) & 1u) && (i == 0 || (adj & in));
-        double bs = score;
+        uint64_t bs = ok ? score : ~0ull;
         int bu = ok ? lane : 32;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-            const double s2 = __shfl_xor_sync(0xffffffffu, bs, o);
+            const uint64_t s2 = __shfl_xor_sync(0xffffffffu, bs, o);
             const int u2 = __shfl_xor_sync(0xffffffffu, bu, o);
-            if (u2 < 32 && (bu == 32 || s2 < bs || (s2 == bs && u2 < bu))) {
+            if (s2 < bs || (s2 == bs && u2 < bu)) {
                 bs = s2;
                 bu = u2;
             }
@@ -2872,10 +2902,11 @@ __device__ int small_plan_warp(const SmallQuery &Q, SmallPlan &sp, SmallOut *out
         if (bu == 32) return 1;   // disconnected query
         if (lane == 0) order_s[i] = bu;
         in |= 1u << bu;
-        for (int e = 0; e < qm; e++) {
-            const int o = Q.qs[e] == bu ? Q.qd[e] : (Q.qd[e] == bu ? Q.qs[e] : -1);
-            if (o == lane) score *= (double)Q.freq[e];
-        }
+        if ((adj >> bu) & 1u)
+            for (int j = 0; j < nmy; j++) {
+                const int e = my[j];
+                if (Q.qs[e] == bu || Q.qd[e] == bu) score = dmul_pos(score, Q.freqd[e]);
+            }
     }
     __syncwarp();
     if (lane < k) {
@@ -2890,9 +2921,8 @@ __device__ int small_plan_warp(const SmallQuery &Q, SmallPlan &sp, SmallOut *out
     if (j >= 1 && j < k) {
         SmallStep &T = sp.st[j - 1];
         const int u = order_s[j];
-        int E = 0, other[kSmallMaxE], raw[kSmallMaxE];
-        long long fr[kSmallMaxE];
-        for (int e = 0; e < qm && !fail; e++) {   // linking edges in query-edge order (as build_steps)
+        int E = 0;
+        for (int e = 0; e < qm; e++) {   // linking edges in query-edge order (as build_steps)
             const int o = Q.qs[e] == u ? Q.qd[e] : (Q.qd[e] == u ? Q.qs[e] : -1);
             if (o < 0 || pos_s[o] >= j) continue;
             if (E == kSmallMaxE) {
@@ -2903,34 +2933,186 @@ __device__ int small_plan_warp(const SmallQuery &Q, SmallPlan &sp, SmallOut *out
             T.lab[E] = (uint32_t)Q.lab[e];
             T.gbase[E] = Q.gbase[e];
             T.ngroups[E] = Q.ngroups[e];
-            other[E] = o;
-            raw[E] = Q.rawlab[e];
-            fr[E] = Q.freq[e];
             E++;
         }
-        if (!fail) {
-            T.E = E;
-            int best = 0;   // the paper's e0 (stats only: each row is bounded by its shortest list)
-            for (int e = 1; e < E; e++)
-                if (fr[e] < fr[best] ||
-                    (fr[e] == fr[best] && (raw[e] < raw[best] || (raw[e] == raw[best] && T.col[e] < T.col[best]))))
-                    best = e;
-            out->n_edges[j] = E;
-            out->first_edge[j] = other[best];
-            T.n_inj = 0;
-            if (!Q.homo)
-                for (int c = 0; c < j && !fail; c++) {
-                    if (Q.qvl[order_s[c]] != Q.qvl[u]) continue;   // C(u) excludes other labels
-                    bool linked = false;
-                    for (int e = 0; e < E; e++) linked |= T.col[e] == c;   // x in N(m[c],l) => x != m[c]
-                    if (linked) continue;
-                    if (T.n_inj == kSmallMaxInj) fail = 1;
-                    else T.inj_col[T.n_inj++] = c;
+        T.E = E;
+        T.n_inj = 0;
+        if (!Q.homo && !fail) {
+            const int lu = Q.qvl[u];
+            for (int c = 0; c < j; c++) {
+                if (Q.qvl[order_s[c]] != lu) continue;   // C(u) excludes other labels
+                bool linked = false;
+                for (int e = 0; e < E; e++) linked |= T.col[e] == c;   // x in N(m[c],l) => x != m[c]
+                if (linked) continue;
+                if (T.n_inj == kSmallMaxInj) {
+                    fail = 1;
+                    break;
                 }
-            T.cu = Q.bm + (long long)u * Q.words;
+                T.inj_col[T.n_inj++] = c;
+            }
         }
+        T.cu = Q.bm + (long long)u * Q.words;
     }
     return __any_sync(0xffffffffu, fail) ? 1 : 0;
+}
+
+// Exclusive scan over the G threads of a group (G = 1024: the block, smem[33]; G = 32: a warp).
+template <int G>
+__device__ __forceinline__ unsigned long long group_exclusive_scan(unsigned long long x, unsigned long long *smem,
+                                                                   unsigned long long *total) {
+    if (G == 32) {
+        const int lane = threadIdx.x & 31;
+        unsigned long long inc = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        *total = __shfl_sync(0xffffffffu, inc, 31);
+        return inc - x;
+    }
+    return block_exclusive_scan(x, smem, total);
+}
+
+// Prealloc of one small-path level (Alg. 4) by a group of G threads: locate every linking list,
+// the per-row shortest list bounds the buffer (any linking edge bounds it, L967-981), F =
+// exclusive scan, F[nM] = |GBA| = *T_s; *el_s = list elements of the active rows.
+template <int G>
+__device__ __forceinline__ void small_prealloc(const SmallStep &S, int t, unsigned long long nM, const int32_t *cur,
+                                               Loc *loc, unsigned long long *Fd, const uint2 *__restrict__ groups,
+                                               int gpn, unsigned long long *sm, unsigned long long *T_s,
+                                               unsigned long long *el_s) {
+    const int gt = threadIdx.x & (G - 1), lane = threadIdx.x & 31;
+    const int E = S.E;
+    if (gt == 0) *el_s = 0;
+    if (G == 32) __syncwarp();
+    else __syncthreads();
+    unsigned long long run = 0;
+    for (unsigned long long b0 = 0; b0 < nM; b0 += G) {
+        const unsigned long long i = b0 + gt;
+        unsigned long long len0 = 0, el = 0;
+        if (i < nM) {
+            Loc best{0u, 0xFFFFFFFFu}, first{0u, 0u};
+            int bi = 0;
+            bool anyzero = false;
+            for (int e = 0; e < E; e++) {
+                const uint32_t v = (uint32_t)cur[i * t + S.col[e]];
+                const Loc r = pcsr_lookup(groups, gpn, S.gbase[e], S.ngroups[e], S.lab[e], v, nullptr);
+                loc[i * E + e] = r;
+                if (e == 0) first = r;
+                if (r.len < best.len) {
+                    best = r;
+                    bi = e;
+                }
+                anyzero |= r.len == 0;
+                el += r.len;
+            }
+            if (bi != 0) {
+                loc[i * E] = best;
+                loc[i * E + bi] = first;
+            }
+            len0 = anyzero ? 0ull : best.len;
+            if (anyzero) el = 0;
+        }
+        unsigned long long agg;
+        const unsigned long long ex = group_exclusive_scan<G>(len0, sm, &agg);
+        if (i < nM) Fd[i] = run + ex;
+        run += agg;
+        el = warp_sum_u64(el);
+        if (lane == 0 && el) atomicAdd(el_s, el);
+    }
+    if (gt == 0) {
+        Fd[nM] = run;
+        *T_s = run;
+    }
+}
+
+// Join + Combine of one small-path level by a group of G threads: slots in rounds of G, the
+// ordered compaction into the next level's rows (or, at the last level, the count /
+// fingerprint / table).  *nout_s = rows produced (~0: over the row capacity).
+template <int G>
+__device__ __forceinline__ void small_join(const SmallQuery &Q, const SmallPlan &sp, const SmallStep &S, int t, bool last,
+                                           unsigned long long nM, unsigned long long T, const int32_t *cur,
+                                           const Loc *loc, const unsigned long long *FF, const int32_t *__restrict__ ci,
+                                           int32_t *nxt, int32_t *table, unsigned long long *sm,
+                                           unsigned long long *nout_s, unsigned long long *cnt_s,
+                                           unsigned long long *h1_s, unsigned long long *h2_s) {
+    const int gt = threadIdx.x & (G - 1), lane = threadIdx.x & 31;
+    const int E = S.E, k = Q.k;
+    unsigned long long nout = 0;
+    for (unsigned long long s0 = 0; s0 < T; s0 += G) {
+        const unsigned long long sl = s0 + gt;
+        bool keep = false;
+        int32_t x = 0;
+        unsigned long long row = 0;
+        if (sl < T) {
+            unsigned long long lo = 0, hi = nM;   // last row with F[row] <= sl
+            while (hi - lo > 1) {
+                const unsigned long long mid = (lo + hi) >> 1;
+                if (FF[mid] <= sl) lo = mid; else hi = mid;
+            }
+            row = lo;
+            const Loc L0 = loc[row * E];
+            x = __ldg(ci + L0.off + (uint32_t)(sl - FF[row]));
+            keep = (__ldg(S.cu + ((uint32_t)x >> 5)) >> (x & 31)) & 1u;              // x in C(u)
+            for (int c = 0; c < S.n_inj && keep; c++) keep = cur[row * t + S.inj_col[c]] != x;   // line 10
+            for (int e = 1; e < E && keep; e++) {                                       // line 13
+                const Loc Le = loc[row * E + e];
+                keep = in_sorted(ci + Le.off, Le.len, x);
+            }
+        }
+        if (last && !Q.want_table) {
+            unsigned long long c = keep ? 1ull : 0ull, a1 = 0, a2 = 0;
+            if (keep && Q.fp) {
+                for (int q = 0; q < k; q++) {
+                    const int col = sp.pos_of_q[q];
+                    const uint32_t val = col < t ? (uint32_t)cur[row * t + col] : (uint32_t)x;
+                    a1 += fp_term(kFpSeed1, q, val);
+                    a2 += fp_term(kFpSeed2, q, val);
+                }
+                a1 = fp_mix(a1);
+                a2 = fp_mix(a2);
+            }
+            c = warp_sum_u64(c);
+            a1 = warp_sum_u64(a1);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) a2 ^= __shfl_xor_sync(0xffffffffu, a2, o);
+            if (lane == 0 && c) {
+                atomicAdd(cnt_s, c);
+                atomicAdd(h1_s, a1);
+                atomicXor(h2_s, a2);
+            }
+            continue;
+        }
+        unsigned long long agg;
+        const unsigned long long ex = group_exclusive_scan<G>(keep ? 1ull : 0ull, sm, &agg);
+        if (nout + agg > kSmallRowCap) {
+            if (gt == 0) *nout_s = ~0ull;
+            return;
+        }
+        if (keep) {
+            const unsigned long long p = nout + ex;
+            if (last) {   // the table in query-id order (+ fingerprint)
+                unsigned long long a1 = 0, a2 = 0;
+                for (int q = 0; q < k; q++) {
+                    const int col = sp.pos_of_q[q];
+                    const int32_t val = col < t ? cur[row * t + col] : x;
+                    table[p * k + q] = val;
+                    a1 += fp_term(kFpSeed1, q, (uint32_t)val);
+                    a2 += fp_term(kFpSeed2, q, (uint32_t)val);
+                }
+                if (Q.fp) {
+                    atomicAdd(h1_s, fp_mix(a1));
+                    atomicXor(h2_s, fp_mix(a2));
+                }
+            } else {
+                for (int c = 0; c < t; c++) nxt[p * (t + 1) + c] = cur[row * t + c];
+                nxt[p * (t + 1) + t] = x;
+            }
+        }
+        nout += agg;
+    }
+    if (gt == 0) *nout_s = nout;
 }
 
 __global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const __grid_constant__ SmallQuery Q,
@@ -2941,7 +3123,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const __grid_c
                                                                   unsigned long long *__restrict__ F,
                                                                   int32_t *__restrict__ table, SmallOut *out) {
     __shared__ unsigned long long sm[34];
-    __shared__ unsigned long long cnt_s, h1_s, h2_s, el_s;
+    __shared__ unsigned long long cnt_s, h1_s, h2_s, el_s, T_s, nout_s;
     __shared__ int fail_s;
     __shared__ SmallPlan sp;
     // F of a level with fewer than kSmallFsh rows stays in shared memory: the join's per-slot
@@ -2956,14 +3138,27 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const __grid_c
     const int k = Q.k;
     // ---- plan (Alg. 2) from |C(u)| (warp 0) ---------------------------------------------
     __shared__ int order_s[GSI_MAX_K], pos_s[GSI_MAX_K];
+    // the planner reads the query from shared memory: indexed reads of the parameter block
+    // miss the constant cache (one L2 round trip each, ~20 us for a 12-vertex plan)
+    __shared__ __align__(16) SmallQuery Qs;
     if (tid == 0) out->clk[0] = clock64();
+    {
+        static_assert(sizeof(SmallQuery) % 16 == 0, "copied as 16 B words");
+        const uint4 *src = reinterpret_cast<const uint4 *>(&Q);
+        uint4 *dst = reinterpret_cast<uint4 *>(&Qs);
+        for (int i = tid; i < (int)(sizeof(SmallQuery) / 16); i += kSmallThreads) dst[i] = src[i];
+    }
     if (tid < k) out->cand[tid] = Q.cand[tid];
+    __syncthreads();
+    if (tid == 0) out->clkp[0] = clock64();
     if (warp == 0) {
         bool any0 = lane < k && Q.cand[lane] == 0;
         any0 = __any_sync(0xffffffffu, any0);
         // an empty C(u) (no match) or a plan beyond the limits: the host's regular path
-        int f = any0 ? 1 : small_plan_warp(Q, sp, out, order_s, pos_s);
+        int f = any0 ? 1 : small_plan_warp(Qs, sp, out, order_s, pos_s, reinterpret_cast<int *>(sB));
         if (!f && Q.cand[order_s[0]] > kSmallMaxRoots) f = 1;
+        if (lane == 0) out->clkp[3] = clock64();
+        if (lane == 0) out->clkp[2] = out->clkp[3];
         if (lane == 0) {
             out->plane_loads = Q.ctr->plane_loads;
             cnt_s = h1_s = h2_s = 0;
@@ -3033,146 +3228,41 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const __grid_c
     }
     if (tid == 0) out->clk[2] = clock64();
     if (tid == 0) out->rows[0] = nM;
-    // rows of the current level: a shared-memory buffer when they fit, else bufA / bufB
+    // rows of the current level: a shared-memory buffer when they fit, else bufA / bufB.  A
+    // level of <= 32 rows runs its Prealloc in warp 0 alone, a join of <= 256 slots likewise
+    // (warp scans instead of block scans: two barriers per level instead of nine — the
+    // C2/C4 queries' deep levels hold a handful of rows).
     const int32_t *cur = sA;
     for (int t = 1; t < k; t++) {
         const SmallStep &S = sp.st[t - 1];
         const int E = S.E;
         const bool last = t == k - 1;
         Loc *const loc = nM * (unsigned long long)E <= (unsigned long long)kSmallSmLoc ? locS : locG;
-        // ---- Prealloc (Alg. 4): locate every linking list, per-row shortest list bounds the
-        //      buffer (any linking edge bounds it, L967-981), F = exclusive scan
-        unsigned long long run = 0;
-        if (tid == 0) el_s = 0;
-        for (unsigned long long b0 = 0; b0 < nM; b0 += kSmallThreads) {
-            const unsigned long long i = b0 + tid;
-            unsigned long long len0 = 0, el = 0;
-            if (i < nM) {
-                Loc best{0u, 0xFFFFFFFFu}, first{0u, 0u};
-                int bi = 0;
-                bool anyzero = false;
-                for (int e = 0; e < E; e++) {
-                    const uint32_t v = (uint32_t)cur[i * t + S.col[e]];
-                    const Loc r = pcsr_lookup(groups, Q.gpn, S.gbase[e], S.ngroups[e], S.lab[e], v, nullptr);
-                    loc[i * E + e] = r;
-                    if (e == 0) first = r;
-                    if (r.len < best.len) {
-                        best = r;
-                        bi = e;
-                    }
-                    anyzero |= r.len == 0;
-                    el += r.len;
-                }
-                if (bi != 0) {
-                    loc[i * E] = best;
-                    loc[i * E + bi] = first;
-                }
-                len0 = anyzero ? 0ull : best.len;
-                if (anyzero) el = 0;
-            }
-            unsigned long long agg;
-            const unsigned long long ex = block_exclusive_scan(len0, sm, &agg);
-            if (i < nM) {
-                if (nM < kSmallFsh) Fs[i] = run + ex;
-                else F[i] = run + ex;
-            }
-            run += agg;
-            el = warp_sum_u64(el);
-            if (lane == 0 && el) atomicAdd(&el_s, el);
-        }
-        const unsigned long long T = run;
-        __syncthreads();
+        unsigned long long *const Fdst = nM < kSmallFsh ? Fs : F;
+        if (nM > 32) small_prealloc<kSmallThreads>(S, t, nM, cur, loc, Fdst, groups, Q.gpn, sm, &T_s, &el_s);
+        else if (warp == 0) small_prealloc<32>(S, t, nM, cur, loc, Fdst, groups, Q.gpn, sm, &T_s, &el_s);
+        __syncthreads();   // F, loc and T visible to the whole block
+        const unsigned long long T = T_s;
         if (tid == 0) {
-            if (nM < kSmallFsh) Fs[nM] = T;
-            else F[nM] = T;
             out->gba[t] = T;
             out->elems[t] = el_s;
         }
-        const unsigned long long *FF = nM < kSmallFsh ? Fs : F;
         if (T > kSmallSlotCap) {
             if (tid == 0) out->aborted = t;
             return;
         }
-        __syncthreads();   // F visible to the whole block
         // the next level's rows (at most T of t + 1 columns): on chip if they fit
         int32_t *nxt;
         if (T * (unsigned long long)(t + 1) <= (unsigned long long)kSmallSmRows) nxt = cur == sA ? sB : sA;
         else nxt = cur == bufA ? bufB : bufA;
-        // ---- join: slots in rounds of 1024, ordered compaction into the next level -------
-        unsigned long long nout = 0;
-        for (unsigned long long s0 = 0; s0 < T; s0 += kSmallThreads) {
-            const unsigned long long sl = s0 + tid;
-            bool keep = false;
-            int32_t x = 0;
-            unsigned long long row = 0;
-            if (sl < T) {
-                unsigned long long lo = 0, hi = nM;   // last row with F[row] <= sl
-                while (hi - lo > 1) {
-                    const unsigned long long mid = (lo + hi) >> 1;
-                    if (FF[mid] <= sl) lo = mid; else hi = mid;
-                }
-                row = lo;
-                const Loc L0 = loc[row * E];
-                x = __ldg(ci + L0.off + (uint32_t)(sl - FF[row]));
-                keep = (__ldg(S.cu + ((uint32_t)x >> 5)) >> (x & 31)) & 1u;              // x in C(u)
-                for (int c = 0; c < S.n_inj && keep; c++) keep = cur[row * t + S.inj_col[c]] != x;   // line 10
-                for (int e = 1; e < E && keep; e++) {                                       // line 13
-                    const Loc Le = loc[row * E + e];
-                    keep = in_sorted(ci + Le.off, Le.len, x);
-                }
-            }
-            if (last && !Q.want_table) {
-                unsigned long long c = keep ? 1ull : 0ull, a1 = 0, a2 = 0;
-                if (keep && Q.fp) {
-                    for (int q = 0; q < k; q++) {
-                        const int col = sp.pos_of_q[q];
-                        const uint32_t val = col < t ? (uint32_t)cur[row * t + col] : (uint32_t)x;
-                        a1 += fp_term(kFpSeed1, q, val);
-                        a2 += fp_term(kFpSeed2, q, val);
-                    }
-                    a1 = fp_mix(a1);
-                    a2 = fp_mix(a2);
-                }
-                c = warp_sum_u64(c);
-                a1 = warp_sum_u64(a1);
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) a2 ^= __shfl_xor_sync(0xffffffffu, a2, o);
-                if (lane == 0 && c) {
-                    atomicAdd(&cnt_s, c);
-                    atomicAdd(&h1_s, a1);
-                    atomicXor(&h2_s, a2);
-                }
-                continue;
-            }
-            unsigned long long agg;
-            const unsigned long long ex = block_exclusive_scan(keep ? 1ull : 0ull, sm, &agg);
-            if (nout + agg > kSmallRowCap) {
-                if (tid == 0) out->aborted = t + 1;
-                return;
-            }
-            if (keep) {
-                const unsigned long long p = nout + ex;
-                if (last) {   // the table in query-id order (+ fingerprint)
-                    unsigned long long a1 = 0, a2 = 0;
-                    for (int q = 0; q < k; q++) {
-                        const int col = sp.pos_of_q[q];
-                        const int32_t val = col < t ? cur[row * t + col] : x;
-                        table[p * k + q] = val;
-                        a1 += fp_term(kFpSeed1, q, (uint32_t)val);
-                        a2 += fp_term(kFpSeed2, q, (uint32_t)val);
-                    }
-                    if (Q.fp) {
-                        atomicAdd(&h1_s, fp_mix(a1));
-                        atomicXor(&h2_s, fp_mix(a2));
-                    }
-                } else {
-                    for (int c = 0; c < t; c++) nxt[p * (t + 1) + c] = cur[row * t + c];
-                    nxt[p * (t + 1) + t] = x;
-                }
-            }
-            nout += agg;
-        }
+        if (T > 256) small_join<kSmallThreads>(Q, sp, S, t, last, nM, T, cur, loc, Fdst, ci, nxt, table, sm, &nout_s, &cnt_s, &h1_s, &h2_s);
+        else if (warp == 0) small_join<32>(Q, sp, S, t, last, nM, T, cur, loc, Fdst, ci, nxt, table, sm, &nout_s, &cnt_s, &h1_s, &h2_s);
         __syncthreads();   // every row of the next level written before it is read
+        const unsigned long long nout = nout_s;
+        if (nout == ~0ull) {   // the next level outgrew the row capacity
+            if (tid == 0) out->aborted = t + 1;
+            return;
+        }
         if (last) {
             if (tid == 0) {
                 out->clk[2 + t] = clock64();
@@ -3193,6 +3283,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const __grid_c
         nM = nout;
         cur = nxt;
         if (nM == 0) break;
+        __syncthreads();   // T_s / nout_s are rewritten by the next level
     }
     if (tid == 0) {   // a level came out empty: no matches (later rows stay 0)
         out->count = 0;
@@ -4671,6 +4762,7 @@ gsi_status run_small(QueryCtx &C, const uint16_t *grp, long long ngrp, long long
         Q.lab[e] = d;
         Q.rawlab[e] = q->qe[e];
         Q.freq[e] = g->freq[d];
+        Q.freqd[e] = dbl_bits((double)g->freq[d]);
         Q.gbase[e] = (unsigned long long)g->gbase[d];
         Q.ngroups[e] = g->ngroups[d];
     }
@@ -4706,21 +4798,43 @@ gsi_status run_small(QueryCtx &C, const uint16_t *grp, long long ngrp, long long
         return GSI_OK;
     }
     const SmallOut &h = *hout;
+    {   // linking edges per step and the paper's e0 (statistics), from the device's order
+        int pos[GSI_MAX_K];
+        for (int j = 0; j < k; j++) pos[h.order[j]] = j;
+        for (int j = 1; j < k; j++) {
+            const int u = h.order[j];
+            int E = 0, best = -1;
+            for (int e = 0; e < qm; e++) {
+                const int o = q->qs[e] == u ? q->qd[e] : (q->qd[e] == u ? q->qs[e] : -1);
+                if (o < 0 || pos[o] >= j) continue;
+                E++;
+                if (best < 0) {
+                    best = e;
+                    continue;
+                }
+                // e0: min freq(l); ties (min raw label id, min column) (reading A9, as build_steps)
+                const long long fb = g->freq[q->qe_dense[best]], fe = g->freq[q->qe_dense[e]];
+                const int ob = q->qs[best] == u ? q->qd[best] : q->qs[best];
+                if (fe < fb || (fe == fb && (q->qe[e] < q->qe[best] || (q->qe[e] == q->qe[best] && pos[o] < pos[ob]))))
+                    best = e;
+            }
+            S.n_edges[j] = E;
+            S.first_edge[j] = best < 0 ? -1 : (q->qs[best] == u ? q->qd[best] : q->qs[best]);
+        }
+    }
     if (getenv("GSI_TRACE")) {   // device phase times (SM clock cycles -> us at the current SM clock)
         int khz = 0;
         cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, g->device);
         const double us = khz > 0 ? 1000.0 / khz : 0.0;
-        fprintf(stderr, "[small] plan %.2f us, M1 %.2f us, levels", (h.clk[1] - h.clk[0]) * us, (h.clk[2] - h.clk[1]) * us);
+        fprintf(stderr, "[small] plan %.2f us (copy %.2f order+steps %.2f flags %.2f), M1 %.2f us, levels",
+                (h.clk[1] - h.clk[0]) * us, (h.clkp[0] - h.clk[0]) * us, (h.clkp[2] - h.clkp[0]) * us,
+                (h.clkp[3] - h.clkp[2]) * us, (h.clk[2] - h.clk[1]) * us);
         for (int t = 1; t < k && h.clk[2 + t]; t++) fprintf(stderr, " %.2f", (h.clk[2 + t] - h.clk[1 + t]) * us);
         fprintf(stderr, " (rows");
         for (int t = 0; t < k; t++) fprintf(stderr, " %llu", h.rows[t]);
         fprintf(stderr, ")\n");
     }
     for (int j = 0; j < k; j++) S.order[j] = h.order[j];
-    for (int t = 1; t < k; t++) {
-        S.n_edges[t] = h.n_edges[t];
-        S.first_edge[t] = h.first_edge[t];
-    }
     S.levels = 1;
     for (int t = 0; t < k; t++) {
         S.rows[t] = h.rows[t];

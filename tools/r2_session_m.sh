@@ -1,0 +1,8 @@
+#!/bin/bash
+# round-2 GPU session M: exact label bits + NC-templated rounds in k_filter_tw, planner from shared memory
+out=gpurun_out; mkdir -p $out
+timeout 900 python -m pytest tests/test_gpu_parity.py -q --timeout 600 -x -k "filter or signature or small or clique or tiny or medium" > $out/m_pytest.log 2>&1; tail -1 $out/m_pytest.log
+timeout 600 python tools/small_latency.py --queries 16 --configs C4 C2 > $out/m_small.log 2> $out/m_small.err; grep -E "median|profiled" $out/m_small.log | cut -c1-200
+GSI_TRACE=1 timeout 600 python tools/small_latency.py --queries 2 --configs C2 C4 > $out/m_small_tr.log 2> $out/m_small_tr.err; grep -E "\[small\]" $out/m_small_tr.err | tail -3
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_filter|k_small_query" -s 2 -c 2 -o $out/m_c4_ncu python tools/small_latency.py --configs C4 --queries 1 --reps 1 > $out/m_ncu_c4.log 2>&1; tail -1 $out/m_ncu_c4.log
+timeout 900 python -m pytest tests/test_gpu_scale.py -q --timeout 800 -x -k "full_config" > $out/m_scale.log 2>&1; tail -1 $out/m_scale.log
