@@ -363,9 +363,7 @@ gsi_status gsi_debug_query_signatures(int32_t k, const int32_t *q_vlabels, int32
  * (host side of the __host__ __device__ functions the kernels use), for known-answer tests:
  * kind 0 = MurmurHash2 of the 4 LE bytes of (uint32)key with (uint32)seed (PCSR group f),
  * kind 1 = MurmurHash64A of the 8 LE bytes of key (signature groups), kind 2 = the fingerprint
- * finaliser mix(key) (seed ignored), kind 3 = the device planner's integer-exact IEEE double
- * product of key and seed read as the bit patterns of two non-negative doubles (+0 or normal
- * with a normal product).  Pure host computation: needs no device.  Unknown kind -> 0. */
+ * finaliser mix(key) (seed ignored).  Pure host computation: needs no device.  Unknown kind -> 0. */
 uint64_t gsi_debug_hash(int32_t kind, uint64_t key, uint64_t seed);
 
 /* ------------------------------------------------------------------ memory ---------- */

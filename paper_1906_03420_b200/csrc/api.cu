@@ -335,7 +335,6 @@ uint64_t gsi_debug_hash(int32_t kind, uint64_t key, uint64_t seed) {
     case 0: return gsi::murmur2_u32((uint32_t)key, (uint32_t)seed);
     case 1: return gsi::murmur64a_u64(key, seed);
     case 2: return gsi::fp_mix(key);
-    case 3: return gsi::dmul_pos(key, seed);
     default: return 0;
     }
 }

@@ -10,7 +10,6 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
-#include <string.h>
 
 #include <mutex>
 #include <string>
@@ -90,48 +89,6 @@ __device__ __forceinline__ uint64_t fp_mix_pre(uint64_t z) {
 // term and one finaliser.
 __host__ __device__ __forceinline__ uint64_t fp_term(uint64_t seed, int q, uint32_t v) {
     return fp_mix(seed ^ ((uint64_t)(uint32_t)(q + 1) << 32) ^ (uint64_t)v);
-}
-
-// Exact IEEE-754 binary64 product (round to nearest, ties to even) of two non-negative finite
-// doubles given as bit patterns, in integer arithmetic: the device planner's FP64 multiplies
-// and compares were its critical path (a single warp, each FP64 instruction on the SM's slow
-// double-precision path).  Operands here are plan scores and label frequencies: +0 or normal
-// numbers whose product stays normal (< 2^1024, > 2^-1022), which is all this handles.
-// Pinned against the native multiply by tests/test_abi.py (gsi_debug_hash kind 3).
-__host__ __device__ inline uint64_t dmul_pos(uint64_t a, uint64_t b) {
-    if (a == 0 || b == 0) return 0;
-    const uint64_t frac = (1ull << 52) - 1;
-    const uint64_t ma = (a & frac) | (1ull << 52), mb = (b & frac) | (1ull << 52);
-    const int ea = (int)(a >> 52), eb = (int)(b >> 52);
-#ifdef __CUDA_ARCH__
-    const uint64_t hi = __umul64hi(ma, mb), lo = ma * mb;
-#else
-    const unsigned __int128 p = (unsigned __int128)ma * mb;
-    const uint64_t hi = (uint64_t)(p >> 64), lo = (uint64_t)p;
-#endif
-    // the product is in [2^104, 2^106): keep 53 bits
-    const int sh = (hi >> 41) & 1 ? 53 : 52;
-    uint64_t m = (hi << (64 - sh)) | (lo >> sh);
-    const uint64_t rem = lo & ((1ull << sh) - 1), half = 1ull << (sh - 1);
-    int e = ea + eb - 1023 + (sh - 52);
-    if (rem > half || (rem == half && (m & 1))) {
-        m++;
-        if (m == (1ull << 53)) {
-            m >>= 1;
-            e++;
-        }
-    }
-    return ((uint64_t)e << 52) | (m & frac);
-}
-
-__host__ __device__ inline uint64_t dbl_bits(double x) {
-#ifdef __CUDA_ARCH__
-    return (uint64_t)__double_as_longlong(x);
-#else
-    uint64_t u;
-    memcpy(&u, &x, 8);
-    return u;
-#endif
 }
 
 // Home group of v in partition l: multiply-high range reduction of f(v) (reading A7).

@@ -156,6 +156,31 @@ struct Counters {
     unsigned long long total;        // scan totals written by the last tile
     unsigned long long total2;       // F'[|M'|] of the probe-ahead (J_NEXT)
 };
+constexpr unsigned long long kCtrWords = (sizeof(Counters) + 31) / 32 * 4;   // 8 B words, 32 B aligned
+
+// Zero-copy publication of the filter's totals (the host's only wait between the filter and the
+// plan): the last CTA to finish — threadFenceReduction's ticket — writes |C(u)| and the plane
+// loads to mapped pinned host memory and raises a flag the host spins on, instead of a
+// device-to-host copy and a stream synchronisation (~15-25 us of DMA set-up and wake-up).
+// hpub: [0, k) |C(u)|, [GSI_MAX_K] plane loads, [GSI_MAX_K + 1] flag (null: not published).
+__device__ __forceinline__ void filter_publish(int k, const unsigned long long *counts, const Counters *ctr,
+                                               unsigned *done, unsigned long long *hpub) {
+    __shared__ bool last;
+    if (!hpub) return;
+    __threadfence();   // this CTA's count atomics are visible device-wide before its ticket
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    volatile unsigned long long *vh = hpub;
+    if (threadIdx.x < k) vh[threadIdx.x] = reinterpret_cast<volatile const unsigned long long *>(counts)[threadIdx.x];
+    if (threadIdx.x == 0) vh[GSI_MAX_K] = reinterpret_cast<volatile const Counters *>(ctr)->plane_loads;
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) vh[GSI_MAX_K + 1] = 1ull;
+}
+
 
 // ---------------------------------------------------------------------- filter ------
 // One pass over the signature table (§III-A): per data vertex v, plane 0 (its label)
@@ -176,7 +201,8 @@ __global__ void __launch_bounds__(kThreads, GSI_FILTER_MINB) k_filter(const uint
                                                      uint32_t *__restrict__ bitmaps, long long words,
                                                      unsigned long long *__restrict__ counts,
                                                      Counters *__restrict__ ctr,
-                                                     uint16_t *__restrict__ grp, long long grp_stride) {
+                                                     uint16_t *__restrict__ grp, long long grp_stride,
+                                                     unsigned *done, unsigned long long *hpub) {
     // grp (optional): grp[u * grp_stride + g] = |C(u)| in bitmap words [g·FW, (g+1)·FW) — a
     // summary the device-planned small path extracts M_1 = C(pi_1) from without a scan of
     // the whole bitmap (a warp's FW words are always one whole group)
@@ -358,6 +384,7 @@ __global__ void __launch_bounds__(kThreads, GSI_FILTER_MINB) k_filter(const uint
     __syncthreads();
     if (threadIdx.x < k && cnt_s[threadIdx.x]) atomicAdd(&counts[threadIdx.x], cnt_s[threadIdx.x]);
     if (threadIdx.x == 0 && loads_s) atomicAdd(&ctr->plane_loads, loads_s);
+    filter_publish(k, counts, ctr, done, hpub);
 }
 
 // Large graphs: one thread per bitmap word (32 consecutive vertices), so the k output words of
@@ -454,7 +481,8 @@ __global__ void __launch_bounds__(kThreads, 4) k_filter_tw(const uint32_t *__res
                                                            uint32_t *__restrict__ bitmaps, long long words,
                                                            unsigned long long *__restrict__ counts,
                                                            Counters *__restrict__ ctr,
-                                                           uint16_t *__restrict__ grp, long long grp_stride) {
+                                                           uint16_t *__restrict__ grp, long long grp_stride,
+                                                           unsigned *done, unsigned long long *hpub) {
     constexpr int kHT = 64;
     constexpr int kCap = 32 * kTwCols;
     __shared__ uint32_t qs[GSI_MAX_K * kPlanes];
@@ -593,6 +621,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_filter_tw(const uint32_t *__res
     __syncthreads();
     if (threadIdx.x < k && cnt_s[threadIdx.x]) atomicAdd(&counts[threadIdx.x], cnt_s[threadIdx.x]);
     if (threadIdx.x == 0 && loads_s) atomicAdd(&ctr->plane_loads, loads_s);
+    filter_publish(k, counts, ctr, done, hpub);
 }
 
 // Filter variant for a graph: the warp-per-word kernel (FW = 1) while one wave of the device
@@ -602,18 +631,20 @@ inline int filter_fw(long long words, int sms) { return words <= (long long)sms 
 
 cudaError_t launch_filter(const uint32_t *sig, long long n, int k, const uint32_t *qsig, int label_only,
                           uint32_t *bm, long long words, unsigned long long *counts, Counters *ctr, uint16_t *grp,
-                          long long grp_stride, int sms, cudaStream_t st) {
+                          long long grp_stride, int sms, cudaStream_t st, unsigned *done = nullptr,
+                          unsigned long long *hpub = nullptr) {
     if (filter_fw(words, sms) == 1) {
         const long long per_cta = kThreads / 32;
         const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>((words + per_cta - 1) / per_cta,
                                                                                     (long long)sms * 8));
-        k_filter<1><<<grid, kThreads, 0, st>>>(sig, n, k, qsig, label_only, bm, words, counts, ctr, grp, grp_stride);
+        k_filter<1><<<grid, kThreads, 0, st>>>(sig, n, k, qsig, label_only, bm, words, counts, ctr, grp, grp_stride,
+                                               done, hpub);
     } else {
         const long long per_cta = 32ll * kTwWarps;
         const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>((words + per_cta - 1) / per_cta,
                                                                                     (long long)sms * 4));
         k_filter_tw<<<grid, kThreads, filter_tw_smem(k), st>>>(sig, n, k, qsig, label_only, bm, words, counts, ctr,
-                                                                grp, grp_stride);
+                                                                grp, grp_stride, done, hpub);
     }
     return cudaGetLastError();
 }
@@ -920,7 +951,7 @@ __global__ void k_tile_rows(const unsigned long long *__restrict__ F, long long 
 //             size its buffers.
 template <int MODE>
 #ifndef GSI_NEXT_MINB
-#define GSI_NEXT_MINB 3
+#define GSI_NEXT_MINB 4   // A/B r2p: 4 -> join_next 358 ms vs 393 (3) over the 16 fp bench queries
 #endif
 __global__ void __launch_bounds__(kThreads, join_items(MODE) > 8 ? 2 : (((MODE == J_NEXT && GSI_NEXT_ITEMS > 4) || MODE == J_CAHEAD) ? GSI_NEXT_MINB : 4)) k_join(const int32_t *__restrict__ M, long long nM,
                                                    const unsigned long long *__restrict__ F,
@@ -2760,7 +2791,6 @@ __global__ void k_abl_link(const int32_t *__restrict__ M, long long nM, const un
 constexpr int kSmallThreads = 1024;
 constexpr int kSmallMaxE = 8;
 constexpr int kSmallMaxInj = 8;
-constexpr int kSmallMaxQE = 64;        // query edges the device planner takes
 constexpr unsigned long long kSmallRowCap = 1ull << 15;
 constexpr unsigned long long kSmallSlotCap = 1ull << 16;
 constexpr unsigned long long kSmallMaxRoots = 4096;
@@ -2773,10 +2803,11 @@ constexpr size_t kSmallDynSmem = 2 * kSmallSmRows * sizeof(int32_t) + kSmallSmLo
 
 // Alg. 2's greedy join order (reading A8 in DESIGN.md): start at the
 // vertex with the smallest score |C(u)|/deg(u), then repeatedly take the connected vertex of
-// smallest score, multiplying the scores of the taken vertex's neighbours by freq(l(e)).  One
-// function for the host planner and the device-planned small path, so both take the same order
-// (same double arithmetic, same tie rule: the smallest query id wins).
-__host__ __device__ inline int plan_greedy(int k, int qm, const int *qs, const int *qd, const long long *freq_e,
+// smallest score, multiplying the scores of the taken vertex's neighbours by freq(l(e)) (tie:
+// the smallest query id).  (A device version — warp 0 of k_small_query, lane = query vertex —
+// was measured at ~37 us for a 12-vertex plan, a single warp's dependent chain of a few
+// thousand instructions, against ~5 us here plus one read-back; the plan stays on the host.)
+inline int plan_greedy(int k, int qm, const int *qs, const int *qd, const long long *freq_e,
                                            const long long *cand, int *order) {
     double score[GSI_MAX_K];
     uint32_t adj[GSI_MAX_K];
@@ -2821,140 +2852,24 @@ struct SmallStep {
     const uint32_t *cu;
 };
 struct SmallPlan {
-    int k;
+    int k, want_table, fp, gpn;
     int pos_of_q[GSI_MAX_K];
     SmallStep st[GSI_MAX_K - 1];   // st[j]: the step joining column j + 1 (j + 1 columns before it)
-};
-// The query as the device planner reads it (passed by value, ~2.5 KB).
-struct __align__(16) SmallQuery {
-    int k, qm, homo, want_table, fp, gpn;
-    int qvl[GSI_MAX_K];
-    int qs[kSmallMaxQE], qd[kSmallMaxQE];
-    int lab[kSmallMaxQE], rawlab[kSmallMaxQE];   // dense / raw edge label
-    long long freq[kSmallMaxQE];                 // |E(P(G, lab))|
-    uint64_t freqd[kSmallMaxQE];                 // the same as a double's bit pattern
-    unsigned long long gbase[kSmallMaxQE];
-    uint32_t ngroups[kSmallMaxQE];
-    const uint32_t *bm;                          // the filter's bitmaps [k][words]
-    long long words;
-    const uint16_t *grp;                         // the filter's per-group counts [k][ngrp_pad]
-    long long ngrp, ngrp_pad;                    // groups of gw bitmap words; row stride (multiple of 8)
+    // level 1: M_1 = C(pi_1), from the filter's bitmap of pi_1 and its per-group counts
+    const uint32_t *bm1;
+    const uint16_t *grp1;          // [ngrp] counts of groups of gw bitmap words (16 B aligned)
+    long long words, ngrp;
     int gw;
-    const unsigned long long *cand;              // |C(u)|
-    const Counters *ctr;                         // the filter's plane-load counter
+    unsigned long long nM1;        // |C(pi_1)| <= kSmallMaxRoots
 };
 struct SmallOut {
     unsigned long long count, fp1, fp2, nout;
     int aborted;                              // 0: done; t: level t exceeded a capacity
-    int planned;                              // the device plan below is valid
     unsigned long long rows[GSI_MAX_K];       // |M_t| at t - 1
     unsigned long long gba[GSI_MAX_K];        // |GBA| of level t at t
     unsigned long long elems[GSI_MAX_K];
-    unsigned long long cand[GSI_MAX_K];       // |C(u)| (copied for the host: one read-back)
-    unsigned long long plane_loads;
-    int order[GSI_MAX_K];                     // pi
-    long long clk[GSI_MAX_K + 2];             // SM clock at: start, plan done, M_1 done, level t done (GSI_TRACE)
-    long long clkp[4];                        // plan phases: query copied, -, planned, flags
+    long long clk[GSI_MAX_K + 2];             // SM clock at: start, -, M_1 done, level t done (GSI_TRACE)
 };
-
-// Warp 0 plans (lane u = query vertex u, lane j = step j): Alg. 2's order with the same
-// arithmetic and tie rule as plan_greedy — scores kept as bit patterns of non-negative doubles
-// (ordered like unsigned integers), one correctly rounded division per lane, the products by
-// freq(l(e)) in query-edge order through dmul_pos (lane o applies the edges between o and the
-// taken vertex, in edge order, exactly the sequence plan_greedy applies to score[o]), the argmin
-// lexicographic in (score, id) — then the steps (linking columns, labels, subtraction columns),
-// one lane per step.  The paper's e0 (a statistic here) is derived on the host afterwards.
-// Returns (on every lane) 0, or 1 if the query is disconnected or a step does not fit.
-__device__ int small_plan_warp(const SmallQuery &Q, SmallPlan &sp, SmallOut *out, int *order_s, int *pos_s,
-                               int *inc_e) {
-    const int lane = threadIdx.x & 31, k = Q.k, qm = Q.qm;
-    int deg = 0, nmy = 0;
-    uint32_t adj = 0u;
-    int *my = inc_e + lane * kSmallMaxQE;   // this lane's incident edges, in edge order
-    for (int e = 0; e < qm; e++) {           // uniform e: broadcast shared-memory reads
-        const int a = Q.qs[e], b = Q.qd[e];
-        if (a == lane) {
-            deg++;
-            adj |= 1u << b;
-        }
-        if (b == lane) {
-            deg++;
-            adj |= 1u << a;
-        }
-        if (a == lane || b == lane) my[nmy++] = e;
-    }
-    uint64_t score = 0;
-    if (lane < k) score = dbl_bits(deg ? (double)Q.cand[lane] / deg : (double)Q.cand[lane]);
-    uint32_t in = 0u;
-    for (int i = 0; i < k; i++) {
-        const bool ok = lane < k && !((in >> lane) & 1u) && (i == 0 || (adj & in));
-        uint64_t bs = ok ? score : ~0ull;
-        int bu = ok ? lane : 32;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const uint64_t s2 = __shfl_xor_sync(0xffffffffu, bs, o);
-            const int u2 = __shfl_xor_sync(0xffffffffu, bu, o);
-            if (s2 < bs || (s2 == bs && u2 < bu)) {
-                bs = s2;
-                bu = u2;
-            }
-        }
-        if (bu == 32) return 1;   // disconnected query
-        if (lane == 0) order_s[i] = bu;
-        in |= 1u << bu;
-        if ((adj >> bu) & 1u)
-            for (int j = 0; j < nmy; j++) {
-                const int e = my[j];
-                if (Q.qs[e] == bu || Q.qd[e] == bu) score = dmul_pos(score, Q.freqd[e]);
-            }
-    }
-    __syncwarp();
-    if (lane < k) {
-        pos_s[order_s[lane]] = lane;
-        out->order[lane] = order_s[lane];
-    }
-    __syncwarp();
-    if (lane < k) sp.pos_of_q[lane] = pos_s[lane];
-    if (lane == 0) sp.k = k;
-    int fail = 0;
-    const int j = lane;
-    if (j >= 1 && j < k) {
-        SmallStep &T = sp.st[j - 1];
-        const int u = order_s[j];
-        int E = 0;
-        for (int e = 0; e < qm; e++) {   // linking edges in query-edge order (as build_steps)
-            const int o = Q.qs[e] == u ? Q.qd[e] : (Q.qd[e] == u ? Q.qs[e] : -1);
-            if (o < 0 || pos_s[o] >= j) continue;
-            if (E == kSmallMaxE) {
-                fail = 1;
-                break;
-            }
-            T.col[E] = pos_s[o];
-            T.lab[E] = (uint32_t)Q.lab[e];
-            T.gbase[E] = Q.gbase[e];
-            T.ngroups[E] = Q.ngroups[e];
-            E++;
-        }
-        T.E = E;
-        T.n_inj = 0;
-        if (!Q.homo && !fail) {
-            const int lu = Q.qvl[u];
-            for (int c = 0; c < j; c++) {
-                if (Q.qvl[order_s[c]] != lu) continue;   // C(u) excludes other labels
-                bool linked = false;
-                for (int e = 0; e < E; e++) linked |= T.col[e] == c;   // x in N(m[c],l) => x != m[c]
-                if (linked) continue;
-                if (T.n_inj == kSmallMaxInj) {
-                    fail = 1;
-                    break;
-                }
-                T.inj_col[T.n_inj++] = c;
-            }
-        }
-        T.cu = Q.bm + (long long)u * Q.words;
-    }
-    return __any_sync(0xffffffffu, fail) ? 1 : 0;
-}
 
 // Exclusive scan over the G threads of a group (G = 1024: the block, smem[33]; G = 32: a warp).
 template <int G>
@@ -3031,14 +2946,14 @@ __device__ __forceinline__ void small_prealloc(const SmallStep &S, int t, unsign
 // ordered compaction into the next level's rows (or, at the last level, the count /
 // fingerprint / table).  *nout_s = rows produced (~0: over the row capacity).
 template <int G>
-__device__ __forceinline__ void small_join(const SmallQuery &Q, const SmallPlan &sp, const SmallStep &S, int t, bool last,
+__device__ __forceinline__ void small_join(const SmallPlan &sp, const SmallStep &S, int t, bool last,
                                            unsigned long long nM, unsigned long long T, const int32_t *cur,
                                            const Loc *loc, const unsigned long long *FF, const int32_t *__restrict__ ci,
                                            int32_t *nxt, int32_t *table, unsigned long long *sm,
                                            unsigned long long *nout_s, unsigned long long *cnt_s,
                                            unsigned long long *h1_s, unsigned long long *h2_s) {
     const int gt = threadIdx.x & (G - 1), lane = threadIdx.x & 31;
-    const int E = S.E, k = Q.k;
+    const int E = S.E, k = sp.k;
     unsigned long long nout = 0;
     for (unsigned long long s0 = 0; s0 < T; s0 += G) {
         const unsigned long long sl = s0 + gt;
@@ -3061,9 +2976,9 @@ __device__ __forceinline__ void small_join(const SmallQuery &Q, const SmallPlan 
                 keep = in_sorted(ci + Le.off, Le.len, x);
             }
         }
-        if (last && !Q.want_table) {
+        if (last && !sp.want_table) {
             unsigned long long c = keep ? 1ull : 0ull, a1 = 0, a2 = 0;
-            if (keep && Q.fp) {
+            if (keep && sp.fp) {
                 for (int q = 0; q < k; q++) {
                     const int col = sp.pos_of_q[q];
                     const uint32_t val = col < t ? (uint32_t)cur[row * t + col] : (uint32_t)x;
@@ -3101,7 +3016,7 @@ __device__ __forceinline__ void small_join(const SmallQuery &Q, const SmallPlan 
                     a1 += fp_term(kFpSeed1, q, (uint32_t)val);
                     a2 += fp_term(kFpSeed2, q, (uint32_t)val);
                 }
-                if (Q.fp) {
+                if (sp.fp) {
                     atomicAdd(h1_s, fp_mix(a1));
                     atomicXor(h2_s, fp_mix(a2));
                 }
@@ -3115,7 +3030,7 @@ __device__ __forceinline__ void small_join(const SmallQuery &Q, const SmallPlan 
     if (gt == 0) *nout_s = nout;
 }
 
-__global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const __grid_constant__ SmallQuery Q,
+__global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const __grid_constant__ SmallPlan sp,
                                                                   const uint2 *__restrict__ groups,
                                                                   const int32_t *__restrict__ ci,
                                                                   int32_t *__restrict__ bufA, int32_t *__restrict__ bufB,
@@ -3124,8 +3039,6 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const __grid_c
                                                                   int32_t *__restrict__ table, SmallOut *out) {
     __shared__ unsigned long long sm[34];
     __shared__ unsigned long long cnt_s, h1_s, h2_s, el_s, T_s, nout_s;
-    __shared__ int fail_s;
-    __shared__ SmallPlan sp;
     // F of a level with fewer than kSmallFsh rows stays in shared memory: the join's per-slot
     // row search then costs shared-memory latency instead of a chain of L2 round trips
     constexpr int kSmallFsh = 4097;
@@ -3135,52 +3048,21 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const __grid_c
     int32_t *const sB = sA + kSmallSmRows;
     Loc *const locS = reinterpret_cast<Loc *>(sB + kSmallSmRows);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int k = Q.k;
-    // ---- plan (Alg. 2) from |C(u)| (warp 0) ---------------------------------------------
-    __shared__ int order_s[GSI_MAX_K], pos_s[GSI_MAX_K];
-    // the planner reads the query from shared memory: indexed reads of the parameter block
-    // miss the constant cache (one L2 round trip each, ~20 us for a 12-vertex plan)
-    __shared__ __align__(16) SmallQuery Qs;
-    if (tid == 0) out->clk[0] = clock64();
-    {
-        static_assert(sizeof(SmallQuery) % 16 == 0, "copied as 16 B words");
-        const uint4 *src = reinterpret_cast<const uint4 *>(&Q);
-        uint4 *dst = reinterpret_cast<uint4 *>(&Qs);
-        for (int i = tid; i < (int)(sizeof(SmallQuery) / 16); i += kSmallThreads) dst[i] = src[i];
+    const int k = sp.k;
+    if (tid == 0) {
+        out->clk[0] = clock64();
+        cnt_s = h1_s = h2_s = 0;
     }
-    if (tid < k) out->cand[tid] = Q.cand[tid];
-    __syncthreads();
-    if (tid == 0) out->clkp[0] = clock64();
-    if (warp == 0) {
-        bool any0 = lane < k && Q.cand[lane] == 0;
-        any0 = __any_sync(0xffffffffu, any0);
-        // an empty C(u) (no match) or a plan beyond the limits: the host's regular path
-        int f = any0 ? 1 : small_plan_warp(Qs, sp, out, order_s, pos_s, reinterpret_cast<int *>(sB));
-        if (!f && Q.cand[order_s[0]] > kSmallMaxRoots) f = 1;
-        if (lane == 0) out->clkp[3] = clock64();
-        if (lane == 0) out->clkp[2] = out->clkp[3];
-        if (lane == 0) {
-            out->plane_loads = Q.ctr->plane_loads;
-            cnt_s = h1_s = h2_s = 0;
-            fail_s = f;
-            out->planned = f ? 0 : 1;
-            if (f) out->aborted = 1;
-        }
-    }
-    __syncthreads();
-    if (fail_s) return;
-    if (tid == 0) out->clk[1] = clock64();
     // ---- level 1 (Alg. 2 line 7): M_1 = C(pi_1) ascending, from the per-group counts ------
     // Each thread sums a contiguous, 16 B aligned range of groups (vector loads, all in flight
     // at once); one block scan gives every thread its output offset and its first
     // non-empty-group index; the non-empty groups (<= |M_1|) are listed in shared memory (Fs,
     // free until level 1's Prealloc) and a warp per group writes its vertices in order.
-    const int u1 = order_s[0];
-    unsigned long long nM = Q.cand[u1];
+    unsigned long long nM = sp.nM1;
     {
-        const uint32_t *bm1 = Q.bm + (long long)u1 * Q.words;
-        const uint16_t *g1 = Q.grp + (long long)u1 * Q.ngrp_pad;
-        const long long ng = Q.ngrp;
+        const uint32_t *bm1 = sp.bm1;
+        const uint16_t *g1 = sp.grp1;
+        const long long ng = sp.ngrp;
         const long long per = ((ng + kSmallThreads - 1) / kSmallThreads + 7) & ~7ll;
         const long long a = tid * per, b = min(ng, a + per);
         unsigned long long sum = 0, ne = 0;
@@ -3205,11 +3087,11 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const __grid_c
         }
         __syncthreads();
         const unsigned long long nne = tot & 0xFFFFFFFFull;
-        const int GW = Q.gw;
+        const int GW = sp.gw;
         for (unsigned long long i = warp; i < nne; i += kSmallThreads / 32) {
             const unsigned long long e = Fs[i];
             const long long w = (long long)(e >> 32) * GW + lane;
-            const uint32_t word = (lane < GW && w < Q.words) ? bm1[w] : 0u;
+            const uint32_t word = (lane < GW && w < sp.words) ? bm1[w] : 0u;
             const unsigned c = __popc(word);
             unsigned inc = c;
 #pragma unroll
@@ -3239,8 +3121,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const __grid_c
         const bool last = t == k - 1;
         Loc *const loc = nM * (unsigned long long)E <= (unsigned long long)kSmallSmLoc ? locS : locG;
         unsigned long long *const Fdst = nM < kSmallFsh ? Fs : F;
-        if (nM > 32) small_prealloc<kSmallThreads>(S, t, nM, cur, loc, Fdst, groups, Q.gpn, sm, &T_s, &el_s);
-        else if (warp == 0) small_prealloc<32>(S, t, nM, cur, loc, Fdst, groups, Q.gpn, sm, &T_s, &el_s);
+        if (nM > 32) small_prealloc<kSmallThreads>(S, t, nM, cur, loc, Fdst, groups, sp.gpn, sm, &T_s, &el_s);
+        else if (warp == 0) small_prealloc<32>(S, t, nM, cur, loc, Fdst, groups, sp.gpn, sm, &T_s, &el_s);
         __syncthreads();   // F, loc and T visible to the whole block
         const unsigned long long T = T_s;
         if (tid == 0) {
@@ -3255,8 +3137,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const __grid_c
         int32_t *nxt;
         if (T * (unsigned long long)(t + 1) <= (unsigned long long)kSmallSmRows) nxt = cur == sA ? sB : sA;
         else nxt = cur == bufA ? bufB : bufA;
-        if (T > 256) small_join<kSmallThreads>(Q, sp, S, t, last, nM, T, cur, loc, Fdst, ci, nxt, table, sm, &nout_s, &cnt_s, &h1_s, &h2_s);
-        else if (warp == 0) small_join<32>(Q, sp, S, t, last, nM, T, cur, loc, Fdst, ci, nxt, table, sm, &nout_s, &cnt_s, &h1_s, &h2_s);
+        if (T > 256) small_join<kSmallThreads>(sp, S, t, last, nM, T, cur, loc, Fdst, ci, nxt, table, sm, &nout_s, &cnt_s, &h1_s, &h2_s);
+        else if (warp == 0) small_join<32>(sp, S, t, last, nM, T, cur, loc, Fdst, ci, nxt, table, sm, &nout_s, &cnt_s, &h1_s, &h2_s);
         __syncthreads();   // every row of the next level written before it is read
         const unsigned long long nout = nout_s;
         if (nout == ~0ull) {   // the next level outgrew the row capacity
@@ -3266,7 +3148,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) k_small_query(const __grid_c
         if (last) {
             if (tid == 0) {
                 out->clk[2 + t] = clock64();
-                const unsigned long long c = Q.want_table ? nout : cnt_s;
+                const unsigned long long c = sp.want_table ? nout : cnt_s;
                 out->count = c;
                 out->nout = nout;
                 out->rows[t] = c;
@@ -3714,14 +3596,16 @@ unsigned long long device_budget(int dev, size_t own_ws) {
 // leaking one page-locked allocation each.  A query holds one block for its lifetime.
 std::mutex g_pinned_mu;
 struct PinnedBlock {
-    Counters c;                              // per-level counters
-    SmallOut so;                             // the small path's result block
-    unsigned long long cand[GSI_MAX_K];      // |C(u)|
+    Counters c;                                   // per-level counters
+    SmallOut so;                                  // the small path's result block
+    unsigned long long rb[kCtrWords + GSI_MAX_K];   // the filter's counters and |C(u)|
+    unsigned long long pub[GSI_MAX_K + 2];        // filter_publish target (mapped: device-written)
 };
 std::vector<PinnedBlock *> g_pinned_free;
 struct PinnedCounters {
     PinnedBlock *blk = nullptr;   // nullptr if pinned memory is unavailable
     Counters *p = nullptr;        // &blk->c
+    unsigned long long *dpub = nullptr;   // device address of blk->pub (mapped), or null
     PinnedCounters() {
         {
             std::lock_guard<std::mutex> lk(g_pinned_mu);
@@ -3729,14 +3613,23 @@ struct PinnedCounters {
                 blk = g_pinned_free.back();
                 g_pinned_free.pop_back();
                 p = &blk->c;
+                map();
                 return;
             }
         }
-        if (cudaMallocHost((void **)&blk, sizeof(PinnedBlock)) != cudaSuccess) {
+        if (cudaHostAlloc((void **)&blk, sizeof(PinnedBlock), cudaHostAllocMapped | cudaHostAllocPortable) !=
+            cudaSuccess) {
             cudaGetLastError();
             blk = nullptr;
         }
         p = blk ? &blk->c : nullptr;
+        map();
+    }
+    void map() {
+        if (blk && cudaHostGetDevicePointer((void **)&dpub, blk->pub, 0) != cudaSuccess) {
+            cudaGetLastError();
+            dpub = nullptr;
+        }
     }
     ~PinnedCounters() {
         if (!blk) return;
@@ -4722,58 +4615,78 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
 }  // namespace
 
 // ------------------------------------------------------------------ small path ---------
-// Eligible before the filter runs: one shard, per-row e0, no test hooks, <= 64 query edges.
-// Whether the query really is small (|C(pi_1)| <= 4096, every step within the kernel's limits,
-// every level within its capacity) is found out on the device; otherwise the kernel stops and
-// the host takes the regular path.
+// Eligible before the filter runs: one shard, per-row e0, no test hooks.  After the plan: a
+// first level of at most 4096 roots and every step within the kernel's limits (<= 8 linking
+// edges and subtraction columns).  A level that outgrows the kernel's capacity stops it and the
+// host takes the regular path from M_1 with the same plan.
 bool small_apriori(const QueryCtx &C) {
     const gsi_query_opts &o = C.opts;
     if (o.small_mode == 1 || env_flag("GSI_SMALL_OFF") || C.W != 1 || o.e0_mode != 0) return false;
     if (o.chunk_slots || o.force_paths || o.ablation || (o.roots && o.n_roots > 0)) return false;
-    if (o.force_order || o.force_first_edge) return false;
-    return C.q->k > 1 && (int)C.q->qs.size() <= kSmallMaxQE && !C.q->absent_label;
+    return C.q->k > 1 && !C.q->absent_label;
 }
 
-// Launch k_small_query right behind the filter (no host round trip) and read its block back.
-// done = true: every level ran on the device and the stats/results are filled in; else the
-// caller takes the regular path (out->cand / plane_loads are valid either way).
-gsi_status run_small(QueryCtx &C, const uint16_t *grp, long long ngrp, long long ngrp_pad, int gw,
-                     const unsigned long long *d_counts,
-                     SmallOut *dout, SmallOut *hout, bool &done) {
+bool small_eligible(const QueryCtx &C, unsigned long long nM1) {
+    if (nM1 == 0 || nM1 > kSmallMaxRoots) return false;
+    for (auto &s : C.steps) {
+        if ((int)s.col.size() > kSmallMaxE) return false;
+        int ninj = 0;
+        if (!C.opts.homomorphism)
+            for (int c = 0; c < s.t; c++) {
+                if (C.q->qvl[C.order[c]] != C.q->qvl[s.u]) continue;
+                bool linked = false;
+                for (int lc : s.col) linked |= lc == c;
+                ninj += linked ? 0 : 1;
+            }
+        if (ninj > kSmallMaxInj) return false;
+    }
+    return true;
+}
+
+// Every level in k_small_query (launched right after the host plan; M_1 is extracted in the
+// kernel from the filter's bitmap and per-group counts), one pinned read-back.  done = false if
+// a level outgrew the kernel (the caller then takes the regular path, same plan).
+gsi_status run_small(QueryCtx &C, const uint16_t *grp, long long ngrp, long long ngrp_pad, int gw, SmallOut *dout,
+                     SmallOut *hout, bool &done) {
     done = false;
     const gsi_graph *g = C.g;
-    const gsi_prepared *q = C.q;
     gsi_stats &S = *C.S;
     Arena &A = *C.A;
-    const int k = q->k, qm = (int)q->qs.size();
-    SmallQuery Q;
-    std::memset(&Q, 0, sizeof(Q));
-    Q.k = k;
-    Q.qm = qm;
-    Q.homo = C.opts.homomorphism ? 1 : 0;
-    Q.want_table = C.opts.want_table ? 1 : 0;
-    Q.fp = C.opts.fingerprint ? 1 : 0;
-    Q.gpn = g->gpn;
-    for (int u = 0; u < k; u++) Q.qvl[u] = q->qvl[u];
-    for (int e = 0; e < qm; e++) {
-        const int d = q->qe_dense[e];   // >= 0: absent labels are not eligible
-        Q.qs[e] = q->qs[e];
-        Q.qd[e] = q->qd[e];
-        Q.lab[e] = d;
-        Q.rawlab[e] = q->qe[e];
-        Q.freq[e] = g->freq[d];
-        Q.freqd[e] = dbl_bits((double)g->freq[d]);
-        Q.gbase[e] = (unsigned long long)g->gbase[d];
-        Q.ngroups[e] = g->ngroups[d];
+    const int k = C.q->k;
+    const int u1 = C.order[0];
+    SmallPlan plan;
+    std::memset(&plan, 0, sizeof(plan));
+    plan.k = k;
+    plan.want_table = C.opts.want_table ? 1 : 0;
+    plan.fp = C.opts.fingerprint ? 1 : 0;
+    plan.gpn = g->gpn;
+    for (int q = 0; q < k; q++) plan.pos_of_q[q] = C.pos_of_q[q];
+    for (size_t j = 0; j < C.steps.size(); j++) {
+        const Step &s = C.steps[j];
+        SmallStep &T = plan.st[j];
+        T.E = (int)s.col.size();
+        for (int e = 0; e < T.E; e++) {
+            T.col[e] = s.col[e];
+            T.lab[e] = (uint32_t)s.lab[e];
+            T.gbase[e] = (unsigned long long)g->gbase[s.lab[e]];
+            T.ngroups[e] = g->ngroups[s.lab[e]];
+        }
+        T.n_inj = 0;
+        if (!C.opts.homomorphism)
+            for (int c = 0; c < s.t; c++) {
+                if (C.q->qvl[C.order[c]] != C.q->qvl[s.u]) continue;   // C(u) excludes other labels
+                bool linked = false;
+                for (int lc : s.col) linked |= lc == c;                // x in N(m[c],l) => x != m[c]
+                if (!linked) T.inj_col[T.n_inj++] = c;
+            }
+        T.cu = C.bm + (long long)s.u * C.words;
     }
-    Q.bm = C.bm;
-    Q.words = C.words;
-    Q.grp = grp;
-    Q.ngrp = ngrp;
-    Q.ngrp_pad = ngrp_pad;
-    Q.gw = gw;
-    Q.cand = d_counts;
-    Q.ctr = C.ctr;
+    plan.bm1 = C.bm + (long long)u1 * C.words;
+    plan.grp1 = grp + (long long)u1 * ngrp_pad;
+    plan.words = C.words;
+    plan.ngrp = ngrp;
+    plan.gw = gw;
+    plan.nM1 = (unsigned long long)S.cand[u1];
     int32_t *bufA = nullptr, *bufB = nullptr, *table = nullptr;
     Loc *loc = nullptr;
     unsigned long long *F = nullptr;
@@ -4782,59 +4695,30 @@ gsi_status run_small(QueryCtx &C, const uint16_t *grp, long long ngrp, long long
     GSI_TRY(A.get(&bufB, kSmallRowCap * (unsigned long long)k));
     GSI_TRY(A.get(&loc, kSmallRowCap * (unsigned long long)kSmallMaxE));
     GSI_TRY(A.get(&F, kSmallRowCap + 1));
-    if (Q.want_table) GSI_TRY(A.get(&table, kSmallRowCap * (unsigned long long)k));
+    if (plan.want_table) GSI_TRY(A.get(&table, kSmallRowCap * (unsigned long long)k));
     C.prof->begin(GSI_K_JOIN, GSI_V_SMALL);   // dout: zeroed with the query's counter pool
     S.variant_launches[GSI_V_SMALL]++;
-    k_small_query<<<1, kSmallThreads, kSmallDynSmem, C.st>>>(Q, g->groups, g->ci, bufA, bufB, loc, F, table, dout);
+    k_small_query<<<1, kSmallThreads, kSmallDynSmem, C.st>>>(plan, g->groups, g->ci, bufA, bufB, loc, F, table, dout);
     C.prof->end();
     GSI_CUDA(d2h(S, hout, dout, sizeof(SmallOut), C.st));
     GSI_CUDA(sync_timed(S, C.st));
     GSI_CUDA(cudaGetLastError());
     if (hout->aborted) {
-        // the regular path takes over from the filter's output (level 1: not planned — too
-        // many roots, an empty C(u) or a step beyond the limits; t > 1: level t outgrew it)
         S.small_aborted = hout->aborted;
         A.reset(mk);
         return GSI_OK;
     }
     const SmallOut &h = *hout;
-    {   // linking edges per step and the paper's e0 (statistics), from the device's order
-        int pos[GSI_MAX_K];
-        for (int j = 0; j < k; j++) pos[h.order[j]] = j;
-        for (int j = 1; j < k; j++) {
-            const int u = h.order[j];
-            int E = 0, best = -1;
-            for (int e = 0; e < qm; e++) {
-                const int o = q->qs[e] == u ? q->qd[e] : (q->qd[e] == u ? q->qs[e] : -1);
-                if (o < 0 || pos[o] >= j) continue;
-                E++;
-                if (best < 0) {
-                    best = e;
-                    continue;
-                }
-                // e0: min freq(l); ties (min raw label id, min column) (reading A9, as build_steps)
-                const long long fb = g->freq[q->qe_dense[best]], fe = g->freq[q->qe_dense[e]];
-                const int ob = q->qs[best] == u ? q->qd[best] : q->qs[best];
-                if (fe < fb || (fe == fb && (q->qe[e] < q->qe[best] || (q->qe[e] == q->qe[best] && pos[o] < pos[ob]))))
-                    best = e;
-            }
-            S.n_edges[j] = E;
-            S.first_edge[j] = best < 0 ? -1 : (q->qs[best] == u ? q->qd[best] : q->qs[best]);
-        }
-    }
-    if (getenv("GSI_TRACE")) {   // device phase times (SM clock cycles -> us at the current SM clock)
+    if (getenv("GSI_TRACE")) {   // device phase times (SM clock cycles -> us at the device's clock rate)
         int khz = 0;
         cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, g->device);
         const double us = khz > 0 ? 1000.0 / khz : 0.0;
-        fprintf(stderr, "[small] plan %.2f us (copy %.2f order+steps %.2f flags %.2f), M1 %.2f us, levels",
-                (h.clk[1] - h.clk[0]) * us, (h.clkp[0] - h.clk[0]) * us, (h.clkp[2] - h.clkp[0]) * us,
-                (h.clkp[3] - h.clkp[2]) * us, (h.clk[2] - h.clk[1]) * us);
+        fprintf(stderr, "[small] M1 %.2f us, levels", (h.clk[2] - h.clk[0]) * us);
         for (int t = 1; t < k && h.clk[2 + t]; t++) fprintf(stderr, " %.2f", (h.clk[2 + t] - h.clk[1 + t]) * us);
         fprintf(stderr, " (rows");
         for (int t = 0; t < k; t++) fprintf(stderr, " %llu", h.rows[t]);
         fprintf(stderr, ")\n");
     }
-    for (int j = 0; j < k; j++) S.order[j] = h.order[j];
     S.levels = 1;
     for (int t = 0; t < k; t++) {
         S.rows[t] = h.rows[t];
@@ -4846,7 +4730,7 @@ gsi_status run_small(QueryCtx &C, const uint16_t *grp, long long ngrp, long long
     C.count = h.count;
     C.fp1 = h.fp1;
     C.fp2 = h.fp2;
-    if (Q.want_table && h.nout) {
+    if (plan.want_table && h.nout) {
         const gsi_status rs = table_put(C, table, h.nout);
         if (rs != GSI_OK) {
             A.reset(mk);
@@ -5070,10 +4954,28 @@ gsi_status run_ablation(QueryCtx &C, int32_t *M, unsigned long long nM) {
     return GSI_OK;
 }
 
-// Plan (a4), level 1 (a5) and the levels (a6-a8) on the host-driven path: every query the
-// small path did not take.  Leaves the count / fingerprint / table pieces in C.
-gsi_status run_regular(QueryCtx &C, const std::vector<long long> &cand, unsigned long long budget, double t_start,
-                       double t_filter, double &t_plan) {
+// Plan (a4): Alg. 2 order, the steps and the stored-column layout, from |C(u)|.
+gsi_status plan_query(QueryCtx &C, const std::vector<long long> &cand) {
+    const gsi_prepared *q = C.q;
+    const gsi_query_opts &opts = C.opts;
+    gsi_stats &S = *C.S;
+    const int k = q->k;
+    GSI_TRY(plan_order(q, cand, opts.force_order, C.order));
+    GSI_TRY(build_steps(q, C.order, opts.force_first_edge, C.steps));
+    for (int j = 0; j < k; j++) S.order[j] = C.order[j];
+    for (auto &s : C.steps) {
+        S.n_edges[s.t] = (int)s.col.size();
+        S.first_edge[s.t] = s.other[s.paper_e0];
+    }
+    C.pos_of_q.assign(k, 0);
+    for (int j = 0; j < k; j++) C.pos_of_q[C.order[j]] = j;
+    plan_layout(C, !opts.want_table && !opts.fingerprint && !opts.ablation);
+    return GSI_OK;
+}
+
+// Level 1 (a5) and the levels (a6-a8) on the host-driven path, after plan_query: every query
+// the small path did not take.  Leaves the count / fingerprint / table pieces in C.
+gsi_status run_regular(QueryCtx &C, const std::vector<long long> &cand, unsigned long long budget, double t_start) {
     const gsi_graph *g = C.g;
     const gsi_prepared *q = C.q;
     const gsi_query_opts &opts = C.opts;
@@ -5086,19 +4988,6 @@ gsi_status run_regular(QueryCtx &C, const std::vector<long long> &cand, unsigned
     const long long words = C.words;
     const uint32_t *bm = C.bm;
     Counters hc;
-    // ---------------- plan (a4) ----------------
-    GSI_TRY(plan_order(q, cand, opts.force_order, C.order));
-    GSI_TRY(build_steps(q, C.order, opts.force_first_edge, C.steps));
-    for (int j = 0; j < k; j++) S.order[j] = C.order[j];
-    for (auto &s : C.steps) {
-        S.n_edges[s.t] = (int)s.col.size();
-        S.first_edge[s.t] = s.other[s.paper_e0];
-    }
-    C.pos_of_q.assign(k, 0);
-    for (int j = 0; j < k; j++) C.pos_of_q[C.order[j]] = j;
-    plan_layout(C, !opts.want_table && !opts.fingerprint && !opts.ablation);
-    t_plan = now_ms();
-    S.ms_plan = (float)(t_plan - t_filter);
 
     // memory budget -> chunk capacity in GBA slots (bytes per slot per level: S,R 8 B,
     // M' 4(t+1) B, the child level's loc/F 8E+8 B), over the k-1 levels that may nest.
@@ -5287,16 +5176,17 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     uint32_t *bm = nullptr;
     unsigned long long *d_counts = nullptr;
     SmallOut *d_small = nullptr;
+    unsigned *d_done = nullptr;   // the filter's CTA ticket (zero-copy publication)
     {
         constexpr unsigned long long kZWords = 1ull << 17;   // 1 MB
-        constexpr unsigned long long kCtrW = (sizeof(Counters) + 31) / 32 * 4;
         constexpr unsigned long long kSmallW = (sizeof(SmallOut) + 31) / 32 * 4;
         if (A.get_big(&C.zpool, kZWords) == GSI_OK && cudaMemsetAsync(C.zpool, 0, 8ull * kZWords, st) == cudaSuccess) {
             C.zcap = kZWords;
             C.ctr = reinterpret_cast<Counters *>(C.zpool);
-            d_counts = C.zpool + kCtrW;
-            d_small = reinterpret_cast<SmallOut *>(C.zpool + kCtrW + 4 * ((GSI_MAX_K + 3) / 4));
-            C.zoff = kCtrW + 4 * ((GSI_MAX_K + 3) / 4) + kSmallW;
+            d_counts = C.zpool + kCtrWords;
+            d_done = reinterpret_cast<unsigned *>(C.zpool + kCtrWords + 4 * ((GSI_MAX_K + 3) / 4));
+            d_small = reinterpret_cast<SmallOut *>(C.zpool + kCtrWords + 4 * ((GSI_MAX_K + 3) / 4) + 4);
+            C.zoff = kCtrWords + 4 * ((GSI_MAX_K + 3) / 4) + 4 + kSmallW;
         } else {
             cudaGetLastError();
             C.zpool = nullptr;
@@ -5326,6 +5216,9 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     GSI_TRY(A.get(&bm, (unsigned long long)words * k));
     if (small_try) GSI_TRY(A.get(&grp, (unsigned long long)ngrp_pad * k));
     C.bm = bm;
+    // zero-copy publication of |C(u)| (single-label graphs, pinned block and zeroed pool)
+    unsigned long long *hpub_dev = (!g->ml && d_done && pinned.dpub) ? pinned.dpub : nullptr;
+    if (hpub_dev) reinterpret_cast<volatile unsigned long long *>(pinned.blk->pub)[GSI_MAX_K + 1] = 0ull;
     {
         prof.begin(GSI_K_FILTER);
         const uint32_t *qsig = q->d_qsig + (opts.homomorphism ? (size_t)k * kPlanes : 0);
@@ -5333,36 +5226,45 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
             GSI_CUDA(launch_filter_ml(g, q, opts.homomorphism, bm, words, d_counts, st));
         else
             GSI_CUDA(launch_filter(g->sig, n, k, qsig, opts.filter_mode == 1, bm, words, d_counts, C.ctr, grp, ngrp_pad,
-                                   sms, st));
+                                   sms, st, d_done, hpub_dev));
         prof.end();
     }
     if (htrace) fprintf(stderr, "[host] filter launched %.3f ms\n", now_ms() - t_start);
-    // the read-back block (pinned when available)
-    SmallOut hsmall_pageable;
-    SmallOut *hsmall = C.pinned ? &pinned.blk->so : &hsmall_pageable;
+    // |C(u)| and the filter's counters back in one copy (adjacent in the zeroed pool)
     std::vector<long long> cand(k);
     unsigned long long plane_loads = 0;
-    bool small_done = false;
-    if (small_try) {
-        // the whole query on the device if it is small; |C(u)| comes back in the same block
-        GSI_TRY(run_small(C, grp, ngrp, ngrp_pad, gw, d_counts, d_small, hsmall, small_done));
-        for (int u = 0; u < k; u++) cand[u] = (long long)hsmall->cand[u];
-        plane_loads = hsmall->plane_loads;
-    } else {
-        unsigned long long *hc_cand = C.pinned ? pinned.blk->cand : nullptr;
-        std::vector<unsigned long long> cand_pageable;
-        if (!hc_cand) {
-            cand_pageable.resize(k);
-            hc_cand = cand_pageable.data();
+    bool published = false;
+    if (hpub_dev) {   // spin on the flag the filter's last CTA raises (bounded; then the copy path)
+        volatile unsigned long long *pub = pinned.blk->pub;
+        const auto t0 = std::chrono::steady_clock::now();
+        while (pub[GSI_MAX_K + 1] == 0ull) {
+            if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(2)) break;
         }
-        Counters hc_pageable;
-        Counters *hcp = C.pinned ? C.pinned : &hc_pageable;
-        GSI_CUDA(d2h(S, hc_cand, d_counts, 8ull * k, st));
-        GSI_CUDA(d2h(S, hcp, C.ctr, sizeof(Counters), st));
+        if (pub[GSI_MAX_K + 1]) {
+            std::atomic_thread_fence(std::memory_order_acquire);
+            for (int u = 0; u < k; u++) cand[u] = (long long)pub[u];
+            plane_loads = pub[GSI_MAX_K];
+            published = true;
+            S.ms_host_sync += (float)std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        }
+    }
+    if (!published) {
+        std::vector<unsigned long long> rb_pageable;
+        unsigned long long *rb = C.pinned ? pinned.blk->rb : nullptr;
+        if (!rb) {
+            rb_pageable.resize(kCtrWords + GSI_MAX_K);
+            rb = rb_pageable.data();
+        }
+        if (C.zpool) {
+            GSI_CUDA(d2h(S, rb, C.zpool, 8ull * (kCtrWords + k), st));
+        } else {
+            GSI_CUDA(d2h(S, rb, C.ctr, sizeof(Counters), st));
+            GSI_CUDA(d2h(S, rb + kCtrWords, d_counts, 8ull * k, st));
+        }
         GSI_CUDA(sync_timed(S, st));
         GSI_CUDA(cudaGetLastError());
-        for (int u = 0; u < k; u++) cand[u] = (long long)hc_cand[u];
-        plane_loads = hcp->plane_loads;
+        for (int u = 0; u < k; u++) cand[u] = (long long)rb[kCtrWords + u];
+        plane_loads = reinterpret_cast<const Counters *>(rb)->plane_loads;
     }
     if (htrace) fprintf(stderr, "[host] read back %.3f ms\n", now_ms() - t_start);
     const double t_filter = now_ms();
@@ -5370,11 +5272,25 @@ gsi_status run_impl(const gsi_graph *g, const gsi_prepared *q, const gsi_query_o
     for (int u = 0; u < k; u++) S.cand[u] = cand[u];
     S.alg_bytes[GSI_K_FILTER] = 4.0 * n + 4.0 * plane_loads + 4.0 * words * k;
 
+    // ---------------- plan (a4) ----------------
+    GSI_TRY(plan_query(C, cand));
+    double t_plan = now_ms();
+    S.ms_plan = (float)(t_plan - t_filter);
+    if (htrace) fprintf(stderr, "[host] planned %.3f ms\n", t_plan - t_start);
+
     gsi_status rc = GSI_OK;
-    double t_plan = t_filter;
+    bool small_done = false;
+    bool all_nonempty = true;
+    for (int u = 0; u < k; u++) all_nonempty &= cand[u] > 0;
+    if (small_try && all_nonempty && small_eligible(C, (unsigned long long)cand[C.order[0]])) {
+        // every level in one kernel, one read-back
+        SmallOut hsmall_pageable;
+        SmallOut *hsmall = C.pinned ? &pinned.blk->so : &hsmall_pageable;
+        GSI_TRY(run_small(C, grp, ngrp, ngrp_pad, gw, d_small, hsmall, small_done));
+    }
     if (!small_done) {
         if (!budget) budget = device_budget(g->device, A.ws_dev >= 0 ? A.cap : 0);
-        rc = run_regular(C, cand, budget, t_start, t_filter, t_plan);
+        rc = run_regular(C, cand, budget, t_start);
     }
     if (rc != GSI_OK) {
         for (auto &p : C.pieces) cudaFreeAsync(p.first, st);
