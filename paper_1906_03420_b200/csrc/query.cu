@@ -397,6 +397,9 @@ __global__ void __launch_bounds__(kThreads, GSI_FILTER_MINB) k_filter(const uint
 // bit of every remaining u in the warp's shared output tile.  Phase C: thread w stores word w
 // of every C(u) — coalesced 128 B per u across the warp — and the warp sums |C(u)| per group
 // of 32 words (grp, gw = 32).
+#ifndef GSI_TW_P
+#define GSI_TW_P 1                               // plane loads per entry per round for queues of <= 64 (A/B r2t: 1-3 equal)
+#endif
 constexpr int kTwCols = 8;                       // queue columns per round (256 entries per warp)
 constexpr int kTwLabelBits = 4096;               // labels below this are matched exactly by a bit test
 constexpr int kTwWarps = kThreads / 32;
@@ -410,9 +413,10 @@ __device__ __forceinline__ uint32_t ht_lookup(const uint32_t *ht_lab, const uint
 }
 
 // Plane rounds on a warp's queue of qn <= 32·NC label-matched vertices (k_filter_tw phase B):
-// lane takes entries lane + 32c; each round issues the next needed plane load of every entry
-// before testing any; a survivor sets its bit of each remaining u in the output tile.
-template <int NC>
+// lane takes entries lane + 32c; each round issues the next P needed plane loads of every
+// entry before testing any (P > 1 for short queues: the chain of dependent rounds, not the
+// bytes, is their critical path); a survivor sets its bit of each remaining u in the output tile.
+template <int NC, int P>
 __device__ __forceinline__ void tw_rounds(const uint32_t *q_v, const uint32_t *q_m, int qn, const uint32_t *qneed,
                                           const uint32_t *qs, const uint32_t *__restrict__ sig, long long n,
                                           uint32_t *outw, long long wb, unsigned long long &plane_words) {
@@ -435,33 +439,40 @@ __device__ __forceinline__ void tw_rounds(const uint32_t *q_v, const uint32_t *q
         }
     }
     for (int round = 0; round < kPlanes; round++) {
-        uint32_t pv[NC];
-        int pls[NC];
+        uint32_t pv[NC][P];
+        int pls[NC][P];
         bool any = false;
 #pragma unroll
         for (int c = 0; c < NC; c++) {
-            pls[c] = -1;
-            pv[c] = 0u;
-            if (m[c] && need[c]) {
-                pls[c] = __ffs(need[c]) - 1;
-                pv[c] = __ldcs(sig + (long long)pls[c] * n + vv[c]);
-                any = true;
+            uint32_t rem = m[c] ? need[c] : 0u;
+#pragma unroll
+            for (int q = 0; q < P; q++) {
+                pls[c][q] = -1;
+                pv[c][q] = 0u;
+                if (rem) {
+                    pls[c][q] = __ffs(rem) - 1;
+                    rem &= rem - 1;
+                    pv[c][q] = __ldcs(sig + (long long)pls[c][q] * n + vv[c]);
+                    any = true;
+                }
             }
         }
         if (!__any_sync(0xffffffffu, any)) break;
 #pragma unroll
-        for (int c = 0; c < NC; c++) {
-            if (pls[c] < 0) continue;
-            need[c] &= ~(1u << pls[c]);
-            plane_words++;
-            uint32_t t = m[c];
-            while (t) {
-                const int u = __ffs(t) - 1;
-                t &= t - 1;
-                const uint32_t sq = qs[u * kPlanes + pls[c]];
-                if ((pv[c] & sq) != sq) m[c] &= ~(1u << u);   // S(v)&S(u)=S(u) fails on this plane
+        for (int c = 0; c < NC; c++)
+#pragma unroll
+            for (int q = 0; q < P; q++) {
+                if (pls[c][q] < 0) continue;
+                need[c] &= ~(1u << pls[c][q]);
+                plane_words++;
+                uint32_t t = m[c];
+                while (t) {
+                    const int u = __ffs(t) - 1;
+                    t &= t - 1;
+                    const uint32_t sq = qs[u * kPlanes + pls[c][q]];
+                    if ((pv[c][q] & sq) != sq) m[c] &= ~(1u << u);   // S(v)&S(u)=S(u) fails on this plane
+                }
             }
-        }
     }
 #pragma unroll
     for (int c = 0; c < NC; c++) {
@@ -536,7 +547,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_filter_tw(const uint32_t *__res
         const long long w = wb + lane;
         const long long v0 = w * 32;
         // ---- phase A: this word's label matches
-        uint32_t mb = 0u;
+        uint32_t mb = 0u, big = 0u;
         if (w < words) {
             const uint4 *src = reinterpret_cast<const uint4 *>(sig + v0);
             const int nv = (int)min(32ll, n - v0);
@@ -546,15 +557,20 @@ __global__ void __launch_bounds__(kThreads, 4) k_filter_tw(const uint32_t *__res
                 const uint32_t l[4] = {l4.x, l4.y, l4.z, l4.w};
 #pragma unroll
                 for (int i = 0; i < 4; i++) {
-                    // exact for labels < 4096 (one shared-memory bit), else the hash table's
-                    // occupancy (a candidate only; the probe below decides)
+                    // exact for labels < 4096 (one shared-memory bit); larger labels are set
+                    // aside and tested below against the hash table's occupancy
                     const int b = c * 4 + i;
-                    const uint32_t L = l[i];
-                    const bool hit = L < (uint32_t)kTwLabelBits ? (lbits[L >> 5] >> (L & 31)) & 1u
-                                                                : (occ >> ((L * 0x9E3779B1u) >> 26)) & 1ull;
-                    if (b < nv && hit) mb |= 1u << b;
+                    const uint32_t L = l[i], Lc = min(L, (uint32_t)kTwLabelBits - 1u);
+                    mb |= ((lbits[Lc >> 5] >> (Lc & 31)) & (L < (uint32_t)kTwLabelBits ? 1u : 0u)) << b;
+                    big |= (L >= (uint32_t)kTwLabelBits ? 1u : 0u) << b;
                 }
             }
+            for (uint32_t t = big; t; t &= t - 1) {   // labels >= 4096 (rare): occupancy, then the probe below
+                const int b = __ffs(t) - 1;
+                const uint32_t L = __ldg(sig + v0 + b);
+                if ((occ >> ((L * 0x9E3779B1u) >> 26)) & 1ull) mb |= 1u << b;
+            }
+            if (nv < 32) mb &= (1u << nv) - 1u;
         }
         if (label_only) {
             // C(u) by label alone: every marked vertex joins all its label's query vertices
@@ -591,10 +607,10 @@ __global__ void __launch_bounds__(kThreads, 4) k_filter_tw(const uint32_t *__res
                 if (qn > kCap - 32 || !more) {
                     __syncwarp();
                     const int nc = (qn + 31) >> 5;   // dense columns: the rounds run on NC >= nc
-                    if (nc <= 1) tw_rounds<1>(q_v, q_m, qn, qneed, qs, sig, n, outw, wb, plane_words);
-                    else if (nc <= 2) tw_rounds<2>(q_v, q_m, qn, qneed, qs, sig, n, outw, wb, plane_words);
-                    else if (nc <= 4) tw_rounds<4>(q_v, q_m, qn, qneed, qs, sig, n, outw, wb, plane_words);
-                    else tw_rounds<kTwCols>(q_v, q_m, qn, qneed, qs, sig, n, outw, wb, plane_words);
+                    if (nc <= 1) tw_rounds<1, GSI_TW_P>(q_v, q_m, qn, qneed, qs, sig, n, outw, wb, plane_words);
+                    else if (nc <= 2) tw_rounds<2, GSI_TW_P>(q_v, q_m, qn, qneed, qs, sig, n, outw, wb, plane_words);
+                    else if (nc <= 4) tw_rounds<4, 1>(q_v, q_m, qn, qneed, qs, sig, n, outw, wb, plane_words);
+                    else tw_rounds<kTwCols, 1>(q_v, q_m, qn, qneed, qs, sig, n, outw, wb, plane_words);
                     __syncwarp();
                     qn = 0;
                     if (!more) break;
