@@ -1000,8 +1000,10 @@ __global__ void __launch_bounds__(kThreads, join_items(MODE) > 8 ? 2 : (((MODE =
     __shared__ unsigned long long sm[34];
     __shared__ unsigned tile_s, agg_s;
     __shared__ unsigned long long base_s, base2_s;
+    __shared__ int s_src[GSI_MAX_K];   // J_NEXT: P.out_src (stored column map of a new row)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) tile_s = atomicAdd(tile_ctr, 1u);
+    if (MODE == J_NEXT && tid < GSI_MAX_K) s_src[tid] = P.out_src[tid];
     {   // zero the row-marker array with 16 B stores
         int4 *z = reinterpret_cast<int4 *>(sR);
         for (int j = tid; j < TILE / 4; j += kThreads) z[j] = make_int4(0, 0, 0, 0);
@@ -1376,12 +1378,17 @@ __global__ void __launch_bounds__(kThreads, join_items(MODE) > 8 ? 2 : (((MODE =
                 }
             }
             // ---- coalesced write of the contiguous block of new rows ------------------------
+            // (the column map comes from shared memory and e / W from a multiply-high: an
+            // indexed parameter read per element serialised in the constant cache and a
+            // division per element dominated this loop — ncu r2x: MIO throttle 23 %)
             const int W = P.out_w;
+            const unsigned mW = 0xFFFFFFFFu / (unsigned)W + 1u;   // e / W exact for e < 2^32 / W
             int32_t *o = out + base * (unsigned long long)W;
+            const int Pt = P.t;
             for (unsigned e = tid; e < cnt * (unsigned)W; e += kThreads) {
-                const unsigned r = e / W, c = e - r * W;
-                const int src = P.out_src[c];
-                o[e] = src >= 0 ? __ldg(M + (long long)si[r] * P.t + src) : (int32_t)sx[r];
+                const unsigned r = W == 1 ? e : __umulhi(e, mW), c = e - r * W;
+                const int src = s_src[c];
+                o[e] = src >= 0 ? __ldg(M + (long long)si[r] * Pt + src) : (int32_t)sx[r];
             }
             if (tile == gridDim.x - 1 && tid == 0) ctr->total = base + cnt;
         }
