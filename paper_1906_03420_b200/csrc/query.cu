@@ -2,8 +2,11 @@
 // L534-552), join-order planner (Alg. 2), and the per-level Prealloc-Combine vertex
 // join (Alg. 3, Alg. 4) re-designed for B200:
 //
-//   k_filter        one streaming pass over the column-first signature table tests all k
-//                   query signatures; ballot writes C(u) bitmap words, popc gives |C(u)|.
+//   k_filter_tw     one pass over the column-first signature table tests all k query
+//                   signatures: a thread per bitmap word (32 vertices), label matches queued
+//                   per warp for the plane rounds, output words bit-assembled; k_filter<1>
+//                   (a warp per word, ballots) for small graphs.  |C(u)|, per-group counts,
+//                   and a zero-copy publication of the totals by the last CTA.
 //   k_compact_*     level 1: M_1 = C(pi_1) in ascending order (Alg. 2 line 7).
 //   k_probe         Prealloc (Alg. 4): one thread per row of M locates N(m_i[c_e], l_e) for
 //                   every linking edge in PCSR (one 128 B group probe each, L740-753), caches
@@ -26,7 +29,8 @@
 //   k_next_lean, k_cahead_lean, k_final_fp, k_final_table
 //                   warp-centric variants on shared N(v,l0) ∩ C(u) runs.
 //   k_abl_*         the paper-style ablation engine (one warp per row, NEXT-3).
-//   k_small_query   every level of a small query in one launch.
+//   k_small_query   every level of a small query in one launch after the host plan (M_1
+//                   extracted from the filter's group counts, rows on chip).
 #include <cooperative_groups.h>
 
 #include <algorithm>
