@@ -1767,7 +1767,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_cahead_lean(const int32_t *__re
 // its candidate read, the subtraction compare and two terms + two finalisers.  The walk is
 // load-balanced like the count kernels: lane-own rows when the unit's runs are even, long
 // rows (>= 32 candidates) by the whole warp, the rest by a shuffle owner search.
-template <int NINJ>
+template <int NINJ, bool TT>   // TT: x's terms from the per-candidate term table T (else computed)
 __global__ void __launch_bounds__(kThreads, 4) k_final_fp(const int32_t *__restrict__ M, long long r0, long long r1,
                                                           const Loc *__restrict__ loc, StepParams P, int qx,
                                                           const int32_t *__restrict__ cip,
@@ -1775,23 +1775,30 @@ __global__ void __launch_bounds__(kThreads, 4) k_final_fp(const int32_t *__restr
     const int lane = threadIdx.x & 31;
     const long long gw = (blockIdx.x * (long long)kThreads + threadIdx.x) >> 5;
     const long long nw = ((long long)gridDim.x * kThreads) >> 5;
+    // cnt: the rows' run lengths minus the subtraction hits (counted per row, not per match)
     unsigned long long cnt = 0, h1 = 0, h2 = 0, act = 0;
     // one match m || x, x = cip[p]: the subtraction test, then the two row hashes from the
-    // parent's summed terms (a1, a2) and x's terms (from T, or computed)
+    // parent's summed terms (a1, a2) and x's terms (from T, or computed) — straight-line code
+    // per match: the term-table choice is a template parameter, not a branch per match
     auto fp_match = [&](uint32_t p, const Inj<NINJ> &in, unsigned long long a1, unsigned long long a2) {
         unsigned long long t1, t2;
-        if (T) {
-            if (NINJ > 0 && in.hit(__ldg(cip + p))) return;
+        if (TT) {
+            if (NINJ > 0 && in.hit(__ldg(cip + p))) {
+                cnt--;
+                return;
+            }
             const ulonglong2 tt = __ldg(T + p);
             t1 = tt.x;
             t2 = tt.y;
         } else {
             const int32_t x = __ldg(cip + p);
-            if (NINJ > 0 && in.hit(x)) return;
+            if (NINJ > 0 && in.hit(x)) {
+                cnt--;
+                return;
+            }
             t1 = fp_term(kFpSeed1, qx, (uint32_t)x);
             t2 = fp_term(kFpSeed2, qx, (uint32_t)x);
         }
-        cnt++;
         h1 += fp_mix_pre(a1 + t1);   // a1, a2 carry fp_mix's leading constant (added per row)
         h2 ^= fp_mix_pre(a2 + t2);
     };
@@ -1803,6 +1810,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_final_fp(const int32_t *__restr
         Inj<NINJ> inj;
         inj.load(row, P, valid && L.len);
         act += (valid && L.len) ? 1u : 0u;
+        cnt += valid ? L.len : 0u;
         unsigned long long s1 = kFpMixAdd, s2 = kFpMixAdd;   // the parent row's terms (every column but x)
         if (valid && L.len) {
             for (int q = 0; q < P.k; q++) {
@@ -4518,11 +4526,13 @@ gsi_status level(QueryCtx &C, size_t si, int32_t *M, unsigned long long nM, Loc 
             const unsigned long long units = ((unsigned long long)(r_hi - r_lo) + 31) / 32;
             const unsigned wg = (unsigned)std::max<unsigned long long>(
                 1, std::min<unsigned long long>((units + 7) / 8, (unsigned long long)sms * 8));
-            if (P.fp && P.n_inj == 0)
-                k_final_fp<0><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, s.u, cip, fpT, lctr);
-            else if (P.fp)
-                k_final_fp<kLeanInj><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, s.u, cip, fpT, lctr);
-            else if (P.n_inj == 0)
+            if (P.fp && P.n_inj == 0) {
+                if (fpT) k_final_fp<0, true><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, s.u, cip, fpT, lctr);
+                else k_final_fp<0, false><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, s.u, cip, fpT, lctr);
+            } else if (P.fp) {
+                if (fpT) k_final_fp<kLeanInj, true><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, s.u, cip, fpT, lctr);
+                else k_final_fp<kLeanInj, false><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, s.u, cip, fpT, lctr);
+            } else if (P.n_inj == 0)
                 k_cahead_lean<0, true><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, P2, cip, g->groups, g->gpn, lctr);
             else
                 k_cahead_lean<1, true><<<wg, kThreads, 0, st>>>(M, r_lo, r_hi, loc, P, P2, cip, g->groups, g->gpn, lctr);
