@@ -452,10 +452,12 @@ def run_gsi(args):
 
     if dname == "final_fp":
         # integer-ALU bound: per match the fingerprint spec needs two splitmix
-        # finalisers and four 64-bit add/xor combines; on the 32-bit ALU pipe (IADD3 / LOP3 /
-        # SHF; the multiplies run on the FMA pipe) that is FP_ALU_OPS lane-ops per match.
+        # finalisers (their leading constant add folded into the row's partial sum) and four
+        # 64-bit add/xor combines; on the 32-bit ALU pipe (SHF / LOP3 / IADD3; the multiplies run
+        # on the FMA pipe) that is 2 x 3 xorshifts x 4 + 4 x 2 = FP_ALU_OPS lane-ops per match
+        # (ncu's ALU-pipe activity of the kernel is reported beside the fraction).
         # Peak = 148 SMs x 4 SMSPs x 16 lanes/clk (ALU pipe, rt = 2) x the SM clock under load.
-        FP_ALU_OPS = 36
+        FP_ALU_OPS = 32
         ops = items_v[dom] * FP_ALU_OPS
         ach = ops / (ms_v[dom] / 1e3) / 1e9
         pk = 148 * 4 * 16 * clk_mhz * 1e6 / 1e9

@@ -1767,6 +1767,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_cahead_lean(const int32_t *__re
 // its candidate read, the subtraction compare and two terms + two finalisers.  The walk is
 // load-balanced like the count kernels: lane-own rows when the unit's runs are even, long
 // rows (>= 32 candidates) by the whole warp, the rest by a shuffle owner search.
+#ifndef GSI_FP_EVEN
+#define GSI_FP_EVEN 16   // k_final_fp: lane-own rows when 32 rows' total >= GSI_FP_EVEN x the longest
+#endif
 template <int NINJ, bool TT>   // TT: x's terms from the per-candidate term table T (else computed)
 __global__ void __launch_bounds__(kThreads, 4) k_final_fp(const int32_t *__restrict__ M, long long r0, long long r1,
                                                           const Loc *__restrict__ loc, StepParams P, int qx,
@@ -1829,7 +1832,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_final_fp(const int32_t *__restr
         }
         const uint32_t T = __shfl_sync(0xffffffffu, inc, 31);
         const uint32_t maxlen = __reduce_max_sync(0xffffffffu, L.len);
-        if (maxlen * 16 <= T) {   // even runs: every lane walks its own row
+        if (maxlen * GSI_FP_EVEN <= T) {   // even runs: every lane walks its own row
             for (uint32_t kk = 0; kk < L.len; kk++) fp_match(L.off + kk, inj, s1, s2);
             continue;
         }
