@@ -1770,8 +1770,11 @@ __global__ void __launch_bounds__(kThreads, 4) k_cahead_lean(const int32_t *__re
 #ifndef GSI_FP_EVEN
 #define GSI_FP_EVEN 16   // k_final_fp: lane-own rows when 32 rows' total >= GSI_FP_EVEN x the longest
 #endif
+#ifndef GSI_FP_MINB
+#define GSI_FP_MINB 4    // k_final_fp: resident CTAs per SM the registers are sized for
+#endif
 template <int NINJ, bool TT>   // TT: x's terms from the per-candidate term table T (else computed)
-__global__ void __launch_bounds__(kThreads, 4) k_final_fp(const int32_t *__restrict__ M, long long r0, long long r1,
+__global__ void __launch_bounds__(kThreads, GSI_FP_MINB) k_final_fp(const int32_t *__restrict__ M, long long r0, long long r1,
                                                           const Loc *__restrict__ loc, StepParams P, int qx,
                                                           const int32_t *__restrict__ cip,
                                                           const ulonglong2 *__restrict__ T, Counters *ctr) {
