@@ -237,6 +237,10 @@ def run_gsi(args):
         small = {}
         for cfg in args.small_configs:
             small[cfg] = small_query_latency(gsi, cfg, args.queries, args.k, local)
+    # ---- the oracle single-threaded on C1-C3 (a baseline, not the target) --
+    cpu_single = None
+    if ws == 1 and not args.no_small and rank == 0:
+        cpu_single = oracle_single_thread(args.queries, args.k)
 
     # ---- workload + graph (rank 0 builds; replicas via NCCL broadcast) ----------------
     if rank == 0:
@@ -536,6 +540,7 @@ def run_gsi(args):
                 "d2h_bytes_per_step": d2h, "ms_per_query": 1000.0 * e2e_s / args.steps / len(qs)},
         "kernel_variants": _variants(launch_stats), "count_only": count_only, "table": table, "roofline": roofline, "multi_gpu_balance_emulated": balance,
         "small_queries": small,
+        "cpu_baseline_single_thread": cpu_single,
         "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": launches,
         "graph": {"n_groups": info["n_groups"], "max_chain": info["max_chain"],
                   "bytes_total": info["bytes_total"], "build_ms": info["ms_build"]},
@@ -551,6 +556,39 @@ def _variants(stats):
     for s_ in stats:
         for k_, v_ in s_["variants"].items():
             out[k_] = out.get(k_, 0) + v_
+    return out
+
+
+def oracle_single_thread(nq, k, timeout_s=2.0):
+    """The CPU oracle, one thread, per query on C1 (the Fig. 1 query) and the C2 / C3 walk
+    queries the GPU latency section runs: median of 3 runs per query (C1) / one run (C2, C3,
+    per-query timeout, partial counts kept), then p50 / mean over the queries."""
+    import oracle
+    out = {}
+    g1, q1 = W.fig1()
+    og = oracle.OracleGraph(g1)
+    ts = []
+    for _ in range(3):
+        t = time.perf_counter()
+        c, _, _ = oracle.match(og, q1, table=False, threads=1)
+        ts.append(1000.0 * (time.perf_counter() - t))
+    out["C1"] = {"queries": 1, "p50_ms": float(np.median(ts)), "matches": int(c)}
+    for cfg in ("C2", "C3"):
+        g, qs = make_workload(cfg, nq, k, "cuda" if _cuda_ok() else "cpu")   # the GPU section's inputs
+        og = oracle.OracleGraph(g)
+        per, tot, touts = [], 0, 0
+        for q in qs:
+            t = time.perf_counter()
+            c, _, _ = oracle.match(og, q, table=False, threads=1, timeout=timeout_s, partial=True)
+            el = 1000.0 * (time.perf_counter() - t)
+            touts += el >= 1000.0 * timeout_s
+            per.append(el)
+            tot += c
+        a = np.array(per)
+        out[cfg] = {"queries": len(per), "p50_ms": float(np.percentile(a, 50)), "mean_ms": float(a.mean()),
+                    "p95_ms": float(np.percentile(a, 95)), "timeouts": int(touts), "matches": int(tot)}
+    out["threads"] = 1
+    out["note"] = "oracle/ backtracker as it stands, one host thread, per-query wall time; a baseline, not the target"
     return out
 
 
@@ -633,7 +671,7 @@ def main():
     ap.add_argument("--no-balance", action="store_true", help="skip the emulated multi-GPU balance")
     ap.add_argument("--shard-pieces", type=int, default=8, help="interleaved shard pieces per rank (N > 1)")
     ap.add_argument("--no-small", action="store_true", help="skip the small-query latency section")
-    ap.add_argument("--small-configs", nargs="*", default=["C2", "C4"])
+    ap.add_argument("--small-configs", nargs="*", default=["C2", "C3", "C4"])
     args = ap.parse_args()
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
