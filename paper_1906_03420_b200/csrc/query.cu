@@ -2170,9 +2170,13 @@ __global__ void __launch_bounds__(kThreads, 4) k_next_lean(const int32_t *__rest
             if (km) {
                 const unsigned long long lo0 = __shfl_sync(0xffffffffu, lo, 0);   // lane 0 is always active
                 int32_t *dst = out + lo0 * (unsigned)W;
-                const unsigned nr = min(32u, T - j0) * (unsigned)W;
-                for (unsigned e = lane; e < nr; e += 32)
-                    if ((km >> ((e * invW) >> 16)) & 1u) dst[e] = sw[e];
+                const unsigned nb = min(32u, T - j0), nr = nb * (unsigned)W;
+                if (km == (nb == 32u ? 0xFFFFFFFFu : (1u << nb) - 1u)) {   // every row kept: a plain copy
+                    for (unsigned e = lane; e < nr; e += 32) dst[e] = sw[e];
+                } else {
+                    for (unsigned e = lane; e < nr; e += 32)
+                        if ((km >> ((e * invW) >> 16)) & 1u) dst[e] = sw[e];
+                }
             }
             __syncwarp();
 #else
